@@ -1,0 +1,87 @@
+/* fbx.h -- C-ABI of libfbx.so, the B200 FeatureBox extraction runtime.
+ *
+ * Replaces, for the per-record extraction path, the reference's
+ *   pipeline._extract_batch(table, prepared, ctx)   pkg/src/featurebox/pipeline.py:718-737
+ *   device.execute_plan(ctx, plan, dag, state, ev)  pkg/src/featurebox/device.py:434-444
+ *   device.NodeEvaluator.__init__ (resolve + bind)  pkg/src/featurebox/device.py:263-293
+ *   mempool.ArenaPool / group_allocate / reset      pkg/src/featurebox/mempool.py:87-145
+ *   featureops.DictTable / dict_lookup              pkg/src/featurebox/featureops.py:104-167
+ *   viewpipe.JoinIndex / join_with_index (probe)    pkg/src/featurebox/viewpipe.py:498-547
+ *
+ * All entry points take plain pointers and sizes.  Every function returns 0
+ * on success or a negative FBX_E* code; fbx_last_error() gives the message
+ * (thread-local).  Device pointers are CUDA device addresses; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Calls release no locks of
+ * their own and are safe to call from a thread without the Python GIL.
+ */
+#ifndef FBX_H
+#define FBX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "fbx_abi.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FBX_OK 0
+#define FBX_E_ARG (-1)
+#define FBX_E_COMPILE (-2)
+#define FBX_E_CUDA (-3)
+#define FBX_E_NOT_FOUND (-4)
+#define FBX_E_DUPLICATE (-5)
+
+typedef struct fbx_program fbx_program; /* a loaded plan module (CUmodule) */
+typedef struct fbx_kernel fbx_kernel;   /* one kernel of a program */
+
+const char* fbx_version(void);
+const char* fbx_last_error(void);
+
+/* -- plan compilation (host-only; no GPU needed) ------------------------
+ * Compile a generated plan source (NVRTC, -arch=sm_100a) to a cubin.
+ * Replaces NodeEvaluator's once-per-run resolution (device.py:271-293) and
+ * the paper's runtime-compiled meta-kernel.  *image is
+ * malloc'ed; free with fbx_free(). */
+int fbx_compile(const char* source, const char* program_name, const char* const* options,
+                int n_options, void** image, size_t* image_bytes, char* log, size_t log_capacity);
+void fbx_free(void* p);
+
+/* -- program loading / launching (needs a GPU) -------------------------- */
+int fbx_program_load(const void* image, size_t image_bytes, fbx_program** out);
+int fbx_program_unload(fbx_program* prog);
+int fbx_program_kernel(fbx_program* prog, const char* name, fbx_kernel** out);
+/* max dynamic shared memory / register info of a kernel */
+int fbx_kernel_attributes(fbx_kernel* k, int* num_regs, int* max_threads, int* static_smem);
+int fbx_kernel_set_max_dynamic_smem(fbx_kernel* k, int bytes);
+
+/* Launch one plan kernel.  The layered operator DAG of a whole driver chunk
+ * runs inside this one launch (execute_plan's per-layer barriers become the
+ * per-row program order, since every operator is row-local). */
+int fbx_launch(fbx_kernel* k, unsigned grid, unsigned block, unsigned dyn_smem, void* stream,
+               const fbx_params* params);
+
+/* -- arena + state helpers ---------------------------------------------- */
+/* Reset the run state (counters, pool head, error word, tile ticket) and the
+ * per-tile look-back status words: mempool.ArenaPool.reset (mempool.py:136). */
+int fbx_state_reset(fbx_state* d_state, unsigned long long* d_tile_status, size_t n_tiles,
+                    void* stream);
+
+/* Build an HBM open-addressing dictionary table (featureops.py:104-167):
+ * n keys given as a byte blob + u32 offsets[n+1] (device), u64 values.
+ * slots: capacity * 32 bytes (capacity a power of two >= 2n).  Returns
+ * FBX_E_DUPLICATE when two keys are equal (load_dict_table's duplicate-key
+ * error, featureops.py:147). */
+int fbx_dict_build(void* d_slots, unsigned long long capacity, const unsigned char* d_keyblob,
+                   const unsigned int* d_key_offsets, const unsigned long long* d_values,
+                   unsigned long long n, unsigned long long* d_dup_flag, void* stream);
+
+/* Write `bytes` of a scratch buffer (an L2 flush between timed steps). */
+int fbx_l2_flush(void* d_buf, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FBX_H */

@@ -1,0 +1,47 @@
+"""Build libfbx.so in-tree with nvcc for sm_100a (the driver's build() check).
+
+The plan kernels themselves are generated per plan and compiled at prepare
+time by NVRTC through ``fbx_compile``; this builds the C-ABI runtime and its
+precompiled kernels.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+LIB = PKG / "libfbx.so"
+SOURCES = [PKG / "csrc" / "fbx_runtime.cu"]
+HEADERS = [ROOT / "include" / "fbx.h", ROOT / "include" / "fbx_abi.h"]
+CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+
+
+def nvcc_command() -> list[str]:
+    return [str(CUDA / "bin" / "nvcc"), "-gencode", "arch=compute_100a,code=sm_100a",
+            "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
+            "-cudart", "static", f"-I{ROOT / 'include'}", "-o", str(LIB),
+            *map(str, SOURCES), f"-L{CUDA / 'lib64'}", "-lnvrtc", "-ldl",
+            "-Xlinker", f"-rpath,{CUDA / 'lib64'}"]
+
+
+def stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
+
+
+def build_library(force: bool = False, verbose: bool = False) -> Path:
+    if force or stale():
+        cmd = nvcc_command()
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    build_library(force=True, verbose=True)

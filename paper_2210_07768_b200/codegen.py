@@ -1,0 +1,1157 @@
+"""Plan -> CUDA: the runtime-compiled fused meta-kernel of a whole plan.
+
+The reference runs each layer of the operator DAG as one "meta-kernel" over
+a chunk (device.py:341-410, runtime compilation :207).
+Every operator is row-local, so on the B200 the whole per-record path of a
+driver chunk -- clean (viewpipe.py:334-431), side-view join probe
+(viewpipe.py:537-547), the layered DAG (device.py:434-444), the uniqueness
+check + basic merge (pipeline.py:1055-1075) and emission (pipeline.py:
+375-433) -- is generated as ONE kernel: one CTA per chunk of ``batch_size``
+rows, one thread per row, the layer order as program order.  The chunk's
+instances are then sorted by instance id in shared memory (the reference's
+merge order, viewpipe.py:521), the CSR offsets are placed with a decoupled
+look-back across chunks, and counters/digest are reduced once per CTA.
+
+Static typing of values lets the generator specialise every node:
+  i64 (Int64 column) | u64 (sign / lookup result) | f32 (Float32 column) | str.
+A string is a view ``fbx::Str`` into the staged record bytes, an input
+column, the HBM pool or a per-thread decimal buffer; only ``lower`` (when a
+byte changes), multi-part ``concat`` and escaped JSON strings allocate, via
+the block-level bump allocator (mempool.py:114-134).
+
+Constructs without a bit-exact device implementation raise
+``UnsupportedOnDevice`` at plan time (never a silent divergence).
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field
+from fractions import Fraction
+from pathlib import Path
+from typing import Mapping, Sequence
+
+from .columns import Kind
+from .config import BoolExpr, Comparison, UnsupportedOnDevice
+from .featureops import FunctionDef, fnv1a64
+
+CSRC = Path(__file__).resolve().parent / "csrc"
+INCLUDE = Path(__file__).resolve().parent.parent / "include"
+
+INT64_MIN, INT64_MAX = -(1 << 63), (1 << 63) - 1
+SPAN_BUDGET = 40 * 1024  # bytes of dynamic shared memory for staged record spans
+MASK64 = (1 << 64) - 1
+
+STAGE = {"prepare": 0, "read": 1, "clean": 2, "join": 3, "extract": 4, "merge": 5, "emit": 6}
+ERR = {"type": 1, "value": 2, "encode": 3, "pool": 4, "null_label": 5, "label_range": 6,
+       "dup_id": 7, "multi_match": 8, "json_bigint": 9, "json_deep": 10,
+       "unicode_lower": 11, "float_overflow": 12, "float_slow": 13}
+
+
+def library_source() -> str:
+    """fbx_abi.h + fbx_core.cuh, flattened for NVRTC (no include paths)."""
+    abi = (INCLUDE / "fbx_abi.h").read_text()
+    core = (CSRC / "device" / "fbx_core.cuh").read_text()
+    return abi + "\n" + core.replace('#include "fbx_abi.h"', "")
+
+
+# ---------------------------------------------------------------------------
+# plan IR consumed by the generator (built by engine.prepare)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class ViewIR:
+    name: str
+    kinds: dict[str, Kind]          # input columns (after projection), ordered
+    fills: dict[str, object]
+    extractions: list               # config.JsonExtraction
+    filter: object | None           # bound filter expression
+    keys: tuple[str, ...] = ()      # join key columns (side views / basic)
+
+    def cleaned_kinds(self) -> dict[str, Kind]:
+        out = dict(self.kinds)
+        for e in self.extractions:
+            out.setdefault(e.output, e.kind)
+        return out
+
+
+@dataclass
+class NodeIR:
+    name: str
+    role: str                       # pre | body | post
+    op: str                         # operator name
+    fn: FunctionDef
+    layer: int
+    rank: int                       # (layer, name) rank: error priority
+    inputs: tuple[str, ...] = ()    # body: operator inputs; pre: (column,)
+    slot: int | None = None
+    writes: tuple[str, ...] = ()
+
+
+@dataclass
+class PlanIR:
+    driver: ViewIR
+    sides: list[ViewIR]
+    basic: ViewIR | None
+    join_keys: tuple[str, ...]
+    nodes: list[NodeIR]             # in (layer, name) order
+    pre_of: dict[str, dict[int, str]]
+    producer: dict[str, str]        # column -> node producing it
+    features: dict[str, int]
+    instance_column: str
+    label_column: str
+    chunk: int
+    tables: dict[str, int]          # dictionary name -> table index
+    table_defaults: dict[str, int]
+    extract_outputs: list[tuple[str, str]] = field(default_factory=list)  # (col, domain)
+    stage_strings: bool = True
+
+
+@dataclass
+class Program:
+    source: str
+    slots: dict[str, int]           # param slot name -> index
+    threads: int
+    smem_bytes: int
+    kernels: list[str]
+    side_kernels: list[str]
+    notes: list[str]
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+@dataclass
+class V:
+    """A value in generated code: C var `c` (+ `c_n` null flag, `c_l` lone)."""
+
+    t: str                # i64 | u64 | f32 | str
+    c: str
+    nullable: bool = True
+    lone: bool = False
+
+    @property
+    def n(self) -> str:
+        return f"{self.c}_n" if self.nullable else "false"
+
+    @property
+    def l(self) -> str:  # noqa: E743
+        return f"{self.c}_l" if self.lone else "false"
+
+
+def _c_bytes(b: bytes) -> str:
+    return "{" + ",".join(str(x) for x in b) + ("}" if b else "0}")
+
+
+def _u64(v: int) -> str:
+    return f"0x{v & MASK64:016X}ull"
+
+
+def _i64(v: int) -> str:
+    return f"((i64){_u64(v)})"
+
+
+def _f32_bits(x: float) -> int:
+    b = struct.unpack("<I", struct.pack("<f", x))[0]
+    if (b & 0x7F800000) == 0x7F800000 and (b & 0x007FFFFF):
+        b |= 0x00400000
+    return b
+
+
+class Gen:
+    """Line emitter with slot + constant pools."""
+
+    def __init__(self):
+        self.lines: list[str] = []
+        self.ind = 0
+        self.slots: dict[str, int] = {}
+        self.consts: list[bytes] = []
+        self.const_off: dict[bytes, int] = {}
+        self.const_size = 0
+        self.tmp = 0
+
+    def __call__(self, line: str = ""):
+        lead = len(line) - len(line.lstrip("}"))
+        self.ind -= lead
+        self.lines.append("  " * self.ind + line if line else "")
+        self.ind += line.count("{") - line.count("}") + lead
+
+    def slot(self, name: str) -> int:
+        if name not in self.slots:
+            self.slots[name] = len(self.slots)
+        return self.slots[name]
+
+    def p(self, name: str, ctype: str = "u64") -> str:
+        return f"(({ctype})P.v[{self.slot(name)}])"
+
+    def const(self, data: bytes) -> str:
+        """Offset expression of a byte constant in the K_STR blob."""
+        if data not in self.const_off:
+            self.const_off[data] = self.const_size
+            self.consts.append(data)
+            self.const_size += len(data)
+        return f"(K_STR + {self.const_off[data]})"
+
+    def fresh(self, base: str) -> str:
+        self.tmp += 1
+        return f"{base}{self.tmp}"
+
+
+# ---------------------------------------------------------------------------
+# the generator
+# ---------------------------------------------------------------------------
+
+class PlanCodegen:
+    def __init__(self, ir: PlanIR):
+        self.ir = ir
+        self.g = Gen()
+        self.notes: list[str] = []
+        if ir.chunk > 1024:
+            raise UnsupportedOnDevice(
+                f"batch_size {ir.chunk} > 1024: one CTA per chunk is the only emission "
+                "order implemented on device")
+        self.nt = max(32, (ir.chunk + 31) // 32 * 32)
+        self.nsort = 1 << (self.nt - 1).bit_length()
+        self.pool_sites = 0
+
+    # -- value helpers ---------------------------------------------------------
+    def kind_t(self, kind: Kind) -> str:
+        return {Kind.INT64: "i64", Kind.FLOAT32: "f32", Kind.UTF8: "str", Kind.JSON: "str"}[kind]
+
+    def decl(self, v: V, init_null: bool = True):
+        g = self.g
+        ctype = {"i64": "u64", "u64": "u64", "f32": "u32", "str": "fbx::Str"}[v.t]
+        init = "fbx::Str{nullptr, 0u}" if v.t == "str" else "0"
+        g(f"{ctype} {v.c} = {init};")
+        if v.nullable:
+            g(f"bool {v.c}_n = {'true' if init_null else 'false'};")
+        if v.lone:
+            g(f"bool {v.c}_l = false;")
+
+    def row_error(self, stage: str, code: str, layer: int = 0, rank: int = 0,
+                  detail: str = "0ull"):
+        self.g(f"fbx::raise_err(ST, fbx::err_key(chunk, {STAGE[stage]}u, {layer}u, {rank}u, "
+               f"{ERR[code]}u), {detail}); alive = false;")
+
+    # stringify a value for lower/trim/token/concat/lookup (Python str(v))
+    def as_str(self, v: V, what: str) -> V:
+        if v.t == "str":
+            return v
+        if v.t == "f32":
+            raise UnsupportedOnDevice(
+                f"{what}: str() of a Float32 value (Python float repr) is not implemented "
+                "on device")
+        g = self.g
+        s = V("str", g.fresh("dec"), v.nullable)
+        buf = s.c + "_buf"
+        g(f"__align__(16) u8 {buf}[24];")
+        self.decl(s)
+        signed = "true" if v.t == "i64" else "false"
+        cond = f"alive && !{v.n}" if v.nullable else "alive"
+        g(f"if ({cond}) {{")
+        g(f"u32 L = fbx::int_dec_len({v.c}, {signed}); fbx::int_dec({buf}, {v.c}, {signed}, L);")
+        g(f"{s.c} = fbx::Str{{{buf}, L}};")
+        if s.nullable:
+            g(f"{s.c}_n = false;")
+        g("}")
+        return s
+
+    def pool_alloc(self, size_expr: str) -> str:
+        """CTA-uniform pool allocation; returns the pointer var."""
+        g = self.g
+        self.pool_sites += 1
+        ptr = g.fresh("pa")
+        g(f"u8* {ptr};")
+        g("{")
+        g("bool exh = false;")
+        g(f"{ptr} = fbx::pool_alloc<NT>(sm.scan, &sm.pool_base, ST, POOL, POOL_CAP, "
+          f"(u32)({size_expr}), &exh);")
+        g(f"if (exh && ({size_expr}) != 0u && alive) {{ fbx::raise_err(ST, fbx::err_key(chunk, "
+          f"CUR_STAGE, CUR_LAYER, CUR_RANK, {ERR['pool']}u), 0ull); alive = false; }}")
+        g("}")
+        return ptr
+
+    # -- column access --------------------------------------------------------------
+    def load_driver_column(self, name: str, kind: Kind) -> V:
+        g = self.g
+        t = self.kind_t(kind)
+        v = V(t, f"d_{name}", True)
+        nul = g.p(f"drv.{name}.nulls", "const u8*")
+        self.decl(v)
+        g(f"if (inrange) {{")
+        g(f"{v.c}_n = fbx::null_bit({nul}, row);")
+        if kind is Kind.INT64:
+            g(f"{v.c} = fbx::ldg_u64({g.p(f'drv.{name}.data', 'const u64*')} + row);")
+        elif kind is Kind.FLOAT32:
+            g(f"{v.c} = fbx::f32_canon_bits(fbx::ldg_u32({g.p(f'drv.{name}.data', 'const u32*')}"
+              f" + row));")
+        else:
+            offs = g.p(f"drv.{name}.offsets", "const u32*")
+            data = g.p(f"drv.{name}.data", "const u8*")
+            g(f"u32 o0 = fbx::ldg_u32({offs} + row), o1 = fbx::ldg_u32({offs} + row + 1);")
+            if self.ir.stage_strings and name in self.staged:
+                idx = self.staged.index(name)
+                g(f"const u8* base = sm_span_ok[{idx}] ? (sm_span_buf[{idx}] - sm_span_lo[{idx}])"
+                  f" : {data};")
+                g(f"{v.c} = fbx::Str{{base + o0, o1 - o0}};")
+            else:
+                g(f"{v.c} = fbx::Str{{{data} + o0, o1 - o0}};")
+        g("}")
+        return v
+
+    # -- JSON extraction ---------------------------------------------------------
+    def json_source(self, view: ViewIR, src: V, exts: list, prefix: str, stage: str,
+                    on_malformed: str) -> dict[str, V]:
+        """Parse one JSON source; returns output column -> V."""
+        g = self.g
+        np_ = len(exts)
+        if np_ > 8:
+            raise UnsupportedOnDevice("more than 8 extractions from one JSON source")
+        segs, offs, lens, nseg = b"", [], [], []
+        for e in exts:
+            parts = [p.encode("utf-8") for p in e.path.split(".")]
+            if len(parts) > 8:
+                raise UnsupportedOnDevice("JSON path deeper than 8 segments")
+            o, ln = [], []
+            for p in parts:
+                o.append(len(segs))
+                ln.append(len(p))
+                segs += p
+            offs += o + [0] * (8 - len(o))
+            lens += ln + [0] * (8 - len(ln))
+            nseg.append(len(parts))
+            if e.kind is Kind.JSON:
+                raise UnsupportedOnDevice(
+                    "Json-kind extraction (json.dumps re-serialisation) is not implemented "
+                    "on device")
+        tag = g.fresh("jp")
+        self.globals.append(f"__device__ const u8 {tag}_seg[] = {_c_bytes(segs)};")
+        self.globals.append(f"__device__ const u16 {tag}_off[] = "
+                            "{" + ",".join(map(str, offs)) + "};")
+        self.globals.append(f"__device__ const u8 {tag}_len[] = "
+                            "{" + ",".join(map(str, lens)) + "};")
+        self.globals.append(f"__device__ const u8 {tag}_ns[] = "
+                            "{" + ",".join(map(str, nseg)) + "};")
+        leaf = g.fresh("leaf")
+        g(f"fbx::JLeaf {leaf}[{np_}];")
+        g(f"bool {leaf}_ok = false;")
+        g(f"if (alive && !{src.n}) {{")
+        g(f"u32 js = fbx::json_extract<{np_}>({src.c}, fbx::JPathSet{{{tag}_seg, {tag}_off, "
+          f"{tag}_len, {tag}_ns}}, {leaf});")
+        g(f"if (js == fbx::JS_OK) {{ {leaf}_ok = true; }}")
+        g(f"else if (js == fbx::JS_MALFORMED) {{ {on_malformed} }}")
+        g("else if (js == fbx::JS_BIGINT) {")
+        self.row_error(stage, "json_bigint")
+        g("} else {")
+        self.row_error(stage, "json_deep")
+        g("}")
+        g("}")
+        out = {}
+        for pi, e in enumerate(exts):
+            lf = f"{leaf}[{pi}]"
+            if e.kind is Kind.UTF8:
+                v = V("str", g.fresh(f"{prefix}x"), True, lone=True)
+                self.decl(v)
+                g(f"bool {v.c}_esc = {leaf}_ok && {lf}.type == fbx::J_STRING && {lf}.esc;")
+                ptr = self.pool_alloc(f"({v.c}_esc && alive) ? ({lf}.end - {lf}.beg) : 0u")
+                g(f"if (alive && {leaf}_ok && {lf}.type == fbx::J_STRING) {{")
+                g(f"if (!{lf}.esc) {{ {v.c} = fbx::Str{{{src.c}.p + {lf}.beg, {lf}.end - {lf}.beg}};"
+                  f" {v.c}_n = false; }}")
+                g(f"else if ({ptr}) {{ u32 lone = 0; u32 L = fbx::j_unescape({src.c}.p, {lf}.beg, "
+                  f"{lf}.end, {ptr}, &lone); {v.c} = fbx::Str{{{ptr}, L}}; {v.c}_n = false; "
+                  f"{v.c}_l = lone != 0; }}")
+                g("}")
+            elif e.kind is Kind.INT64:
+                v = V("i64", g.fresh(f"{prefix}x"), True)
+                self.decl(v)
+                g(f"if (alive && {leaf}_ok && {lf}.type == fbx::J_INT) {{")
+                g(f"i64 t; if (fbx::j_to_i64({src.c}.p, {lf}.beg, {lf}.end, &t)) "
+                  f"{{ {v.c} = (u64)t; {v.c}_n = false; }}")
+                g("}")
+            else:  # FLOAT32
+                v = V("f32", g.fresh(f"{prefix}x"), True)
+                self.decl(v)
+                g(f"if (alive && {leaf}_ok) {{")
+                g(f"u32 bits = 0; u32 fs = fbx::j_to_f32({src.c}.p, {lf}, &bits);")
+                g(f"if (fs == 0u) {{ {v.c} = bits; {v.c}_n = false; }}")
+                g(f"else if (fs == 2u) {{")
+                self.row_error(stage, "float_overflow")
+                g("} else if (fs == 3u) {")
+                self.row_error(stage, "float_slow")
+                g("}")
+                g("}")
+            out[e.output] = v
+        return out
+
+    # -- filter -------------------------------------------------------------------------
+    def filter_expr(self, expr, vals: Mapping[str, V]) -> str:
+        if isinstance(expr, BoolExpr):
+            j = " && " if expr.kind == "and" else " || "
+            return "(" + j.join(self.filter_expr(p, vals) for p in expr.parts) + ")"
+        assert isinstance(expr, Comparison)
+        v = vals[expr.column]
+        nn = f"!{v.n}" if v.nullable else "true"
+        op, lit = expr.op, expr.literal
+        if v.t == "str":
+            b = lit.encode("utf-8", "surrogatepass")
+            k = self.g.const(b)
+            return f"({nn} && (fbx::str_cmp({v.c}, {k}, {len(b)}u) {op} 0))"
+        if v.t == "f32":
+            bits = _f32_bits(float(lit))
+            return f"({nn} && (__uint_as_float({v.c}) {op} __uint_as_float({bits}u)))"
+        # Int64 column vs int / float literal: exact Python semantics
+        x = f"((i64){v.c})"
+        if isinstance(lit, float):
+            if lit != lit:
+                return "false" if op != "!=" else nn
+            fr = Fraction(lit)
+        else:
+            fr = Fraction(lit)
+        return f"({nn} && {self._int_cmp(x, op, fr)})"
+
+    def _int_cmp(self, x: str, op: str, fr: Fraction) -> str:
+        import math
+        lo, hi = INT64_MIN, INT64_MAX
+        if op in ("==", "!="):
+            if fr.denominator != 1 or not lo <= fr.numerator <= hi:
+                return "true" if op == "!=" else "false"
+            return f"({x} {op} {_i64(fr.numerator)})"
+        if op in ("<", ">="):
+            c = math.ceil(fr)  # x < fr  <=>  x < ceil(fr)
+            if c > hi:
+                return "true" if op == "<" else "false"
+            if c <= lo:
+                return "false" if op == "<" else "true"
+            return f"({x} {op} {_i64(c)})"
+        c = math.floor(fr)  # x <= fr <=> x <= floor(fr) ; x > fr <=> x > floor(fr)
+        if c >= hi:
+            return "true" if op == "<=" else "false"
+        if c < lo:
+            return "false" if op == "<=" else "true"
+        return f"({x} {op} {_i64(c)})"
+
+    # -- clean ---------------------------------------------------------------------------
+    def clean_view(self, view: ViewIR, prefix: str, loader, stage: str, used: set[str],
+                   count_prefix: str) -> dict[str, V]:
+        """Cleaned values of one row: loads, JSON extraction, fills, filter."""
+        g = self.g
+        ckinds = view.cleaned_kinds()
+        raw: dict[str, V] = {}
+        sources = sorted({e.source for e in view.extractions})
+        need = set(used) | set(sources)
+        if view.filter is not None:
+            need |= _filter_columns(view.filter)
+        for name, kind in view.kinds.items():
+            if name in need:
+                raw[name] = loader(name, kind)
+        vals: dict[str, V] = dict(raw)
+        if sources:
+            g(f"bool {prefix}malformed = false;")
+        for s in sources:
+            exts = [e for e in view.extractions if e.source == s]
+            vals.update(self.json_source(view, raw[s], exts, prefix, stage,
+                                         f"{prefix}malformed = true;"))
+        if sources:
+            g(f"if (alive && {prefix}malformed) {{ alive = false; {count_prefix}malformed += 1u; }}")
+        ext_out = {e.output for e in view.extractions}
+        for name, fill in view.fills.items():
+            if name in ext_out or name not in vals:
+                continue  # an extraction output replaces the filled column
+            vals[name] = self.apply_fill(vals[name], view.kinds[name], fill)
+        if view.filter is not None:
+            cond = self.filter_expr(view.filter, vals)
+            g(f"if (alive && !({cond})) {{ alive = false; {count_prefix}filtered += 1u; }}")
+        return {k: v for k, v in vals.items() if k in ckinds}
+
+    def apply_fill(self, v: V, kind: Kind, fill) -> V:
+        g = self.g
+        out = V(v.t, g.fresh("f"), False, v.lone)
+        if kind is Kind.INT64:
+            if not INT64_MIN <= int(fill) <= INT64_MAX:
+                raise UnsupportedOnDevice("Int64 fill value outside int64")
+            g(f"u64 {out.c} = {v.n} ? {_u64(int(fill))} : {v.c};")
+        elif kind is Kind.FLOAT32:
+            g(f"u32 {out.c} = {v.n} ? {_f32_bits(float(fill))}u : {v.c};")
+        else:
+            b = str(fill).encode("utf-8", "surrogatepass")
+            k = g.const(b)
+            g(f"fbx::Str {out.c} = {v.n} ? fbx::Str{{{k}, {len(b)}u}} : {v.c};")
+        if v.lone:
+            g(f"bool {out.c}_l = !{v.n} && {v.l};")
+        return out
+
+    # -- join keys ----------------------------------------------------------------------
+    def key_hash(self, vals: Sequence[V], kinds: Sequence[Kind], out: str):
+        """FNV over the canonical key bytes (viewpipe.py:451-460): kind tag,
+        u32 BE length, BE payload -- identical on the build and probe sides."""
+        g = self.g
+        g(f"u64 {out};")
+        g("{")
+        g("fbx::Fnv h;")
+        for v, k in zip(vals, kinds):
+            g(f"h.byte({int(k)}u);")
+            if k is Kind.INT64:
+                g("h.word_be(8u);")
+                g(f"h.u64_be({v.c});")
+            elif k is Kind.FLOAT32:
+                g("h.word_be(4u);")
+                g(f"h.word_be({v.c});")
+            else:
+                g(f"h.word_be({v.c}.n); h.bytes({v.c}.p, {v.c}.n);")
+        g(f"{out} = fbx::table_tag(h.value());")
+        g("}")
+
+    def key_eq(self, a: Sequence[V], b: Sequence[V]) -> str:
+        terms = []
+        for x, y in zip(a, b):
+            if x.t == "str":
+                terms.append(f"fbx::str_eq({x.c}, {y.c})")
+            else:
+                terms.append(f"({x.c} == {y.c})")
+        return " && ".join(terms) if terms else "true"
+
+    # -- side views ----------------------------------------------------------------------
+    def side_loader(self, k: int, row: str):
+        g = self.g
+
+        def load(name: str, kind: Kind) -> V:
+            t = self.kind_t(kind)
+            v = V(t, g.fresh(f"s{k}_{name}_"), True)
+            self.decl(v)
+            nul = g.p(f"side{k}.{name}.nulls", "const u8*")
+            g(f"{v.c}_n = fbx::null_bit({nul}, {row});")
+            if kind is Kind.INT64:
+                g(f"{v.c} = fbx::ldg_u64({g.p(f'side{k}.{name}.data', 'const u64*')} + {row});")
+            elif kind is Kind.FLOAT32:
+                g(f"{v.c} = fbx::f32_canon_bits(fbx::ldg_u32("
+                  f"{g.p(f'side{k}.{name}.data', 'const u32*')} + {row}));")
+            else:
+                offs = g.p(f"side{k}.{name}.offsets", "const u32*")
+                data = g.p(f"side{k}.{name}.data", "const u8*")
+                g(f"{{ u32 o0 = fbx::ldg_u32({offs} + {row}), o1 = fbx::ldg_u32({offs} + {row} + 1);"
+                  f" {v.c} = fbx::Str{{{data} + o0, o1 - o0}}; }}")
+            return v
+        return load
+
+    def side_value(self, k: int, view: ViewIR, name: str, row: str) -> V:
+        """Cleaned value of side column `name` at side row `row` (gather)."""
+        g = self.g
+        ext = {e.output: e for e in view.extractions}
+        if name in ext:
+            e = ext[name]
+            t = self.kind_t(e.kind)
+            v = V(t, g.fresh(f"s{k}e_"), True, lone=(t == "str"))
+            self.decl(v)
+            if t == "str":
+                g(f"{{ u64 pp = fbx::ldg_u64({g.p(f'side{k}.ext.{name}.ptr', 'const u64*')} + {row});"
+                  f" u32 ll = fbx::ldg_u32({g.p(f'side{k}.ext.{name}.len', 'const u32*')} + {row});")
+                g(f"  {v.c}_n = (ll == 0xFFFFFFFFu); {v.c}_l = (ll & 0x80000000u) != 0u && !{v.c}_n;"
+                  f" {v.c} = fbx::Str{{(const u8*)pp, {v.c}_n ? 0u : (ll & 0x7FFFFFFFu)}}; }}")
+            else:
+                arr = g.p(f"side{k}.ext.{name}.val", "const u64*")
+                g(f"{{ u64 w = fbx::ldg_u64({arr} + {row}); "
+                  f"u8 nn = fbx::ldg_u8({g.p(f'side{k}.ext.{name}.null', 'const u8*')} + {row});"
+                  f" {v.c} = ({'u32' if t == 'f32' else 'u64'})w; {v.c}_n = nn != 0; }}")
+            return v
+        v = self.side_loader(k, row)(name, view.kinds[name])
+        if name in view.fills:
+            v = self.apply_fill(v, view.kinds[name], view.fills[name])
+        return v
+
+    # ------------------------------------------------------------------------------------
+    def side_prep_kernel(self, k: int, view: ViewIR, is_basic: bool) -> str:
+        """Index one side view (or the basic view) into its HBM join table."""
+        g = self.g
+        name = f"fbx_side_prep_{k}"
+        g(f'extern "C" __global__ void __launch_bounds__(256) {name}(const fbx_params P) {{')
+        g("fbx_state* ST = (fbx_state*)P.v[0];")
+        g(f"const u64 n = {g.p(f'side{k}.rows')};")
+        g(f"fbx::Slot* TBL = {g.p(f'side{k}.table', 'fbx::Slot*')};")
+        g(f"const u64 MASK = {g.p(f'side{k}.mask')};")
+        g(f"u8* POOL = {g.p('side_pool', 'u8*')}; const u64 POOL_CAP = {g.p('side_pool_cap')};")
+        g("u32 nmal = 0, nfilt = 0, nidx = 0;")
+        g("const u64 chunk = 0;")
+        g("for (u64 base = (u64)blockIdx.x * 256u; base < n; base += (u64)gridDim.x * 256u) {")
+        g("const u64 srow = base + threadIdx.x;")
+        g("bool alive = srow < n;")
+        g("const u64 row = alive ? srow : 0ull;")
+        g("__shared__ struct { fbx::BlockScanU32<256> scan; u64 pool_base; } sm;")
+        g("constexpr int NT = 256;")
+        g(f"u32 CUR_STAGE = {STAGE['prepare']}u, CUR_LAYER = 0u, CUR_RANK = 0u;")
+        g("u32 malformed = 0, filtered = 0;")
+        ckinds = view.cleaned_kinds()
+        loader = self.side_loader(k, "row")
+        used = set(view.keys)
+        vals = self.clean_view(view, f"sp{k}_", loader, "prepare", used, "")
+        g("nmal += malformed; nfilt += filtered;")
+        # store extraction outputs for the gather side
+        for e in view.extractions:
+            v = vals[e.output]
+            if v.t == "str":
+                g(f"if (srow < n) {{ {g.p(f'side{k}.ext.{e.output}.ptr', 'u64*')}[row] = (u64){v.c}.p;"
+                  f" {g.p(f'side{k}.ext.{e.output}.len', 'u32*')}[row] = (!alive || {v.n}) ? 0xFFFFFFFFu"
+                  f" : ({v.c}.n | ({v.l} ? 0x80000000u : 0u)); }}")
+            else:
+                g(f"if (srow < n) {{ {g.p(f'side{k}.ext.{e.output}.val', 'u64*')}[row] = (u64){v.c};"
+                  f" {g.p(f'side{k}.ext.{e.output}.null', 'u8*')}[row] = (!alive || {v.n}) ? 1 : 0; }}")
+        keys = [vals[c] for c in view.keys]
+        kk = [ckinds[c] for c in view.keys]
+        null_any = " || ".join(v.n for v in keys if v.nullable) or "false"
+        lone_any = " || ".join(v.l for v in keys if v.lone) or "false"
+        g(f"if (alive && ({lone_any}) && !({null_any})) {{")
+        self.row_error("prepare", "encode")
+        g("}")
+        g(f"if (alive && !({null_any})) {{")
+        self.key_hash(keys, kk, "tag")
+        g("u64 i = tag & MASK;")
+        g("while (true) {")
+        g("unsigned long long old = atomicCAS((unsigned long long*)&TBL[i].tag, 0ull, "
+          "(unsigned long long)tag);")
+        g("if (old == 0ull) { TBL[i].ref = (u32)row; __threadfence(); "
+          "atomicExch(&TBL[i].aux, 1u); ++nidx; break; }")
+        g("if (old == tag) {")
+        g("u32 c; do { c = *((volatile u32*)&TBL[i].aux); } while (c == 0u);")
+        g("const u64 other = *((volatile u32*)&TBL[i].ref);")
+        other = [self.side_value(k, view, c, "other") for c in view.keys]
+        g(f"if ({self.key_eq(keys, other)}) {{ atomicAdd(&TBL[i].aux, 1u); ++nidx; break; }}")
+        g("}")
+        g("i = (i + 1) & MASK;")
+        g("}")
+        g("}")
+        g("}")
+        g("if (nmal) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)nmal);")
+        g("if (nfilt) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)nfilt);")
+        g("if (nidx) atomicAdd((unsigned long long*)&ST->side_rows, (unsigned long long)nidx);")
+        g("}")
+        return name
+
+    # -- operator library --------------------------------------------------------------
+    def node_code(self, nd: NodeIR, args: list[V]) -> V:
+        fn = nd.fn
+        g = self.g
+        stage_ctx = f"CUR_STAGE = {STAGE['extract']}u; CUR_LAYER = {nd.layer}u; CUR_RANK = {nd.rank}u;"
+        g(f"// node {nd.name} [{fn.spec}] layer {nd.layer}")
+        g(stage_ctx)
+        err = lambda code: self.row_error("extract", code, nd.layer, nd.rank)  # noqa: E731
+        op = fn.op
+        if op == "id":
+            return args[0]
+        if op in ("mix", "fold"):
+            a = args[0]
+            if a.t in ("str", "f32"):
+                out = V("u64", g.fresh("n"), True)
+                self.decl(out)
+                g(f"if (alive && !{a.n}) {{")
+                err("type")
+                g("}")
+                return out
+            t = "u64" if (op == "mix" or a.t == "u64") else "i64"
+            out = V(t, g.fresh("n"), a.nullable)
+            if op == "mix":
+                g(f"u64 {out.c} = fbx::fnv_mix({a.c});")
+            elif a.t == "u64":
+                g(f"u64 {out.c} = ({a.c} >> 32) ^ ({a.c} & 0xFFFFFFFFull);")
+            else:
+                g(f"u64 {out.c} = (u64)(((i64){a.c}) >> 32) ^ ({a.c} & 0xFFFFFFFFull);")
+            if a.nullable:
+                g(f"bool {out.c}_n = {a.n};")
+            return out
+        if op == "token":
+            a = self.as_str(args[0], fn.spec)
+            out = V("str", g.fresh("n"), a.nullable, a.lone)
+            self.decl(out)
+            cond = f"alive && !{a.n}" if a.nullable else "alive"
+            g(f"if ({cond}) {{")
+            if len(fn.delim.encode("utf-8")) != 1:
+                err("value")
+            else:
+                if a.lone:
+                    g(f"if ({a.l}) {{")
+                    err("encode")
+                    g("}")
+                g(f"{out.c} = fbx::str_token({a.c}, {ord(fn.delim)}u, {fn.index}u);")
+                if out.nullable:
+                    g(f"{out.c}_n = false;")
+                if out.lone:
+                    g(f"{out.c}_l = {a.l};")
+            g("}")
+            return out
+        if op == "trim":
+            a = self.as_str(args[0], fn.spec)
+            out = V("str", g.fresh("n"), a.nullable, a.lone)
+            self.decl(out)
+            cond = f"alive && !{a.n}" if a.nullable else "alive"
+            g(f"if ({cond}) {{ {out.c} = fbx::str_trim({a.c});"
+              + (f" {out.c}_n = false;" if out.nullable else "")
+              + (f" {out.c}_l = {a.l};" if out.lone else "") + " }")
+            return out
+        if op == "lower":
+            a = self.as_str(args[0], fn.spec)
+            out = V("str", g.fresh("n"), a.nullable, a.lone)
+            self.decl(out)
+            cls = g.fresh("lc")
+            cond = f"alive && !{a.n}" if a.nullable else "alive"
+            g(f"u32 {cls} = ({cond}) ? fbx::str_lower_class({a.c}) : 0u;")
+            g(f"if ({cls} == 2u) {{")
+            err("unicode_lower")
+            g("}")
+            ptr = self.pool_alloc(f"({cls} == 1u && alive) ? {a.c}.n : 0u")
+            g(f"if ({cond}) {{")
+            g(f"if ({cls} == 1u) {{ if ({ptr}) {{ fbx::str_lower_copy({ptr}, {a.c}); "
+              f"{out.c} = fbx::Str{{{ptr}, {a.c}.n}}; }} }} else {{ {out.c} = {a.c}; }}")
+            if out.nullable:
+                g(f"{out.c}_n = false;")
+            if out.lone:
+                g(f"{out.c}_l = {a.l};")
+            g("}")
+            return out
+        if op == "lookup":
+            a = args[0]
+            out = V("u64", g.fresh("n"), False)
+            ti = self.ir.tables[fn.table]
+            dflt = self.ir.table_defaults[fn.table]
+            g(f"u64 {out.c} = {_u64(dflt)};")
+            s = self.as_str(a, fn.spec)
+            cond = f"alive && !{s.n}" if s.nullable else "alive"
+            lone = f" && !{s.l}" if s.lone else ""
+            g(f"if ({cond}{lone}) {{")
+            g(f"{out.c} = fbx::dict_lookup({g.p(f'dict{ti}.slots', 'const fbx::Slot*')}, "
+              f"{g.p(f'dict{ti}.mask')}, {g.p(f'dict{ti}.keys', 'const u8*')}, {s.c}, "
+              f"{_u64(dflt)});")
+            g("}")
+            return out
+        if op == "hash":
+            nullable = any(a.nullable for a in args)
+            out = V("u64", g.fresh("n"), nullable)
+            self.decl(out)
+            nulls = [a.n for a in args if a.nullable]
+            cond = "alive" + "".join(f" && !{x}" for x in nulls)
+            g(f"if ({cond}) {{")
+            lones = [a.l for a in args if a.t == "str" and a.lone]
+            if lones:
+                g(f"if ({' || '.join(lones)}) {{")
+                err("encode")
+                g("}")
+            h0 = fnv1a64(fn.slot.to_bytes(2, "big"))
+            g(f"fbx::Fnv h({_u64(h0)});")
+            for i, a in enumerate(args):
+                if i:
+                    g("h.byte(0u);")
+                if a.t == "str":
+                    g(f"h.bytes({a.c}.p, {a.c}.n);")
+                elif a.t == "f32":
+                    g(f"h.word_be({a.c});")
+                else:
+                    g(f"h.u64_be({a.c});")
+            g(f"{out.c} = h.value();")
+            if nullable:
+                g(f"{out.c}_n = false;")
+            g("}")
+            return out
+        if op == "concat":
+            parts = [self.as_str(a, fn.spec) for a in args]
+            nullable = any(p.nullable for p in parts)
+            lone = any(p.lone for p in parts)
+            if len(parts) == 1:
+                return parts[0]  # sep.join([s]) == s: a view
+            out = V("str", g.fresh("n"), nullable, lone)
+            self.decl(out)
+            sep = fn.sep.encode("utf-8", "surrogatepass")
+            nulls = [p.n for p in parts if p.nullable]
+            ok = g.fresh("ok")
+            g(f"bool {ok} = alive" + "".join(f" && !{x}" for x in nulls) + ";")
+            total = " + ".join(f"{p.c}.n" for p in parts) + f" + {len(sep) * (len(parts) - 1)}u"
+            ptr = self.pool_alloc(f"{ok} ? ({total}) : 0u")
+            g(f"if ({ok} && {ptr}) {{")
+            g(f"u8* d = {ptr};")
+            k = g.const(sep) if sep else None
+            for i, p in enumerate(parts):
+                if i and sep:
+                    g(f"for (u32 q = 0; q < {len(sep)}u; ++q) d[q] = {k}[q]; d += {len(sep)}u;")
+                g(f"fbx::str_copy(d, {p.c}); d += {p.c}.n;")
+            g(f"{out.c} = fbx::Str{{{ptr}, {total}}};")
+            if nullable:
+                g(f"{out.c}_n = false;")
+            if lone:
+                g(f"{out.c}_l = " + " || ".join(p.l for p in parts if p.lone) + ";")
+            g("}")
+            return out
+        raise UnsupportedOnDevice(f"function {fn.spec!r}")
+
+    # ------------------------------------------------------------------------------------
+    def pipeline_kernel(self) -> str:
+        ir, g = self.ir, self.g
+        nt, ns = self.nt, self.nsort
+        drv = ir.driver
+        dk = drv.cleaned_kinds()
+        # which driver var-length columns get staged through shared memory
+        needed = self.driver_needed()
+        self.staged = ([c for c, k in drv.kinds.items() if k.var_length and c in needed]
+                       if ir.stage_strings else [])[:16]
+        g(f"constexpr int NT = {nt};")
+        g(f"constexpr int NSORT = {ns};")
+        g(f"constexpr u32 SPAN_BUDGET = {self.span_cap}u;")
+        g(f'extern "C" __global__ void __launch_bounds__(NT) fbx_pipeline(const fbx_params P) {{')
+        g("fbx_state* ST = (fbx_state*)P.v[0];")
+        g(f"u64* STATUS = {g.p('tile_status', 'u64*')};")
+        g(f"const u64 ROW_LO = {g.p('row_lo')}, ROW_HI = {g.p('row_hi')};")
+        g(f"const u64 CHUNK0 = {g.p('chunk0')};")
+        g(f"u8* POOL = {g.p('pool', 'u8*')}; const u64 POOL_CAP = {g.p('pool_cap')};")
+        g("extern __shared__ __align__(16) u8 dyn_smem[];")
+        g("__shared__ struct {")
+        g("fbx::BlockScanU32<NT> scan;")
+        g("u64 pool_base; u32 tile; u64 ex_inst, ex_signs;")
+        g("u64 keys[NSORT]; u32 vals[NSORT];")
+        g("u32 rank[NT]; u32 soff[NT]; u32 m[NT];")
+        g("u64 span_lo[16]; u32 span_len[16];")
+        g("u64 red[NT / 32][5];")
+        g("} sm;")
+        g("if (threadIdx.x == 0) sm.tile = (u32)atomicAdd((unsigned long long*)&ST->tile_ticket, 1ull);")
+        g("__syncthreads();")
+        g("const u32 tile = sm.tile;")
+        g(f"const u64 chunk = CHUNK0 + tile;")
+        g(f"const u64 row0 = ROW_LO + (u64)tile * {ir.chunk}ull;")
+        g(f"const u64 row_end = (row0 + {ir.chunk}ull < ROW_HI) ? row0 + {ir.chunk}ull : ROW_HI;")
+        g("const u64 srow = row0 + threadIdx.x;")
+        g("const bool inrange = srow < row_end;")
+        g("const u64 row = inrange ? srow : row0;")
+        g("bool alive = inrange;")
+        g("u32 malformed = 0, filtered = 0;")
+        g(f"u32 CUR_STAGE = {STAGE['clean']}u, CUR_LAYER = 0u, CUR_RANK = 0u;")
+        # ---- stage the chunk's var-length spans into shared memory --------------
+        if self.staged:
+            g("// stage the chunk's var-length spans into shared memory (one budget,")
+            g("// first-fit in column order; a span that does not fit is read from HBM)")
+            ns_ = len(self.staged)
+            g(f"__shared__ const u8* sm_span_buf[{ns_}];")
+            g(f"__shared__ u64 sm_span_lo[{ns_}];")
+            g(f"__shared__ bool sm_span_ok[{ns_}];")
+            g("if (threadIdx.x == 0) {")
+            g("u32 used = 0;")
+            for i, c in enumerate(self.staged):
+                offs = g.p(f"drv.{c}.offsets", "const u32*")
+                g("{")
+                g(f"u64 lo = fbx::ldg_u32({offs} + row0), hi = fbx::ldg_u32({offs} + row_end);")
+                g("u64 alo = lo & ~15ull, ahi = (hi + 15ull) & ~15ull;")
+                g("bool ok = used + (ahi - alo) <= SPAN_BUDGET;")
+                g(f"sm_span_lo[{i}] = alo; sm_span_ok[{i}] = ok; sm_span_buf[{i}] = dyn_smem + used;")
+                g(f"sm.span_lo[{i}] = alo; sm.span_len[{i}] = ok ? (u32)(ahi - alo) : 0u;")
+                g("if (ok) used += (u32)(ahi - alo);")
+                g("}")
+            g("}")
+            g("__syncthreads();")
+            for i, c in enumerate(self.staged):
+                data = g.p(f"drv.{c}.data", "const u8*")
+                g("{")
+                g(f"const uint4* src = (const uint4*)({data} + sm.span_lo[{i}]);")
+                g(f"uint4* dst = (uint4*)sm_span_buf[{i}];")
+                g(f"for (u32 q = threadIdx.x; q < sm.span_len[{i}] / 16u; q += NT) dst[q] = __ldg(src + q);")
+                g("}")
+            g("__syncthreads();")
+        # ---- clean ----------------------------------------------------------------
+        g("// ---- clean (viewpipe.clean_views) ----")
+        vals = self.clean_view(drv, "d_", self.load_driver_column, "clean", needed, "")
+        # ---- join -----------------------------------------------------------------
+        g(f"CUR_STAGE = {STAGE['join']}u;")
+        env: dict[str, V] = dict(vals)
+        side_rows: list[str] = []
+        self.side_rows = side_rows
+        for k, sv in enumerate(ir.sides):
+            g(f"// ---- join side view {sv.name!r} on {list(ir.join_keys)} ----")
+            keys = [env[c] for c in ir.join_keys]
+            kinds = [dk[c] for c in ir.join_keys]
+            srow = f"sr{k}"
+            g(f"u64 {srow} = 0ull;")
+            null_any = " || ".join(v.n for v in keys if v.nullable) or "false"
+            lone_any = " || ".join(v.l for v in keys if v.lone) or "false"
+            g(f"if (alive && ({null_any})) alive = false;")
+            g(f"if (alive && ({lone_any})) {{")
+            self.row_error("join", "encode")
+            g("}")
+            g("if (alive) {")
+            self.key_hash(keys, kinds, "tag")
+            g(f"const fbx::Slot* T = {g.p(f'side{k}.table', 'const fbx::Slot*')};")
+            g(f"const u64 MASK = {g.p(f'side{k}.mask')};")
+            g("u64 i = tag & MASK; u32 cnt = 0;")
+            g("while (true) {")
+            g("u64 t = __ldg(&T[i].tag);")
+            g("if (t == 0ull) break;")
+            g("if (t == tag) {")
+            g("const u64 other = __ldg(&T[i].ref);")
+            other = [self.side_value(k, sv, c, "other") for c in ir.join_keys]
+            g(f"if ({self.key_eq(keys, other)}) {{ cnt = __ldg(&T[i].aux); {srow} = other; break; }}")
+            g("}")
+            g("i = (i + 1) & MASK;")
+            g("}")
+            g("if (cnt == 0u) alive = false;")
+            g("else if (cnt > 1u) {")
+            idv = env.get(ir.instance_column)
+            g(f"if (!{idv.n}) {{")
+            self.row_error("merge", "multi_match")
+            g("} else { alive = false; }")
+            g("}")
+            g("}")
+            side_rows.append(srow)
+            for c in sv.cleaned_kinds():
+                if c in ir.join_keys:
+                    continue
+                env[c] = ("side", k, c)  # lazily gathered
+        g("u32 joined = alive ? 1u : 0u;")
+        self.env = env
+        # ---- DAG --------------------------------------------------------------------
+        g(f"CUR_STAGE = {STAGE['extract']}u;")
+        g("// ---- operator DAG in (layer, name) order ----")
+        node_out: dict[str, V] = {}
+        for nd in ir.nodes:
+            if nd.role == "pre":
+                args = [self.col(nd.inputs[0], node_out)]
+            elif nd.role == "post":
+                args = [node_out[nd.op]]
+            else:
+                pre = ir.pre_of.get(nd.op, {})
+                args = [node_out[pre[i]] if i in pre else self.col(c, node_out)
+                        for i, c in enumerate(nd.inputs)]
+            node_out[nd.name] = self.node_code(nd, args)
+        self.node_out = node_out
+        # u64-domain output columns must be u64 images (wrap_u64, pipeline.py:731)
+        for col, domain in ir.extract_outputs:
+            v = node_out[ir.producer[col]]
+            if domain == "u64" and v.t == "i64":
+                g(f"if (alive && !{v.n} && (i64){v.c} < 0) {{")
+                self.row_error("extract", "value")
+                g("}")
+        # ---- uniqueness check + merge ----------------------------------------------
+        g(f"CUR_STAGE = {STAGE['merge']}u;")
+        idv = self.col(ir.instance_column, node_out)
+        lab = self.col(ir.label_column, node_out)
+        g("// ---- check_unique_ids over the run (pipeline.py:1071) ----")
+        g(f"if (alive && !{idv.n}) {{")
+        g(f"u64* IDS = {g.p('idset', 'u64*')}; const u64 IMASK = {g.p('idset_mask')};")
+        g(f"const u64 key = {idv.c};")
+        g("if (key == 0ull) {")
+        g("if (atomicAdd((unsigned long long*)&IDS[IMASK + 1], 1ull) != 0ull) {")
+        self.row_error("merge", "dup_id", detail="key")
+        g("}")
+        g("} else {")
+        g("u64 i = (key * 0x9E3779B97F4A7C15ull) >> 20 & IMASK;")
+        g("while (true) {")
+        g("unsigned long long old = atomicCAS((unsigned long long*)&IDS[i], 0ull, "
+          "(unsigned long long)key);")
+        g("if (old == 0ull) break;")
+        g("if (old == key) {")
+        self.row_error("merge", "dup_id", detail="key")
+        g("break; }")
+        g("i = (i + 1) & IMASK;")
+        g("}")
+        g("}")
+        g("}")
+        if ir.basic is not None:
+            bk = len(ir.sides)
+            g("// ---- merge with the basic view on the instance id ----")
+            g(f"u64 br = 0ull;")
+            g(f"if (alive && {idv.n}) alive = false;")
+            g("if (alive) {")
+            self.key_hash([idv], [Kind.INT64], "tag")
+            g(f"const fbx::Slot* T = {g.p(f'side{bk}.table', 'const fbx::Slot*')};")
+            g(f"const u64 MASK = {g.p(f'side{bk}.mask')};")
+            g("u64 i = tag & MASK; bool hit = false;")
+            g("while (true) {")
+            g("u64 t = __ldg(&T[i].tag);")
+            g("if (t == 0ull) break;")
+            g("if (t == tag) {")
+            g("const u64 other = __ldg(&T[i].ref);")
+            ov = self.side_value(bk, ir.basic, ir.instance_column, "other")
+            g(f"if (!{ov.n} && {ov.c} == {idv.c}) {{ br = other; hit = true; break; }}")
+            g("}")
+            g("i = (i + 1) & MASK;")
+            g("}")
+            g("if (!hit) alive = false;")
+            g("}")
+            for c in ir.basic.cleaned_kinds():
+                if c != ir.instance_column and c not in env:
+                    env[c] = ("side", bk, c)
+            side_rows.append("br")
+        # ---- emit ------------------------------------------------------------------
+        g(f"CUR_STAGE = {STAGE['merge']}u;")
+        g("// ---- emit_minibatch: sorted, de-duplicated (slot, sign) ----")
+        g(f"if (alive && {lab.n}) {{")
+        self.row_error("merge", "null_label")
+        g("}")
+        g(f"if (alive && ({lab.c} > 1ull)) {{")
+        self.row_error("merge", "label_range", detail=lab.c)
+        g("}")
+        feats = sorted(ir.features.items(), key=lambda kv: (kv[1], kv[0]))
+        fv = []
+        for col, slot in feats:
+            v = self.col(col, node_out)
+            if v.t not in ("i64", "u64"):
+                raise UnsupportedOnDevice(f"feature column {col!r} is not integer-valued")
+            fv.append((slot, v))
+        K = len(fv)
+        g(f"u64 fsg[{max(K, 1)}]; u32 fpres = 0u;")
+        # group equal slots: sort + dedup inside a group
+        i = 0
+        while i < K:
+            j = i
+            while j < K and fv[j][0] == fv[i][0]:
+                j += 1
+            for q in range(i, j):
+                v = fv[q][1]
+                g(f"fsg[{q}] = {v.c}; if (!{v.n}) fpres |= {1 << q}u;")
+            if j - i > 1:
+                # small sorting network over the group (absent = +inf), then dedup
+                for a in range(i, j):
+                    for b in range(i, j - 1 - (a - i)):
+                        g(f"{{ bool pa = (fpres >> {b}) & 1u, pb = (fpres >> {b + 1}) & 1u;"
+                          f" bool sw = (!pa && pb) || (pa && pb && fsg[{b}] > fsg[{b + 1}]);"
+                          f" if (sw) {{ u64 t = fsg[{b}]; fsg[{b}] = fsg[{b + 1}]; fsg[{b + 1}] = t;"
+                          f" fpres = (fpres & ~{(1 << b) | (1 << (b + 1))}u) | ((u32)pb << {b}) |"
+                          f" ((u32)pa << {b + 1}); }} }}")
+                for b in range(i + 1, j):
+                    g(f"if (((fpres >> {b}) & 1u) && ((fpres >> {b - 1}) & 1u) && "
+                      f"fsg[{b}] == fsg[{b - 1}]) fpres &= ~{1 << b}u;")
+            i = j
+        g("if (!alive) fpres = 0u;")
+        g("const u32 m = alive ? __popc(fpres) : 0u;")
+        g("u64 digest = 0ull;")
+        g("if (alive) {")
+        g("fbx::Fnv h;")
+        g(f"h.u64_le({idv.c}); h.byte((u32)({lab.c} & 1ull));")
+        for q, (slot, _) in enumerate(fv):
+            g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
+        g("digest = h.value();")
+        g("}")
+        # ---- tile: sort by instance id, offsets, look-back, write -------------------
+        g("// ---- chunk emission order: ascending u64 instance id (viewpipe.py:521) ----")
+        g(f"const u64 myid = alive ? {idv.c} : ~0ull;")
+        g("for (u32 q = threadIdx.x; q < NSORT; q += NT) {")
+        g("sm.keys[q] = ~0ull; sm.vals[q] = 0x80000000u | q; }")
+        g("__syncthreads();")
+        g("sm.keys[threadIdx.x] = myid; sm.vals[threadIdx.x] = (alive ? 0u : 0x40000000u) | threadIdx.x;")
+        g("sm.m[threadIdx.x] = m;")
+        g("__syncthreads();")
+        g("fbx::smem_bitonic_sort2<NSORT, NT>(sm.keys, sm.vals);")
+        g("// rank + exclusive sign offsets in sorted order")
+        g("const u32 sv = sm.vals[threadIdx.x];")
+        g("const bool s_alive = (sv & 0xC0000000u) == 0u;")
+        g("const u32 s_tid = sv & 0x3FFu;")
+        g("const u32 s_m = s_alive ? sm.m[s_tid] : 0u;")
+        g("const u32 s_off = sm.scan.exclusive(s_m);")
+        g("const u32 tile_signs = sm.scan.total;")
+        g("if (s_alive) { sm.rank[s_tid] = threadIdx.x; sm.soff[s_tid] = s_off; }")
+        g("const u32 n_inst = __syncthreads_count(alive);")
+        g("// counters + digest: one atomic per CTA")
+        g("{")
+        g("u64 r0 = digest, r1 = malformed, r2 = filtered, r3 = joined;")
+        g("#pragma unroll")
+        g("for (int d = 16; d > 0; d >>= 1) {")
+        g("r0 ^= __shfl_xor_sync(0xFFFFFFFFu, r0, d); r1 += __shfl_xor_sync(0xFFFFFFFFu, r1, d);")
+        g("r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, d); r3 += __shfl_xor_sync(0xFFFFFFFFu, r3, d); }")
+        g("if ((threadIdx.x & 31u) == 0) { sm.red[threadIdx.x >> 5][0] = r0; sm.red[threadIdx.x >> 5][1] = r1;"
+          " sm.red[threadIdx.x >> 5][2] = r2; sm.red[threadIdx.x >> 5][3] = r3; }")
+        g("}")
+        g("__syncthreads();")
+        g("if (threadIdx.x < 32u) {")
+        g("u64 ei = 0, es = 0;")
+        g("fbx::lookback(STATUS, tile, n_inst, tile_signs, &ei, &es);")
+        g("if (threadIdx.x == 0) {")
+        g("sm.ex_inst = ei; sm.ex_signs = es;")
+        g("u64 r0 = 0, r1 = 0, r2 = 0, r3 = 0;")
+        g("for (int w = 0; w < NT / 32; ++w) { r0 ^= sm.red[w][0]; r1 += sm.red[w][1]; r2 += sm.red[w][2]; r3 += sm.red[w][3]; }")
+        g("if (r0) atomicXor((unsigned long long*)&ST->digest, (unsigned long long)r0);")
+        g("atomicAdd((unsigned long long*)&ST->instances, (unsigned long long)n_inst);")
+        g("atomicAdd((unsigned long long*)&ST->signs, (unsigned long long)tile_signs);")
+        g("if (r1) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)r1);")
+        g("if (r2) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)r2);")
+        g("if (r3) atomicAdd((unsigned long long*)&ST->joined, (unsigned long long)r3);")
+        g("}")
+        g("}")
+        g("__syncthreads();")
+        g(f"u64* O_IDS = {g.p('out.ids', 'u64*')}; u8* O_LAB = {g.p('out.labels', 'u8*')};")
+        g(f"u64* O_OFF = {g.p('out.offsets', 'u64*')}; u16* O_SLOT = {g.p('out.slots', 'u16*')};")
+        g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
+        g("if (alive) {")
+        g("const u64 pos = sm.ex_inst + sm.rank[threadIdx.x];")
+        g("u64 so = sm.ex_signs + sm.soff[threadIdx.x];")
+        g(f"O_IDS[pos] = {idv.c}; O_LAB[pos] = (u8)({lab.c});")
+        g("O_OFF[pos] = so;")
+        for q, (slot, _) in enumerate(fv):
+            g(f"if ((fpres >> {q}) & 1u) {{ O_SLOT[so] = (u16){slot}u; O_SIGN[so] = fsg[{q}]; ++so; }}")
+        g("}")
+        g("if (threadIdx.x == 0) O_OFF[sm.ex_inst + n_inst] = sm.ex_signs + tile_signs;")
+        g("}")
+        return "fbx_pipeline"
+
+    def driver_needed(self) -> set[str]:
+        """Driver (cleaned) columns the kernel must read."""
+        ir = self.ir
+        need = set(ir.join_keys) | {ir.instance_column, ir.label_column} | set(ir.features)
+        for nd in ir.nodes:
+            need |= set(nd.inputs)
+        need |= {e.source for e in ir.driver.extractions}
+        if ir.driver.filter is not None:
+            need |= _filter_columns(ir.driver.filter)
+        return need
+
+    def col(self, name: str, node_out: Mapping[str, V]) -> V:
+        ir = self.ir
+        if name in ir.producer:
+            return node_out[ir.producer[name]]
+        v = self.env[name]
+        if isinstance(v, tuple):  # lazily gathered side / basic column
+            _, k, c = v
+            view = ir.sides[k] if k < len(ir.sides) else ir.basic
+            g = self.g
+            row = self.side_rows[k] if k < len(self.side_rows) else f"sr{k}"
+            g("// gather " + f"{view.name}.{c}")
+            out = self.side_value(k, view, c, row)
+            # side rows are only valid for joined rows
+            if out.nullable:
+                g(f"if (!alive) {out.c}_n = true;")
+            self.env[name] = out
+            return out
+        return v
+
+    # ------------------------------------------------------------------------------------
+    def generate(self) -> Program:
+        ir = self.ir
+        self.globals: list[str] = []
+        self.span_cap = 0
+        needed = self.driver_needed()
+        nstaged = sum(1 for c, k in ir.driver.kinds.items() if k.var_length and c in needed) \
+            if ir.stage_strings else 0
+        # shared-memory span budget per staged column (bytes, multiple of 16)
+        self.span_cap = SPAN_BUDGET if nstaged else 0
+        self.g.slot("state")  # slot 0
+        side_names = []
+        for k, sv in enumerate(ir.sides):
+            side_names.append(self.side_prep_kernel(k, sv, False))
+            self.g("")
+        if ir.basic is not None:
+            side_names.append(self.side_prep_kernel(len(ir.sides), ir.basic, True))
+            self.g("")
+        body_start = len(self.g.lines)
+        kname = self.pipeline_kernel()
+        consts = b"".join(self.g.consts)
+        head = [library_source(), "",
+                "// ===== generated plan =====",
+                f"__device__ const __align__(16) u8 K_STR[] = {_c_bytes(consts + bytes(16))};",
+                *self.globals, ""]
+        src = "\n".join(head + self.g.lines)
+        smem = self.span_cap
+        del body_start
+        return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes)
+
+
+def _filter_columns(expr) -> set[str]:
+    if isinstance(expr, BoolExpr):
+        out = set()
+        for p in expr.parts:
+            out |= _filter_columns(p)
+        return out
+    return {expr.column}
+
+
+def generate(ir: PlanIR) -> Program:
+    return PlanCodegen(ir).generate()

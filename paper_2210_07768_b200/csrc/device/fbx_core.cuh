@@ -1,0 +1,913 @@
+// fbx_core.cuh -- device library for the fused FeatureBox extraction kernels.
+//
+// This header is prepended to every plan-specialised kernel the host planner
+// generates (paper_2210_07768_b200/codegen.py) and compiled at prepare time
+// by NVRTC for sm_100a (the paper's "runtime-compiled meta-kernel",
+// reference PAPER.md:207).  It must stay NVRTC-clean: no host headers.
+//
+// Contents: integer types, FNV-1a-64 in 32-bit halves, FBXC column access,
+// the string functions of the operator library (reference featureops.py:
+// 298-367), a validating JSON scanner with dot-path extraction (viewpipe.py:
+// 254-280 over CPython json.loads), HBM hash-table probes (dictionary lookups
+// featureops.py:414-426, side-view join viewpipe.py:498-547), the block-level
+// bump allocator (mempool.py:114-134 / PAPER.md Alg. 1) and the tile
+// primitives for emission (scan, sort by instance id, decoupled look-back).
+#pragma once
+
+typedef unsigned char u8;
+typedef unsigned short u16;
+typedef unsigned int u32;
+typedef unsigned long long u64;
+typedef int i32;
+typedef long long i64;
+
+#define FBX_DI __device__ __forceinline__
+#define FBX_NI __device__ __noinline__
+
+#include "fbx_abi.h"
+
+namespace fbx {
+
+// ---------------------------------------------------------------------------
+// FNV-1a 64 (featureops.py:37-42).  State kept as two 32-bit halves:
+//   h*P = h*0x1B3 + (h << 40)  =>  lo' = lo*0x1B3, hi' = hi*0x1B3 + mulhi + (lo<<8)
+// which ptxas lowers to IMAD.WIDE.U32 + IMAD + LEA (+ the LOP3 xor).
+// ---------------------------------------------------------------------------
+struct Fnv {
+  u32 lo, hi;
+  FBX_DI Fnv() : lo(0x84222325u), hi(0xCBF29CE4u) {}
+  FBX_DI Fnv(u64 h) : lo((u32)h), hi((u32)(h >> 32)) {}
+  FBX_DI u64 value() const { return ((u64)hi << 32) | lo; }
+  FBX_DI void mul(u32 x) {
+    u64 w = (u64)x * 0x1B3u;
+    hi = hi * 0x1B3u + (u32)(w >> 32) + (x << 8);
+    lo = (u32)w;
+  }
+  FBX_DI void byte(u32 b) { mul(lo ^ b); }
+  // four bytes of a little-endian word, low byte first
+  FBX_DI void word_le(u32 w) {
+    mul(lo ^ (w & 0xFFu));
+    mul(lo ^ ((w >> 8) & 0xFFu));
+    mul(lo ^ ((w >> 16) & 0xFFu));
+    mul(lo ^ (w >> 24));
+  }
+  FBX_DI void word_be(u32 w) {  // big-endian image of w
+    mul(lo ^ (w >> 24));
+    mul(lo ^ ((w >> 16) & 0xFFu));
+    mul(lo ^ ((w >> 8) & 0xFFu));
+    mul(lo ^ (w & 0xFFu));
+  }
+  FBX_DI void u64_be(u64 v) { word_be((u32)(v >> 32)); word_be((u32)v); }
+  FBX_DI void u64_le(u64 v) { word_le((u32)v); word_le((u32)(v >> 32)); }
+  FBX_DI void u16_le(u32 v) { mul(lo ^ (v & 0xFFu)); mul(lo ^ ((v >> 8) & 0xFFu)); }
+  // arbitrary byte span; reads whole aligned 32-bit words (buffers are padded
+  // to 16 bytes by the engine, so the over-read stays inside the allocation)
+  FBX_DI void bytes(const u8* p, u32 n) {
+    if (n == 0) return;
+    u64 a = (u64)p;
+    u32 mis = (u32)(a & 3u);
+    const u32* wp = (const u32*)(a - mis);
+    u32 w0 = wp[0];
+    if (mis) {
+      u32 take = 4u - mis;
+      u32 w = w0 >> (mis * 8u);
+      if (take > n) take = n;
+      for (u32 i = 0; i < take; ++i) { mul(lo ^ (w & 0xFFu)); w >>= 8; }
+      n -= take;
+      ++wp;
+      if (n == 0) return;
+      w0 = wp[0];
+    }
+    while (n >= 8u) {
+      u32 w1 = wp[1];
+      word_le(w0);
+      word_le(w1);
+      wp += 2;
+      n -= 8u;
+      if (n) w0 = wp[0];
+    }
+    if (n >= 4u) {
+      word_le(w0);
+      ++wp;
+      n -= 4u;
+      if (n) w0 = wp[0];
+    }
+    for (u32 i = 0; i < n; ++i) { mul(lo ^ (w0 & 0xFFu)); w0 >>= 8; }
+  }
+};
+
+FBX_DI u64 fnv_mix(u64 v) {  // featureops.py:306-307, mix(v) = FNV(8 BE bytes)
+  Fnv h;
+  h.u64_be(v);
+  return h.value();
+}
+
+// ---------------------------------------------------------------------------
+// Loads
+// ---------------------------------------------------------------------------
+FBX_DI u64 ldg_u64(const void* p) { return __ldg((const u64*)p); }
+FBX_DI u32 ldg_u32(const void* p) { return __ldg((const u32*)p); }
+FBX_DI u32 ldg_u8(const void* p) { return __ldg((const u8*)p); }
+
+// FBXC null bitmap, LSB-first, bit set = null (columnstore.py:117-130)
+FBX_DI bool null_bit(const u8* nulls, u64 row) {
+  return (__ldg(nulls + (row >> 3)) >> (row & 7u)) & 1u;
+}
+
+// A string value: generic pointer (global, pool or shared) + byte length.
+struct Str {
+  const u8* p;
+  u32 n;
+};
+
+FBX_DI u32 str_byte(const u8* p, u32 i) { return p[i]; }
+
+FBX_DI bool str_eq(Str a, Str b) {
+  if (a.n != b.n) return false;
+  for (u32 i = 0; i < a.n; ++i)
+    if (a.p[i] != b.p[i]) return false;
+  return true;
+}
+
+FBX_DI bool str_eq_const(Str a, const u8* c, u32 cn) {
+  if (a.n != cn) return false;
+  for (u32 i = 0; i < cn; ++i)
+    if (a.p[i] != c[i]) return false;
+  return true;
+}
+
+// Python str ordering == UTF-8 byte order (code points are order-preserving)
+FBX_DI int str_cmp(Str a, const u8* c, u32 cn) {
+  u32 m = a.n < cn ? a.n : cn;
+  for (u32 i = 0; i < m; ++i) {
+    u32 x = a.p[i], y = c[i];
+    if (x != y) return x < y ? -1 : 1;
+  }
+  return a.n == cn ? 0 : (a.n < cn ? -1 : 1);
+}
+
+// ---------------------------------------------------------------------------
+// token:<delim>:<index> (featureops.py:318-349, 392-412): field `index` of a
+// single-byte split, "" past the end.  Returned as a view into the input.
+// ---------------------------------------------------------------------------
+FBX_DI Str str_token(Str s, u32 delim, u32 index) {
+  u32 field = 0, start = 0;
+  for (u32 i = 0; i < s.n; ++i) {
+    if (s.p[i] == delim) {
+      if (field == index) return Str{s.p + start, i - start};
+      ++field;
+      start = i + 1;
+    }
+  }
+  if (field == index) return Str{s.p + start, s.n - start};
+  return Str{s.p, 0u};
+}
+
+// Up to 4 fields of one split in one pass (codegen groups token calls that
+// share an input and a delimiter).  fields[k] = field number wanted at k.
+template <int K>
+FBX_DI void str_tokens(Str s, u32 delim, const u32 (&want)[K], Str (&out)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = Str{s.p, 0u};
+  u32 field = 0, start = 0;
+  for (u32 i = 0; i <= s.n; ++i) {
+    bool end = (i == s.n);
+    if (end || s.p[i] == delim) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (want[k] == field) out[k] = Str{s.p + start, i - start};
+      ++field;
+      start = i + 1;
+    }
+  }
+}
+
+// str.isspace() for a decoded code point (CPython 3.12 / Unicode 15)
+FBX_DI bool py_isspace(u32 cp) {
+  if (cp <= 0x7F) return (cp >= 0x09 && cp <= 0x0D) || (cp >= 0x1C && cp <= 0x20);
+  return cp == 0x85 || cp == 0xA0 || cp == 0x1680 || (cp >= 0x2000 && cp <= 0x200A) ||
+         cp == 0x2028 || cp == 0x2029 || cp == 0x202F || cp == 0x205F || cp == 0x3000;
+}
+
+// decode the code point starting at p[i] (valid UTF-8 assumed); returns length
+FBX_DI u32 utf8_at(const u8* p, u32 i, u32 n, u32* cp) {
+  u32 c = p[i];
+  if (c < 0x80u) { *cp = c; return 1; }
+  if (c < 0xE0u && i + 1 < n) { *cp = ((c & 0x1Fu) << 6) | (p[i + 1] & 0x3Fu); return 2; }
+  if (c < 0xF0u && i + 2 < n) {
+    *cp = ((c & 0x0Fu) << 12) | ((p[i + 1] & 0x3Fu) << 6) | (p[i + 2] & 0x3Fu);
+    return 3;
+  }
+  if (i + 3 < n) {
+    *cp = ((c & 0x07u) << 18) | ((p[i + 1] & 0x3Fu) << 12) | ((p[i + 2] & 0x3Fu) << 6) |
+          (p[i + 3] & 0x3Fu);
+    return 4;
+  }
+  *cp = c;
+  return 1;
+}
+
+// trim = str.strip() (featureops.py:302-303): a view narrowing
+FBX_DI Str str_trim(Str s) {
+  u32 b = 0, e = s.n;
+  while (b < e) {
+    u32 c = s.p[b];
+    if (c < 0x80u) {
+      if (!py_isspace(c)) break;
+      ++b;
+    } else {
+      u32 cp, l = utf8_at(s.p, b, e, &cp);
+      if (!py_isspace(cp)) break;
+      b += l;
+    }
+  }
+  while (e > b) {
+    u32 c = s.p[e - 1];
+    if (c < 0x80u) {
+      if (!py_isspace(c)) break;
+      --e;
+    } else {
+      u32 k = e - 1;  // walk back to the lead byte
+      while (k > b && (s.p[k] & 0xC0u) == 0x80u) --k;
+      u32 cp;
+      utf8_at(s.p, k, e, &cp);
+      if (!py_isspace(cp)) break;
+      e = k;
+    }
+  }
+  return Str{s.p + b, e - b};
+}
+
+// lower (featureops.py:298-299): 0 = unchanged (view ok), 1 = ASCII changes,
+// 2 = non-ASCII present (needs the Unicode tables: not supported on device)
+FBX_DI u32 str_lower_class(Str s) {
+  u32 cls = 0;
+  for (u32 i = 0; i < s.n; ++i) {
+    u32 c = s.p[i];
+    if (c >= 0x80u) return 2;
+    if (c >= 'A' && c <= 'Z') cls = 1;
+  }
+  return cls;
+}
+
+FBX_DI void str_lower_copy(u8* dst, Str s) {
+  for (u32 i = 0; i < s.n; ++i) {
+    u32 c = s.p[i];
+    dst[i] = (u8)((c >= 'A' && c <= 'Z') ? c + 32u : c);
+  }
+}
+
+FBX_DI void str_copy(u8* dst, Str s) {
+  for (u32 i = 0; i < s.n; ++i) dst[i] = s.p[i];
+}
+
+// decimal text of a Python int (str(v)); buf >= 20 bytes (+1 for '-')
+FBX_DI u32 u64_dec_len(u64 v) {
+  u32 n = 1;
+  while (v >= 10u) { v /= 10u; ++n; }
+  return n;
+}
+FBX_DI u32 int_dec_len(u64 bits, bool is_signed) {
+  if (is_signed && (i64)bits < 0) return 1 + u64_dec_len(0ull - bits);
+  return u64_dec_len(bits);
+}
+FBX_DI void u64_dec(u8* dst, u64 v, u32 len) {
+  for (u32 i = len; i > 0; --i) { dst[i - 1] = (u8)('0' + v % 10u); v /= 10u; }
+}
+FBX_DI void int_dec(u8* dst, u64 bits, bool is_signed, u32 len) {
+  if (is_signed && (i64)bits < 0) {
+    dst[0] = '-';
+    u64_dec(dst + 1, 0ull - bits, len - 1);
+  } else {
+    u64_dec(dst, bits, len);
+  }
+}
+
+// Float32 value canonicalisation: Python floats re-packed with struct '>f'
+// quiet a signalling NaN (columnstore.py:97, featureops.py:86).
+FBX_DI u32 f32_canon_bits(u32 b) {
+  return ((b & 0x7F800000u) == 0x7F800000u && (b & 0x007FFFFFu)) ? (b | 0x00400000u) : b;
+}
+
+// ---------------------------------------------------------------------------
+// Error word: the first failure in pipeline order wins (atomicMin on a key).
+//   key = chunk(32) | stage(4) | layer(8) | node rank(12) | code(8)
+// ---------------------------------------------------------------------------
+FBX_DI u64 err_key(u64 chunk, u32 stage, u32 layer, u32 node, u32 code) {
+  return (chunk << 32) | ((u64)(stage & 0xFu) << 28) | ((u64)(layer & 0xFFu) << 20) |
+         ((u64)(node & 0xFFFu) << 8) | (code & 0xFFu);
+}
+FBX_DI void raise_err(fbx_state* st, u64 key, u64 detail) {
+  u64 old = atomicMin((unsigned long long*)&st->error_key, (unsigned long long)key);
+  if (key < old) atomicExch((unsigned long long*)&st->error_detail, (unsigned long long)detail);
+}
+
+// ---------------------------------------------------------------------------
+// Block-level primitives (blockDim.x == NT, a multiple of 32, <= 1024)
+// ---------------------------------------------------------------------------
+template <int NT>
+struct BlockScanU32 {
+  u32 warp_tot[NT / 32];
+  u32 total;
+  // exclusive scan; returns the exclusive prefix, total in `total`
+  FBX_DI u32 exclusive(u32 v) {
+    const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    u32 x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      u32 y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+      if (lane >= (u32)d) x += y;
+    }
+    if (lane == 31u) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      u32 t = lane < (u32)(NT / 32) ? warp_tot[lane] : 0u;
+      u32 s = t;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        u32 y = __shfl_up_sync(0xFFFFFFFFu, s, d);
+        if (lane >= (u32)d) s += y;
+      }
+      if (lane < (u32)(NT / 32)) warp_tot[lane] = s - t;
+      if (lane == (u32)(NT / 32) - 1u) total = s;
+    }
+    __syncthreads();
+    u32 r = warp_tot[wid] + x - v;
+    __syncthreads();
+    return r;
+  }
+};
+
+// Block bump allocation from the HBM arena (Algorithm 1; reference
+// mempool.py:114-134): exclusive prefix of lane sizes, ONE atomicAdd per CTA,
+// 128-byte group alignment.  Returns the lane's pointer (nullptr when its size
+// is 0 or the pool is exhausted -- then *exhausted is set CTA-uniformly).
+template <int NT>
+FBX_DI u8* pool_alloc(BlockScanU32<NT>& scan, u64* base_smem, fbx_state* st, u8* pool,
+                      u64 pool_cap, u32 size, bool* exhausted) {
+  u32 pre = scan.exclusive(size);
+  u32 total = scan.total;
+  if (threadIdx.x == 0) {
+    u64 tot = ((u64)total + 127ull) & ~127ull;
+    u64 b = tot ? atomicAdd((unsigned long long*)&st->pool_head, (unsigned long long)tot) : 0ull;
+    if (tot && b + tot > pool_cap) {
+      // exhausted: report (requested, remaining) like PoolExhausted
+      u64 rem = b < pool_cap ? pool_cap - b : 0ull;
+      atomicMax((unsigned long long*)&st->pool_overflow, (unsigned long long)((tot << 32) | (rem & 0xFFFFFFFFull)));
+      b = ~0ull;
+    }
+    *base_smem = b;
+  }
+  __syncthreads();
+  u64 b = *base_smem;
+  __syncthreads();
+  *exhausted = (b == ~0ull);
+  if (b == ~0ull || size == 0) return nullptr;
+  return pool + b + pre;
+}
+
+// Bitonic sort of (key, payload) pairs held in shared memory, N = power of 2.
+template <int N, int NT>
+FBX_DI void smem_bitonic_sort(u64* keys, u32* vals) {
+  for (u32 k = 2; k <= (u32)N; k <<= 1) {
+    for (u32 j = k >> 1; j > 0; j >>= 1) {
+      for (u32 i = threadIdx.x; i < (u32)N; i += NT) {
+        u32 ixj = i ^ j;
+        if (ixj > i) {
+          u64 a = keys[i], b = keys[ixj];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            keys[i] = b;
+            keys[ixj] = a;
+            u32 t = vals[i];
+            vals[i] = vals[ixj];
+            vals[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+
+// Bitonic sort of (key, val) pairs, ascending by (key, val), in shared memory.
+template <int N, int NT>
+FBX_DI void smem_bitonic_sort2(u64* keys, u32* vals) {
+  for (u32 k = 2; k <= (u32)N; k <<= 1) {
+    for (u32 j = k >> 1; j > 0; j >>= 1) {
+      for (u32 i = threadIdx.x; i < (u32)N; i += NT) {
+        u32 ixj = i ^ j;
+        if (ixj > i) {
+          u64 a = keys[i], b = keys[ixj];
+          u32 va = vals[i], vb = vals[ixj];
+          bool gt = (a > b) || (a == b && va > vb);
+          bool up = (i & k) == 0;
+          if (gt == up) {
+            keys[i] = b;
+            keys[ixj] = a;
+            vals[i] = vb;
+            vals[ixj] = va;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back over tiles (chunks) for the global CSR offsets.
+// status word: flag(2) | instances(28) | signs(34); flag 1 = aggregate,
+// 2 = inclusive prefix.
+// ---------------------------------------------------------------------------
+FBX_DI u64 ld_acquire(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+FBX_DI void st_release(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+FBX_DI u64 pack_status(u64 flag, u64 inst, u64 signs) {
+  return (flag << 62) | ((inst & 0xFFFFFFFull) << 34) | (signs & 0x3FFFFFFFFull);
+}
+
+// Called by warp 0 only.  Returns (exclusive instances, exclusive signs).
+FBX_DI void lookback(u64* status, u32 tile, u64 inst, u64 signs, u64* ex_inst, u64* ex_signs) {
+  const u32 lane = threadIdx.x & 31u;
+  if (tile == 0) {
+    if (lane == 0) st_release(status, pack_status(2, inst, signs));
+    *ex_inst = 0;
+    *ex_signs = 0;
+    return;
+  }
+  if (lane == 0) st_release(status + tile, pack_status(1, inst, signs));
+  u64 acc_i = 0, acc_s = 0;
+  i64 base = (i64)tile - 1;
+  while (true) {
+    i64 idx = base - (i64)lane;
+    u64 w = 0;
+    if (idx >= 0) {
+      do { w = ld_acquire(status + idx); } while ((w >> 62) == 0);
+    } else {
+      w = pack_status(2, 0, 0);
+    }
+    u32 incl = __ballot_sync(0xFFFFFFFFu, (w >> 62) == 2);
+    // lanes up to and including the first inclusive one contribute
+    u32 stop = incl ? (__ffs(incl) - 1) : 31u;
+    u64 vi = (lane <= stop) ? ((w >> 34) & 0xFFFFFFFull) : 0;
+    u64 vs = (lane <= stop) ? (w & 0x3FFFFFFFFull) : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      vi += __shfl_xor_sync(0xFFFFFFFFu, vi, d);
+      vs += __shfl_xor_sync(0xFFFFFFFFu, vs, d);
+    }
+    acc_i += vi;
+    acc_s += vs;
+    if (incl) break;
+    base -= 32;
+  }
+  if (lane == 0) st_release(status + tile, pack_status(2, acc_i + inst, acc_s + signs));
+  *ex_inst = acc_i;
+  *ex_signs = acc_s;
+}
+
+// ---------------------------------------------------------------------------
+// HBM hash tables.  Slot layout (32 B, one sector per probe):
+//   u64 tag (0 = empty), u32 ref (row / key offset), u32 aux (count / key len),
+//   u64 value, u64 pad.  Capacity is a power of two; linear probing.
+// ---------------------------------------------------------------------------
+struct Slot {
+  u64 tag;
+  u32 ref;
+  u32 aux;
+  u64 value;
+  u64 pad;
+};
+
+FBX_DI u64 table_tag(u64 h) { return h | 1ull; }  // never 0
+
+// dictionary lookup (featureops.py:104-167): key bytes -> u64, default on miss
+FBX_DI u64 dict_lookup(const Slot* slots, u64 mask, const u8* keyblob, Str key, u64 dflt) {
+  Fnv f;
+  f.bytes(key.p, key.n);
+  u64 tag = table_tag(f.value());
+  u64 i = tag & mask;
+  while (true) {
+    const Slot* s = slots + i;
+    u64 t = __ldg(&s->tag);
+    if (t == 0) return dflt;
+    if (t == tag) {
+      u32 ref = __ldg(&s->ref), len = __ldg(&s->aux);
+      if (len == key.n) {
+        bool eq = true;
+        for (u32 k = 0; k < len; ++k)
+          if (__ldg(keyblob + ref + k) != key.p[k]) { eq = false; break; }
+        if (eq) return __ldg(&s->value);
+      }
+    }
+    i = (i + 1) & mask;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// JSON (CPython json.loads, strict=True) validation + dot-path extraction.
+// Leaves are reported for up to NP paths of up to 8 segments each.
+// ---------------------------------------------------------------------------
+enum : u32 {
+  J_MISSING = 0, J_STRING = 1, J_INT = 2, J_FLOAT = 3, J_TRUE = 4, J_FALSE = 5,
+  J_NULL = 6, J_CONTAINER = 7, J_NAN = 8, J_POSINF = 9, J_NEGINF = 10
+};
+enum : u32 { JS_OK = 0, JS_MALFORMED = 1, JS_BIGINT = 2, JS_DEEP = 3 };
+
+struct JLeaf {
+  u32 beg, end;  // value text [beg, end) (strings: inside the quotes)
+  u32 type;
+  u32 esc;       // string contains a backslash escape
+};
+
+struct JPathSet {
+  const u8* seg;       // concatenated segment bytes
+  const u16* seg_off;  // [NP][8]
+  const u8* seg_len;   // [NP][8]
+  const u8* nseg;      // [NP]
+};
+
+FBX_DI bool j_ws(u32 c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r'; }
+FBX_DI bool j_digit(u32 c) { return c - '0' < 10u; }
+FBX_DI bool j_hex(u32 c) { return (c - '0' < 10u) || ((c | 0x20u) - 'a' < 6u); }
+
+// scan a string starting after the opening quote; returns index of closing quote
+// or ~0 when malformed.  *esc set when any escape is present.
+FBX_DI u32 j_string(const u8* s, u32 i, u32 n, u32* esc) {
+  while (i < n) {
+    u32 c = s[i];
+    if (c == '"') return i;
+    if (c < 0x20u) return ~0u;
+    if (c == '\\') {
+      *esc = 1;
+      if (i + 1 >= n) return ~0u;
+      u32 e = s[i + 1];
+      if (e == 'u') {
+        if (i + 5 >= n) return ~0u;
+        if (!(j_hex(s[i + 2]) && j_hex(s[i + 3]) && j_hex(s[i + 4]) && j_hex(s[i + 5]))) return ~0u;
+        i += 6;
+      } else if (e == '"' || e == '\\' || e == '/' || e == 'b' || e == 'f' || e == 'n' ||
+                 e == 'r' || e == 't') {
+        i += 2;
+      } else {
+        return ~0u;
+      }
+    } else {
+      ++i;
+    }
+  }
+  return ~0u;
+}
+
+FBX_DI u32 j_hexval(u32 c) { return c <= '9' ? c - '0' : (c | 0x20u) - 'a' + 10u; }
+
+// decode the escaped JSON string body s[b, e) into dst (UTF-8, lone surrogates
+// as WTF-8); returns the byte length, *lone set if a lone surrogate occurs.
+FBX_DI u32 j_unescape(const u8* s, u32 b, u32 e, u8* dst, u32* lone) {
+  u32 o = 0;
+  u32 i = b;
+  while (i < e) {
+    u32 c = s[i];
+    if (c != '\\') { if (dst) dst[o] = (u8)c; ++o; ++i; continue; }
+    u32 x = s[i + 1];
+    if (x != 'u') {
+      u32 v = x == 'b' ? 8u : x == 'f' ? 12u : x == 'n' ? 10u : x == 'r' ? 13u : x == 't' ? 9u : x;
+      if (dst) dst[o] = (u8)v;
+      ++o;
+      i += 2;
+      continue;
+    }
+    u32 cp = (j_hexval(s[i + 2]) << 12) | (j_hexval(s[i + 3]) << 8) | (j_hexval(s[i + 4]) << 4) |
+             j_hexval(s[i + 5]);
+    i += 6;
+    if (cp >= 0xD800u && cp <= 0xDBFFu && i + 1 < e && s[i] == '\\' && s[i + 1] == 'u') {
+      u32 lo2 = (j_hexval(s[i + 2]) << 12) | (j_hexval(s[i + 3]) << 8) |
+                (j_hexval(s[i + 4]) << 4) | j_hexval(s[i + 5]);
+      if (lo2 >= 0xDC00u && lo2 <= 0xDFFFu) {
+        cp = 0x10000u + ((cp - 0xD800u) << 10) + (lo2 - 0xDC00u);
+        i += 6;
+      }
+    }
+    if (cp >= 0xD800u && cp <= 0xDFFFu) *lone = 1;
+    if (cp < 0x80u) {
+      if (dst) dst[o] = (u8)cp;
+      o += 1;
+    } else if (cp < 0x800u) {
+      if (dst) { dst[o] = (u8)(0xC0u | (cp >> 6)); dst[o + 1] = (u8)(0x80u | (cp & 0x3Fu)); }
+      o += 2;
+    } else if (cp < 0x10000u) {
+      if (dst) {
+        dst[o] = (u8)(0xE0u | (cp >> 12));
+        dst[o + 1] = (u8)(0x80u | ((cp >> 6) & 0x3Fu));
+        dst[o + 2] = (u8)(0x80u | (cp & 0x3Fu));
+      }
+      o += 3;
+    } else {
+      if (dst) {
+        dst[o] = (u8)(0xF0u | (cp >> 18));
+        dst[o + 1] = (u8)(0x80u | ((cp >> 12) & 0x3Fu));
+        dst[o + 2] = (u8)(0x80u | ((cp >> 6) & 0x3Fu));
+        dst[o + 3] = (u8)(0x80u | (cp & 0x3Fu));
+      }
+      o += 4;
+    }
+  }
+  return o;
+}
+
+// key comparison against a path segment, decoding escapes when present
+FBX_DI bool j_key_eq(const u8* s, u32 b, u32 e, u32 esc, const u8* seg, u32 slen) {
+  if (!esc) {
+    if (e - b != slen) return false;
+    for (u32 k = 0; k < slen; ++k)
+      if (s[b + k] != seg[k]) return false;
+    return true;
+  }
+  // slow path: decode into a small local buffer (segments are short)
+  u8 tmp[64];
+  u32 lone = 0;
+  u32 dl = j_unescape(s, b, e, nullptr, &lone);
+  if (dl != slen || dl > 64u) return false;
+  j_unescape(s, b, e, tmp, &lone);
+  if (lone) return false;
+  for (u32 k = 0; k < slen; ++k)
+    if (tmp[k] != seg[k]) return false;
+  return true;
+}
+
+// number at s[i]; returns end index (or ~0 malformed); *type J_INT / J_FLOAT,
+// *digits = number of integer digits (for the 4300-digit int limit).
+FBX_DI u32 j_number(const u8* s, u32 i, u32 n, u32* type, u32* digits) {
+  u32 st = i;
+  if (i < n && s[i] == '-') ++i;
+  if (i >= n || !j_digit(s[i])) return ~0u;
+  if (s[i] == '0') {
+    ++i;
+  } else {
+    while (i < n && j_digit(s[i])) ++i;
+  }
+  *digits = i - st - (s[st] == '-' ? 1u : 0u);
+  *type = J_INT;
+  if (i + 1 < n && s[i] == '.' && j_digit(s[i + 1])) {
+    i += 2;
+    while (i < n && j_digit(s[i])) ++i;
+    *type = J_FLOAT;
+  }
+  if (i < n && (s[i] | 0x20u) == 'e') {
+    u32 k = i + 1;
+    if (k < n && (s[k] == '+' || s[k] == '-')) ++k;
+    if (k < n && j_digit(s[k])) {
+      while (k < n && j_digit(s[k])) ++k;
+      i = k;
+      *type = J_FLOAT;
+    }
+  }
+  return i;
+}
+
+FBX_DI bool j_lit(const u8* s, u32 i, u32 n, const char* w, u32 wl) {
+  if (i + wl > n) return false;
+  for (u32 k = 0; k < wl; ++k)
+    if (s[i + k] != (u8)w[k]) return false;
+  return true;
+}
+
+// Validate the whole document and extract the NP paths.  Returns JS_*.
+template <int NP>
+FBX_NI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
+#pragma unroll
+  for (int p = 0; p < NP; ++p) leaf[p] = JLeaf{0, 0, J_MISSING, 0};
+  const u8* s = doc.p;
+  const u32 n = doc.n;
+  u64 kind_stack = 0;  // bit d: container at depth d+1 is an object
+  u32 depth = 0;
+  u64 live = 0;        // byte d (d < 8): paths live for the object at depth d+1
+  u32 i = 0;
+  while (i < n && j_ws(s[i])) ++i;
+  // current value context: paths for which this value is a leaf / may descend
+  u32 leafm = 0, descm = (1u << NP) - 1u;
+  bool top = true;
+  while (true) {
+    // ---- parse one value at s[i] ----
+    if (i >= n) return JS_MALFORMED;
+    u32 c = s[i];
+    u32 vb = i, ve, vt, vesc = 0;
+    bool opened = false;
+    if (c == '{' || c == '[') {
+      if (depth >= 64u) return JS_DEEP;
+      bool obj = (c == '{');
+      if (obj) kind_stack |= (1ull << depth); else kind_stack &= ~(1ull << depth);
+      ++depth;
+      // leaf of a container type for the paths ending here
+      for (int p = 0; p < NP; ++p)
+        if (leafm & (1u << p)) leaf[p] = JLeaf{vb, vb, J_CONTAINER, 0};
+      u32 childlive = (obj && depth <= 8u) ? (top ? ((1u << NP) - 1u) : descm) : 0u;
+      if (depth <= 8u) {
+        live &= ~(0xFFull << ((depth - 1) * 8));
+        live |= (u64)(childlive & 0xFFu) << ((depth - 1) * 8);
+      }
+      ++i;
+      while (i < n && j_ws(s[i])) ++i;
+      if (i < n && s[i] == (obj ? '}' : ']')) {
+        ++i;
+        --depth;
+        opened = false;  // empty container: value complete
+      } else {
+        opened = true;
+      }
+      top = false;
+      if (opened) {
+        if (obj) goto member_key;
+        leafm = 0;
+        descm = 0;
+        continue;  // first array element
+      }
+      goto after_value;
+    }
+    top = false;
+    if (c == '"') {
+      u32 e = j_string(s, i + 1, n, &vesc);
+      if (e == ~0u) return JS_MALFORMED;
+      vb = i + 1;
+      ve = e;
+      vt = J_STRING;
+      i = e + 1;
+    } else if (c == '-' || j_digit(c)) {
+      if (c == '-' && j_lit(s, i, n, "-Infinity", 9)) {
+        vt = J_NEGINF;
+        i += 9;
+        ve = i;
+      } else {
+        u32 digits = 0;
+        u32 e = j_number(s, i, n, &vt, &digits);
+        if (e == ~0u) return JS_MALFORMED;
+        if (vt == J_INT && digits > 4300u) return JS_BIGINT;
+        ve = e;
+        i = e;
+      }
+    } else if (c == 't' && j_lit(s, i, n, "true", 4)) {
+      vt = J_TRUE; i += 4; ve = i;
+    } else if (c == 'f' && j_lit(s, i, n, "false", 5)) {
+      vt = J_FALSE; i += 5; ve = i;
+    } else if (c == 'n' && j_lit(s, i, n, "null", 4)) {
+      vt = J_NULL; i += 4; ve = i;
+    } else if (c == 'N' && j_lit(s, i, n, "NaN", 3)) {
+      vt = J_NAN; i += 3; ve = i;
+    } else if (c == 'I' && j_lit(s, i, n, "Infinity", 8)) {
+      vt = J_POSINF; i += 8; ve = i;
+    } else {
+      return JS_MALFORMED;
+    }
+    for (int p = 0; p < NP; ++p)
+      if (leafm & (1u << p)) leaf[p] = JLeaf{vb, ve, vt, vesc};
+  after_value:
+    // ---- after a complete value: separators / closers ----
+    while (true) {
+      while (i < n && j_ws(s[i])) ++i;
+      if (depth == 0) return i == n ? JS_OK : JS_MALFORMED;
+      if (i >= n) return JS_MALFORMED;
+      bool obj = (kind_stack >> (depth - 1)) & 1ull;
+      u32 ch = s[i];
+      if (ch == ',') {
+        ++i;
+        while (i < n && j_ws(s[i])) ++i;
+        if (obj) goto member_key;
+        leafm = 0;
+        descm = 0;
+        goto next_value;
+      }
+      if (ch == (obj ? '}' : ']')) {
+        ++i;
+        --depth;
+        continue;
+      }
+      return JS_MALFORMED;
+    }
+  member_key : {
+    // s[i] must be a key string
+    if (i >= n || s[i] != '"') return JS_MALFORMED;
+    u32 kesc = 0;
+    u32 ke = j_string(s, i + 1, n, &kesc);
+    if (ke == ~0u) return JS_MALFORMED;
+    u32 kb = i + 1;
+    i = ke + 1;
+    while (i < n && j_ws(s[i])) ++i;
+    if (i >= n || s[i] != ':') return JS_MALFORMED;
+    ++i;
+    while (i < n && j_ws(s[i])) ++i;
+    // which live paths does this key continue?
+    leafm = 0;
+    descm = 0;
+    if (depth <= 8u) {
+      u32 lv = (u32)((live >> ((depth - 1) * 8)) & 0xFFull);
+      u32 sidx = depth - 1;
+      for (int p = 0; p < NP; ++p) {
+        if (!(lv & (1u << p))) continue;
+        u32 ns = ps.nseg[p];
+        if (sidx >= ns) continue;
+        u32 off = ps.seg_off[p * 8 + sidx], sl = ps.seg_len[p * 8 + sidx];
+        if (!j_key_eq(s, kb, ke, kesc, ps.seg + off, sl)) continue;
+        // a later duplicate key replaces the earlier value: clear the result
+        leaf[p] = JLeaf{0, 0, J_MISSING, 0};
+        if (sidx + 1 == ns) leafm |= (1u << p); else descm |= (1u << p);
+      }
+    }
+    continue;
+  }
+  next_value:
+    continue;
+  }
+}
+
+
+// JSON leaf -> Float32 bits (viewpipe.py:278-279: canon_f32(float(value))).
+// 0 = ok, 1 = not a number (-> null), 2 = OverflowError (struct.pack 'f'),
+// 3 = needs a bignum decimal conversion (not implemented on device).
+FBX_DI u32 j_to_f32(const u8* s, JLeaf lf, u32* bits) {
+  const double p10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
+                          1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+  if (lf.type == J_NAN) { *bits = 0x7FC00000u; return 0; }
+  if (lf.type == J_POSINF) { *bits = 0x7F800000u; return 0; }
+  if (lf.type == J_NEGINF) { *bits = 0xFF800000u; return 0; }
+  if (lf.type != J_INT && lf.type != J_FLOAT) return 1;
+  u32 i = lf.beg;
+  bool neg = s[i] == '-';
+  if (neg) ++i;
+  u64 m = 0;
+  u32 sig = 0;   // significant digits consumed into m
+  i32 e10 = 0;
+  bool nz = false;
+  for (; i < lf.end && j_digit(s[i]); ++i) {
+    u32 d = s[i] - '0';
+    if (!nz && d == 0) continue;
+    nz = true;
+    if (sig < 19) { m = m * 10u + d; ++sig; } else { ++e10; if (sig < 40) return 3; }
+  }
+  if (lf.type == J_INT) {
+    if (e10 > 0) return 3;  // > 19 digits: float(int) needs exact big-int rounding
+    double d = (double)m;   // u64 -> double, round-to-nearest-even (exact for int())
+    d = __ull2double_rn(m);
+    if (neg && m != 0) d = -d;
+    float f = __double2float_rn(d);
+    *bits = __float_as_uint(f);
+    if (isinf(f) && !isinf(d)) return 2;
+    return 0;
+  }
+  if (i < lf.end && s[i] == '.') {
+    ++i;
+    for (; i < lf.end && j_digit(s[i]); ++i) {
+      u32 d = s[i] - '0';
+      if (!nz && d == 0) { --e10; continue; }
+      nz = true;
+      if (sig < 19) { m = m * 10u + d; ++sig; --e10; } else if (d) { return 3; }
+    }
+  }
+  if (i < lf.end && (s[i] | 0x20u) == 'e') {
+    ++i;
+    bool eneg = false;
+    if (s[i] == '+' || s[i] == '-') { eneg = s[i] == '-'; ++i; }
+    i32 ev = 0;
+    for (; i < lf.end; ++i) {
+      if (ev < 100000) ev = ev * 10 + (i32)(s[i] - '0');
+    }
+    e10 += eneg ? -ev : ev;
+  }
+  double d;
+  if (m == 0) {
+    d = 0.0;
+  } else if (m <= (1ull << 53) && e10 >= -22 && e10 <= 22) {
+    d = (double)m;  // exact
+    d = e10 >= 0 ? d * p10[e10] : d / p10[-e10];  // one correctly-rounded op (Clinger)
+  } else {
+    return 3;
+  }
+  if (neg) d = -d;
+  float f = __double2float_rn(d);
+  *bits = __float_as_uint(f);
+  if (isinf(f) && !isinf(d)) return 2;
+  return 0;
+}
+
+// JSON int literal -> int64 with range check (viewpipe.py:271-274)
+FBX_DI bool j_to_i64(const u8* s, u32 b, u32 e, i64* out) {
+  bool neg = s[b] == '-';
+  u32 i = b + (neg ? 1u : 0u);
+  u64 v = 0;
+  const u64 lim = neg ? (1ull << 63) : ((1ull << 63) - 1ull);
+  for (; i < e; ++i) {
+    u32 d = s[i] - '0';
+    if (v > (lim - d) / 10ull) return false;
+    v = v * 10ull + d;
+  }
+  *out = neg ? (i64)(0ull - v) : (i64)v;
+  return true;
+}
+
+}  // namespace fbx

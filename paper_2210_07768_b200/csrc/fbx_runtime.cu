@@ -1,0 +1,324 @@
+// fbx_runtime.cu -- libfbx.so: the C-ABI runtime of the B200 extraction engine.
+//
+// * fbx_compile: NVRTC compile of a generated plan for sm_100a (host-only).
+// * fbx_program_*: load the cubin through the CUDA driver API.  libcuda is
+//   dlopen'ed on first use so the library also loads on GPU-less hosts (the
+//   build/CPU test box), where only compilation is exercised.
+// * fbx_launch: one launch of a plan kernel with its u64 parameter block,
+//   on the caller's stream (torch's current stream in the Python host).
+// * precompiled kernels: run-state reset, HBM dictionary build, L2 flush.
+//
+// Declarations and the reference interfaces they replace: include/fbx.h.
+
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <cuda_runtime.h>
+#include <string>
+#include <vector>
+
+#include "fbx.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+// ---- minimal driver API surface, resolved at runtime ----------------------
+typedef int CUresult_t;
+typedef void* CUmodule_t;
+typedef void* CUfunction_t;
+struct Driver {
+  bool loaded = false;
+  void* lib = nullptr;
+  CUresult_t (*cuInit)(unsigned) = nullptr;
+  CUresult_t (*cuModuleLoadData)(CUmodule_t*, const void*) = nullptr;
+  CUresult_t (*cuModuleUnload)(CUmodule_t) = nullptr;
+  CUresult_t (*cuModuleGetFunction)(CUfunction_t*, CUmodule_t, const char*) = nullptr;
+  CUresult_t (*cuLaunchKernel)(CUfunction_t, unsigned, unsigned, unsigned, unsigned, unsigned,
+                               unsigned, unsigned, void*, void**, void**) = nullptr;
+  CUresult_t (*cuFuncGetAttribute)(int*, int, CUfunction_t) = nullptr;
+  CUresult_t (*cuFuncSetAttribute)(CUfunction_t, int, int) = nullptr;
+  CUresult_t (*cuGetErrorString)(CUresult_t, const char**) = nullptr;
+};
+Driver g_drv;
+
+const char* drv_str(CUresult_t r) {
+  const char* s = nullptr;
+  if (g_drv.cuGetErrorString) g_drv.cuGetErrorString(r, &s);
+  return s ? s : "unknown CUDA driver error";
+}
+
+int load_driver() {
+  if (g_drv.loaded) return FBX_OK;
+  // make sure the runtime has created/bound the primary context first
+  cudaError_t ce = cudaFree(0);
+  if (ce != cudaSuccess) return fail(FBX_E_CUDA, std::string("cuda init: ") + cudaGetErrorString(ce));
+  void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(FBX_E_CUDA, std::string("dlopen libcuda.so.1: ") + dlerror());
+  g_drv.lib = h;
+#define FBX_SYM(name, sym)                                                 \
+  *(void**)(&g_drv.name) = dlsym(h, sym);                                  \
+  if (!g_drv.name) return fail(FBX_E_CUDA, std::string("missing ") + sym);
+  FBX_SYM(cuInit, "cuInit");
+  FBX_SYM(cuModuleLoadData, "cuModuleLoadData");
+  FBX_SYM(cuModuleUnload, "cuModuleUnload");
+  FBX_SYM(cuModuleGetFunction, "cuModuleGetFunction");
+  FBX_SYM(cuLaunchKernel, "cuLaunchKernel");
+  FBX_SYM(cuFuncGetAttribute, "cuFuncGetAttribute");
+  FBX_SYM(cuFuncSetAttribute, "cuFuncSetAttribute");
+  FBX_SYM(cuGetErrorString, "cuGetErrorString");
+#undef FBX_SYM
+  g_drv.cuInit(0);
+  g_drv.loaded = true;
+  return FBX_OK;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return FBX_OK;
+  return fail(FBX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- precompiled kernels ----------------------------------------------------
+__global__ void k_state_reset(fbx_state* st, unsigned long long* status, size_t n) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    memset(st, 0, sizeof(fbx_state));
+    st->error_key = ~0ull;
+  }
+  for (; i < n; i += (size_t)gridDim.x * blockDim.x) status[i] = 0ull;
+}
+
+struct Slot {
+  unsigned long long tag;
+  unsigned int ref;
+  unsigned int aux;
+  unsigned long long value;
+  unsigned long long pad;
+};
+
+__device__ __forceinline__ unsigned long long fnv_bytes(const unsigned char* p, unsigned int n) {
+  unsigned long long h = 0xCBF29CE484222325ull;
+  for (unsigned int i = 0; i < n; ++i) h = (h ^ p[i]) * 0x100000001B3ull;
+  return h;
+}
+
+__global__ void k_dict_init(Slot* slots, unsigned long long cap) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < cap;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    slots[i].tag = 0ull;
+    slots[i].ref = 0u;
+    slots[i].aux = 0xFFFFFFFFu;
+    slots[i].value = 0ull;
+    slots[i].pad = 0ull;
+  }
+}
+
+// One thread per key: claim a slot with a CAS on its tag, publish ref/len,
+// detect an equal key already present (load_dict_table's duplicate error).
+__global__ void k_dict_insert(Slot* slots, unsigned long long mask, const unsigned char* blob,
+                              const unsigned int* offs, const unsigned long long* vals,
+                              unsigned long long n, unsigned long long* dup) {
+  for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    unsigned int b = offs[k], len = offs[k + 1] - b;
+    unsigned long long tag = fnv_bytes(blob + b, len) | 1ull;
+    unsigned long long i = tag & mask;
+    while (true) {
+      unsigned long long old = atomicCAS(&slots[i].tag, 0ull, tag);
+      if (old == 0ull) {
+        slots[i].ref = b;
+        slots[i].value = vals[k];
+        __threadfence();
+        atomicExch(&slots[i].aux, len);
+        break;
+      }
+      if (old == tag) {
+        unsigned int ol;
+        do { ol = *((volatile unsigned int*)&slots[i].aux); } while (ol == 0xFFFFFFFFu);
+        if (ol == len) {
+          unsigned int ob = *((volatile unsigned int*)&slots[i].ref);
+          bool eq = true;
+          for (unsigned int q = 0; q < len; ++q)
+            if (blob[ob + q] != blob[b + q]) { eq = false; break; }
+          if (eq) { atomicAdd(dup, 1ull); break; }
+        }
+      }
+      i = (i + 1) & mask;
+    }
+  }
+}
+
+__global__ void k_flush(unsigned int* buf, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    buf[i] = buf[i] + 1u;
+}
+
+}  // namespace
+
+struct fbx_program {
+  CUmodule_t mod;
+  std::vector<fbx_kernel*> kernels;
+};
+struct fbx_kernel {
+  CUfunction_t fn;
+};
+
+extern "C" {
+
+const char* fbx_version(void) { return "fbx 0.1 (sm_100a, abi " "1" ")"; }
+const char* fbx_last_error(void) { return g_err.c_str(); }
+void fbx_free(void* p) { free(p); }
+
+int fbx_compile(const char* source, const char* name, const char* const* options, int n_options,
+                void** image, size_t* image_bytes, char* log, size_t log_capacity) {
+  if (!source || !image || !image_bytes) return fail(FBX_E_ARG, "null argument");
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, source, name ? name : "plan.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail(FBX_E_COMPILE, nvrtcGetErrorString(r));
+  std::vector<const char*> opts;
+  bool has_arch = false;
+  for (int i = 0; i < n_options; ++i) {
+    opts.push_back(options[i]);
+    if (strncmp(options[i], "-arch", 5) == 0 || strncmp(options[i], "--gpu-architecture", 18) == 0)
+      has_arch = true;
+  }
+  if (!has_arch) opts.push_back("-arch=sm_100a");
+  r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+  size_t lsz = 0;
+  nvrtcGetProgramLogSize(prog, &lsz);
+  std::string lg(lsz, '\0');
+  if (lsz) nvrtcGetProgramLog(prog, &lg[0]);
+  if (log && log_capacity) {
+    size_t n = lg.size() < log_capacity - 1 ? lg.size() : log_capacity - 1;
+    memcpy(log, lg.data(), n);
+    log[n] = '\0';
+  }
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail(FBX_E_COMPILE, std::string("nvrtc: ") + nvrtcGetErrorString(r) + "\n" + lg);
+  }
+  size_t n = 0;
+  r = nvrtcGetCUBINSize(prog, &n);
+  if (r != NVRTC_SUCCESS || n == 0) {
+    nvrtcDestroyProgram(&prog);
+    return fail(FBX_E_COMPILE, "nvrtc produced no cubin (is the arch sm_100a?)");
+  }
+  void* buf = malloc(n);
+  nvrtcGetCUBIN(prog, (char*)buf);
+  nvrtcDestroyProgram(&prog);
+  *image = buf;
+  *image_bytes = n;
+  return FBX_OK;
+}
+
+int fbx_program_load(const void* image, size_t image_bytes, fbx_program** out) {
+  (void)image_bytes;
+  if (!image || !out) return fail(FBX_E_ARG, "null argument");
+  int rc = load_driver();
+  if (rc) return rc;
+  CUmodule_t mod = nullptr;
+  CUresult_t r = g_drv.cuModuleLoadData(&mod, image);
+  if (r != 0) return fail(FBX_E_CUDA, std::string("cuModuleLoadData: ") + drv_str(r));
+  fbx_program* p = new fbx_program();
+  p->mod = mod;
+  *out = p;
+  return FBX_OK;
+}
+
+int fbx_program_unload(fbx_program* prog) {
+  if (!prog) return FBX_OK;
+  for (auto* k : prog->kernels) delete k;
+  if (g_drv.loaded) g_drv.cuModuleUnload(prog->mod);
+  delete prog;
+  return FBX_OK;
+}
+
+int fbx_program_kernel(fbx_program* prog, const char* name, fbx_kernel** out) {
+  if (!prog || !name || !out) return fail(FBX_E_ARG, "null argument");
+  CUfunction_t f = nullptr;
+  CUresult_t r = g_drv.cuModuleGetFunction(&f, prog->mod, name);
+  if (r != 0) return fail(FBX_E_NOT_FOUND, std::string("kernel ") + name + ": " + drv_str(r));
+  fbx_kernel* k = new fbx_kernel{f};
+  prog->kernels.push_back(k);
+  *out = k;
+  return FBX_OK;
+}
+
+int fbx_kernel_attributes(fbx_kernel* k, int* num_regs, int* max_threads, int* static_smem) {
+  if (!k) return fail(FBX_E_ARG, "null kernel");
+  // CU_FUNC_ATTRIBUTE_NUM_REGS = 4, MAX_THREADS_PER_BLOCK = 0, SHARED_SIZE_BYTES = 1
+  if (num_regs) g_drv.cuFuncGetAttribute(num_regs, 4, k->fn);
+  if (max_threads) g_drv.cuFuncGetAttribute(max_threads, 0, k->fn);
+  if (static_smem) g_drv.cuFuncGetAttribute(static_smem, 1, k->fn);
+  return FBX_OK;
+}
+
+int fbx_kernel_set_max_dynamic_smem(fbx_kernel* k, int bytes) {
+  if (!k) return fail(FBX_E_ARG, "null kernel");
+  // CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES = 8
+  CUresult_t r = g_drv.cuFuncSetAttribute(k->fn, 8, bytes);
+  if (r != 0) return fail(FBX_E_CUDA, std::string("cuFuncSetAttribute: ") + drv_str(r));
+  return FBX_OK;
+}
+
+int fbx_launch(fbx_kernel* k, unsigned grid, unsigned block, unsigned dyn_smem, void* stream,
+               const fbx_params* params) {
+  if (!k || !params) return fail(FBX_E_ARG, "null argument");
+  if (grid == 0) return FBX_OK;
+  void* args[] = {(void*)params};
+  CUresult_t r = g_drv.cuLaunchKernel(k->fn, grid, 1, 1, block, 1, 1, dyn_smem, stream, args, nullptr);
+  if (r != 0) return fail(FBX_E_CUDA, std::string("cuLaunchKernel: ") + drv_str(r));
+  return FBX_OK;
+}
+
+int fbx_state_reset(fbx_state* d_state, unsigned long long* d_status, size_t n_tiles, void* stream) {
+  size_t blocks = (n_tiles + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 1184) blocks = 1184;
+  k_state_reset<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_state, d_status, n_tiles);
+  return cuda_check(cudaGetLastError(), "fbx_state_reset");
+}
+
+int fbx_dict_build(void* d_slots, unsigned long long capacity, const unsigned char* d_keyblob,
+                   const unsigned int* d_key_offsets, const unsigned long long* d_values,
+                   unsigned long long n, unsigned long long* d_dup_flag, void* stream) {
+  if (capacity == 0 || (capacity & (capacity - 1)) != 0)
+    return fail(FBX_E_ARG, "capacity must be a power of two");
+  if (n * 2 > capacity) return fail(FBX_E_ARG, "capacity must be >= 2n");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc0 = cuda_check(cudaMemsetAsync(d_dup_flag, 0, sizeof(unsigned long long), s), "dup reset");
+  if (rc0) return rc0;
+  k_dict_init<<<1184, 256, 0, s>>>((Slot*)d_slots, capacity);
+  if (n) {
+    unsigned blocks = (unsigned)((n + 255) / 256);
+    if (blocks > 4736) blocks = 4736;
+    k_dict_insert<<<blocks, 256, 0, s>>>((Slot*)d_slots, capacity - 1, d_keyblob, d_key_offsets,
+                                         d_values, n, d_dup_flag);
+  }
+  int rc = cuda_check(cudaGetLastError(), "fbx_dict_build");
+  if (rc) return rc;
+  unsigned long long dup = 0;
+  rc = cuda_check(cudaMemcpyAsync(&dup, d_dup_flag, sizeof(dup), cudaMemcpyDeviceToHost, s),
+                  "dup flag");
+  if (rc) return rc;
+  rc = cuda_check(cudaStreamSynchronize(s), "dict build sync");
+  if (rc) return rc;
+  if (dup) return fail(FBX_E_DUPLICATE, "duplicate dictionary key");
+  return FBX_OK;
+}
+
+int fbx_l2_flush(void* d_buf, size_t bytes, void* stream) {
+  k_flush<<<1184, 512, 0, (cudaStream_t)stream>>>((unsigned int*)d_buf, bytes / 4);
+  return cuda_check(cudaGetLastError(), "fbx_l2_flush");
+}
+
+}  // extern "C"

@@ -1,0 +1,720 @@
+"""The B200 extraction engine: prepare a plan, keep views in HBM, run chunks.
+
+Drop-in boundary (SURVEY.md §8 b): the reference's per-record path between
+``read_columns`` of a driver chunk and the training sink --
+``clean_views`` -> ``join_with_index`` -> ``_extract_batch`` ->
+``check_unique_ids`` + basic merge -> ``_Emitter`` / ``emit_minibatch`` ->
+``TrainingSink`` (pipeline.py:952-1094) -- runs as one generated CUDA kernel
+per launch (codegen.py) through the C-ABI (include/fbx.h).
+
+* ``prepare(config)`` mirrors the reference's ``prepare`` (pipeline.py:568-694):
+  the same validation and errors, then the plan IR, code generation and NVRTC
+  compilation (host only: no GPU needed).
+* ``Engine`` owns the device state: the compiled program, side-view join
+  indexes, the basic-view index, dictionary hash tables, the run-wide
+  instance-id set, the bump pool and the output CSR arena.
+* ``Engine.run(driver_rows)`` launches the fused kernel over a row range of a
+  device-resident driver view and returns a ``CsrBatch`` (device tensors) and
+  the counters; ``run_pipelined(config)`` is the whole reference run and
+  returns the reference's ``RunReport``.
+
+There is no CPU execution path: without a CUDA device ``Engine`` raises.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Mapping
+
+import numpy as np
+
+from . import codegen, runtime
+from .columns import ColumnImage, Kind, ViewImage, open_view, read_view
+from .config import (ConfigError, EmitError, BatchInvariantError, CleanConfigError,
+                     LayerExecutionError, MergeUniquenessError, PipelineConfig, PoolExhausted,
+                     StageError, UnsupportedOnDevice, bind_filter, cleaned_kinds,
+                     validate_clean_policy)
+from .featureops import FeatureConfigError, output_domains, resolve_function
+from .opgraph import (OperatorDag, LayerPlan, PlacementBudget, expand_call_graph,
+                      layer_schedule, place_operators)
+
+STAGE_NAMES = {v: k for k, v in codegen.STAGE.items()}
+ERR_NAMES = {v: k for k, v in codegen.ERR.items()}
+
+
+# ---------------------------------------------------------------------------
+# prepare (host, once per run)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Prepared:
+    config: PipelineConfig
+    dag: OperatorDag
+    plan: LayerPlan
+    ir: codegen.PlanIR
+    program: codegen.Program
+    cubin: bytes
+    extract_outputs: tuple[tuple[str, Kind, str], ...]
+    node_names: list[str]
+    schemas: dict[str, dict[str, Kind]]
+    basic_kinds: dict[str, Kind]
+
+
+def _schema(view: ViewImage | None, path: Path, wanted, where: str) -> dict[str, Kind]:
+    if view is not None:
+        kinds = {n: view.columns[n].kind for n in view.order}
+    else:
+        try:
+            kinds = dict(open_view(path).schema)
+        except OSError as exc:
+            raise ConfigError(f"{where}: cannot open: {exc}") from exc
+    if wanted is not None:
+        missing = set(wanted) - set(kinds)
+        if missing:
+            raise ConfigError(f"{where}: columns {sorted(missing)} not in file")
+        kinds = {n: k for n, k in kinds.items() if n in set(wanted)}
+    return kinds
+
+
+def prepare(config: PipelineConfig, views: Mapping[str, ViewImage] | None = None,
+            basic: ViewImage | None = None, stage_strings: bool = True,
+            compile_program: bool = True) -> Prepared:
+    """Validate the config against the schemas and build + compile the plan."""
+    views = views or {}
+    cleaned: dict[str, dict[str, Kind]] = {}
+    raw: dict[str, dict[str, Kind]] = {}
+    for v in config.views:
+        kinds = _schema(views.get(v.name), v.path, v.columns, f"view {v.name!r}")
+        try:
+            validate_clean_policy(kinds, v.policy)
+        except (CleanConfigError, KeyError) as exc:
+            raise ConfigError(f"view {v.name!r}: {exc}") from exc
+        raw[v.name] = kinds
+        cleaned[v.name] = cleaned_kinds(kinds, v.policy)
+    dk = cleaned[config.driver]
+    for col in (config.instance_column, config.label_column):
+        if col not in dk:
+            raise ConfigError(f"driver view lacks required column {col!r}")
+        if dk[col] is not Kind.INT64:
+            raise ConfigError(f"column {col!r} must be Int64")
+    joined = dict(dk)
+    for v in config.views:
+        if v.name == config.driver:
+            continue
+        side = cleaned[v.name]
+        for key in config.join_keys:
+            if key not in joined or key not in side:
+                raise ConfigError(f"join key {key!r} missing from an input view")
+            if dk[key] is not side[key]:
+                raise ConfigError(f"join key {key!r}: kind mismatch across views")
+        for name, kind in side.items():
+            if name in config.join_keys:
+                continue
+            if name in joined:
+                raise ConfigError(f"column {name!r} appears in two views; project or rename")
+            joined[name] = kind
+    try:
+        dag = expand_call_graph(config.operators)
+        plan = place_operators(layer_schedule(dag), PlacementBudget(config.device_budget_bytes),
+                               dag)
+        fns = {}
+        for name, node in dag.nodes.items():
+            fn = resolve_function(node.func.spec, config.tables)
+            want = "tuple" if node.role == "body" else "scalar"
+            if fn.arity != want:
+                raise FeatureConfigError(f"{name}: function {node.func.spec!r} has arity "
+                                         f"{fn.arity}, {node.role} node needs {want}")
+            fns[name] = fn
+    except (FeatureConfigError, ValueError) as exc:
+        if isinstance(exc, ConfigError):
+            raise
+        raise ConfigError(str(exc)) from exc
+    missing = set(dag.external_inputs()) - set(joined)
+    if missing:
+        raise ConfigError(f"operator inputs {sorted(missing)} not present after the join")
+    for node in dag.nodes:
+        if node in joined:
+            raise ConfigError(f"operator node {node!r} collides with a table column name")
+    extract_outputs, produced = [], set()
+    for spec in config.operators:
+        domains = output_domains(spec, config.tables)
+        for col in spec.outputs:
+            if col in joined:
+                raise ConfigError(f"output column {col!r} collides with a table column")
+            extract_outputs.append((col, Kind.INT64 if domains[col] == "u64" else Kind.UTF8,
+                                    domains[col]))
+            produced.add(col)
+    bkinds = _schema(basic, config.basic_path, config.basic_columns, "basic features")
+    if config.instance_column not in bkinds:
+        raise ConfigError(f"basic features lack instance column {config.instance_column!r}")
+    overlap = (set(bkinds) - {config.instance_column}) & (set(joined) | produced)
+    if overlap:
+        raise ConfigError(f"basic columns {sorted(overlap)} collide with pipeline columns")
+    merged = set(joined) | produced | set(bkinds)
+    doms = {c: d for c, _, d in extract_outputs}
+    for col in config.features:
+        if col not in merged:
+            raise ConfigError(f"feature column {col!r} not in the merged table")
+        if col in doms:
+            if doms[col] != "u64":
+                raise ConfigError(f"feature column {col!r} is not sign-valued")
+        else:
+            kind = bkinds.get(col, joined.get(col))
+            if kind is not Kind.INT64:
+                raise ConfigError(f"feature column {col!r} must be Int64")
+
+    # ---- plan IR --------------------------------------------------------------
+    def view_ir(name: str) -> codegen.ViewIR:
+        v = config.view(name)
+        pol = v.policy
+        flt = bind_filter(pol.filter, cleaned[name]) if pol.filter is not None else None
+        keys = () if name == config.driver else tuple(config.join_keys)
+        return codegen.ViewIR(name, dict(raw[name]), dict(pol.fills), list(pol.extractions),
+                              flt, keys)
+
+    order = plan.node_order()
+    rank = {n: i for i, (_, n) in enumerate(order)}
+    specs = {s.name: s for s in config.operators}
+    pre_of: dict[str, dict[int, str]] = {}
+    nodes = []
+    for layer, name in order:
+        nd = dag.nodes[name]
+        if nd.role == "pre":
+            pre_of.setdefault(nd.op, {})[nd.slot] = name
+            inputs = nd.reads
+        elif nd.role == "body":
+            inputs = specs[nd.op].inputs
+        else:
+            inputs = ()
+        nodes.append(codegen.NodeIR(name, nd.role, nd.op, fns[name], layer, rank[name],
+                                    tuple(inputs), nd.slot, nd.writes))
+    tables = {t: i for i, t in enumerate(sorted(config.tables))}
+    ir = codegen.PlanIR(
+        driver=view_ir(config.driver),
+        sides=[view_ir(v.name) for v in config.views if v.name != config.driver],
+        basic=codegen.ViewIR("basic", dict(bkinds), {}, [], None, (config.instance_column,)),
+        join_keys=tuple(config.join_keys), nodes=nodes, pre_of=pre_of,
+        producer=dict(dag.col_producer), features=dict(config.features),
+        instance_column=config.instance_column, label_column=config.label_column,
+        chunk=config.batch_size, tables=tables,
+        table_defaults={t: config.tables[t].default for t in config.tables},
+        extract_outputs=[(c, d) for c, _, d in extract_outputs], stage_strings=stage_strings)
+    prog = codegen.generate(ir)
+    cubin = runtime.compile_source(prog.source) if compile_program else b""
+    return Prepared(config, dag, plan, ir, prog, cubin, tuple(extract_outputs),
+                    [n for _, n in order], raw, bkinds)
+
+
+# ---------------------------------------------------------------------------
+# device views
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 engine needs a CUDA device (no CPU execution path)")
+    return torch
+
+
+def _pad16(a: np.ndarray) -> np.ndarray:
+    raw = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
+    out = np.zeros(((raw.size + 31) // 16) * 16, dtype=np.uint8)
+    out[: raw.size] = raw
+    return out
+
+
+class DeviceView:
+    """FBXC column images resident in HBM (16-byte padded segments)."""
+
+    def __init__(self, view: ViewImage, columns=None, device="cuda"):
+        torch = _torch()
+        self.n = view.row_count
+        self.kinds = {n: view.columns[n].kind for n in view.order}
+        self.tensors: dict[str, dict[str, "torch.Tensor"]] = {}
+        self.bytes = 0
+        for name in view.order:
+            if columns is not None and name not in columns:
+                continue
+            col = view.columns[name]
+            parts = {"nulls": col.nulls[: (col.n + 7) // 8], "data": col.data}
+            if col.kind.var_length:
+                parts["offsets"] = col.offsets
+            self.tensors[name] = {}
+            for part, arr in parts.items():
+                host = torch.from_numpy(_pad16(arr))
+                t = host.to(device, non_blocking=False)
+                self.tensors[name][part] = t
+                self.bytes += arr.nbytes
+        self.torch = torch
+
+    def ptr(self, name: str, part: str) -> int:
+        t = self.tensors[name].get(part)
+        return 0 if t is None else t.data_ptr()
+
+
+# ---------------------------------------------------------------------------
+# results
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Counters:
+    digest: int = 0
+    instances: int = 0
+    signs: int = 0
+    malformed: int = 0
+    filtered: int = 0
+    joined: int = 0
+    launches: int = 0
+
+
+@dataclass
+class CsrBatch:
+    """Emitted instances of one launch, in the reference's emission order:
+    per driver chunk of ``batch_size`` rows, ascending u64 instance id."""
+
+    ids: object      # torch uint64-as-int64 [n]
+    labels: object   # torch uint8 [n]
+    offsets: object  # torch int64 [n + 1]
+    slots: object    # torch int16 (u16 bits) [m]
+    signs: object    # torch int64 (u64 bits) [m]
+    counters: Counters
+
+    def to_numpy(self) -> dict[str, np.ndarray]:
+        n, m = self.counters.instances, self.counters.signs
+        return {"ids": self.ids[:n].cpu().numpy().view(np.uint64),
+                "labels": self.labels[:n].cpu().numpy(),
+                "offsets": self.offsets[: n + 1].cpu().numpy().view(np.uint64),
+                "slots": self.slots[:m].cpu().numpy().view(np.uint16),
+                "signs": self.signs[:m].cpu().numpy().view(np.uint64)}
+
+
+def _next_pow2(n: int) -> int:
+    return 1 << max(4, (max(n, 1) - 1).bit_length())
+
+
+class Engine:
+    """Device state of one prepared plan on one GPU."""
+
+    def __init__(self, prepared: Prepared, views: Mapping[str, ViewImage] | None = None,
+                 basic: ViewImage | None = None, device: str = "cuda",
+                 max_rows_per_launch: int = 1 << 22, pool_bytes_per_row: int = 96):
+        torch = _torch()
+        self.torch = torch
+        self.prepared = prepared
+        self.device = torch.device(device)
+        self.config = cfg = prepared.config
+        self.ir = ir = prepared.ir
+        self.prog = prepared.program
+        self.slots = self.prog.slots
+        self.params = np.zeros(runtime.FBX_MAX_PARAM_SLOTS, dtype=np.uint64)
+        self.max_rows = max_rows_per_launch - max_rows_per_launch % ir.chunk or ir.chunk
+        self.pool_bytes_per_row = pool_bytes_per_row
+        with torch.cuda.device(self.device):
+            self.module = runtime.Program(prepared.cubin)
+            self.state = torch.zeros(runtime.STATE_BYTES // 8, dtype=torch.int64,
+                                     device=self.device)
+            self._set("state", self.state.data_ptr())
+            self.prepare_counters = Counters()
+            self._keep: list = []
+            self._upload_sides(views or {}, basic)
+            self._upload_tables()
+            self._idset_cap = 0
+            self.idset = None
+            self.streams = None
+            if self.prog.smem_bytes:
+                # static + dynamic > 48 KB needs the opt-in attribute
+                self.module.set_dynamic_smem("fbx_pipeline", self.prog.smem_bytes)
+
+    # -- params ----------------------------------------------------------------
+    def _set(self, name: str, value: int):
+        if name in self.slots:
+            self.params[self.slots[name]] = np.uint64(int(value) & ((1 << 64) - 1))
+
+    def _stream(self) -> int:
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    # -- prepare-time device work -------------------------------------------------
+    def _load_view(self, name: str, path: Path, columns, given: ViewImage | None) -> ViewImage:
+        if given is not None:
+            return given.project(columns)
+        return read_view(path, columns)
+
+    def _upload_sides(self, views: Mapping[str, ViewImage], basic: ViewImage | None):
+        torch, cfg, ir = self.torch, self.config, self.ir
+        sides = [(k, v) for k, v in enumerate(ir.sides)]
+        if ir.basic is not None:
+            sides.append((len(ir.sides), ir.basic))
+        side_pool_cap = 0
+        prepared_views = []
+        self.side_tables = {}
+        for k, v in sides:
+            if v is ir.basic:
+                img = self._load_view("basic", cfg.basic_path, cfg.basic_columns, basic)
+            else:
+                src = cfg.view(v.name)
+                img = self._load_view(v.name, src.path, src.columns, views.get(v.name))
+            dv = DeviceView(img, device=self.device)
+            self._keep.append(dv)
+            n = img.row_count
+            cap = _next_pow2(2 * n)
+            table = torch.zeros(cap * 32, dtype=torch.uint8, device=self.device)
+            self._keep.append(table)
+            self.side_tables[k] = table
+            self._set(f"side{k}.rows", n)
+            self._set(f"side{k}.table", table.data_ptr())
+            self._set(f"side{k}.mask", cap - 1)
+            for c in img.order:
+                for part in ("nulls", "data", "offsets"):
+                    self._set(f"side{k}.{c}.{part}", dv.ptr(c, part))
+            for e in v.extractions:
+                if e.kind is Kind.UTF8:
+                    ptr = torch.zeros(n + 2, dtype=torch.int64, device=self.device)
+                    ln = torch.zeros(n + 4, dtype=torch.int32, device=self.device)
+                    self._keep += [ptr, ln]
+                    self._set(f"side{k}.ext.{e.output}.ptr", ptr.data_ptr())
+                    self._set(f"side{k}.ext.{e.output}.len", ln.data_ptr())
+                else:
+                    val = torch.zeros(n + 2, dtype=torch.int64, device=self.device)
+                    nul = torch.zeros(n + 16, dtype=torch.uint8, device=self.device)
+                    self._keep += [val, nul]
+                    self._set(f"side{k}.ext.{e.output}.val", val.data_ptr())
+                    self._set(f"side{k}.ext.{e.output}.null", nul.data_ptr())
+                src_col = img.columns[e.source]
+                side_pool_cap += int(src_col.data.nbytes) + 128 * (n // 256 + 1)
+            prepared_views.append((k, v, n))
+        pool = torch.zeros(side_pool_cap + 256, dtype=torch.uint8, device=self.device)
+        self._keep.append(pool)
+        self._set("side_pool", pool.data_ptr())
+        self._set("side_pool_cap", side_pool_cap)
+        stream = self._stream()
+        status = torch.zeros(1, dtype=torch.int64, device=self.device)
+        runtime.state_reset(self.state.data_ptr(), status.data_ptr(), 1, stream)
+        for k, v, n in prepared_views:
+            grid = max(1, min((n + 255) // 256, 1184))
+            self.module.launch(f"fbx_side_prep_{k}", grid, 256, 0, stream, self.params)
+        st = self._read_state()
+        self.prepare_counters.malformed = st["malformed"]
+        self.prepare_counters.filtered = st["filtered"]
+        self._raise_if_error(st, prepare=True)
+        # basic uniqueness (pipeline.py:975): any basic key indexed twice
+        if ir.basic is not None:
+            self._check_basic_unique(len(ir.sides))
+
+    def _check_basic_unique(self, k: int):
+        torch = self.torch
+        aux = self.side_tables[k].view(torch.int32).view(-1, 8)[:, 3]
+        mx = int(aux.max().item()) if aux.numel() else 0
+        if mx > 1:
+            raise StageError("prepare", None,
+                             MergeUniquenessError("basic features: duplicate instance id"))
+
+    def _upload_tables(self):
+        torch = self.torch
+        stream = self._stream()
+        for name, ti in self.ir.tables.items():
+            if f"dict{ti}.slots" not in self.slots:
+                continue
+            t = self.config.tables[name]
+            blob, offs, vals = t.arrays()
+            cap = _next_pow2(2 * len(vals))
+            slots = torch.empty(cap * 32, dtype=torch.uint8, device=self.device)
+            dblob = torch.from_numpy(_pad16(blob)).to(self.device)
+            doffs = torch.from_numpy(_pad16(offs)).to(self.device)
+            dvals = torch.from_numpy(_pad16(vals)).to(self.device)
+            dup = torch.zeros(1, dtype=torch.int64, device=self.device)
+            self._keep += [slots, dblob, doffs, dvals, dup]
+            try:
+                runtime.dict_build(slots.data_ptr(), cap, dblob.data_ptr(), doffs.data_ptr(),
+                                   dvals.data_ptr(), len(vals), dup.data_ptr(), stream)
+            except runtime.FbxError as exc:
+                raise ConfigError(f"table {name!r}: {exc}") from exc
+            self._set(f"dict{ti}.slots", slots.data_ptr())
+            self._set(f"dict{ti}.mask", cap - 1)
+            self._set(f"dict{ti}.keys", dblob.data_ptr())
+
+    # -- state ---------------------------------------------------------------------
+    def _read_state(self) -> dict[str, int]:
+        raw = self.state.cpu().numpy().view(np.uint64)
+        return {f: int(raw[i]) for i, f in enumerate(runtime.STATE_FIELDS)}
+
+    def _raise_if_error(self, st: dict, prepare: bool = False):
+        key = st["error_key"]
+        if key == (1 << 64) - 1:
+            if st["pool_overflow"]:
+                req, rem = st["pool_overflow"] >> 32, st["pool_overflow"] & 0xFFFFFFFF
+                raise StageError("extract", None, PoolExhausted(req, rem))
+            return
+        chunk = key >> 32
+        stage = STAGE_NAMES.get((key >> 28) & 0xF, "extract")
+        layer = (key >> 20) & 0xFF
+        rank = (key >> 8) & 0xFFF
+        code = ERR_NAMES.get(key & 0xFF, "value")
+        detail = st["error_detail"]
+        cause = _cause(code, detail, st)
+        if stage == "extract" and layer:
+            node = self.prepared.node_names[rank]
+            cause = LayerExecutionError(layer, node, cause)
+        raise StageError(stage, None if stage == "prepare" else chunk, cause)
+
+    def begin_run(self, rows_hint: int):
+        """Clear the run-wide instance-id set (check_unique_ids' `seen`)."""
+        torch = self.torch
+        cap = _next_pow2(2 * max(rows_hint, 1))
+        if self.idset is None or self._idset_cap < cap:
+            self.idset = torch.zeros(cap + 2, dtype=torch.int64, device=self.device)
+            self._idset_cap = cap
+        else:
+            self.idset.zero_()
+        self._set("idset", self.idset.data_ptr())
+        self._set("idset_mask", self._idset_cap - 1)
+
+    def _arena(self, rows: int):
+        """Per-launch buffers: look-back status, CSR outputs, bump pool."""
+        torch = self.torch
+        tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
+        k = max(1, len(self.ir.features))
+        need = (tiles, rows, k)
+        if getattr(self, "_arena_key", None) != need:
+            dev = self.device
+            self.status = torch.zeros(tiles + 1, dtype=torch.int64, device=dev)
+            self.o_ids = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+            self.o_lab = torch.empty(rows + 16, dtype=torch.uint8, device=dev)
+            self.o_off = torch.empty(rows + 2, dtype=torch.int64, device=dev)
+            self.o_slot = torch.empty(rows * k + 8, dtype=torch.int16, device=dev)
+            self.o_sign = torch.empty(rows * k + 1, dtype=torch.int64, device=dev)
+            pool_cap = 0
+            if codegen_pool_sites(self.prog):
+                pool_cap = self.pool_bytes_per_row * rows + 128 * tiles * 8 + (1 << 20)
+            self.pool = torch.empty(pool_cap + 256, dtype=torch.uint8, device=dev)
+            self.pool_cap = pool_cap
+            self._arena_key = need
+        self._set("tile_status", self.status.data_ptr())
+        self._set("out.ids", self.o_ids.data_ptr())
+        self._set("out.labels", self.o_lab.data_ptr())
+        self._set("out.offsets", self.o_off.data_ptr())
+        self._set("out.slots", self.o_slot.data_ptr())
+        self._set("out.signs", self.o_sign.data_ptr())
+        self._set("pool", self.pool.data_ptr())
+        self._set("pool_cap", self.pool_cap)
+        return tiles
+
+    def bind_driver(self, dview: DeviceView):
+        for c in dview.tensors:
+            for part in ("nulls", "data", "offsets"):
+                self._set(f"drv.{c}.{part}", dview.ptr(c, part))
+        self.dview = dview
+
+    def launch(self, row_lo: int, row_hi: int, stream: int | None = None) -> int:
+        """Enqueue one fused launch over driver rows [row_lo, row_hi) (no sync).
+
+        ``row_lo`` must be a multiple of ``batch_size`` (chunk boundaries are
+        the reference's read boundaries, pipeline.py:994)."""
+        if row_lo % self.ir.chunk:
+            raise ValueError("row_lo must start a driver chunk")
+        rows = row_hi - row_lo
+        tiles = self._arena(rows)
+        stream = self._stream() if stream is None else stream
+        self._set("row_lo", row_lo)
+        self._set("row_hi", row_hi)
+        self._set("chunk0", row_lo // self.ir.chunk)
+        runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(), tiles + 1, stream)
+        self.module.launch("fbx_pipeline", tiles, self.prog.threads, self.prog.smem_bytes,
+                           stream, self.params)
+        return tiles
+
+    def finish(self) -> CsrBatch:
+        """Synchronise, read counters, raise the first error in pipeline order."""
+        st = self._read_state()
+        self._raise_if_error(st)
+        c = Counters(st["digest"], st["instances"], st["signs"], st["malformed"],
+                     st["filtered"], st["joined"], 1)
+        return CsrBatch(self.o_ids, self.o_lab, self.o_off, self.o_slot, self.o_sign, c)
+
+    def run(self, row_lo: int, row_hi: int) -> CsrBatch:
+        self.launch(row_lo, row_hi)
+        return self.finish()
+
+
+def codegen_pool_sites(prog: codegen.Program) -> bool:
+    return "fbx::pool_alloc<NT>" in prog.source.split("// ===== generated plan =====", 1)[-1]
+
+
+def _cause(code: str, detail: int, st: dict) -> BaseException:
+    if code == "type":
+        return TypeError("unsupported operand type for mix/fold")
+    if code == "encode":
+        return UnicodeEncodeError("utf-8", "", 0, 1, "surrogates not allowed")
+    if code == "pool":
+        req, rem = st["pool_overflow"] >> 32, st["pool_overflow"] & 0xFFFFFFFF
+        return PoolExhausted(req, rem)
+    if code == "null_label":
+        return EmitError("null label at emission")
+    if code == "label_range":
+        return BatchInvariantError(f"label {detail - (1 << 64) if detail >> 63 else detail!r} not 0/1")
+    if code == "dup_id":
+        return MergeUniquenessError(f"extracted features: duplicate instance id {detail}")
+    if code == "multi_match":
+        return MergeUniquenessError("extracted features: duplicate instance id (side view "
+                                    "key matched more than one row)")
+    if code == "json_bigint":
+        return ValueError("Exceeds the limit (4300 digits) for integer string conversion")
+    if code == "float_overflow":
+        return OverflowError("float too large to pack with f format")
+    if code in ("json_deep", "unicode_lower", "float_slow"):
+        return UnsupportedOnDevice(f"row needs an unimplemented device path: {code}")
+    return ValueError(f"value error ({code})")
+
+
+# ---------------------------------------------------------------------------
+# run reports (pipeline.py:461-540)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class RunReport:
+    mode: str
+    digest: int
+    batches: int
+    instances: int
+    signs: int
+    launches: int
+    overhead_us: float
+    bytes_h2d: int
+    transfer_seconds: float
+    intermediate_bytes_written: int
+    intermediate_files: tuple[str, ...]
+    rows_dropped: int
+    rows_filtered: int
+    batch_size: int
+    workers: int
+    wall_seconds: float
+    stage_seconds: dict[str, float] = field(default_factory=dict)
+
+    def to_text(self) -> str:
+        lines = [
+            f"== run report ({self.mode}) ==",
+            f"batches emitted: {self.batches} x batch_size {self.batch_size}",
+            f"instances: {self.instances} ({self.rows_dropped} dropped malformed, "
+            f"{self.rows_filtered} filtered)",
+            f"feature signs: {self.signs}",
+            f"device launches: {self.launches} (measured overhead {self.overhead_us:.3f} us)",
+            f"h2d transfers: {self.bytes_h2d} bytes ({self.transfer_seconds:.9f} s measured)",
+            f"intermediate bytes written: {self.intermediate_bytes_written}",
+        ]
+        for stage in sorted(self.stage_seconds):
+            lines.append(f"stage {stage}: {self.stage_seconds[stage]:.3f} s")
+        lines.append(f"wall: {self.wall_seconds:.3f} s on {self.workers} worker(s)")
+        lines.append(f"batch digest: 0x{self.digest:016x}")
+        lines += ["", "[report]"]
+        kv = {"mode": self.mode, "digest": f"0x{self.digest:016x}", "batches": self.batches,
+              "instances": self.instances, "signs": self.signs, "launches": self.launches,
+              "overhead_us": f"{self.overhead_us:.3f}", "bytes_h2d": self.bytes_h2d,
+              "transfer_seconds": f"{self.transfer_seconds:.9f}",
+              "intermediate_bytes": self.intermediate_bytes_written,
+              "rows_dropped": self.rows_dropped, "rows_filtered": self.rows_filtered,
+              "batch_size": self.batch_size, "workers": self.workers,
+              "wall_seconds": f"{self.wall_seconds:.3f}"}
+        for stage in sorted(self.stage_seconds):
+            kv[f"stage_{stage}_s"] = f"{self.stage_seconds[stage]:.3f}"
+        lines.extend(f"{k}={v}" for k, v in kv.items())
+        return "\n".join(lines)
+
+
+def parse_report_block(text: str) -> dict[str, str]:
+    out, seen = {}, False
+    for line in text.splitlines():
+        if line.strip() == "[report]":
+            seen = True
+            continue
+        if seen and "=" in line:
+            k, _, v = line.partition("=")
+            out[k.strip()] = v.strip()
+    return out
+
+
+@dataclass
+class RunResult:
+    report: RunReport
+    csr: dict[str, np.ndarray] | None
+
+
+def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: ViewImage,
+              collect: bool = False, device: str = "cuda", prepared: Prepared | None = None,
+              max_rows_per_launch: int = 1 << 22) -> RunResult:
+    """The pipelined run over in-memory views (H2D once, device-resident)."""
+    t0 = time.perf_counter()
+    stage: dict[str, float] = {}
+    prep = prepared or prepare(config, views, basic)
+    stage["prepare"] = time.perf_counter() - t0
+    eng = Engine(prep, views, basic, device=device, max_rows_per_launch=max_rows_per_launch)
+    torch = eng.torch
+    drv = views[config.driver].project(config.view(config.driver).columns)
+    t1 = time.perf_counter()
+    dv = DeviceView(drv, device=eng.device)
+    torch.cuda.synchronize(eng.device)
+    stage["read"] = time.perf_counter() - t1
+    eng.bind_driver(dv)
+    n = drv.row_count
+    eng.begin_run(n)
+    total = Counters()
+    parts = []
+    t2 = time.perf_counter()
+    step = eng.max_rows
+    for lo in range(0, n, step):
+        hi = min(lo + step, n)
+        eng.launch(lo, hi)
+        b = eng.finish()
+        c = b.counters
+        total.digest ^= c.digest
+        for f in ("instances", "signs", "malformed", "filtered", "joined", "launches"):
+            setattr(total, f, getattr(total, f) + getattr(c, f))
+        if collect:
+            parts.append((b.to_numpy(), total.signs - c.signs))
+    stage["extract"] = time.perf_counter() - t2
+    csr = None
+    if collect:
+        ids = [p["ids"] for p, _ in parts]
+        offs = [p["offsets"][:-1] + base for p, base in parts]
+        csr = {"ids": np.concatenate(ids) if ids else np.zeros(0, np.uint64),
+               "labels": np.concatenate([p["labels"] for p, _ in parts]) if parts else
+               np.zeros(0, np.uint8),
+               "offsets": np.concatenate(offs + [np.array([total.signs], np.uint64)]),
+               "slots": np.concatenate([p["slots"] for p, _ in parts]) if parts else
+               np.zeros(0, np.uint16),
+               "signs": np.concatenate([p["signs"] for p, _ in parts]) if parts else
+               np.zeros(0, np.uint64)}
+    bs = config.batch_size
+    rep = RunReport(
+        mode="pipelined", digest=total.digest, batches=math.ceil(total.instances / bs),
+        instances=total.instances, signs=total.signs, launches=total.launches + len(eng.ir.sides)
+        + 1, overhead_us=0.0, bytes_h2d=dv.bytes, transfer_seconds=stage["read"],
+        intermediate_bytes_written=0, intermediate_files=(),
+        rows_dropped=total.malformed + eng.prepare_counters.malformed,
+        rows_filtered=total.filtered + eng.prepare_counters.filtered,
+        batch_size=bs, workers=1, wall_seconds=time.perf_counter() - t0, stage_seconds=stage)
+    return RunResult(rep, csr)
+
+
+def run_pipelined(config: PipelineConfig, collect: bool = False) -> RunReport:
+    """Reference-compatible ``run_pipelined`` (pipeline.py:952) on the B200."""
+    views = {}
+    for v in config.views:
+        try:
+            views[v.name] = read_view(v.path, v.columns)
+        except Exception as exc:  # noqa: BLE001
+            raise StageError("prepare", None, exc) from exc
+    try:
+        basic = read_view(config.basic_path, config.basic_columns)
+    except Exception as exc:  # noqa: BLE001
+        raise StageError("prepare", None, exc) from exc
+    return run_views(config, views, basic, collect=collect).report
+
+
+def run_pipeline(config: PipelineConfig, mode: str | None = None) -> RunReport:
+    effective = mode or config.mode
+    if effective != "pipelined":
+        raise UnsupportedOnDevice(f"mode {effective!r}: only the pipelined path is on device "
+                                  "(staged mode writes intermediate files; out of scope)")
+    return run_pipelined(config)

@@ -1,0 +1,169 @@
+"""ctypes binding of libfbx.so (include/fbx.h).
+
+ctypes releases the GIL for the duration of every foreign call, so a host
+thread driving one engine never blocks other Python threads.  The library is
+built in-tree (``build.py``); a missing library is an error, never a
+fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .build import LIB, build_library
+
+_lock = threading.Lock()
+_lib = None
+
+FBX_MAX_PARAM_SLOTS = 384
+STATE_FIELDS = ("tile_ticket", "pool_head", "pool_overflow", "error_key", "error_detail",
+                "digest", "instances", "signs", "malformed", "filtered", "joined", "side_rows",
+                "r0", "r1", "r2", "r3")
+STATE_BYTES = 8 * len(STATE_FIELDS)
+
+EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_program_load",
+           "fbx_program_unload", "fbx_program_kernel", "fbx_kernel_attributes",
+           "fbx_kernel_set_max_dynamic_smem", "fbx_launch", "fbx_state_reset",
+           "fbx_dict_build", "fbx_l2_flush")
+
+
+class FbxError(RuntimeError):
+    pass
+
+
+def lib() -> ctypes.CDLL:
+    """Load (building first if the in-tree library is missing) libfbx.so."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB.exists():
+                build_library()
+            L = ctypes.CDLL(str(LIB))
+            vp, sz, c = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+            L.fbx_version.restype = ctypes.c_char_p
+            L.fbx_last_error.restype = ctypes.c_char_p
+            L.fbx_compile.argtypes = [ctypes.c_char_p, ctypes.c_char_p,
+                                      ctypes.POINTER(ctypes.c_char_p), c,
+                                      ctypes.POINTER(vp), ctypes.POINTER(sz),
+                                      ctypes.c_char_p, sz]
+            L.fbx_free.argtypes = [vp]
+            L.fbx_program_load.argtypes = [vp, sz, ctypes.POINTER(vp)]
+            L.fbx_program_unload.argtypes = [vp]
+            L.fbx_program_kernel.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(vp)]
+            L.fbx_kernel_attributes.argtypes = [vp, ctypes.POINTER(c), ctypes.POINTER(c),
+                                                ctypes.POINTER(c)]
+            L.fbx_kernel_set_max_dynamic_smem.argtypes = [vp, c]
+            L.fbx_launch.argtypes = [vp, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, vp, vp]
+            L.fbx_state_reset.argtypes = [vp, vp, sz, vp]
+            L.fbx_dict_build.argtypes = [vp, ctypes.c_ulonglong, vp, vp, vp,
+                                         ctypes.c_ulonglong, vp, vp]
+            L.fbx_l2_flush.argtypes = [vp, sz, vp]
+            for name in EXPORTS:
+                getattr(L, name).restype = getattr(L, name).restype or c
+            L.fbx_version.restype = ctypes.c_char_p
+            L.fbx_last_error.restype = ctypes.c_char_p
+            L.fbx_free.restype = None
+            _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().fbx_last_error().decode(errors="replace")
+        raise FbxError(f"{what} failed ({rc}): {msg}")
+
+
+_CUBIN_CACHE: dict[str, bytes] = {}
+
+
+def compile_source(source: str, name: str = "plan.cu", options: tuple[str, ...] = ()) -> bytes:
+    """NVRTC -> sm_100a cubin (host-only).  Cached per process and on disk."""
+    opts = ("-arch=sm_100a", "-std=c++17", "-lineinfo", *options)
+    key = hashlib.sha256((source + "\0" + "\0".join(opts)).encode()).hexdigest()
+    if key in _CUBIN_CACHE:
+        return _CUBIN_CACHE[key]
+    cache_dir = Path(os.environ.get("FBX_CACHE", Path.home() / ".cache" / "fbx_b200"))
+    cpath = cache_dir / f"{key}.cubin"
+    if cpath.exists():
+        data = cpath.read_bytes()
+        _CUBIN_CACHE[key] = data
+        return data
+    L = lib()
+    arr = (ctypes.c_char_p * len(opts))(*[o.encode() for o in opts])
+    img = ctypes.c_void_p()
+    n = ctypes.c_size_t()
+    log = ctypes.create_string_buffer(1 << 16)
+    rc = L.fbx_compile(source.encode(), name.encode(), arr, len(opts), ctypes.byref(img),
+                       ctypes.byref(n), log, len(log))
+    if rc != 0:
+        raise FbxError(f"plan compilation failed: {L.fbx_last_error().decode(errors='replace')}")
+    data = ctypes.string_at(img, n.value)
+    L.fbx_free(img)
+    _CUBIN_CACHE[key] = data
+    try:
+        cache_dir.mkdir(parents=True, exist_ok=True)
+        tmp = cpath.with_suffix(".tmp")
+        tmp.write_bytes(data)
+        tmp.replace(cpath)
+    except OSError:
+        pass
+    return data
+
+
+class Program:
+    """A loaded plan module and its kernels."""
+
+    def __init__(self, cubin: bytes):
+        self._cubin = ctypes.create_string_buffer(cubin, len(cubin))
+        h = ctypes.c_void_p()
+        _check(lib().fbx_program_load(self._cubin, len(cubin), ctypes.byref(h)), "program load")
+        self.handle = h
+        self.kernels: dict[str, ctypes.c_void_p] = {}
+
+    def kernel(self, name: str) -> ctypes.c_void_p:
+        if name not in self.kernels:
+            k = ctypes.c_void_p()
+            _check(lib().fbx_program_kernel(self.handle, name.encode(), ctypes.byref(k)),
+                   f"kernel {name}")
+            self.kernels[name] = k
+        return self.kernels[name]
+
+    def attributes(self, name: str) -> dict:
+        regs, thr, smem = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().fbx_kernel_attributes(self.kernel(name), ctypes.byref(regs),
+                                           ctypes.byref(thr), ctypes.byref(smem)), "attributes")
+        return {"registers": regs.value, "max_threads": thr.value, "static_smem": smem.value}
+
+    def set_dynamic_smem(self, name: str, nbytes: int):
+        _check(lib().fbx_kernel_set_max_dynamic_smem(self.kernel(name), int(nbytes)),
+               "set dynamic smem")
+
+    def launch(self, name: str, grid: int, block: int, smem: int, stream: int,
+               params: np.ndarray):
+        assert params.dtype == np.uint64 and params.size == FBX_MAX_PARAM_SLOTS
+        _check(lib().fbx_launch(self.kernel(name), int(grid), int(block), int(smem),
+                                ctypes.c_void_p(stream), params.ctypes.data_as(ctypes.c_void_p)),
+               f"launch {name}")
+
+
+def state_reset(d_state: int, d_status: int, n_tiles: int, stream: int):
+    _check(lib().fbx_state_reset(ctypes.c_void_p(d_state), ctypes.c_void_p(d_status),
+                                 int(n_tiles), ctypes.c_void_p(stream)), "state reset")
+
+
+def dict_build(d_slots: int, capacity: int, d_blob: int, d_offs: int, d_vals: int, n: int,
+               d_dup: int, stream: int):
+    _check(lib().fbx_dict_build(ctypes.c_void_p(d_slots), capacity, ctypes.c_void_p(d_blob),
+                                ctypes.c_void_p(d_offs), ctypes.c_void_p(d_vals), n,
+                                ctypes.c_void_p(d_dup), ctypes.c_void_p(stream)), "dict build")
+
+
+def l2_flush(d_buf: int, nbytes: int, stream: int):
+    _check(lib().fbx_l2_flush(ctypes.c_void_p(d_buf), int(nbytes), ctypes.c_void_p(stream)),
+           "l2 flush")
