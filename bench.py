@@ -1,0 +1,425 @@
+"""Benchmark: raw log records/s through the fused B200 extraction path.
+
+Workload (BASELINE.json configs[1]): the 1M-record synthetic ads log
+(gen_corpus rows=1,000,000 users=5,000 seed=11) through the sign-heavy DAG
+ with the reference's full emit (basic merge
+included).  A *step* is one pass of the hot path over the whole log:
+clean -> side join -> 18-node DAG -> uniqueness check + basic merge ->
+sorted/deduplicated CSR + digests.  Every step's digest is checked against
+the reference golden (0xb30824efab77470b).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--dag sign_heavy]
+    python bench.py --impl reference ...   # the CPU reference arm (oracle port)
+
+N > 1 runs under torchrun: one record shard (its own 1M-row log, seed 11 + r)
+per GPU, no per-record communication, one NCCL all-gather of the per-shard
+{records, instances, signs, digest} at the end (SURVEY.md §8 e).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GOLDEN_1M = {  # SURVEY.md Appendix B, 1M / 5000 / seed 11 (reference output, full emit)
+    "default": (0xD81834ED0893E11E, 907463, 5203686),
+    "fig4": (0xD75A8D50AF79290B, 907463, 4537315),
+    "sign_heavy": (0xB30824EFAB77470B, 907463, 11586442),
+    "cross_heavy": (0xE504098333D34E53, 907463, 8653476),
+    "lookup_heavy": (0x5A153AB37CE08E96, 907463, 9074630),
+}
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--dag", default="sign_heavy")
+    ap.add_argument("--rows", type=int, default=1_000_000)
+    ap.add_argument("--users", type=int, default=5000)
+    ap.add_argument("--seed", type=int, default=11)
+    ap.add_argument("--cpu-sample-rows", type=int, default=8192)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md): nvidia-smi during the timed region
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.out, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.out.flush()
+        rows = []
+        for line in Path(self.out.name).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port over a bounded sample on all host cores
+# ---------------------------------------------------------------------------
+
+_CPU_CTX = {}
+
+
+def _cpu_worker(args):
+    lo, hi = args
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import featurebox_oracle as O
+    ctx = _CPU_CTX
+    drv = ctx["driver"].slice(lo, hi)
+    basic = ctx["basic"].slice(lo, hi)  # gen_corpus: basic row i <-> driver row i
+    t = time.perf_counter()
+    O.run_pipelined(ctx["cfg"], {"user_events": drv, "user_profile": ctx["profile"]},
+                    basic, ctx["tables"], ctx["sizes"])
+    return hi - lo, time.perf_counter() - t
+
+
+def cpu_baseline(corpus, raw_cfg, tables_dir, sample_rows, procs=None):
+    import multiprocessing as mp
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import featurebox_oracle as O
+    procs = procs or os.cpu_count() or 1
+    tables, sizes = O.load_tables(raw_cfg.get("tables", {}), tables_dir)
+    _CPU_CTX.update(driver=corpus.driver, profile=corpus.profile, basic=corpus.basic,
+                    cfg=raw_cfg, tables=tables, sizes=sizes)
+    jobs = [(k * sample_rows, (k + 1) * sample_rows) for k in range(procs)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    rows = sum(r for r, _ in res)
+    slowest = max(t for _, t in res)
+    return {"value": rows / slowest, "unit": "records/s", "cores": procs, "kind": "port",
+            "sample": f"{procs} processes x {sample_rows} driver rows of the same log "
+                      f"(oracle/featurebox_oracle.py, CPython); rate = rows / slowest "
+                      f"process ({slowest:.1f}s, wall {wall:.1f}s)"}
+
+
+# ---------------------------------------------------------------------------
+
+def algorithmic_bytes(corpus, counters) -> dict:
+    """Compulsory HBM bytes of one step (SURVEY.md §8 d)."""
+    d = corpus.driver
+    inp = sum(d.columns[c].nbytes() for c in d.order)
+    b = corpus.basic
+    basic = sum(b.columns[c].nbytes() for c in ("instance_id", "basic_a", "basic_b"))
+    probe = 32 * counters.joined  # one 32-B sector of the basic index per merged row
+    out = counters.instances * (8 + 1 + 8) + counters.signs * (2 + 8)
+    return {"input": inp, "basic": basic, "basic_probe": probe, "output": out,
+            "total": inp + basic + probe + out}
+
+
+def main():
+    args = parse_args()
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    import torch
+    from paper_2210_07768_b200 import engine as E
+    from paper_2210_07768_b200 import runtime
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.corpus import make_corpus, write_corpus
+    from paper_2210_07768_b200.workloads import workload_config, write_lookup_tables
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    seed = args.seed + rank
+    t0 = time.time()
+    corpus = make_corpus(args.rows, args.users, seed)
+    gen_s = time.time() - t0
+    tmp = Path(tempfile.mkdtemp(prefix="fbxbench"))
+    write_corpus(corpus, tmp)
+    raw = workload_config(args.dag)
+    if args.dag == "lookup_heavy":
+        write_lookup_tables(tmp, args.users)
+    cfg = config_from_dict(raw, tmp)
+    views = {"user_events": corpus.driver, "user_profile": corpus.profile}
+    t1 = time.time()
+    prep = E.prepare(cfg, views, corpus.basic)
+    eng = E.Engine(prep, views, corpus.basic, device=str(dev), max_rows_per_launch=args.rows)
+    dview = E.DeviceView(corpus.driver, device=dev)
+    eng.bind_driver(dview)
+    prep_s = time.time() - t1
+    n = corpus.driver.row_count
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        eng.begin_run(n)
+        eng.launch(0, n)
+
+    # ---- warmup + correctness of every step --------------------------------
+    for _ in range(max(args.warmup, 3)):
+        step()
+    batch = eng.finish()
+    c = batch.counters
+    if args.rows == 1_000_000 and args.users == 5000 and args.seed == 11 and rank == 0:
+        want = GOLDEN_1M.get(args.dag)
+        if want and (c.digest, c.instances, c.signs) != want:
+            raise SystemExit(f"parity failure: got digest 0x{c.digest:016x} / {c.instances} / "
+                             f"{c.signs}, want 0x{want[0]:016x} / {want[1]} / {want[2]}")
+    ab = algorithmic_bytes(corpus, c)
+
+    # ---- timed device-resident steps ---------------------------------------
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = Clocks(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    for k in range(K):
+        runtime.l2_flush(flush.data_ptr(), flush.numel(), stream.cuda_stream)  # L2 flush
+        ev[k][0].record(stream)
+        eng.begin_run(n)
+        ev[k][1].record(stream)
+        eng.launch(0, n)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b2) for a, _, b2 in ev]
+    kern_ms = [b1.elapsed_time(b2) for _, b1, b2 in ev]
+    c = eng.finish().counters
+    total_ms = sum(step_ms)
+    tot = torch.tensor([total_ms, sum(kern_ms)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms, kern_total = float(tot[0]), float(tot[1])
+    # the one collective: all-gather of per-shard {records, instances, signs, digest}
+    shard = torch.tensor([n, c.instances, c.signs, c.digest - (1 << 64) if c.digest >> 63
+                          else c.digest], dtype=torch.int64, device=dev)
+    if dist:
+        parts = [torch.empty_like(shard) for _ in range(world)]
+        dist.all_gather(parts, shard)
+        gathered = torch.stack(parts).cpu().numpy()
+    else:
+        gathered = shard.cpu().numpy()[None]
+    run_digest = 0
+    for g in gathered:
+        run_digest ^= int(g[3]) & ((1 << 64) - 1)
+    records_all = int(gathered[:, 0].sum())
+    value = records_all * K / (total_ms / 1e3)
+    ms_per_step = total_ms / K
+    kern_avg_s = kern_total / K / 1e3
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = ab["total"] / kern_avg_s / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "bytes_per_launch": ab, "kernel_ms": round(kern_avg_s * 1e3, 4),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            t = json.loads(prof.read_text()).get(args.dag)
+            if t:
+                roofline["traffic"] = t["dram_bytes"]
+        except (OSError, ValueError):
+            pass
+
+    # ---- e2e through the public API with host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(corpus, raw, tmp, args.cpu_sample_rows)
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "error": str(exc)[:200]}
+    launches_per_step = 2  # fbx_state_reset + fbx_pipeline (id-set clear is a memset)
+    out = {
+        "metric": "raw log records/sec extracted (device-resident input)",
+        "value": round(value, 1), "unit": "records/s", "n_gpus": world, "steps": K,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (gen_corpus restatement, byte-identical to the reference)",
+        "config": {"workload": f"{args.dag} DAG (SURVEY Appendix B), {args.rows} records/GPU, "
+                               f"users {args.users}, seed {args.seed}+rank, full emit incl. "
+                               "basic merge", "batch_size": cfg.batch_size,
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)",
+                   "parallelism": f"record-sharded x{world}"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches_per_step * K, "clocks": clk,
+        "parity": {"digest": f"0x{run_digest:016x}", "instances": int(gathered[:, 1].sum()),
+                   "signs": int(gathered[:, 2].sum())},
+        "setup_s": {"corpus": round(gen_s, 1), "prepare": round(prep_s, 1)},
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist):
+    """Same metric through Engine + host buffers: pinned H2D of the driver
+    columns, the fused launch, D2H of the emitted CSR, every step."""
+    dv = eng.dview
+    host = {}
+    h2d = 0
+    for c, parts in dv.tensors.items():
+        host[c] = {}
+        for p, t in parts.items():
+            h = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+            h.copy_(t.cpu())
+            host[c][p] = h
+            h2d += t.numel() * t.element_size()
+    n = dv.n
+    out_host = None
+    times = []
+    d2h_total = 0
+    if dist:
+        dist.barrier()
+    for k in range(K + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for c, parts in dv.tensors.items():
+            for p, t in parts.items():
+                t.copy_(host[c][p], non_blocking=True)
+        eng.begin_run(n)
+        eng.launch(0, n)
+        b = eng.finish()  # syncs, reads counters
+        ni, ms = b.counters.instances, b.counters.signs
+        if out_host is None:
+            out_host = {"ids": torch.empty(n + 1, dtype=torch.int64, pin_memory=True),
+                        "labels": torch.empty(n + 16, dtype=torch.uint8, pin_memory=True),
+                        "offsets": torch.empty(n + 2, dtype=torch.int64, pin_memory=True),
+                        "slots": torch.empty(b.slots.numel(), dtype=torch.int16, pin_memory=True),
+                        "signs": torch.empty(b.signs.numel(), dtype=torch.int64, pin_memory=True)}
+        out_host["ids"][:ni].copy_(b.ids[:ni], non_blocking=True)
+        out_host["labels"][:ni].copy_(b.labels[:ni], non_blocking=True)
+        out_host["offsets"][:ni + 1].copy_(b.offsets[:ni + 1], non_blocking=True)
+        out_host["slots"][:ms].copy_(b.slots[:ms], non_blocking=True)
+        out_host["signs"][:ms].copy_(b.signs[:ms], non_blocking=True)
+        torch.cuda.synchronize(dev)
+        dt = time.perf_counter() - t0
+        d2h = ni * 17 + 8 + ms * 10
+        if k:  # first pass is a warm-up
+            times.append(dt)
+            d2h_total = d2h
+    tt = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    rate = n * world * K / float(tt[0])
+    return {"value": round(rate, 1), "unit": "records/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h_total,
+            "path": "Engine.launch over pinned host column images: H2D copy, fused kernel, "
+                    "counter read-back, D2H of the CSR (ids, labels, offsets, slots, signs)"}
+
+
+def reference_arm(args, rank, world):
+    """The reference's CPU path (oracle port) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2210_07768_b200.corpus import make_corpus, write_corpus
+    from paper_2210_07768_b200.workloads import workload_config, write_lookup_tables
+    sample = args.cpu_sample_rows
+    procs = os.cpu_count() or 1
+    rows = max(sample * procs, 1)
+    corpus = make_corpus(min(rows, args.rows), args.users, args.seed)
+    tmp = Path(tempfile.mkdtemp(prefix="fbxref"))
+    write_corpus(corpus, tmp)
+    raw = workload_config(args.dag)
+    if args.dag == "lookup_heavy":
+        write_lookup_tables(tmp, args.users)
+    rates = []
+    last = None
+    for k in range(args.warmup + args.steps):
+        last = cpu_baseline(corpus, raw, tmp, sample, procs)
+        if k >= args.warmup:
+            rates.append(last["value"])
+    value = statistics.mean(rates) if rates else 0.0
+    out = {"impl": "reference", "metric": "raw log records/sec extracted (device-resident input)",
+           "value": round(value, 1), "unit": "records/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(sample * procs / value * 1e3, 3) if value
+           else None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "u64", "data": "synthetic",
+           "config": {"workload": f"{args.dag} DAG, sample of the {args.rows}-record log "
+                                  f"(users {args.users}, seed {args.seed})",
+                      "batch_size": 512, "parallelism": f"{procs} host processes"},
+           "cpu_baseline": {**(last or {}), "value": round(value, 1)},
+           "e2e": {"value": round(value, 1), "unit": "records/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -85,7 +85,11 @@ _CUBIN_CACHE: dict[str, bytes] = {}
 def compile_source(source: str, name: str = "plan.cu", options: tuple[str, ...] = ()) -> bytes:
     """NVRTC -> sm_100a cubin (host-only).  Cached per process and on disk."""
     opts = ("-arch=sm_100a", "-std=c++17", "-lineinfo", *options)
-    key = hashlib.sha256((source + "\0" + "\0".join(opts)).encode()).hexdigest()
+    dump = os.environ.get("FBX_DUMP_SOURCE")
+    if dump:  # profiling aid: keep the generated plan so ncu can import it by name
+        Path(dump).write_text(source)
+        name = str(Path(dump).resolve())
+    key = hashlib.sha256((name + "\0" + source + "\0" + "\0".join(opts)).encode()).hexdigest()
     if key in _CUBIN_CACHE:
         return _CUBIN_CACHE[key]
     cache_dir = Path(os.environ.get("FBX_CACHE", Path.home() / ".cache" / "fbx_b200"))
