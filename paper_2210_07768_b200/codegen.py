@@ -40,6 +40,8 @@ INCLUDE = Path(__file__).resolve().parent.parent / "include"
 
 INT64_MIN, INT64_MAX = -(1 << 63), (1 << 63) - 1
 SPAN_BUDGET = 40 * 1024  # bytes of dynamic shared memory for staged record spans
+OUT_BUDGET = 96 * 1024   # cap for staging a tile's CSR before the coalesced write-out
+STATIC_SMEM_EST = 6 * 1024
 MASK64 = (1 << 64) - 1
 
 STAGE = {"prepare": 0, "read": 1, "clean": 2, "join": 3, "extract": 4, "merge": 5, "emit": 6}
@@ -130,6 +132,7 @@ class V:
     c: str
     nullable: bool = True
     lone: bool = False
+    lower: bool = False   # str view whose (ASCII) bytes are lowercased on read
 
     @property
     def n(self) -> str:
@@ -211,8 +214,19 @@ class PlanCodegen:
             raise UnsupportedOnDevice(
                 f"batch_size {ir.chunk} > 1024: one CTA per chunk is the only emission "
                 "order implemented on device")
-        self.nt = max(32, (ir.chunk + 31) // 32 * 32)
-        self.nsort = 1 << (self.nt - 1).bit_length()
+        self.nt = 1 << (max(32, ir.chunk) - 1).bit_length()  # power of two
+        self.nsort = self.nt
+        if len(ir.features) > 64:
+            raise UnsupportedOnDevice("more than 64 emitted features")
+        import os
+        # CTAs per SM (sets the register budget): 3 x 512 threads (<= 40 regs)
+        # when the tile's CSR staging fits a third of the SM's shared memory,
+        # else 2 (64 regs) -- both measured on B200 (profiles/r1_*.md)
+        k = max(1, len(ir.features))
+        need = self.nt * (17 + 10 * k) + 64
+        default_mb = 3 if need <= (227 * 1024) // 3 - STATIC_SMEM_EST - 1024 else 2
+        default_mb = max(1, min(default_mb, 2048 // self.nt))
+        self.min_blocks = int(os.environ.get("FBX_MIN_BLOCKS", str(default_mb)))
         self.pool_sites = 0
 
     # -- value helpers ---------------------------------------------------------
@@ -256,6 +270,22 @@ class PlanCodegen:
             g(f"{s.c}_n = false;")
         g("}")
         return s
+
+    def materialize(self, v: V) -> V:
+        """Copy a lazily-lowered view into the pool (consumers that compare
+        or store bytes)."""
+        if v.t != "str" or not v.lower:
+            return v
+        g = self.g
+        out = V("str", g.fresh("mz"), v.nullable, v.lone)
+        self.decl(out)
+        cond = f"alive && !{v.n}" if v.nullable else "alive"
+        ptr = self.pool_alloc(f"({cond}) ? {v.c}.n : 0u")
+        g(f"if (({cond}) && ({ptr} || {v.c}.n == 0u)) {{ if ({v.c}.n) fbx::str_copy_lower({ptr}, {v.c});"
+          f" {out.c} = fbx::Str{{{ptr} ? {ptr} : {v.c}.p, {v.c}.n}};"
+          + (f" {out.c}_n = false;" if out.nullable else "")
+          + (f" {out.c}_l = {v.l};" if out.lone else "") + " }")
+        return out
 
     def pool_alloc(self, size_expr: str) -> str:
         """CTA-uniform pool allocation; returns the pointer var."""
@@ -657,9 +687,34 @@ class PlanCodegen:
             if a.nullable:
                 g(f"bool {out.c}_n = {a.n};")
             return out
+        if op == "token" and nd.name in getattr(self, "token_groups", {}) and args[0].t == "str":
+            (col, delim), fields = self.token_groups[nd.name]
+            gk = f"{col}|{delim}"
+            a = args[0]
+            if gk not in self.token_done:
+                base = g.fresh("tg")
+                kk = len(fields)
+                g(f"fbx::Str {base}[{kk}];")
+                g(f"{{ const u32 want[{kk}] = {{{', '.join(map(str, fields))}}};")
+                cond = f"alive && !{a.n}" if a.nullable else "alive"
+                g(f"if ({cond}) fbx::str_tokens<{kk}>({a.c}, {ord(delim)}u, want, {base}); }}")
+                self.token_done[gk] = V("str", base, a.nullable, a.lone)
+            grp = self.token_done[gk]
+            out = V("str", g.fresh("n"), a.nullable, a.lone)
+            g(f"fbx::Str {out.c} = {grp.c}[{fields.index(fn.index)}];")
+            if out.nullable:
+                g(f"bool {out.c}_n = {a.n} || !alive;")
+            if out.lone:
+                g(f"bool {out.c}_l = {a.l};")
+                g(f"if (alive && !{out.n} && {out.l}) {{")
+                err("encode")
+                g("}")
+            return out
         if op == "token":
             a = self.as_str(args[0], fn.spec)
-            out = V("str", g.fresh("n"), a.nullable, a.lone)
+            if a.lower and fn.delim.isascii() and fn.delim.isalpha():
+                a = self.materialize(a)  # a letter delimiter must see lowered bytes
+            out = V("str", g.fresh("n"), a.nullable, a.lone, a.lower)
             self.decl(out)
             cond = f"alive && !{a.n}" if a.nullable else "alive"
             g(f"if ({cond}) {{")
@@ -679,7 +734,7 @@ class PlanCodegen:
             return out
         if op == "trim":
             a = self.as_str(args[0], fn.spec)
-            out = V("str", g.fresh("n"), a.nullable, a.lone)
+            out = V("str", g.fresh("n"), a.nullable, a.lone, a.lower)
             self.decl(out)
             cond = f"alive && !{a.n}" if a.nullable else "alive"
             g(f"if ({cond}) {{ {out.c} = fbx::str_trim({a.c});"
@@ -688,31 +743,23 @@ class PlanCodegen:
             return out
         if op == "lower":
             a = self.as_str(args[0], fn.spec)
-            out = V("str", g.fresh("n"), a.nullable, a.lone)
-            self.decl(out)
+            if a.lower:
+                return a
             cls = g.fresh("lc")
             cond = f"alive && !{a.n}" if a.nullable else "alive"
             g(f"u32 {cls} = ({cond}) ? fbx::str_lower_class({a.c}) : 0u;")
             g(f"if ({cls} == 2u) {{")
             err("unicode_lower")
             g("}")
-            ptr = self.pool_alloc(f"({cls} == 1u && alive) ? {a.c}.n : 0u")
-            g(f"if ({cond}) {{")
-            g(f"if ({cls} == 1u) {{ if ({ptr}) {{ fbx::str_lower_copy({ptr}, {a.c}); "
-              f"{out.c} = fbx::Str{{{ptr}, {a.c}.n}}; }} }} else {{ {out.c} = {a.c}; }}")
-            if out.nullable:
-                g(f"{out.c}_n = false;")
-            if out.lone:
-                g(f"{out.c}_l = {a.l};")
-            g("}")
-            return out
+            # ASCII-only from here on: a lazy view, lowercased by its consumers
+            return V("str", a.c, a.nullable, a.lone, lower=True)
         if op == "lookup":
             a = args[0]
             out = V("u64", g.fresh("n"), False)
             ti = self.ir.tables[fn.table]
             dflt = self.ir.table_defaults[fn.table]
             g(f"u64 {out.c} = {_u64(dflt)};")
-            s = self.as_str(a, fn.spec)
+            s = self.materialize(self.as_str(a, fn.spec))
             cond = f"alive && !{s.n}" if s.nullable else "alive"
             lone = f" && !{s.l}" if s.lone else ""
             g(f"if ({cond}{lone}) {{")
@@ -739,7 +786,7 @@ class PlanCodegen:
                 if i:
                     g("h.byte(0u);")
                 if a.t == "str":
-                    g(f"h.bytes({a.c}.p, {a.c}.n);")
+                    g(f"h.bytes{'_lower' if a.lower else ''}({a.c}.p, {a.c}.n);")
                 elif a.t == "f32":
                     g(f"h.word_be({a.c});")
                 else:
@@ -769,7 +816,7 @@ class PlanCodegen:
             for i, p in enumerate(parts):
                 if i and sep:
                     g(f"for (u32 q = 0; q < {len(sep)}u; ++q) d[q] = {k}[q]; d += {len(sep)}u;")
-                g(f"fbx::str_copy(d, {p.c}); d += {p.c}.n;")
+                g(f"fbx::str_copy{'_lower' if p.lower else ''}(d, {p.c}); d += {p.c}.n;")
             g(f"{out.c} = fbx::Str{{{ptr}, {total}}};")
             if nullable:
                 g(f"{out.c}_n = false;")
@@ -780,19 +827,72 @@ class PlanCodegen:
         raise UnsupportedOnDevice(f"function {fn.spec!r}")
 
     # ------------------------------------------------------------------------------------
+    def probe(self, k: int, view: ViewIR, keys: list[V], kinds: list[Kind], row_var: str,
+              cnt_var: str, pre: str | None):
+        """Emit a hash-table probe of side table k; sets row_var / cnt_var.
+
+        With ``pre`` the first slot (tag/ref/aux) was loaded in the prologue."""
+        g = self.g
+        g(f"const fbx::Slot* T = {g.p(f'side{k}.table', 'const fbx::Slot*')};")
+        g(f"const u64 MASK = {g.p(f'side{k}.mask')};")
+        if pre:
+            g(f"u64 tag = {pre}_tag;")
+        else:
+            self.key_hash(keys, kinds, "tag")
+        g("u64 i = tag & MASK;")
+        g("bool first = true;")
+        g("while (true) {")
+        if pre:
+            g(f"u64 t = first ? {pre}_t : __ldg(&T[i].tag);")
+        else:
+            g("u64 t = __ldg(&T[i].tag);")
+        g("if (t == 0ull) break;")
+        g("if (t == tag) {")
+        if pre:
+            g(f"const u64 other = first ? (u64){pre}_ref : (u64)__ldg(&T[i].ref);")
+        else:
+            g("const u64 other = __ldg(&T[i].ref);")
+        other = [self.side_value(k, view, c, "other") for c in view.keys]
+        if pre:
+            g(f"if ({self.key_eq(keys, other)}) {{ {cnt_var} = first ? {pre}_aux : __ldg(&T[i].aux);"
+              f" {row_var} = other; break; }}")
+        else:
+            g(f"if ({self.key_eq(keys, other)}) {{ {cnt_var} = __ldg(&T[i].aux); {row_var} = other;"
+              " break; }")
+        g("}")
+        g("first = false;")
+        g("i = (i + 1) & MASK;")
+        g("}")
+
+    def prefetch(self, k: int, keys: list[V], kinds: list[Kind], name: str) -> str:
+        """Prologue: hash the raw key and load the first probe slot."""
+        g = self.g
+        g(f"u64 {name}_tag = 0, {name}_t = 0; u32 {name}_ref = 0, {name}_aux = 0;")
+        nn = " && ".join(f"!{v.n}" for v in keys if v.nullable) or "true"
+        g(f"if (inrange && {nn}) {{")
+        self.key_hash(keys, kinds, "tg")
+        g(f"{name}_tag = tg;")
+        g(f"const fbx::Slot* T = {g.p(f'side{k}.table', 'const fbx::Slot*')};")
+        g(f"const fbx::Slot* sl = T + (tg & {g.p(f'side{k}.mask')});")
+        g(f"{name}_t = __ldg(&sl->tag); {name}_ref = __ldg(&sl->ref); {name}_aux = __ldg(&sl->aux);")
+        g("}")
+        return name
+
     def pipeline_kernel(self) -> str:
         ir, g = self.ir, self.g
-        nt, ns = self.nt, self.nsort
+        nt = self.nt
         drv = ir.driver
         dk = drv.cleaned_kinds()
-        # which driver var-length columns get staged through shared memory
         needed = self.driver_needed()
         self.staged = ([c for c, k in drv.kinds.items() if k.var_length and c in needed]
                        if ir.stage_strings else [])[:16]
+        feats = sorted(ir.features.items(), key=lambda kv: (kv[1], kv[0]))
+        K = max(1, len(feats))
         g(f"constexpr int NT = {nt};")
-        g(f"constexpr int NSORT = {ns};")
         g(f"constexpr u32 SPAN_BUDGET = {self.span_cap}u;")
-        g(f'extern "C" __global__ void __launch_bounds__(NT) fbx_pipeline(const fbx_params P) {{')
+        g(f"constexpr u32 DYN_SMEM = {self.dyn_smem}u;")
+        g(f'extern "C" __global__ void __launch_bounds__(NT, {self.min_blocks}) '
+          'fbx_pipeline(const fbx_params P) {')
         g("fbx_state* ST = (fbx_state*)P.v[0];")
         g(f"u64* STATUS = {g.p('tile_status', 'u64*')};")
         g(f"const u64 ROW_LO = {g.p('row_lo')}, ROW_HI = {g.p('row_hi')};")
@@ -801,34 +901,33 @@ class PlanCodegen:
         g("extern __shared__ __align__(16) u8 dyn_smem[];")
         g("__shared__ struct {")
         g("fbx::BlockScanU32<NT> scan;")
-        g("u64 pool_base; u32 tile; u64 ex_inst, ex_signs;")
-        g("u64 keys[NSORT]; u32 vals[NSORT];")
-        g("u32 rank[NT]; u32 soff[NT]; u32 m[NT];")
+        g("u64 pool_base; u32 tile; u64 ex_inst, ex_signs; u64 bar;")
+        g("u32 rank[NT]; u32 soff[NT];")
         g("u64 span_lo[16]; u32 span_len[16];")
-        g("u64 red[NT / 32][5];")
+        g("u64 red[NT / 32][4];")
         g("} sm;")
-        g("if (threadIdx.x == 0) sm.tile = (u32)atomicAdd((unsigned long long*)&ST->tile_ticket, 1ull);")
-        g("__syncthreads();")
-        g("const u32 tile = sm.tile;")
-        g(f"const u64 chunk = CHUNK0 + tile;")
+        g("// tiles in blockIdx order: the hardware dispatches CTAs in order, so every")
+        g("// predecessor a look-back waits on is resident or done (as CUB relies on)")
+        g("const u32 tile = blockIdx.x;")
+        g("const u64 chunk = CHUNK0 + tile;")
         g(f"const u64 row0 = ROW_LO + (u64)tile * {ir.chunk}ull;")
         g(f"const u64 row_end = (row0 + {ir.chunk}ull < ROW_HI) ? row0 + {ir.chunk}ull : ROW_HI;")
         g("const u64 srow = row0 + threadIdx.x;")
-        g("const bool inrange = srow < row_end;")
+        g(f"const bool inrange = threadIdx.x < {ir.chunk}u && srow < row_end;")
         g("const u64 row = inrange ? srow : row0;")
         g("bool alive = inrange;")
         g("u32 malformed = 0, filtered = 0;")
         g(f"u32 CUR_STAGE = {STAGE['clean']}u, CUR_LAYER = 0u, CUR_RANK = 0u;")
-        # ---- stage the chunk's var-length spans into shared memory --------------
         if self.staged:
-            g("// stage the chunk's var-length spans into shared memory (one budget,")
-            g("// first-fit in column order; a span that does not fit is read from HBM)")
             ns_ = len(self.staged)
+            g("// TMA bulk-copy each var-length column's contiguous chunk span into shared")
+            g("// memory (first fit in column order; a span that does not fit stays in HBM)")
             g(f"__shared__ const u8* sm_span_buf[{ns_}];")
             g(f"__shared__ u64 sm_span_lo[{ns_}];")
             g(f"__shared__ bool sm_span_ok[{ns_}];")
             g("if (threadIdx.x == 0) {")
             g("u32 used = 0;")
+            g("fbx::mbar_init(&sm.bar, 1u);")
             for i, c in enumerate(self.staged):
                 offs = g.p(f"drv.{c}.offsets", "const u32*")
                 g("{")
@@ -839,24 +938,46 @@ class PlanCodegen:
                 g(f"sm.span_lo[{i}] = alo; sm.span_len[{i}] = ok ? (u32)(ahi - alo) : 0u;")
                 g("if (ok) used += (u32)(ahi - alo);")
                 g("}")
-            g("}")
-            g("__syncthreads();")
+            g("fbx::mbar_expect_tx(&sm.bar, used);")
             for i, c in enumerate(self.staged):
                 data = g.p(f"drv.{c}.data", "const u8*")
-                g("{")
-                g(f"const uint4* src = (const uint4*)({data} + sm.span_lo[{i}]);")
-                g(f"uint4* dst = (uint4*)sm_span_buf[{i}];")
-                g(f"for (u32 q = threadIdx.x; q < sm.span_len[{i}] / 16u; q += NT) dst[q] = __ldg(src + q);")
-                g("}")
+                g(f"if (sm.span_len[{i}]) fbx::bulk_g2s((void*)sm_span_buf[{i}], "
+                  f"{data} + sm.span_lo[{i}], sm.span_len[{i}], &sm.bar);")
+            g("}")
             g("__syncthreads();")
-        # ---- clean ----------------------------------------------------------------
+        # ---- prologue loads: every driver column this plan reads ----------------
+        g("// ---- prologue: coalesced loads of the row's fixed columns / offsets ----")
+        raw: dict[str, V] = {}
+        for name, kind in drv.kinds.items():
+            if name in needed:
+                raw[name] = self.load_driver_column(name, kind)
+        # ---- prefetch the first slot of every probe whose key is a raw column -----
+        ext_out = {e.output for e in drv.extractions}
+
+        def raw_key(cols):
+            return all(c in raw and c not in ext_out and c not in drv.fills for c in cols)
+        pre_side: dict[int, str | None] = {}
+        for k, sv in enumerate(ir.sides):
+            if raw_key(ir.join_keys):
+                pre_side[k] = self.prefetch(k, [raw[c] for c in ir.join_keys],
+                                            [dk[c] for c in ir.join_keys], f"pf{k}")
+            else:
+                pre_side[k] = None
+        bk = len(ir.sides)
+        pre_basic = None
+        if ir.basic is not None and raw_key([ir.instance_column]):
+            pre_basic = self.prefetch(bk, [raw[ir.instance_column]], [Kind.INT64], "pfb")
+        if self.staged:
+            g("fbx::mbar_wait(&sm.bar, 0u);")
+        # ---- clean ------------------------------------------------------------------
         g("// ---- clean (viewpipe.clean_views) ----")
-        vals = self.clean_view(drv, "d_", self.load_driver_column, "clean", needed, "")
-        # ---- join -----------------------------------------------------------------
+        vals = self.clean_view(drv, "d_", lambda n, k: raw[n], "clean", needed, "")
+        # ---- join -------------------------------------------------------------------
         g(f"CUR_STAGE = {STAGE['join']}u;")
         env: dict[str, V] = dict(vals)
         side_rows: list[str] = []
         self.side_rows = side_rows
+        idv0 = env.get(ir.instance_column)
         for k, sv in enumerate(ir.sides):
             g(f"// ---- join side view {sv.name!r} on {list(ir.join_keys)} ----")
             keys = [env[c] for c in ir.join_keys]
@@ -870,40 +991,50 @@ class PlanCodegen:
             self.row_error("join", "encode")
             g("}")
             g("if (alive) {")
-            self.key_hash(keys, kinds, "tag")
-            g(f"const fbx::Slot* T = {g.p(f'side{k}.table', 'const fbx::Slot*')};")
-            g(f"const u64 MASK = {g.p(f'side{k}.mask')};")
-            g("u64 i = tag & MASK; u32 cnt = 0;")
-            g("while (true) {")
-            g("u64 t = __ldg(&T[i].tag);")
-            g("if (t == 0ull) break;")
-            g("if (t == tag) {")
-            g("const u64 other = __ldg(&T[i].ref);")
-            other = [self.side_value(k, sv, c, "other") for c in ir.join_keys]
-            g(f"if ({self.key_eq(keys, other)}) {{ cnt = __ldg(&T[i].aux); {srow} = other; break; }}")
-            g("}")
-            g("i = (i + 1) & MASK;")
-            g("}")
+            g("u32 cnt = 0;")
+            self.probe(k, sv, keys, kinds, srow, "cnt", pre_side[k])
             g("if (cnt == 0u) alive = false;")
             g("else if (cnt > 1u) {")
-            idv = env.get(ir.instance_column)
-            g(f"if (!{idv.n}) {{")
+            g(f"if (!{idv0.n}) {{")
             self.row_error("merge", "multi_match")
             g("} else { alive = false; }")
             g("}")
             g("}")
             side_rows.append(srow)
             for c in sv.cleaned_kinds():
-                if c in ir.join_keys:
-                    continue
-                env[c] = ("side", k, c)  # lazily gathered
+                if c not in ir.join_keys:
+                    env[c] = ("side", k, c)
         g("u32 joined = alive ? 1u : 0u;")
         self.env = env
+        # ---- basic merge probe (side-effect free; the drop is applied later) -------
+        idv = env[ir.instance_column]
+        if ir.basic is not None:
+            g("// ---- basic-view probe on the instance id (merge_features) ----")
+            g("u64 br = 0ull; bool bhit = false;")
+            g(f"if (alive && !{idv.n}) {{")
+            g("u32 bcnt = 0;")
+            self.probe(bk, ir.basic, [idv], [Kind.INT64], "br", "bcnt", pre_basic)
+            g("bhit = bcnt != 0u;")
+            g("}")
+            for c in ir.basic.cleaned_kinds():
+                if c != ir.instance_column and c not in env:
+                    env[c] = ("side", bk, c)
+            side_rows.append("br")
+        # eager gathers: every side / basic column the DAG or emit will read
+        used_cols = set(ir.features)
+        for nd in ir.nodes:
+            used_cols |= set(nd.inputs)
+        g("// ---- gathers of joined side / basic columns (issued before the DAG) ----")
+        for c in sorted(used_cols):
+            if isinstance(env.get(c), tuple):
+                self.col(c, {})
         # ---- DAG --------------------------------------------------------------------
         g(f"CUR_STAGE = {STAGE['extract']}u;")
-        g("// ---- operator DAG in (layer, name) order ----")
+        g("// ---- operator DAG: layer order (driver-only nodes first) ----")
+        self.token_groups = self.plan_token_groups()
+        self.token_done: dict[str, V] = {}
         node_out: dict[str, V] = {}
-        for nd in ir.nodes:
+        for nd in self.node_schedule():
             if nd.role == "pre":
                 args = [self.col(nd.inputs[0], node_out)]
             elif nd.role == "post":
@@ -914,16 +1045,14 @@ class PlanCodegen:
                         for i, c in enumerate(nd.inputs)]
             node_out[nd.name] = self.node_code(nd, args)
         self.node_out = node_out
-        # u64-domain output columns must be u64 images (wrap_u64, pipeline.py:731)
         for col, domain in ir.extract_outputs:
             v = node_out[ir.producer[col]]
             if domain == "u64" and v.t == "i64":
                 g(f"if (alive && !{v.n} && (i64){v.c} < 0) {{")
                 self.row_error("extract", "value")
                 g("}")
-        # ---- uniqueness check + merge ----------------------------------------------
+        # ---- uniqueness check + merge ------------------------------------------------
         g(f"CUR_STAGE = {STAGE['merge']}u;")
-        idv = self.col(ir.instance_column, node_out)
         lab = self.col(ir.label_column, node_out)
         g("// ---- check_unique_ids over the run (pipeline.py:1071) ----")
         g(f"if (alive && !{idv.n}) {{")
@@ -941,39 +1070,15 @@ class PlanCodegen:
         g("if (old == 0ull) break;")
         g("if (old == key) {")
         self.row_error("merge", "dup_id", detail="key")
-        g("break; }")
+        g("break;")
+        g("}")
         g("i = (i + 1) & IMASK;")
         g("}")
         g("}")
         g("}")
         if ir.basic is not None:
-            bk = len(ir.sides)
-            g("// ---- merge with the basic view on the instance id ----")
-            g(f"u64 br = 0ull;")
-            g(f"if (alive && {idv.n}) alive = false;")
-            g("if (alive) {")
-            self.key_hash([idv], [Kind.INT64], "tag")
-            g(f"const fbx::Slot* T = {g.p(f'side{bk}.table', 'const fbx::Slot*')};")
-            g(f"const u64 MASK = {g.p(f'side{bk}.mask')};")
-            g("u64 i = tag & MASK; bool hit = false;")
-            g("while (true) {")
-            g("u64 t = __ldg(&T[i].tag);")
-            g("if (t == 0ull) break;")
-            g("if (t == tag) {")
-            g("const u64 other = __ldg(&T[i].ref);")
-            ov = self.side_value(bk, ir.basic, ir.instance_column, "other")
-            g(f"if (!{ov.n} && {ov.c} == {idv.c}) {{ br = other; hit = true; break; }}")
-            g("}")
-            g("i = (i + 1) & MASK;")
-            g("}")
-            g("if (!hit) alive = false;")
-            g("}")
-            for c in ir.basic.cleaned_kinds():
-                if c != ir.instance_column and c not in env:
-                    env[c] = ("side", bk, c)
-            side_rows.append("br")
-        # ---- emit ------------------------------------------------------------------
-        g(f"CUR_STAGE = {STAGE['merge']}u;")
+            g(f"if (alive && ({idv.n} || !bhit)) alive = false;  // inner merge drops it")
+        # ---- emit ---------------------------------------------------------------------
         g("// ---- emit_minibatch: sorted, de-duplicated (slot, sign) ----")
         g(f"if (alive && {lab.n}) {{")
         self.row_error("merge", "null_label")
@@ -981,26 +1086,23 @@ class PlanCodegen:
         g(f"if (alive && ({lab.c} > 1ull)) {{")
         self.row_error("merge", "label_range", detail=lab.c)
         g("}")
-        feats = sorted(ir.features.items(), key=lambda kv: (kv[1], kv[0]))
         fv = []
         for col, slot in feats:
             v = self.col(col, node_out)
             if v.t not in ("i64", "u64"):
                 raise UnsupportedOnDevice(f"feature column {col!r} is not integer-valued")
             fv.append((slot, v))
-        K = len(fv)
-        g(f"u64 fsg[{max(K, 1)}]; u32 fpres = 0u;")
-        # group equal slots: sort + dedup inside a group
+        Kf = len(fv)
+        g(f"u64 fsg[{max(Kf, 1)}]; u32 fpres = 0u;")
         i = 0
-        while i < K:
+        while i < Kf:
             j = i
-            while j < K and fv[j][0] == fv[i][0]:
+            while j < Kf and fv[j][0] == fv[i][0]:
                 j += 1
             for q in range(i, j):
                 v = fv[q][1]
                 g(f"fsg[{q}] = {v.c}; if (!{v.n}) fpres |= {1 << q}u;")
             if j - i > 1:
-                # small sorting network over the group (absent = +inf), then dedup
                 for a in range(i, j):
                     for b in range(i, j - 1 - (a - i)):
                         g(f"{{ bool pa = (fpres >> {b}) & 1u, pb = (fpres >> {b + 1}) & 1u;"
@@ -1022,43 +1124,58 @@ class PlanCodegen:
             g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
         g("digest = h.value();")
         g("}")
-        # ---- tile: sort by instance id, offsets, look-back, write -------------------
+        # ---- tile: sort by instance id, offsets, look-back, write -----------------------
         g("// ---- chunk emission order: ascending u64 instance id (viewpipe.py:521) ----")
-        g(f"const u64 myid = alive ? {idv.c} : ~0ull;")
-        g("for (u32 q = threadIdx.x; q < NSORT; q += NT) {")
-        g("sm.keys[q] = ~0ull; sm.vals[q] = 0x80000000u | q; }")
-        g("__syncthreads();")
-        g("sm.keys[threadIdx.x] = myid; sm.vals[threadIdx.x] = (alive ? 0u : 0x40000000u) | threadIdx.x;")
-        g("sm.m[threadIdx.x] = m;")
-        g("__syncthreads();")
-        g("fbx::smem_bitonic_sort2<NSORT, NT>(sm.keys, sm.vals);")
-        g("// rank + exclusive sign offsets in sorted order")
-        g("const u32 sv = sm.vals[threadIdx.x];")
-        g("const bool s_alive = (sv & 0xC0000000u) == 0u;")
-        g("const u32 s_tid = sv & 0x3FFu;")
-        g("const u32 s_m = s_alive ? sm.m[s_tid] : 0u;")
+        g(f"u64 skey = alive ? {idv.c} : ~0ull;")
+        g("u32 sval = (alive ? 0u : 0x40000000u) | threadIdx.x;")
+        g("const u32 both = sm.scan.sum((alive ? 0x10000u : 0u) + m);  // one reduction")
+        g("const u32 n_inst = both >> 16, tile_signs = both & 0xFFFFu;")
+        g("// publish the aggregate now: successors' look-back overlaps our sort")
+        g("if (threadIdx.x == 0) fbx::publish_aggregate(STATUS, tile, n_inst, tile_signs);")
+        g("sm.soff[threadIdx.x] = m;")
+        g("// the staged record spans are dead now: the sort exchanges reuse that memory")
+        g("fbx::block_sort_pairs<NT>(skey, sval, (u64*)dyn_smem, (u32*)(dyn_smem + 16 * NT));")
+        g("const bool s_alive = (sval & 0x40000000u) == 0u;")
+        g("const u32 s_tid = sval & 0x3FFu;")
+        g("const u32 s_m = s_alive ? sm.soff[s_tid] : 0u;")
         g("const u32 s_off = sm.scan.exclusive(s_m);")
-        g("const u32 tile_signs = sm.scan.total;")
         g("if (s_alive) { sm.rank[s_tid] = threadIdx.x; sm.soff[s_tid] = s_off; }")
-        g("const u32 n_inst = __syncthreads_count(alive);")
-        g("// counters + digest: one atomic per CTA")
         g("{")
         g("u64 r0 = digest, r1 = malformed, r2 = filtered, r3 = joined;")
         g("#pragma unroll")
         g("for (int d = 16; d > 0; d >>= 1) {")
         g("r0 ^= __shfl_xor_sync(0xFFFFFFFFu, r0, d); r1 += __shfl_xor_sync(0xFFFFFFFFu, r1, d);")
-        g("r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, d); r3 += __shfl_xor_sync(0xFFFFFFFFu, r3, d); }")
-        g("if ((threadIdx.x & 31u) == 0) { sm.red[threadIdx.x >> 5][0] = r0; sm.red[threadIdx.x >> 5][1] = r1;"
-          " sm.red[threadIdx.x >> 5][2] = r2; sm.red[threadIdx.x >> 5][3] = r3; }")
+        g("r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, d); r3 += __shfl_xor_sync(0xFFFFFFFFu, r3, d);")
         g("}")
+        g("if ((threadIdx.x & 31u) == 0) { sm.red[threadIdx.x >> 5][0] = r0; "
+          "sm.red[threadIdx.x >> 5][1] = r1; sm.red[threadIdx.x >> 5][2] = r2; "
+          "sm.red[threadIdx.x >> 5][3] = r3; }")
+        g("}")
+        # stage the tile's CSR in shared memory in final order (coalesced write-out)
+        g("// stage the tile's CSR in emission order in shared memory (reuses the span buffer)")
+        g("const u32 out_bytes = tile_signs * 10u + n_inst * 17u + 64u;")
+        g("const bool staged_out = out_bytes <= DYN_SMEM;")
+        g("u64* s_sign = (u64*)dyn_smem;")
+        g("u64* s_ids = s_sign + tile_signs;")
+        g("u32* st_off = (u32*)(s_ids + n_inst);")
+        g("u16* s_slot = (u16*)(st_off + n_inst);")
+        g("u8* s_lab = (u8*)(s_slot + tile_signs);")
         g("__syncthreads();")
+        g("if (staged_out && alive) {")
+        g("const u32 r = sm.rank[threadIdx.x];")
+        g("u32 so = sm.soff[threadIdx.x];")
+        g(f"s_ids[r] = {idv.c}; s_lab[r] = (u8)({lab.c}); st_off[r] = so;")
+        for q, (slot, _) in enumerate(fv):
+            g(f"if ((fpres >> {q}) & 1u) {{ s_slot[so] = (u16){slot}u; s_sign[so] = fsg[{q}]; ++so; }}")
+        g("}")
         g("if (threadIdx.x < 32u) {")
         g("u64 ei = 0, es = 0;")
         g("fbx::lookback(STATUS, tile, n_inst, tile_signs, &ei, &es);")
         g("if (threadIdx.x == 0) {")
         g("sm.ex_inst = ei; sm.ex_signs = es;")
         g("u64 r0 = 0, r1 = 0, r2 = 0, r3 = 0;")
-        g("for (int w = 0; w < NT / 32; ++w) { r0 ^= sm.red[w][0]; r1 += sm.red[w][1]; r2 += sm.red[w][2]; r3 += sm.red[w][3]; }")
+        g("for (int w = 0; w < NT / 32; ++w) { r0 ^= sm.red[w][0]; r1 += sm.red[w][1]; "
+          "r2 += sm.red[w][2]; r3 += sm.red[w][3]; }")
         g("if (r0) atomicXor((unsigned long long*)&ST->digest, (unsigned long long)r0);")
         g("atomicAdd((unsigned long long*)&ST->instances, (unsigned long long)n_inst);")
         g("atomicAdd((unsigned long long*)&ST->signs, (unsigned long long)tile_signs);")
@@ -1071,17 +1188,61 @@ class PlanCodegen:
         g(f"u64* O_IDS = {g.p('out.ids', 'u64*')}; u8* O_LAB = {g.p('out.labels', 'u8*')};")
         g(f"u64* O_OFF = {g.p('out.offsets', 'u64*')}; u16* O_SLOT = {g.p('out.slots', 'u16*')};")
         g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
-        g("if (alive) {")
-        g("const u64 pos = sm.ex_inst + sm.rank[threadIdx.x];")
-        g("u64 so = sm.ex_signs + sm.soff[threadIdx.x];")
+        g("const u64 ei = sm.ex_inst, es = sm.ex_signs;")
+        g("if (staged_out) {")
+        g("for (u32 q = threadIdx.x; q < tile_signs; q += NT) { O_SIGN[es + q] = s_sign[q]; "
+          "O_SLOT[es + q] = s_slot[q]; }")
+        g("for (u32 q = threadIdx.x; q < n_inst; q += NT) { O_IDS[ei + q] = s_ids[q]; "
+          "O_OFF[ei + q] = es + st_off[q]; O_LAB[ei + q] = s_lab[q]; }")
+        g("} else if (alive) {")
+        g("const u64 pos = ei + sm.rank[threadIdx.x];")
+        g("u64 so = es + sm.soff[threadIdx.x];")
         g(f"O_IDS[pos] = {idv.c}; O_LAB[pos] = (u8)({lab.c});")
         g("O_OFF[pos] = so;")
         for q, (slot, _) in enumerate(fv):
             g(f"if ((fpres >> {q}) & 1u) {{ O_SLOT[so] = (u16){slot}u; O_SIGN[so] = fsg[{q}]; ++so; }}")
         g("}")
-        g("if (threadIdx.x == 0) O_OFF[sm.ex_inst + n_inst] = sm.ex_signs + tile_signs;")
+        g("if (threadIdx.x == 0) O_OFF[ei + n_inst] = es + tile_signs;")
         g("}")
         return "fbx_pipeline"
+
+    def node_schedule(self) -> list[NodeIR]:
+        """Layer order, with nodes that need no joined column first (their work
+        hides the latency of the side/basic gathers)."""
+        ir = self.ir
+        side_cols = set(self.env) - set(ir.driver.cleaned_kinds())
+        dep: set[str] = set()
+        for nd in ir.nodes:
+            if nd.role == "post":
+                if nd.op in dep:
+                    dep.add(nd.name)
+                continue
+            reads = set(nd.inputs)
+            pre = ir.pre_of.get(nd.op, {}) if nd.role == "body" else {}
+            direct = {c for i, c in enumerate(nd.inputs) if i not in pre}
+            if nd.role == "pre":
+                direct = reads
+            if any(c in side_cols or (c in ir.producer and ir.producer[c] in dep)
+                   for c in direct) or any(pre[i] in dep for i in pre):
+                dep.add(nd.name)
+        first = [nd for nd in ir.nodes if nd.name not in dep]
+        return first + [nd for nd in ir.nodes if nd.name in dep]
+
+    def plan_token_groups(self) -> dict[str, tuple]:
+        """token pre-calls that split the same column on the same delimiter are
+        computed by one scan: node name -> (group key, field list)."""
+        groups: dict[tuple, list[NodeIR]] = {}
+        for nd in self.ir.nodes:
+            if nd.role == "pre" and nd.fn.op == "token" and len(nd.fn.delim.encode()) == 1:
+                groups.setdefault((nd.inputs[0], nd.fn.delim), []).append(nd)
+        out = {}
+        for key, nds in groups.items():
+            if len(nds) < 2:
+                continue
+            fields = sorted({nd.fn.index for nd in nds})
+            for nd in nds:
+                out[nd.name] = (key, fields)
+        return out
 
     def driver_needed(self) -> set[str]:
         """Driver (cleaned) columns the kernel must read."""
@@ -1123,6 +1284,13 @@ class PlanCodegen:
             if ir.stage_strings else 0
         # shared-memory span budget per staged column (bytes, multiple of 16)
         self.span_cap = SPAN_BUDGET if nstaged else 0
+        k = max(1, len(ir.features))
+        # one dynamic region, reused: staged spans -> sort exchange -> CSR staging.
+        # Sized so MIN_BLOCKS CTAs fit an SM (227 KB); a tile whose CSR does not
+        # fit is written directly.
+        per_cta = (227 * 1024) // self.min_blocks - STATIC_SMEM_EST - 1024
+        need = max(self.span_cap, 24 * self.nt, self.nt * (17 + 10 * k) + 64)
+        self.dyn_smem = max(self.span_cap, 24 * self.nt, min(need, per_cta, OUT_BUDGET)) // 16 * 16
         self.g.slot("state")  # slot 0
         side_names = []
         for k, sv in enumerate(ir.sides):
@@ -1139,7 +1307,7 @@ class PlanCodegen:
                 f"__device__ const __align__(16) u8 K_STR[] = {_c_bytes(consts + bytes(16))};",
                 *self.globals, ""]
         src = "\n".join(head + self.g.lines)
-        smem = self.span_cap
+        smem = self.dyn_smem
         del body_start
         return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes)
 

@@ -60,39 +60,43 @@ struct Fnv {
   FBX_DI void u64_be(u64 v) { word_be((u32)(v >> 32)); word_be((u32)v); }
   FBX_DI void u64_le(u64 v) { word_le((u32)v); word_le((u32)(v >> 32)); }
   FBX_DI void u16_le(u32 v) { mul(lo ^ (v & 0xFFu)); mul(lo ^ ((v >> 8) & 0xFFu)); }
-  // arbitrary byte span; reads whole aligned 32-bit words (buffers are padded
-  // to 16 bytes by the engine, so the over-read stays inside the allocation)
-  FBX_DI void bytes(const u8* p, u32 n) {
+  // arbitrary byte span.  Reads whole aligned 32-bit words and funnel-shifts
+  // them into place; a word past the last byte is only touched when the span
+  // really extends into it, so staged shared-memory spans are never overrun.
+  template <bool LOWER>
+  FBX_DI void bytes_t(const u8* p, u32 n) {
     if (n == 0) return;
-    u64 a = (u64)p;
-    u32 mis = (u32)(a & 3u);
-    const u32* wp = (const u32*)(a - mis);
-    u32 w0 = wp[0];
-    if (mis) {
-      u32 take = 4u - mis;
-      u32 w = w0 >> (mis * 8u);
-      if (take > n) take = n;
-      for (u32 i = 0; i < take; ++i) { mul(lo ^ (w & 0xFFu)); w >>= 8; }
-      n -= take;
-      ++wp;
-      if (n == 0) return;
-      w0 = wp[0];
+    const u64 a = (u64)p;
+    const u32 sh = (u32)(a & 3u) * 8u;
+    const u32* wp = (const u32*)(a & ~3ull);
+    const u32 nw = n >> 2, r = n & 3u;
+    u32 lo_w = wp[0];
+    for (u32 k = 0; k < nw; ++k) {
+      // the next word is needed when the span continues into it
+      const bool need = sh || (4u * (k + 1u) < n);
+      u32 nxt = need ? wp[k + 1] : 0u;
+      u32 w = __funnelshift_r(lo_w, nxt, sh);
+      if (LOWER) w = lower_word(w);
+      word_le(w);
+      lo_w = nxt;
     }
-    while (n >= 8u) {
-      u32 w1 = wp[1];
-      word_le(w0);
-      word_le(w1);
-      wp += 2;
-      n -= 8u;
-      if (n) w0 = wp[0];
+    if (r) {
+      u32 hi_w = (sh + r * 8u > 32u) ? wp[nw + 1] : 0u;
+      u32 w = __funnelshift_r(lo_w, hi_w, sh);
+      if (LOWER) w = lower_word(w);
+      mul(lo ^ (w & 0xFFu));
+      if (r > 1u) mul(lo ^ ((w >> 8) & 0xFFu));
+      if (r > 2u) mul(lo ^ ((w >> 16) & 0xFFu));
     }
-    if (n >= 4u) {
-      word_le(w0);
-      ++wp;
-      n -= 4u;
-      if (n) w0 = wp[0];
-    }
-    for (u32 i = 0; i < n; ++i) { mul(lo ^ (w0 & 0xFFu)); w0 >>= 8; }
+  }
+  FBX_DI void bytes(const u8* p, u32 n) { bytes_t<false>(p, n); }
+  FBX_DI void bytes_lower(const u8* p, u32 n) { bytes_t<true>(p, n); }
+  // ASCII lowercase of 4 packed bytes (all < 0x80): 'A'..'Z' -> 'a'..'z'
+  static FBX_DI u32 lower_word(u32 w) {
+    u32 ge_a = w + 0x3F3F3F3Fu;  // byte >= 0x41 -> bit 7 set
+    u32 gt_z = w + 0x25252525u;  // byte >= 0x5B -> bit 7 set
+    u32 up = ge_a & ~gt_z & 0x80808080u;
+    return w | (up >> 2);
   }
 };
 
@@ -257,6 +261,8 @@ FBX_DI void str_lower_copy(u8* dst, Str s) {
   }
 }
 
+FBX_DI void str_copy_lower(u8* dst, Str s) { str_lower_copy(dst, s); }
+
 FBX_DI void str_copy(u8* dst, Str s) {
   for (u32 i = 0; i < s.n; ++i) dst[i] = s.p[i];
 }
@@ -309,6 +315,19 @@ template <int NT>
 struct BlockScanU32 {
   u32 warp_tot[NT / 32];
   u32 total;
+  // block-wide sum (all threads get it)
+  FBX_DI u32 sum(u32 v) {
+    const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+    if (lane == 0) warp_tot[wid] = v;
+    __syncthreads();
+    u32 t = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) t += warp_tot[w];
+    __syncthreads();
+    return t;
+  }
   // exclusive scan; returns the exclusive prefix, total in `total`
   FBX_DI u32 exclusive(u32 v) {
     const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
@@ -345,6 +364,10 @@ struct BlockScanU32 {
 template <int NT>
 FBX_DI u8* pool_alloc(BlockScanU32<NT>& scan, u64* base_smem, fbx_state* st, u8* pool,
                       u64 pool_cap, u32 size, bool* exhausted) {
+  if (!__syncthreads_or(size != 0u)) {
+    *exhausted = false;
+    return nullptr;
+  }
   u32 pre = scan.exclusive(size);
   u32 total = scan.total;
   if (threadIdx.x == 0) {
@@ -416,6 +439,77 @@ FBX_DI void smem_bitonic_sort2(u64* keys, u32* vals) {
   }
 }
 
+
+// Bitonic sort of one (key, val) pair per thread, NT a power of two.  Steps
+// with partner distance < 32 exchange through warp shuffles; the few wider
+// steps go through shared memory.  On return thread i holds the i-th
+// smallest pair in (key, val) order.
+template <int NT>
+FBX_DI void block_sort_pairs(u64& key, u32& val, u64* sk, u32* sv) {
+  // sk/sv hold 2*NT entries: wide exchanges alternate between two halves so
+  // one barrier per exchange suffices (a half is rewritten only after the
+  // next exchange's barrier, by which time every reader of it is done).
+  const u32 i = threadIdx.x;
+  u32 buf = 0;
+#pragma unroll 1
+  for (u32 k = 2; k <= (u32)NT; k <<= 1) {
+#pragma unroll 1
+    for (u32 j = k >> 1; j > 0; j >>= 1) {
+      u64 ok;
+      u32 ov;
+      if (j >= 32u) {
+        sk[buf + i] = key;
+        sv[buf + i] = val;
+        __syncthreads();
+        ok = sk[buf + (i ^ j)];
+        ov = sv[buf + (i ^ j)];
+        buf ^= (u32)NT;
+      } else {
+        ok = __shfl_xor_sync(0xFFFFFFFFu, key, (int)j);
+        ov = __shfl_xor_sync(0xFFFFFFFFu, val, (int)j);
+      }
+      bool other_lt = (ok < key) || (ok == key && ov < val);
+      bool take_min = ((i & k) == 0) == ((i & j) == 0);
+      if (other_lt == take_min) {
+        key = ok;
+        val = ov;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk copy global -> shared with an mbarrier (cp.async.bulk, sm_90+)
+// ---------------------------------------------------------------------------
+FBX_DI u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+FBX_DI void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+FBX_DI void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes) : "memory");
+}
+FBX_DI void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+FBX_DI void mbar_wait(u64* bar, u32 phase) {
+  u32 done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Decoupled look-back over tiles (chunks) for the global CSR offsets.
 // status word: flag(2) | instances(28) | signs(34); flag 1 = aggregate,
@@ -433,16 +527,21 @@ FBX_DI u64 pack_status(u64 flag, u64 inst, u64 signs) {
   return (flag << 62) | ((inst & 0xFFFFFFFull) << 34) | (signs & 0x3FFFFFFFFull);
 }
 
-// Called by warp 0 only.  Returns (exclusive instances, exclusive signs).
+// Thread 0, as soon as the tile's totals are known: tile 0 publishes its
+// inclusive prefix, every other tile its aggregate (decoupled look-back).
+FBX_DI void publish_aggregate(u64* status, u32 tile, u64 inst, u64 signs) {
+  st_release(status + tile, pack_status(tile == 0 ? 2 : 1, inst, signs));
+}
+
+// Warp 0, later: sum predecessors back to the first inclusive prefix, then
+// publish this tile's inclusive prefix.  Returns the exclusive prefix.
 FBX_DI void lookback(u64* status, u32 tile, u64 inst, u64 signs, u64* ex_inst, u64* ex_signs) {
   const u32 lane = threadIdx.x & 31u;
   if (tile == 0) {
-    if (lane == 0) st_release(status, pack_status(2, inst, signs));
     *ex_inst = 0;
     *ex_signs = 0;
     return;
   }
-  if (lane == 0) st_release(status + tile, pack_status(1, inst, signs));
   u64 acc_i = 0, acc_s = 0;
   i64 base = (i64)tile - 1;
   while (true) {
@@ -454,7 +553,6 @@ FBX_DI void lookback(u64* status, u32 tile, u64 inst, u64 signs, u64* ex_inst, u
       w = pack_status(2, 0, 0);
     }
     u32 incl = __ballot_sync(0xFFFFFFFFu, (w >> 62) == 2);
-    // lanes up to and including the first inclusive one contribute
     u32 stop = incl ? (__ffs(incl) - 1) : 31u;
     u64 vi = (lane <= stop) ? ((w >> 34) & 0xFFFFFFFull) : 0;
     u64 vs = (lane <= stop) ? (w & 0x3FFFFFFFFull) : 0;

@@ -267,6 +267,8 @@ int fbx_kernel_set_max_dynamic_smem(fbx_kernel* k, int bytes) {
   // CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES = 8
   CUresult_t r = g_drv.cuFuncSetAttribute(k->fn, 8, bytes);
   if (r != 0) return fail(FBX_E_CUDA, std::string("cuFuncSetAttribute: ") + drv_str(r));
+  // (the shared-memory carveout is left to the driver: forcing 100 % starves L1,
+  //  which the side-view gathers and un-staged strings rely on -- measured)
   return FBX_OK;
 }
 

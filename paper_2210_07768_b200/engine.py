@@ -80,10 +80,13 @@ def _schema(view: ViewImage | None, path: Path, wanted, where: str) -> dict[str,
 
 
 def prepare(config: PipelineConfig, views: Mapping[str, ViewImage] | None = None,
-            basic: ViewImage | None = None, stage_strings: bool = True,
+            basic: ViewImage | None = None, stage_strings: bool | None = None,
             compile_program: bool = True) -> Prepared:
     """Validate the config against the schemas and build + compile the plan."""
+    import os
     views = views or {}
+    if stage_strings is None:
+        stage_strings = os.environ.get("FBX_STAGE", "1") != "0"
     cleaned: dict[str, dict[str, Kind]] = {}
     raw: dict[str, dict[str, Kind]] = {}
     for v in config.views:

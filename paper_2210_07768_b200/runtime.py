@@ -84,7 +84,7 @@ _CUBIN_CACHE: dict[str, bytes] = {}
 
 def compile_source(source: str, name: str = "plan.cu", options: tuple[str, ...] = ()) -> bytes:
     """NVRTC -> sm_100a cubin (host-only).  Cached per process and on disk."""
-    opts = ("-arch=sm_100a", "-std=c++17", "-lineinfo", *options)
+    opts = ("-arch=sm_100a", "-std=c++17", "-lineinfo", "-diag-suppress=177,550", *options)
     dump = os.environ.get("FBX_DUMP_SOURCE")
     if dump:  # profiling aid: keep the generated plan so ncu can import it by name
         Path(dump).write_text(source)
