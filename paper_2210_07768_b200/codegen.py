@@ -513,23 +513,20 @@ class PlanCodegen:
 
     # -- join keys ----------------------------------------------------------------------
     def key_hash(self, vals: Sequence[V], kinds: Sequence[Kind], out: str):
-        """FNV over the canonical key bytes (viewpipe.py:451-460): kind tag,
-        u32 BE length, BE payload -- identical on the build and probe sides."""
+        """Table hash of a join key (identical on the build and probe sides;
+        equality is always re-checked on the canonical values)."""
         g = self.g
         g(f"u64 {out};")
         g("{")
-        g("fbx::Fnv h;")
+        g("u64 h = 0x243F6A8885A308D3ull;")
         for v, k in zip(vals, kinds):
-            g(f"h.byte({int(k)}u);")
             if k is Kind.INT64:
-                g("h.word_be(8u);")
-                g(f"h.u64_be({v.c});")
+                g(f"h = fbx::tbl_hash_u64(h, {v.c});")
             elif k is Kind.FLOAT32:
-                g("h.word_be(4u);")
-                g(f"h.word_be({v.c});")
+                g(f"h = fbx::tbl_hash_u64(h, (u64){v.c} | (1ull << 40));")
             else:
-                g(f"h.word_be({v.c}.n); h.bytes({v.c}.p, {v.c}.n);")
-        g(f"{out} = fbx::table_tag(h.value());")
+                g(f"h = fbx::tbl_hash_bytes(h, {v.c}.p, {v.c}.n);")
+        g(f"{out} = fbx::table_tag(h);")
         g("}")
 
     def key_eq(self, a: Sequence[V], b: Sequence[V]) -> str:
@@ -1127,19 +1124,29 @@ class PlanCodegen:
         # ---- tile: sort by instance id, offsets, look-back, write -----------------------
         g("// ---- chunk emission order: ascending u64 instance id (viewpipe.py:521) ----")
         g(f"u64 skey = alive ? {idv.c} : ~0ull;")
-        g("u32 sval = (alive ? 0u : 0x40000000u) | threadIdx.x;")
-        g("const u32 both = sm.scan.sum((alive ? 0x10000u : 0u) + m);  // one reduction")
-        g("const u32 n_inst = both >> 16, tile_signs = both & 0xFFFFu;")
+        if self.nt * max(1, len(ir.features)) < 65536:
+            g("const u32 both = sm.scan.sum((alive ? 0x10000u : 0u) + m);  // one reduction")
+            g("const u32 n_inst = both >> 16, tile_signs = both & 0xFFFFu;")
+        else:
+            g("const u32 n_inst = sm.scan.sum(alive ? 1u : 0u);")
+            g("const u32 tile_signs = sm.scan.sum(m);")
         g("// publish the aggregate now: successors' look-back overlaps our sort")
         g("if (threadIdx.x == 0) fbx::publish_aggregate(STATUS, tile, n_inst, tile_signs);")
-        g("sm.soff[threadIdx.x] = m;")
-        g("// the staged record spans are dead now: the sort exchanges reuse that memory")
-        g("fbx::block_sort_pairs<NT>(skey, sval, (u64*)dyn_smem, (u32*)(dyn_smem + 16 * NT));")
-        g("const bool s_alive = (sval & 0x40000000u) == 0u;")
-        g("const u32 s_tid = sval & 0x3FFu;")
-        g("const u32 s_m = s_alive ? sm.soff[s_tid] : 0u;")
-        g("const u32 s_off = sm.scan.exclusive(s_m);")
-        g("if (s_alive) { sm.rank[s_tid] = threadIdx.x; sm.soff[s_tid] = s_off; }")
+        g("// the staged record spans are dead now: the sort reuses that memory.")
+        g("// Emitted ids are unique (else the run fails), so a row's rank is the")
+        g("// number of sorted keys below its id; dead rows sort last as ~0.")
+        g("u64* sbuf = (u64*)dyn_smem;")
+        g("const u64 sorted = fbx::bitonic_keys<NT>(skey, sbuf);")
+        g("sm.soff[threadIdx.x] = 0u;")
+        g("sbuf[2 * NT + threadIdx.x] = sorted;")
+        g("__syncthreads();")
+        g("const u32 myrank = alive ? fbx::lower_rank<NT>(sbuf + 2 * NT, skey) : 0u;")
+        g("if (alive) sm.soff[myrank] = m;")
+        g("__syncthreads();")
+        g("const u32 s_off = sm.scan.exclusive(sm.soff[threadIdx.x]);")
+        g("sm.rank[threadIdx.x] = s_off;  // sign offset by sorted position")
+        g("__syncthreads();")
+        g("const u32 myoff = alive ? sm.rank[myrank] : 0u;")
         g("{")
         g("u64 r0 = digest, r1 = malformed, r2 = filtered, r3 = joined;")
         g("#pragma unroll")
@@ -1162,8 +1169,8 @@ class PlanCodegen:
         g("u8* s_lab = (u8*)(s_slot + tile_signs);")
         g("__syncthreads();")
         g("if (staged_out && alive) {")
-        g("const u32 r = sm.rank[threadIdx.x];")
-        g("u32 so = sm.soff[threadIdx.x];")
+        g("const u32 r = myrank;")
+        g("u32 so = myoff;")
         g(f"s_ids[r] = {idv.c}; s_lab[r] = (u8)({lab.c}); st_off[r] = so;")
         for q, (slot, _) in enumerate(fv):
             g(f"if ((fpres >> {q}) & 1u) {{ s_slot[so] = (u16){slot}u; s_sign[so] = fsg[{q}]; ++so; }}")
@@ -1195,8 +1202,8 @@ class PlanCodegen:
         g("for (u32 q = threadIdx.x; q < n_inst; q += NT) { O_IDS[ei + q] = s_ids[q]; "
           "O_OFF[ei + q] = es + st_off[q]; O_LAB[ei + q] = s_lab[q]; }")
         g("} else if (alive) {")
-        g("const u64 pos = ei + sm.rank[threadIdx.x];")
-        g("u64 so = es + sm.soff[threadIdx.x];")
+        g("const u64 pos = ei + myrank;")
+        g("u64 so = es + myoff;")
         g(f"O_IDS[pos] = {idv.c}; O_LAB[pos] = (u8)({lab.c});")
         g("O_OFF[pos] = so;")
         for q, (slot, _) in enumerate(fv):
@@ -1290,7 +1297,8 @@ class PlanCodegen:
         # fit is written directly.
         per_cta = (227 * 1024) // self.min_blocks - STATIC_SMEM_EST - 1024
         need = max(self.span_cap, 24 * self.nt, self.nt * (17 + 10 * k) + 64)
-        self.dyn_smem = max(self.span_cap, 24 * self.nt, min(need, per_cta, OUT_BUDGET)) // 16 * 16
+        self.dyn_smem = max(self.span_cap, 24 * self.nt,
+                            min(need, per_cta, OUT_BUDGET)) // 16 * 16  # sort: 3*NT u64
         self.g.slot("state")  # slot 0
         side_names = []
         for k, sv in enumerate(ir.sides):

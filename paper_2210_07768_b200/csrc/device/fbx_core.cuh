@@ -479,6 +479,77 @@ FBX_DI void block_sort_pairs(u64& key, u32& val, u64* sk, u32* sv) {
   __syncthreads();
 }
 
+
+// Fully unrolled bitonic sort of one u64 key per thread (NT a power of two):
+// exchanges with partner distance < 32 use warp shuffles, wider ones go through
+// `buf` (2*NT u64, alternating halves: one barrier per exchange).  Returns the
+// key of sorted position threadIdx.x.
+template <int NT>
+FBX_DI u64 bitonic_keys(u64 key, u64* buf) {
+  const u32 i = threadIdx.x;
+  u32 b = 0;
+#pragma unroll
+  for (u32 k = 2; k <= (u32)NT; k <<= 1) {
+#pragma unroll
+    for (u32 j = k >> 1; j > 0; j >>= 1) {
+      u64 o;
+      if (j >= 32u) {
+        buf[b + i] = key;
+        __syncthreads();
+        o = buf[b + (i ^ j)];
+        b ^= (u32)NT;
+      } else {
+        o = __shfl_xor_sync(0xFFFFFFFFu, key, (int)j);
+      }
+      const bool take_min = ((i & k) == 0) == ((i & j) == 0);
+      if ((o < key) == take_min) key = o;
+    }
+  }
+  return key;
+}
+
+// Rank of `key` among the NT sorted keys in buf (number of keys < key).
+template <int NT>
+FBX_DI u32 lower_rank(const u64* sorted, u64 key) {
+  u32 lo = 0;
+#pragma unroll
+  for (u32 step = (u32)NT >> 1; step > 0; step >>= 1)
+    if (sorted[lo + step - 1] < key) lo += step;
+  return lo;
+}
+
+// Table hashing (join indexes, dictionaries): a word-at-a-time splitmix
+// mix -- any deterministic hash works, equality is always checked exactly.
+FBX_DI u64 mix64(u64 x) {
+  x ^= x >> 31;
+  x *= 0x7FB5D329728EA185ull;
+  x ^= x >> 27;
+  x *= 0x81DADEF4BC2DD44Dull;
+  x ^= x >> 33;
+  return x;
+}
+// first min(n, 8) bytes of a span as a little-endian u64 (zero padded)
+FBX_DI u64 load_prefix8(const u8* p, u32 n) {
+  if (n == 0) return 0ull;
+  const u64 a = (u64)p;
+  const u32 sh = (u32)(a & 3u) * 8u;
+  const u32* wp = (const u32*)(a & ~3ull);
+  const u32 m = n < 8u ? n : 8u;
+  const u32 last = ((u32)(a & 3u) + m - 1u) >> 2;  // last word index touched
+  u32 w0 = wp[0];
+  u32 w1 = last >= 1u ? wp[1] : 0u;
+  u32 w2 = last >= 2u ? wp[2] : 0u;
+  u32 lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+  u64 v = ((u64)hi << 32) | lo;
+  return m == 8u ? v : (v & ((1ull << (m * 8u)) - 1ull));
+}
+FBX_DI u64 tbl_hash_bytes(u64 h, const u8* p, u32 n) {
+  h = mix64(h ^ ((u64)n * 0x9E3779B97F4A7C15ull));
+  for (u32 k = 0; k < n; k += 8u) h = mix64(h ^ load_prefix8(p + k, n - k));
+  return h;
+}
+FBX_DI u64 tbl_hash_u64(u64 h, u64 v) { return mix64(h ^ mix64(v)); }
+
 // ---------------------------------------------------------------------------
 // TMA bulk copy global -> shared with an mbarrier (cp.async.bulk, sm_90+)
 // ---------------------------------------------------------------------------
@@ -586,24 +657,22 @@ struct Slot {
 
 FBX_DI u64 table_tag(u64 h) { return h | 1ull; }  // never 0
 
-// dictionary lookup (featureops.py:104-167): key bytes -> u64, default on miss
+// dictionary lookup (featureops.py:104-167): key bytes -> u64, default on miss.
+// Slot.pad holds the key's first 8 bytes, so short keys compare in one word.
 FBX_DI u64 dict_lookup(const Slot* slots, u64 mask, const u8* keyblob, Str key, u64 dflt) {
-  Fnv f;
-  f.bytes(key.p, key.n);
-  u64 tag = table_tag(f.value());
+  u64 tag = table_tag(tbl_hash_bytes(0x5DB2CEB4C16A9E87ull, key.p, key.n));
+  u64 pre = load_prefix8(key.p, key.n);
   u64 i = tag & mask;
   while (true) {
     const Slot* s = slots + i;
     u64 t = __ldg(&s->tag);
     if (t == 0) return dflt;
-    if (t == tag) {
-      u32 ref = __ldg(&s->ref), len = __ldg(&s->aux);
-      if (len == key.n) {
-        bool eq = true;
-        for (u32 k = 0; k < len; ++k)
-          if (__ldg(keyblob + ref + k) != key.p[k]) { eq = false; break; }
-        if (eq) return __ldg(&s->value);
-      }
+    if (t == tag && __ldg(&s->aux) == key.n && __ldg(&s->pad) == pre) {
+      bool eq = true;
+      u32 ref = __ldg(&s->ref);
+      for (u32 k = 8; k < key.n; ++k)
+        if (__ldg(keyblob + ref + k) != key.p[k]) { eq = false; break; }
+      if (eq) return __ldg(&s->value);
     }
     i = (i + 1) & mask;
   }
@@ -632,39 +701,73 @@ struct JPathSet {
   const u8* nseg;      // [NP]
 };
 
-FBX_DI bool j_ws(u32 c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r'; }
+FBX_DI bool j_ws(u32 c) { return c <= 0x20u && ((0x100002600ull >> c) & 1ull); }
 FBX_DI bool j_digit(u32 c) { return c - '0' < 10u; }
 FBX_DI bool j_hex(u32 c) { return (c - '0' < 10u) || ((c | 0x20u) - 'a' < 6u); }
+FBX_DI u32 j_hexval(u32 c) { return c <= '9' ? c - '0' : (c | 0x20u) - 'a' + 10u; }
 
-// scan a string starting after the opening quote; returns index of closing quote
-// or ~0 when malformed.  *esc set when any escape is present.
-FBX_DI u32 j_string(const u8* s, u32 i, u32 n, u32* esc) {
-  while (i < n) {
-    u32 c = s[i];
+// Forward reader over a byte span: loads each aligned 32-bit word once and
+// never touches a word past the span's last byte.
+struct JReader {
+  const u32* wp;
+  u32 off, n, wi, w;
+  FBX_DI void init(const u8* p, u32 len) {
+    u64 a = (u64)p;
+    off = (u32)(a & 3u);
+    wp = (const u32*)(a & ~3ull);
+    n = len;
+    wi = 0;
+    w = len ? wp[0] : 0u;
+  }
+  FBX_DI u32 at(u32 k) {  // byte k, k < n
+    u32 pos = off + k, idx = pos >> 2;
+    if (idx != wi) { wi = idx; w = wp[idx]; }
+    return (w >> ((pos & 3u) * 8u)) & 0xFFu;
+  }
+  FBX_DI u32 skip_ws(u32 i) {
+    while (i < n && j_ws(at(i))) ++i;
+    return i;
+  }
+};
+
+// JSON string body starting at i (after the quote): index of the closing quote
+// or ~0 when malformed.  Four bytes at a time until a quote, backslash or
+// control byte shows up (SWAR), then byte-wise escape validation.
+FBX_DI u32 j_string(JReader& r, u32 i, u32* esc) {
+  while (i < r.n) {
+    u32 pos = r.off + i, idx = pos >> 2;
+    if (idx != r.wi) { r.wi = idx; r.w = r.wp[idx]; }
+    u32 sh = (pos & 3u) * 8u;
+    u32 v = r.w >> sh;
+    u32 avail = 4u - (pos & 3u), left = r.n - i;
+    u32 m = avail < left ? avail : left;
+    u32 q = v ^ 0x22222222u, b = v ^ 0x5C5C5C5Cu;
+    u32 sp = (((q - 0x01010101u) & ~q) | ((b - 0x01010101u) & ~b) | ((v - 0x20202020u) & ~v)) &
+             0x80808080u;
+    if (m < 4u) sp &= (1u << (m * 8u)) - 1u;
+    if (sp == 0u) { i += m; continue; }
+    i += (u32)(__ffs(sp) - 1) >> 3;
+    u32 c = r.at(i);
     if (c == '"') return i;
     if (c < 0x20u) return ~0u;
-    if (c == '\\') {
-      *esc = 1;
-      if (i + 1 >= n) return ~0u;
-      u32 e = s[i + 1];
-      if (e == 'u') {
-        if (i + 5 >= n) return ~0u;
-        if (!(j_hex(s[i + 2]) && j_hex(s[i + 3]) && j_hex(s[i + 4]) && j_hex(s[i + 5]))) return ~0u;
-        i += 6;
-      } else if (e == '"' || e == '\\' || e == '/' || e == 'b' || e == 'f' || e == 'n' ||
-                 e == 'r' || e == 't') {
-        i += 2;
-      } else {
+    // backslash escape
+    *esc = 1;
+    if (i + 1 >= r.n) return ~0u;
+    u32 e = r.at(i + 1);
+    if (e == 'u') {
+      if (i + 5 >= r.n) return ~0u;
+      if (!(j_hex(r.at(i + 2)) && j_hex(r.at(i + 3)) && j_hex(r.at(i + 4)) && j_hex(r.at(i + 5))))
         return ~0u;
-      }
+      i += 6;
+    } else if (e == '"' || e == '\\' || e == '/' || e == 'b' || e == 'f' || e == 'n' || e == 'r' ||
+               e == 't') {
+      i += 2;
     } else {
-      ++i;
+      return ~0u;
     }
   }
   return ~0u;
 }
-
-FBX_DI u32 j_hexval(u32 c) { return c <= '9' ? c - '0' : (c | 0x20u) - 'a' + 10u; }
 
 // decode the escaped JSON string body s[b, e) into dst (UTF-8, lone surrogates
 // as WTF-8); returns the byte length, *lone set if a lone surrogate occurs.
@@ -721,14 +824,13 @@ FBX_DI u32 j_unescape(const u8* s, u32 b, u32 e, u8* dst, u32* lone) {
 }
 
 // key comparison against a path segment, decoding escapes when present
-FBX_DI bool j_key_eq(const u8* s, u32 b, u32 e, u32 esc, const u8* seg, u32 slen) {
+FBX_DI bool j_key_eq(JReader& r, const u8* s, u32 b, u32 e, u32 esc, const u8* seg, u32 slen) {
   if (!esc) {
     if (e - b != slen) return false;
     for (u32 k = 0; k < slen; ++k)
-      if (s[b + k] != seg[k]) return false;
+      if (r.at(b + k) != seg[k]) return false;
     return true;
   }
-  // slow path: decode into a small local buffer (segments are short)
   u8 tmp[64];
   u32 lone = 0;
   u32 dl = j_unescape(s, b, e, nullptr, &lone);
@@ -740,29 +842,31 @@ FBX_DI bool j_key_eq(const u8* s, u32 b, u32 e, u32 esc, const u8* seg, u32 slen
   return true;
 }
 
-// number at s[i]; returns end index (or ~0 malformed); *type J_INT / J_FLOAT,
+// number at i; returns end index (or ~0 malformed); *type J_INT / J_FLOAT,
 // *digits = number of integer digits (for the 4300-digit int limit).
-FBX_DI u32 j_number(const u8* s, u32 i, u32 n, u32* type, u32* digits) {
+FBX_DI u32 j_number(JReader& r, u32 i, u32* type, u32* digits) {
+  const u32 n = r.n;
   u32 st = i;
-  if (i < n && s[i] == '-') ++i;
-  if (i >= n || !j_digit(s[i])) return ~0u;
-  if (s[i] == '0') {
+  bool neg = r.at(i) == '-';
+  if (neg) ++i;
+  if (i >= n || !j_digit(r.at(i))) return ~0u;
+  if (r.at(i) == '0') {
     ++i;
   } else {
-    while (i < n && j_digit(s[i])) ++i;
+    while (i < n && j_digit(r.at(i))) ++i;
   }
-  *digits = i - st - (s[st] == '-' ? 1u : 0u);
+  *digits = i - st - (neg ? 1u : 0u);
   *type = J_INT;
-  if (i + 1 < n && s[i] == '.' && j_digit(s[i + 1])) {
+  if (i + 1 < n && r.at(i) == '.' && j_digit(r.at(i + 1))) {
     i += 2;
-    while (i < n && j_digit(s[i])) ++i;
+    while (i < n && j_digit(r.at(i))) ++i;
     *type = J_FLOAT;
   }
-  if (i < n && (s[i] | 0x20u) == 'e') {
+  if (i < n && (r.at(i) | 0x20u) == 'e') {
     u32 k = i + 1;
-    if (k < n && (s[k] == '+' || s[k] == '-')) ++k;
-    if (k < n && j_digit(s[k])) {
-      while (k < n && j_digit(s[k])) ++k;
+    if (k < n && (r.at(k) == '+' || r.at(k) == '-')) ++k;
+    if (k < n && j_digit(r.at(k))) {
+      while (k < n && j_digit(r.at(k))) ++k;
       i = k;
       *type = J_FLOAT;
     }
@@ -770,40 +874,38 @@ FBX_DI u32 j_number(const u8* s, u32 i, u32 n, u32* type, u32* digits) {
   return i;
 }
 
-FBX_DI bool j_lit(const u8* s, u32 i, u32 n, const char* w, u32 wl) {
-  if (i + wl > n) return false;
+FBX_DI bool j_lit(JReader& r, u32 i, const char* w, u32 wl) {
+  if (i + wl > r.n) return false;
   for (u32 k = 0; k < wl; ++k)
-    if (s[i + k] != (u8)w[k]) return false;
+    if (r.at(i + k) != (u8)w[k]) return false;
   return true;
 }
 
-// Validate the whole document and extract the NP paths.  Returns JS_*.
+// Validate the whole document (CPython json.loads, strict) and extract the NP
+// dot paths.  Inlined so the leaves live in registers.  Returns JS_*.
 template <int NP>
-FBX_NI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
+FBX_DI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
 #pragma unroll
   for (int p = 0; p < NP; ++p) leaf[p] = JLeaf{0, 0, J_MISSING, 0};
-  const u8* s = doc.p;
+  JReader r;
+  r.init(doc.p, doc.n);
   const u32 n = doc.n;
   u64 kind_stack = 0;  // bit d: container at depth d+1 is an object
   u32 depth = 0;
   u64 live = 0;        // byte d (d < 8): paths live for the object at depth d+1
-  u32 i = 0;
-  while (i < n && j_ws(s[i])) ++i;
-  // current value context: paths for which this value is a leaf / may descend
+  u32 i = r.skip_ws(0);
   u32 leafm = 0, descm = (1u << NP) - 1u;
   bool top = true;
   while (true) {
-    // ---- parse one value at s[i] ----
     if (i >= n) return JS_MALFORMED;
-    u32 c = s[i];
+    u32 c = r.at(i);
     u32 vb = i, ve, vt, vesc = 0;
-    bool opened = false;
     if (c == '{' || c == '[') {
       if (depth >= 64u) return JS_DEEP;
       bool obj = (c == '{');
       if (obj) kind_stack |= (1ull << depth); else kind_stack &= ~(1ull << depth);
       ++depth;
-      // leaf of a container type for the paths ending here
+#pragma unroll
       for (int p = 0; p < NP; ++p)
         if (leafm & (1u << p)) leaf[p] = JLeaf{vb, vb, J_CONTAINER, 0};
       u32 childlive = (obj && depth <= 8u) ? (top ? ((1u << NP) - 1u) : descm) : 0u;
@@ -811,71 +913,64 @@ FBX_NI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
         live &= ~(0xFFull << ((depth - 1) * 8));
         live |= (u64)(childlive & 0xFFu) << ((depth - 1) * 8);
       }
-      ++i;
-      while (i < n && j_ws(s[i])) ++i;
-      if (i < n && s[i] == (obj ? '}' : ']')) {
+      i = r.skip_ws(i + 1);
+      top = false;
+      if (i < n && r.at(i) == (obj ? '}' : ']')) {
         ++i;
         --depth;
-        opened = false;  // empty container: value complete
-      } else {
-        opened = true;
+        goto after_value;
       }
-      top = false;
-      if (opened) {
-        if (obj) goto member_key;
-        leafm = 0;
-        descm = 0;
-        continue;  // first array element
-      }
-      goto after_value;
+      if (obj) goto member_key;
+      leafm = 0;
+      descm = 0;
+      continue;  // first array element
     }
     top = false;
     if (c == '"') {
-      u32 e = j_string(s, i + 1, n, &vesc);
+      u32 e = j_string(r, i + 1, &vesc);
       if (e == ~0u) return JS_MALFORMED;
       vb = i + 1;
       ve = e;
       vt = J_STRING;
       i = e + 1;
     } else if (c == '-' || j_digit(c)) {
-      if (c == '-' && j_lit(s, i, n, "-Infinity", 9)) {
+      if (c == '-' && j_lit(r, i, "-Infinity", 9)) {
         vt = J_NEGINF;
         i += 9;
         ve = i;
       } else {
         u32 digits = 0;
-        u32 e = j_number(s, i, n, &vt, &digits);
+        u32 e = j_number(r, i, &vt, &digits);
         if (e == ~0u) return JS_MALFORMED;
         if (vt == J_INT && digits > 4300u) return JS_BIGINT;
         ve = e;
         i = e;
       }
-    } else if (c == 't' && j_lit(s, i, n, "true", 4)) {
+    } else if (c == 't' && j_lit(r, i, "true", 4)) {
       vt = J_TRUE; i += 4; ve = i;
-    } else if (c == 'f' && j_lit(s, i, n, "false", 5)) {
+    } else if (c == 'f' && j_lit(r, i, "false", 5)) {
       vt = J_FALSE; i += 5; ve = i;
-    } else if (c == 'n' && j_lit(s, i, n, "null", 4)) {
+    } else if (c == 'n' && j_lit(r, i, "null", 4)) {
       vt = J_NULL; i += 4; ve = i;
-    } else if (c == 'N' && j_lit(s, i, n, "NaN", 3)) {
+    } else if (c == 'N' && j_lit(r, i, "NaN", 3)) {
       vt = J_NAN; i += 3; ve = i;
-    } else if (c == 'I' && j_lit(s, i, n, "Infinity", 8)) {
+    } else if (c == 'I' && j_lit(r, i, "Infinity", 8)) {
       vt = J_POSINF; i += 8; ve = i;
     } else {
       return JS_MALFORMED;
     }
+#pragma unroll
     for (int p = 0; p < NP; ++p)
       if (leafm & (1u << p)) leaf[p] = JLeaf{vb, ve, vt, vesc};
   after_value:
-    // ---- after a complete value: separators / closers ----
     while (true) {
-      while (i < n && j_ws(s[i])) ++i;
+      i = r.skip_ws(i);
       if (depth == 0) return i == n ? JS_OK : JS_MALFORMED;
       if (i >= n) return JS_MALFORMED;
       bool obj = (kind_stack >> (depth - 1)) & 1ull;
-      u32 ch = s[i];
+      u32 ch = r.at(i);
       if (ch == ',') {
-        ++i;
-        while (i < n && j_ws(s[i])) ++i;
+        i = r.skip_ws(i + 1);
         if (obj) goto member_key;
         leafm = 0;
         descm = 0;
@@ -889,32 +984,30 @@ FBX_NI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
       return JS_MALFORMED;
     }
   member_key : {
-    // s[i] must be a key string
-    if (i >= n || s[i] != '"') return JS_MALFORMED;
+    if (i >= n || r.at(i) != '"') return JS_MALFORMED;
     u32 kesc = 0;
-    u32 ke = j_string(s, i + 1, n, &kesc);
+    u32 ke = j_string(r, i + 1, &kesc);
     if (ke == ~0u) return JS_MALFORMED;
     u32 kb = i + 1;
-    i = ke + 1;
-    while (i < n && j_ws(s[i])) ++i;
-    if (i >= n || s[i] != ':') return JS_MALFORMED;
-    ++i;
-    while (i < n && j_ws(s[i])) ++i;
-    // which live paths does this key continue?
+    i = r.skip_ws(ke + 1);
+    if (i >= n || r.at(i) != ':') return JS_MALFORMED;
+    i = r.skip_ws(i + 1);
     leafm = 0;
     descm = 0;
     if (depth <= 8u) {
       u32 lv = (u32)((live >> ((depth - 1) * 8)) & 0xFFull);
       u32 sidx = depth - 1;
-      for (int p = 0; p < NP; ++p) {
-        if (!(lv & (1u << p))) continue;
-        u32 ns = ps.nseg[p];
-        if (sidx >= ns) continue;
-        u32 off = ps.seg_off[p * 8 + sidx], sl = ps.seg_len[p * 8 + sidx];
-        if (!j_key_eq(s, kb, ke, kesc, ps.seg + off, sl)) continue;
-        // a later duplicate key replaces the earlier value: clear the result
-        leaf[p] = JLeaf{0, 0, J_MISSING, 0};
-        if (sidx + 1 == ns) leafm |= (1u << p); else descm |= (1u << p);
+      if (lv) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          if (!(lv & (1u << p))) continue;
+          u32 ns = ps.nseg[p];
+          if (sidx >= ns) continue;
+          u32 off = ps.seg_off[p * 8 + sidx], sl = ps.seg_len[p * 8 + sidx];
+          if (!j_key_eq(r, doc.p, kb, ke, kesc, ps.seg + off, sl)) continue;
+          leaf[p] = JLeaf{0, 0, J_MISSING, 0};  // a later duplicate key replaces the value
+          if (sidx + 1 == ns) leafm |= (1u << p); else descm |= (1u << p);
+        }
       }
     }
     continue;
@@ -923,7 +1016,6 @@ FBX_NI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
     continue;
   }
 }
-
 
 // JSON leaf -> Float32 bits (viewpipe.py:278-279: canon_f32(float(value))).
 // 0 = ok, 1 = not a number (-> null), 2 = OverflowError (struct.pack 'f'),

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "fbx.h"
+#include "device/fbx_core.cuh"
 
 namespace {
 
@@ -96,19 +97,7 @@ __global__ void k_state_reset(fbx_state* st, unsigned long long* status, size_t 
   for (; i < n; i += (size_t)gridDim.x * blockDim.x) status[i] = 0ull;
 }
 
-struct Slot {
-  unsigned long long tag;
-  unsigned int ref;
-  unsigned int aux;
-  unsigned long long value;
-  unsigned long long pad;
-};
-
-__device__ __forceinline__ unsigned long long fnv_bytes(const unsigned char* p, unsigned int n) {
-  unsigned long long h = 0xCBF29CE484222325ull;
-  for (unsigned int i = 0; i < n; ++i) h = (h ^ p[i]) * 0x100000001B3ull;
-  return h;
-}
+using fbx::Slot;
 
 __global__ void k_dict_init(Slot* slots, unsigned long long cap) {
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < cap;
@@ -129,13 +118,14 @@ __global__ void k_dict_insert(Slot* slots, unsigned long long mask, const unsign
   for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (unsigned long long)gridDim.x * blockDim.x) {
     unsigned int b = offs[k], len = offs[k + 1] - b;
-    unsigned long long tag = fnv_bytes(blob + b, len) | 1ull;
+    unsigned long long tag = fbx::table_tag(fbx::tbl_hash_bytes(0x5DB2CEB4C16A9E87ull, blob + b, len));
     unsigned long long i = tag & mask;
     while (true) {
       unsigned long long old = atomicCAS(&slots[i].tag, 0ull, tag);
       if (old == 0ull) {
         slots[i].ref = b;
         slots[i].value = vals[k];
+        slots[i].pad = fbx::load_prefix8(blob + b, len);
         __threadfence();
         atomicExch(&slots[i].aux, len);
         break;
