@@ -11,6 +11,7 @@ files come from its own ``gen_corpus``.  Python version is recorded.
 
 from __future__ import annotations
 
+import hashlib
 import json
 import platform
 import sys
@@ -74,7 +75,9 @@ def main():
     with tempfile.TemporaryDirectory() as tmp:
         for rows, users, seed, views in CORPORA:
             dest = Path(tmp) / f"c{rows}_{seed}_{views}"
-            gen_corpus(dest, rows=rows, users=users, seed=seed, views=views)
+            files = gen_corpus(dest, rows=rows, users=users, seed=seed, views=views)
+            out.setdefault("corpus_sha256", {})[f"{rows}_{users}_{seed}_{views}"] = {
+                k: hashlib.sha256(Path(v).read_bytes()).hexdigest() for k, v in files.items()}
             write_lookup_tables(dest, users)
             dags = DAGS if views == 2 else ("default",)
             for dag in dags:

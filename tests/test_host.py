@@ -1,0 +1,125 @@
+"""CPU: corpus, FBXC format, config/planner semantics, code generation + NVRTC,
+and the C-ABI library surface (no GPU calls)."""
+
+from __future__ import annotations
+
+import hashlib
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, corpus
+
+from paper_2210_07768_b200 import codegen, engine
+from paper_2210_07768_b200.columns import (ChecksumError, ColumnImage, Kind, ViewImage, read_view,
+                                           write_view)
+from paper_2210_07768_b200.config import ConfigError, UnsupportedOnDevice, config_from_dict, load_config
+from paper_2210_07768_b200.corpus import gen_corpus
+from paper_2210_07768_b200.opgraph import expand_call_graph, layer_schedule
+from paper_2210_07768_b200.workloads import DAGS, workload_config
+
+
+def test_corpus_is_byte_identical_to_reference(goldens, tmp_path):
+    for key, want in goldens["corpus_sha256"].items():
+        rows, users, seed, views = map(int, key.split("_"))
+        files = gen_corpus(tmp_path / key, rows=rows, users=users, seed=seed, views=views)
+        got = {k: hashlib.sha256(Path(v).read_bytes()).hexdigest() for k, v in files.items()}
+        assert got == want, key
+
+
+def test_fbxc_roundtrip_and_crc(tmp_path):
+    v = ViewImage.from_pydict([("a", Kind.INT64), ("s", Kind.UTF8), ("f", Kind.FLOAT32)],
+                              {"a": [1, None, -3], "s": ["x", "é", None], "f": [0.5, None, 2.0]})
+    p = write_view(v, tmp_path / "v.fbxc")
+    r = read_view(p)
+    for c in ("a", "s", "f"):
+        assert r.columns[c].to_pylist() == v.columns[c].to_pylist()
+    raw = bytearray(p.read_bytes())
+    raw[-10] ^= 0xFF
+    p.write_bytes(bytes(raw))
+    with pytest.raises(ChecksumError):
+        read_view(p)
+
+
+# node / layer counts of the Appendix-B DAGs
+@pytest.mark.parametrize("dag,nodes,layers", [("default", 7, 2), ("fig4", 8, 3),
+                                              ("sign_heavy", 18, 2), ("cross_heavy", 18, 3),
+                                              ("lookup_heavy", 24, 4)])
+def test_layer_schedule_matches_reference_shape(dag, nodes, layers):
+    c, d = corpus(2000, 300, 7)
+    cfg = config_from_dict(workload_config(dag), d)
+    dg = expand_call_graph(cfg.operators)
+    plan = layer_schedule(dg)
+    assert (len(dg.nodes), len(plan.layers)) == (nodes, layers)
+
+
+def test_config_errors_mirror_reference(tmp_path):
+    c, d = corpus(2000, 300, 7)
+    raw = workload_config("default")
+    raw["operators"][0]["body"]["fn"] = "nope:1"
+    with pytest.raises(ConfigError):
+        engine.prepare(config_from_dict(raw, d), compile_program=False)
+    raw = workload_config("default")
+    raw["emit"]["features"]["missing_col"] = 3
+    with pytest.raises(ConfigError):
+        engine.prepare(config_from_dict(raw, d), compile_program=False)
+    raw = workload_config("default")
+    raw["views"][0]["clean"]["filter"] = "nosuch < 3"
+    with pytest.raises(ConfigError):
+        engine.prepare(config_from_dict(raw, d), compile_program=False)
+    (tmp_path / "bad.json").write_text("{")
+    with pytest.raises(ConfigError):
+        load_config(tmp_path / "bad.json")
+
+
+def test_unsupported_constructs_are_plan_time_errors():
+    c, d = corpus(2000, 300, 7)
+    raw = workload_config("default")
+    raw["views"][0]["clean"]["extract"].append(
+        {"source": "meta", "path": "u", "output": "u_json", "kind": "json"})
+    with pytest.raises(UnsupportedOnDevice):
+        engine.prepare(config_from_dict(raw, d), compile_program=False)
+    raw = workload_config("default")
+    raw["operators"].append({"name": "sc", "inputs": ["score"], "outputs": ["sc"],
+                             "pre": [{"fn": "lower"}], "body": {"fn": "hash:90"}})
+    with pytest.raises(UnsupportedOnDevice):  # str(float) = Python repr
+        engine.prepare(config_from_dict(raw, d), compile_program=False)
+
+
+@pytest.mark.parametrize("dag", DAGS)
+def test_plans_compile_for_sm100a(dag):
+    """Every Appendix-B plan generates and NVRTC-compiles to an sm_100a cubin."""
+    c, d = corpus(2000, 300, 7)
+    p = engine.prepare(config_from_dict(workload_config(dag), d),
+                       {"user_events": c.driver, "user_profile": c.profile}, c.basic)
+    assert p.cubin[:4] == b"\x7fELF"
+    assert "fbx_pipeline" in p.program.kernels
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    from paper_2210_07768_b200 import runtime
+    L = runtime.lib()
+    declared = set()
+    for h in (ROOT / "include").glob("*.h"):
+        declared |= set(re.findall(r"\b(fbx_\w+)\s*\(", h.read_text()))
+    assert declared, "no declarations found"
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert L.fbx_version().decode().startswith("fbx")
+    assert isinstance(L.fbx_last_error(), bytes)
+    assert ctypes.sizeof(ctypes.c_uint64) * 384 == 3072  # fbx_params
+
+
+def test_engine_refuses_cpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    c, d = corpus(2000, 300, 7)
+    p = engine.prepare(config_from_dict(workload_config("default"), d),
+                       {"user_events": c.driver, "user_profile": c.profile}, c.basic,
+                       compile_program=False)
+    with pytest.raises(RuntimeError):
+        engine.Engine(p, {"user_events": c.driver, "user_profile": c.profile}, c.basic)
