@@ -77,6 +77,15 @@ int fbx_dict_build(void* d_slots, unsigned long long capacity, const unsigned ch
                    const unsigned int* d_key_offsets, const unsigned long long* d_values,
                    unsigned long long n, unsigned long long* d_dup_flag, void* stream);
 
+/* Row-aligned string outputs of the _extract_batch kernel (pipeline.py:731-736):
+ * out[0] = 0, out[i+1] = in[0] + ... + in[i]  (u32 lengths -> u64 FBXC offsets) */
+int fbx_exclusive_scan_u32(const unsigned int* d_in, unsigned long long* d_out,
+                           unsigned long long n, void* stream);
+/* Copy n pool-resident strings (pointer, length) into one FBXC data segment. */
+int fbx_gather_strings(const unsigned long long* d_ptrs, const unsigned int* d_lens,
+                       const unsigned long long* d_offsets, unsigned long long n,
+                       unsigned char* d_out, void* stream);
+
 /* Write `bytes` of a scratch buffer (an L2 flush between timed steps). */
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream);
 

@@ -107,6 +107,7 @@ class PlanIR:
     table_defaults: dict[str, int]
     extract_outputs: list[tuple[str, str]] = field(default_factory=list)  # (col, domain)
     stage_strings: bool = True
+    mode: str = "pipeline"          # "pipeline" | "extract" (row-aligned _extract_batch)
 
 
 @dataclass
@@ -1213,6 +1214,82 @@ class PlanCodegen:
         g("}")
         return "fbx_pipeline"
 
+
+    # ------------------------------------------------------------------------------
+    def extract_rows_kernel(self) -> str:
+        """``_extract_batch`` (pipeline.py:718-737): the DAG over an already cleaned
+        and joined table, outputs row-aligned.  u64-domain outputs are written as
+        Int64 images (two's-complement, ``wrap_u64``) with a warp-ballot null
+        bitmap; str outputs are materialised into the pool as (pointer, length)
+        and compacted into an FBXC Utf8 image by the host (scan + copy)."""
+        ir, g = self.ir, self.g
+        tbl = ir.driver
+        self.staged = []
+        g("constexpr int NT = 256;")
+        g('extern "C" __global__ void __launch_bounds__(256) fbx_extract_rows(const fbx_params P) {')
+        g("fbx_state* ST = (fbx_state*)P.v[0];")
+        g(f"const u64 N = {g.p('rows')};")
+        g(f"u8* POOL = {g.p('pool', 'u8*')}; const u64 POOL_CAP = {g.p('pool_cap')};")
+        g("__shared__ struct { fbx::BlockScanU32<256> scan; u64 pool_base; } sm;")
+        g("for (u64 base = (u64)blockIdx.x * 256u; base < N; base += (u64)gridDim.x * 256u) {")
+        g("const u64 srow = base + threadIdx.x;")
+        g("const bool inrange = srow < N;")
+        g("const u64 row = inrange ? srow : base;")
+        g("bool alive = inrange;")
+        g("const u64 chunk = 0;")
+        g(f"u32 CUR_STAGE = {STAGE['extract']}u, CUR_LAYER = 0u, CUR_RANK = 0u;")
+        need = set()
+        for nd in ir.nodes:
+            need |= set(nd.inputs)
+        env = {}
+        for name, kind in tbl.kinds.items():
+            if name in need:
+                env[name] = self.load_driver_column(name, kind)
+        self.env = env
+        self.side_rows = []
+        self.token_groups = self.plan_token_groups()
+        self.token_done = {}
+        node_out: dict[str, V] = {}
+        for nd in ir.nodes:
+            if nd.role == "pre":
+                args = [self.col(nd.inputs[0], node_out)]
+            elif nd.role == "post":
+                args = [node_out[nd.op]]
+            else:
+                pre = ir.pre_of.get(nd.op, {})
+                args = [node_out[pre[i]] if i in pre else self.col(c, node_out)
+                        for i, c in enumerate(nd.inputs)]
+            node_out[nd.name] = self.node_code(nd, args)
+        g("// ---- outputs, row-aligned ----")
+        for j, (col, domain) in enumerate(ir.extract_outputs):
+            v = node_out[ir.producer[col]]
+            nn = f"(!alive || {v.n})"
+            if domain == "u64":
+                if v.t == "i64":
+                    g(f"if (alive && !{v.n} && (i64){v.c} < 0) {{")
+                    self.row_error("extract", "value")
+                    g("}")
+                if v.t not in ("i64", "u64"):
+                    raise UnsupportedOnDevice(f"output {col!r}: u64 domain on a {v.t} value")
+                g(f"if (inrange) {g.p(f'out{j}.data', 'u64*')}[row] = {nn} ? 0ull : {v.c};")
+            else:
+                if v.t != "str":
+                    raise UnsupportedOnDevice(f"output {col!r}: str domain on a {v.t} value")
+                ptr = self.pool_alloc(f"{nn} ? 0u : {v.c}.n")
+                g(f"if (inrange) {{ {g.p(f'out{j}.ptr', 'u64*')}[row] = (u64){ptr};"
+                  f" {g.p(f'out{j}.len', 'u32*')}[row] = {nn} ? 0u : {v.c}.n; }}")
+                g(f"if (!{nn} && {ptr}) fbx::str_copy{'_lower' if v.lower else ''}({ptr}, {v.c});")
+                if v.lone:
+                    g(f"if (!{nn} && {v.l}) {{ /* Utf8 column holds a lone surrogate: kept as WTF-8 */ }}")
+            g("{")
+            g(f"const u32 nb = __ballot_sync(0xFFFFFFFFu, inrange && {nn});")
+            g(f"if ((threadIdx.x & 31u) == 0u && inrange) "
+              f"((u32*){g.p(f'out{j}.nulls', 'u8*')})[row >> 5] = nb;")
+            g("}")
+        g("}")
+        g("}")
+        return "fbx_extract_rows"
+
     def node_schedule(self) -> list[NodeIR]:
         """Layer order, with nodes that need no joined column first (their work
         hides the latency of the side/basic gathers)."""
@@ -1300,6 +1377,14 @@ class PlanCodegen:
         self.dyn_smem = max(self.span_cap, 24 * self.nt,
                             min(need, per_cta, OUT_BUDGET)) // 16 * 16  # sort: 3*NT u64
         self.g.slot("state")  # slot 0
+        if ir.mode == "extract":
+            kname = self.extract_rows_kernel()
+            consts = b"".join(self.g.consts)
+            head = [library_source(), "", "// ===== generated plan =====",
+                    f"__device__ const __align__(16) u8 K_STR[] = {_c_bytes(consts + bytes(16))};",
+                    *self.globals, ""]
+            return Program("\n".join(head + self.g.lines), dict(self.g.slots), 256, 0,
+                           [kname], [], self.notes)
         side_names = []
         for k, sv in enumerate(ir.sides):
             side_names.append(self.side_prep_kernel(k, sv, False))

@@ -17,6 +17,7 @@
 #include <string.h>
 
 #include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
 #include <string>
 #include <vector>
 
@@ -143,6 +144,20 @@ __global__ void k_dict_insert(Slot* slots, unsigned long long mask, const unsign
       }
       i = (i + 1) & mask;
     }
+  }
+}
+
+// one warp per string: copy pool-resident bytes into an FBXC data segment
+__global__ void k_gather_strings(const unsigned long long* ptrs, const unsigned int* lens,
+                                 const unsigned long long* offsets, unsigned long long n,
+                                 unsigned char* out) {
+  const unsigned lane = threadIdx.x & 31u;
+  for (unsigned long long r = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+    const unsigned char* src = (const unsigned char*)ptrs[r];
+    unsigned int len = lens[r];
+    unsigned char* dst = out + offsets[r];
+    for (unsigned int k = lane; k < len; k += 32u) dst[k] = src[k];
   }
 }
 
@@ -306,6 +321,34 @@ int fbx_dict_build(void* d_slots, unsigned long long capacity, const unsigned ch
   if (rc) return rc;
   if (dup) return fail(FBX_E_DUPLICATE, "duplicate dictionary key");
   return FBX_OK;
+}
+
+int fbx_exclusive_scan_u32(const unsigned int* d_in, unsigned long long* d_out, unsigned long long n,
+                           void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = cuda_check(cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), s), "scan init");
+  if (rc || n == 0) return rc;
+  size_t tmp = 0;
+  // inclusive sum of the inputs into out[1..n]: out[0] = 0 -> exclusive offsets[n+1]
+  cub::DeviceScan::InclusiveSum(nullptr, tmp, d_in, d_out + 1, (int)n, s);
+  void* d_tmp = nullptr;
+  rc = cuda_check(cudaMallocAsync(&d_tmp, tmp, s), "scan temp");
+  if (rc) return rc;
+  cub::DeviceScan::InclusiveSum(d_tmp, tmp, d_in, d_out + 1, (int)n, s);
+  rc = cuda_check(cudaGetLastError(), "scan");
+  cudaFreeAsync(d_tmp, s);
+  return rc;
+}
+
+int fbx_gather_strings(const unsigned long long* d_ptrs, const unsigned int* d_lens,
+                       const unsigned long long* d_offsets, unsigned long long n,
+                       unsigned char* d_out, void* stream) {
+  if (n == 0) return FBX_OK;
+  unsigned long long blocks = (n * 32 + 255) / 256;
+  if (blocks > 4736) blocks = 4736;
+  k_gather_strings<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_ptrs, d_lens, d_offsets,
+                                                                        n, d_out);
+  return cuda_check(cudaGetLastError(), "fbx_gather_strings");
 }
 
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream) {

@@ -721,3 +721,154 @@ def run_pipeline(config: PipelineConfig, mode: str | None = None) -> RunReport:
         raise UnsupportedOnDevice(f"mode {effective!r}: only the pipelined path is on device "
                                   "(staged mode writes intermediate files; out of scope)")
     return run_pipelined(config)
+
+
+# ---------------------------------------------------------------------------
+# _extract_batch drop-in (pipeline.py:718-737): row-aligned output columns
+# ---------------------------------------------------------------------------
+
+def prepare_extract(config: PipelineConfig, table_kinds: Mapping[str, Kind]) -> Prepared:
+    """Plan the operator DAG over an already cleaned + joined table."""
+    kinds = dict(table_kinds)
+    try:
+        dag = expand_call_graph(config.operators)
+        plan = place_operators(layer_schedule(dag), PlacementBudget(config.device_budget_bytes),
+                               dag)
+        fns = {}
+        for name, node in dag.nodes.items():
+            fn = resolve_function(node.func.spec, config.tables)
+            want = "tuple" if node.role == "body" else "scalar"
+            if fn.arity != want:
+                raise FeatureConfigError(f"{name}: function {node.func.spec!r} has arity "
+                                         f"{fn.arity}, {node.role} node needs {want}")
+            fns[name] = fn
+    except (FeatureConfigError, ValueError) as exc:
+        if isinstance(exc, ConfigError):
+            raise
+        raise ConfigError(str(exc)) from exc
+    missing = set(dag.external_inputs()) - set(kinds)
+    if missing:
+        raise ConfigError(f"operator inputs {sorted(missing)} not present in the table")
+    extract_outputs = []
+    for spec in config.operators:
+        domains = output_domains(spec, config.tables)
+        for col in spec.outputs:
+            if col in kinds:
+                raise ConfigError(f"output column {col!r} collides with a table column")
+            extract_outputs.append((col, Kind.INT64 if domains[col] == "u64" else Kind.UTF8,
+                                    domains[col]))
+    order = plan.node_order()
+    rank = {n: i for i, (_, n) in enumerate(order)}
+    specs = {s.name: s for s in config.operators}
+    pre_of: dict[str, dict[int, str]] = {}
+    nodes = []
+    for layer, name in order:
+        nd = dag.nodes[name]
+        if nd.role == "pre":
+            pre_of.setdefault(nd.op, {})[nd.slot] = name
+            inputs = nd.reads
+        elif nd.role == "body":
+            inputs = specs[nd.op].inputs
+        else:
+            inputs = ()
+        nodes.append(codegen.NodeIR(name, nd.role, nd.op, fns[name], layer, rank[name],
+                                    tuple(inputs), nd.slot, nd.writes))
+    ir = codegen.PlanIR(
+        driver=codegen.ViewIR("table", kinds, {}, [], None), sides=[], basic=None,
+        join_keys=(), nodes=nodes, pre_of=pre_of, producer=dict(dag.col_producer),
+        features={}, instance_column=config.instance_column, label_column=config.label_column,
+        chunk=256, tables={t: i for i, t in enumerate(sorted(config.tables))},
+        table_defaults={t: config.tables[t].default for t in config.tables},
+        extract_outputs=[(c, d) for c, _, d in extract_outputs], stage_strings=False,
+        mode="extract")
+    prog = codegen.generate(ir)
+    return Prepared(config, dag, plan, ir, prog, runtime.compile_source(prog.source),
+                    tuple(extract_outputs), [n for _, n in order], {"table": kinds}, {})
+
+
+class ExtractEngine(Engine):
+    """Device state for the row-aligned ``_extract_batch`` kernel."""
+
+    def __init__(self, prepared: Prepared, device: str = "cuda", pool_bytes_per_row: int = 64):
+        torch = _torch()
+        self.torch = torch
+        self.prepared = prepared
+        self.device = torch.device(device)
+        self.config = prepared.config
+        self.ir = prepared.ir
+        self.prog = prepared.program
+        self.slots = self.prog.slots
+        self.params = np.zeros(runtime.FBX_MAX_PARAM_SLOTS, dtype=np.uint64)
+        self.pool_bytes_per_row = pool_bytes_per_row
+        self._keep: list = []
+        with torch.cuda.device(self.device):
+            self.module = runtime.Program(prepared.cubin)
+            self.state = torch.zeros(runtime.STATE_BYTES // 8, dtype=torch.int64,
+                                     device=self.device)
+            self._set("state", self.state.data_ptr())
+            self._upload_tables()
+
+    def extract(self, table: ViewImage) -> ViewImage:
+        """``_extract_batch``: the table's columns plus the output columns."""
+        torch, dev = self.torch, self.device
+        n = table.row_count
+        dv = DeviceView(table, device=dev)
+        for c in dv.tensors:
+            for part in ("nulls", "data", "offsets"):
+                self._set(f"drv.{c}.{part}", dv.ptr(c, part))
+        self._set("rows", n)
+        pool_cap = self.pool_bytes_per_row * n + 128 * ((n + 255) // 256) * 8 + (1 << 16)
+        pool = torch.empty(pool_cap + 256, dtype=torch.uint8, device=dev)
+        self._set("pool", pool.data_ptr())
+        self._set("pool_cap", pool_cap)
+        outs = []
+        words = (n + 31) // 32 + 1
+        for j, (col, kind, domain) in enumerate(self.prepared.extract_outputs):
+            nulls = torch.zeros(words, dtype=torch.int32, device=dev)
+            self._set(f"out{j}.nulls", nulls.data_ptr())
+            if domain == "u64":
+                data = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+                self._set(f"out{j}.data", data.data_ptr())
+                outs.append((col, kind, nulls, data, None))
+            else:
+                ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+                ln = torch.zeros(n + 1, dtype=torch.int32, device=dev)
+                self._set(f"out{j}.ptr", ptr.data_ptr())
+                self._set(f"out{j}.len", ln.data_ptr())
+                outs.append((col, kind, nulls, ptr, ln))
+        stream = self._stream()
+        status = torch.zeros(1, dtype=torch.int64, device=dev)
+        runtime.state_reset(self.state.data_ptr(), status.data_ptr(), 1, stream)
+        grid = max(1, min((n + 255) // 256, 148 * 8))
+        self.module.launch("fbx_extract_rows", grid, 256, 0, stream, self.params)
+        st = self._read_state()
+        key = st["error_key"]
+        if key != (1 << 64) - 1 or st["pool_overflow"]:
+            try:
+                self._raise_if_error(st)
+            except StageError as exc:
+                raise exc.__cause__ from None
+        cols = {c: table.columns[c] for c in table.order}
+        for col, kind, nulls, a, b in outs:
+            nb = nulls.cpu().numpy().view(np.uint8)[: (n + 7) // 8].copy()
+            if b is None:
+                cols[col] = ColumnImage(Kind.INT64, n, nb, a[:n].cpu().numpy().copy())
+            else:
+                offs = torch.empty(n + 1, dtype=torch.int64, device=dev)
+                runtime.exclusive_scan_u32(b.data_ptr(), offs.data_ptr(), n, stream)
+                total = int(offs[n].item()) if n else 0
+                data = torch.empty(total + 16, dtype=torch.uint8, device=dev)
+                runtime.gather_strings(a.data_ptr(), b.data_ptr(), offs.data_ptr(), n,
+                                       data.data_ptr(), stream)
+                if total > 0xFFFFFFFF:
+                    raise ValueError("var-length payload exceeds u32 offset range")
+                cols[col] = ColumnImage(Kind.UTF8, n, nb, data[:total].cpu().numpy().copy(),
+                                        offs.cpu().numpy().astype(np.uint32))
+        return ViewImage(cols, table.key_columns, tuple(table.order) + tuple(
+            c for c, *_ in outs))
+
+
+def extract_batch(table: ViewImage, config: PipelineConfig, device: str = "cuda") -> ViewImage:
+    """One-call ``_extract_batch`` equivalent (plans, compiles, runs)."""
+    kinds = {c: table.columns[c].kind for c in table.order}
+    return ExtractEngine(prepare_extract(config, kinds), device=device).extract(table)

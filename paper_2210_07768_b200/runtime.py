@@ -30,7 +30,7 @@ STATE_BYTES = 8 * len(STATE_FIELDS)
 EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_program_load",
            "fbx_program_unload", "fbx_program_kernel", "fbx_kernel_attributes",
            "fbx_kernel_set_max_dynamic_smem", "fbx_launch", "fbx_state_reset",
-           "fbx_dict_build", "fbx_l2_flush")
+           "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings")
 
 
 class FbxError(RuntimeError):
@@ -64,6 +64,8 @@ def lib() -> ctypes.CDLL:
             L.fbx_dict_build.argtypes = [vp, ctypes.c_ulonglong, vp, vp, vp,
                                          ctypes.c_ulonglong, vp, vp]
             L.fbx_l2_flush.argtypes = [vp, sz, vp]
+            L.fbx_exclusive_scan_u32.argtypes = [vp, vp, ctypes.c_ulonglong, vp]
+            L.fbx_gather_strings.argtypes = [vp, vp, vp, ctypes.c_ulonglong, vp, vp]
             for name in EXPORTS:
                 getattr(L, name).restype = getattr(L, name).restype or c
             L.fbx_version.restype = ctypes.c_char_p
@@ -171,3 +173,14 @@ def dict_build(d_slots: int, capacity: int, d_blob: int, d_offs: int, d_vals: in
 def l2_flush(d_buf: int, nbytes: int, stream: int):
     _check(lib().fbx_l2_flush(ctypes.c_void_p(d_buf), int(nbytes), ctypes.c_void_p(stream)),
            "l2 flush")
+
+
+def exclusive_scan_u32(d_in: int, d_out: int, n: int, stream: int):
+    _check(lib().fbx_exclusive_scan_u32(ctypes.c_void_p(d_in), ctypes.c_void_p(d_out), n,
+                                        ctypes.c_void_p(stream)), "scan")
+
+
+def gather_strings(d_ptrs: int, d_lens: int, d_offsets: int, n: int, d_out: int, stream: int):
+    _check(lib().fbx_gather_strings(ctypes.c_void_p(d_ptrs), ctypes.c_void_p(d_lens),
+                                    ctypes.c_void_p(d_offsets), n, ctypes.c_void_p(d_out),
+                                    ctypes.c_void_p(stream)), "gather strings")

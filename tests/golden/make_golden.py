@@ -70,6 +70,43 @@ def to_csr(batches):
             "batch_sizes": np.array([len(b) for b in batches], np.int64)}
 
 
+def extract_fixtures(dest: Path):
+    """Reference `_extract_batch` over the whole cleaned + joined 2k table
+    (what staged mode extracts, pipeline.py:839-845), one fixture per DAG."""
+    from featurebox.columnstore import read_columns, write_view
+    from featurebox.device import ExecContext, LaunchCostModel
+    from featurebox.mempool import create_pool
+    from featurebox.pipeline import _extract_batch, prepare
+    from featurebox.viewpipe import JoinSpec, clean_views, join_views
+    joined = None
+    for dag in DAGS:
+        path = dest / "cfg_x.json"
+        path.write_text(json.dumps(workload_config(dag)))
+        cfg = load_config(path)
+        prep = prepare(cfg)
+        if joined is None:
+            drv = cfg.views[0]
+            side = cfg.views[1]
+            a, _ = read_columns(drv.path)
+            b, _ = read_columns(side.path)
+            joined = join_views(clean_views(a, drv.policy), clean_views(b, side.policy),
+                                JoinSpec(cfg.join_keys))
+            write_view(joined, HERE / "joined_2k.fbxc")
+        ctx = ExecContext(cost_model=LaunchCostModel(3.45), pool=create_pool(64 << 20))
+        out = _extract_batch(joined, prep, ctx)
+        arrays = {}
+        for col, kind, domain in prep.extract_outputs:
+            vals = out.columns[col].to_pylist()
+            arrays[col + ".null"] = np.array([v is None for v in vals], bool)
+            if domain == "u64":
+                arrays[col] = np.array([0 if v is None else v for v in vals], np.int64)
+            else:
+                blob = [b"" if v is None else v.encode("utf-8") for v in vals]
+                arrays[col + ".offsets"] = np.cumsum([0] + [len(x) for x in blob]).astype(np.uint64)
+                arrays[col] = np.frombuffer(b"".join(blob), np.uint8)
+        np.savez_compressed(HERE / f"extract_{dag}.npz", **arrays)
+
+
 def main():
     out = {"python": platform.python_version(), "runs": []}
     with tempfile.TemporaryDirectory() as tmp:
@@ -99,6 +136,8 @@ def main():
                     print(out["runs"][-1], flush=True)
                     if capture:
                         np.savez_compressed(HERE / f"csr_{dag}.npz", **to_csr(batches))
+            if rows == 2000 and views == 2:
+                extract_fixtures(dest)
     (HERE / "goldens.json").write_text(json.dumps(out, indent=1) + "\n")
 
 

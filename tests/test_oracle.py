@@ -100,3 +100,25 @@ def test_oracle_clean_matches_reference_clean(doc):
                                     "kind": "utf8"}]}, oc)
     assert [r["cx"] for r in mine.rows] == ref.columns["cx"].to_pylist()
     assert oc.get("malformed", 0) == rc.malformed_rows
+
+
+@pytest.mark.parametrize("dag", DAGS)
+def test_oracle_extract_matches_reference_extract_batch(dag):
+    """The oracle's `_extract_batch` restatement vs the reference's outputs."""
+    from paper_2210_07768_b200.columns import read_view
+    from paper_2210_07768_b200.workloads import workload_config
+    c, d = corpus(2000, 300, 7)
+    cfg = workload_config(dag)
+    tables, sizes = O.load_tables(cfg.get("tables", {}), d)
+    plan = O.build_plan(cfg["operators"], tables, cfg["device"]["budget_bytes"], sizes)
+    t = O.Table.from_view(read_view(GOLDEN / "joined_2k.fbxc"))
+    out = O.extract(plan, t)
+    ref = np.load(GOLDEN / f"extract_{dag}.npz")
+    for col in [k for k in ref.files if "." not in k]:
+        vals = [r[col] for r in out.rows]
+        assert [v is None for v in vals] == list(ref[col + ".null"]), col
+        if col + ".offsets" in ref.files:
+            blob = b"".join(b"" if v is None else v.encode() for v in vals)
+            assert blob == ref[col].tobytes(), col
+        else:
+            assert [0 if v is None else v for v in vals] == list(ref[col]), col
