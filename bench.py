@@ -258,19 +258,12 @@ def main():
     if dist:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     total_ms, kern_total = float(tot[0]), float(tot[1])
-    # the one collective: all-gather of per-shard {records, instances, signs, digest}
-    shard = torch.tensor([n, c.instances, c.signs, c.digest - (1 << 64) if c.digest >> 63
-                          else c.digest], dtype=torch.int64, device=dev)
-    if dist:
-        parts = [torch.empty_like(shard) for _ in range(world)]
-        dist.all_gather(parts, shard)
-        gathered = torch.stack(parts).cpu().numpy()
-    else:
-        gathered = shard.cpu().numpy()[None]
-    run_digest = 0
-    for g in gathered:
-        run_digest ^= int(g[3]) & ((1 << 64) - 1)
-    records_all = int(gathered[:, 0].sum())
+    # the one collective: all-gather of per-shard counters (distributed.py)
+    from paper_2210_07768_b200.distributed import ShardResult, all_gather_results, combine
+    shard = ShardResult(n, c.instances, c.signs, c.digest, c.malformed, c.filtered)
+    totals = all_gather_results(shard, device=dev) if dist else combine([shard])
+    run_digest = totals.digest
+    records_all = totals.records
     value = records_all * K / (total_ms / 1e3)
     ms_per_step = total_ms / K
     kern_avg_s = kern_total / K / 1e3
@@ -319,8 +312,8 @@ def main():
                    "parallelism": f"record-sharded x{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * K, "clocks": clk,
-        "parity": {"digest": f"0x{run_digest:016x}", "instances": int(gathered[:, 1].sum()),
-                   "signs": int(gathered[:, 2].sum())},
+        "parity": {"digest": f"0x{run_digest:016x}", "instances": totals.instances,
+                   "signs": totals.signs},
         "setup_s": {"corpus": round(gen_s, 1), "prepare": round(prep_s, 1)},
     }
     if rank == 0:

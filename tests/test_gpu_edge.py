@@ -1,0 +1,237 @@
+"""GPU: adversarial records and error paths, engine vs the CPU oracle.
+
+Edge cases follow SURVEY.md Appendix A and the reference's tests: JSON grammar
+corners, escapes, duplicate keys, fills, exact int/float filters, null join
+keys, shared emit slots, tokens past the end, upper-case lower(), tiny and odd
+batch sizes -- and the failure modes (TypeError, UnicodeEncodeError, duplicate
+ids, null / out-of-range labels) located by stage like the reference.
+"""
+
+from __future__ import annotations
+
+import json
+import random
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import featurebox_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+JSON_DOCS = [
+    '{"u": {"city": "tokyo", "tier": 2}, "src": "app"}', '{"u":{"city":"Kyoto"}}',
+    '{"u": {"city": "a\\u00e9b"}}', '{"u": {"city": "\\ud83d\\ude00x"}}', '{"u": {"city": 5}}',
+    '{"u": [1, 2]}', "not json{", '{"u": {"city": "x"}, "u": 5}', '{"a":1,}', " [1] ",
+    '{"u":{"city":"x"}}x', '"s"', "NaN", '{"u":{}}', '{"u":{"city":"q","city":"r"}}',
+    '{"\\u0075":{"city":"k"}}', "{", "", '{"u":{"city":"tab\\there"}}',
+    '{"u":{"city":"ok"},"n":-0.5e-3}', "1e400", '{"u":{"city":"  padded  "}}',
+    '{"u" : {"city" : "SP ACE"} }', '{"u":{"city":"a"},"x":[{"y":[1,{"z":null}]}]}',
+    '{"u":{"city":"line\\nbreak"}}', '{"u":{"city":"\\"quoted\\""}}', "[]", "{}",
+    '{"u":{"city":"x"},"t":true,"f":false,"n":null,"i":-Infinity}', '{"u":{"city":"é"}}',
+    '{"u":{"city":"x"}', '{"u":{"city":"x"}}}', '{"u":{"city":"x"},}', '{"u":{"city":"x"} "v":1}',
+    '{"u":{"city":01}}', '{"u":{"city":"\\x"}}', '{"u":{"city":"ctl\x01"}}', '{"u":{"city":"x"}}\n',
+]
+QUERIES = ["running shoes", "Coffee Beans", "  desk  ", "", "a  b", "x", "mechanical keyboard gravel bike",
+           "ÉCOLE café", "tab\tsep", None]
+
+
+def _views(n, seed):
+    from paper_2210_07768_b200.columns import Kind, ViewImage
+    rng = random.Random(seed)
+    ids, labels, users, queries, metas, ages = [], [], [], [], [], []
+    for i in range(n):
+        ids.append((i * 0x9E3779B97F4A7C15 + 12345) % (1 << 63) * (-1 if i % 7 == 0 else 1))
+        labels.append(rng.choice([0, 1]))
+        users.append(rng.choice([None] + list(range(40))) if rng.random() < 0.1 else rng.randrange(40))
+        queries.append(rng.choice(QUERIES))
+        metas.append(rng.choice(JSON_DOCS + [None]))
+        ages.append(rng.choice([None, -5, 0, 18, 120, 121, 2**40, -2**62]))
+    drv = ViewImage.from_pydict(
+        [("instance_id", Kind.INT64), ("label", Kind.INT64), ("user_id", Kind.INT64),
+         ("query", Kind.UTF8), ("meta", Kind.JSON), ("age", Kind.INT64)],
+        {"instance_id": ids, "label": labels, "user_id": users, "query": queries,
+         "meta": metas, "age": ages}, ("user_id",))
+    pu, pc, ps = [], [], []
+    for u in range(40):
+        if u % 9 == 4:
+            continue
+        pu.append(u)
+        pc.append(rng.choice([None, " tokyo", "Osaka ", "kyoto", "é", ""]))
+        ps.append(rng.choice([None, 0.5, -0.0, 1e-7, 3.25, float("nan")]))
+    prof = ViewImage.from_pydict([("user_id", Kind.INT64), ("city", Kind.UTF8),
+                                  ("score", Kind.FLOAT32)],
+                                 {"user_id": pu, "city": pc, "score": ps}, ("user_id",))
+    bas = ViewImage.from_pydict([("instance_id", Kind.INT64), ("basic_a", Kind.INT64)],
+                                {"instance_id": [x for j, x in enumerate(ids) if j % 11],
+                                 "basic_a": [rng.choice([None, 7, -7]) for j in range(n) if j % 11]},
+                                ("instance_id",))
+    return drv, prof, bas
+
+
+def _config(batch_size, ops, features, filt="age <= 120 and age != -5", tables=None):
+    return {
+        "driver": "ev", "batch_size": batch_size, "basic": {"path": "basic.fbxc"},
+        "views": [{"name": "ev", "path": "ev.fbxc",
+                   "clean": {"fills": {"query": ""},
+                             "extract": [{"source": "meta", "path": "u.city", "output": "cx",
+                                          "kind": "utf8"},
+                                         {"source": "meta", "path": "u.tier", "output": "tier",
+                                          "kind": "int64"}],
+                             "filter": filt}},
+                  {"name": "pr", "path": "pr.fbxc", "clean": {"fills": {"city": "unknown"}}}],
+        "join": {"keys": ["user_id"]}, "tables": tables or {}, "operators": ops,
+        "emit": {"features": features}, "device": {"budget_bytes": 65536}}
+
+
+def _run_both(raw, drv, prof, bas, tmp: Path):
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.engine import run_views
+    cfg = config_from_dict(raw, tmp)
+    views = {"ev": drv, "pr": prof}
+    tables, sizes = O.load_tables(raw.get("tables", {}), tmp)
+    try:
+        ref = O.run_pipelined(raw, views, bas, tables, sizes)
+        ref_err = None
+    except O.OracleError as e:
+        ref, ref_err = None, e
+    try:
+        got = run_views(cfg, views, bas, collect=True, max_rows_per_launch=1 << 20)
+        got_err = None
+    except Exception as e:  # noqa: BLE001
+        got, got_err = None, e
+    return ref, ref_err, got, got_err
+
+
+OPS = [
+    {"name": "q_low", "inputs": ["query"], "outputs": ["q_low"], "pre": [{"fn": "lower"}],
+     "body": {"fn": "hash:3"}},
+    {"name": "q_tr", "inputs": ["query"], "outputs": ["q_tr"], "pre": [{"fn": "trim"}],
+     "body": {"fn": "hash:4"}},
+    {"name": "q_t5", "inputs": ["query"], "outputs": ["q_t5"], "pre": [{"fn": "token: :5"}],
+     "body": {"fn": "hash:5"}},
+    {"name": "x", "inputs": ["cx", "city", "score"], "outputs": ["x_m", "x_f"],
+     "body": {"fn": "hash:6"}, "post": [{"fn": "mix"}, {"fn": "fold"}]},
+    {"name": "cc", "inputs": ["city", "cx", "tier"], "outputs": ["cc"], "body": {"fn": "concat:/"}},
+    {"name": "cc_sig", "inputs": ["cc"], "outputs": ["cc_sig"], "pre": [{"fn": "trim"}],
+     "body": {"fn": "hash:7"}},
+    {"name": "age_s", "inputs": ["age", "user_id"], "outputs": ["age_s"],
+     "pre": [{"fn": "fold", "arg": 0}], "body": {"fn": "hash:8"}},
+    {"name": "tier_s", "inputs": ["tier"], "outputs": ["tier_s"], "pre": [{"fn": "trim"}],
+     "body": {"fn": "hash:9"}},
+]
+FEATS = {"q_low": 3, "q_tr": 4, "q_t5": 5, "x_m": 6, "x_f": 6, "cc_sig": 7, "age_s": 8,
+         "tier_s": 9, "basic_a": 9}
+
+
+def _write_views(tmp, drv, prof, bas):
+    from paper_2210_07768_b200.columns import write_view
+    write_view(drv, tmp / "ev.fbxc")
+    write_view(prof, tmp / "pr.fbxc")
+    write_view(bas, tmp / "basic.fbxc")
+
+
+@pytest.mark.parametrize("batch_size,seed", [(512, 1), (64, 2), (7, 3), (1000, 4)])
+def test_adversarial_records_match_oracle(batch_size, seed, tmp_path):
+    drv, prof, bas = _views(3000, seed)
+    _write_views(tmp_path, drv, prof, bas)
+    # non-ASCII lower() is a declared device gap: keep those rows away from lower
+    raw = _config(batch_size, OPS, FEATS)
+    raw["views"][0]["clean"]["filter"] = "age <= 120 and age != -5 and query < 'É'"
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is None, ref_err
+    assert got_err is None, got_err
+    rep = got.report
+    assert (rep.digest, rep.instances, rep.signs) == (ref.digest, ref.instances, ref.signs)
+    assert (rep.rows_dropped, rep.rows_filtered) == (ref.malformed, ref.filtered)
+    np.testing.assert_array_equal(got.csr["ids"], np.array(ref.ids, np.uint64))
+    np.testing.assert_array_equal(got.csr["offsets"], np.array(ref.offsets, np.uint64))
+    np.testing.assert_array_equal(got.csr["slots"], np.array(ref.slots, np.uint16))
+    np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
+
+
+@pytest.mark.parametrize("filt", ["age < 120.5", "age >= -4611686018427387904", "age == 20.0",
+                                  "age != 9999999999999999999999", "age > -1.5 or tier == 2",
+                                  "(age < 30 or age > 60) and query != ''", "cx >= 'kyoto'",
+                                  "tier <= 1 && cx != 'x'"])
+def test_filters_match_oracle(filt, tmp_path):
+    drv, prof, bas = _views(1500, 9)
+    _write_views(tmp_path, drv, prof, bas)
+    raw = _config(256, OPS[3:4], {"x_m": 6, "x_f": 7}, filt=filt)
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is None and got_err is None, (ref_err, got_err)
+    assert (got.report.digest, got.report.instances) == (ref.digest, ref.instances)
+    assert (got.report.rows_dropped, got.report.rows_filtered) == (ref.malformed, ref.filtered)
+
+
+def _err(kind, tmp_path, mutate):
+    drv, prof, bas = _views(2000, 5)
+    drv, prof, bas = mutate(drv, prof, bas)
+    _write_views(tmp_path, drv, prof, bas)
+    raw = kind
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is not None, "oracle did not fail"
+    assert got_err is not None, "engine did not fail"
+    from paper_2210_07768_b200.config import StageError
+    assert isinstance(got_err, StageError), got_err
+    assert got_err.stage == ref_err.stage
+    assert type(got_err.__cause__).__name__ in (type(ref_err.cause).__name__,
+                                                "LayerExecutionError")
+    return ref_err, got_err
+
+
+def _same(*a):
+    return a
+
+
+def test_type_error_mix_of_str(tmp_path):
+    ops = [{"name": "m", "inputs": ["query"], "outputs": ["m"], "pre": [{"fn": "mix"}],
+            "body": {"fn": "hash:3"}}]
+    ref_err, got_err = _err(_config(512, ops, {"m": 3}), tmp_path, _same)
+    assert got_err.__cause__.node == ref_err.node == "m.pre1"
+    assert isinstance(got_err.__cause__.__cause__, TypeError)
+    assert got_err.batch_index == ref_err.chunk
+
+
+def test_lone_surrogate_hash_is_encode_error(tmp_path):
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+
+    def mut(drv, prof, bas):
+        metas = drv.columns["meta"].to_pylist()
+        metas[700] = '{"u": {"city": "\\ud800"}}'
+        drv.columns["meta"] = ColumnImage.from_values(Kind.JSON, metas)
+        return drv, prof, bas
+    ops = [{"name": "c", "inputs": ["cx"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    ref_err, got_err = _err(_config(512, ops, {"c": 3}, filt="age != -12345"), tmp_path, mut)
+    assert isinstance(got_err.__cause__.__cause__, UnicodeEncodeError)
+
+
+def test_duplicate_instance_ids(tmp_path):
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+
+    def mut(drv, prof, bas):
+        ids = drv.columns["instance_id"].to_pylist()
+        for i in range(1000, 1100):  # many rows share one id: some survive to the merge
+            ids[i] = ids[999]
+        drv.columns["instance_id"] = ColumnImage.from_values(Kind.INT64, ids)
+        return drv, prof, bas
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    raw = _config(512, ops, {"c": 3}, filt="age != -12345")
+    ref_err, got_err = _err(raw, tmp_path, mut)
+    assert got_err.stage == "merge"
+
+
+@pytest.mark.parametrize("label", [None, 2, -1])
+def test_bad_labels(label, tmp_path):
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+
+    def mut(drv, prof, bas):
+        labels = drv.columns["label"].to_pylist()
+        for i in range(0, 2000, 97):
+            labels[i] = label
+        drv.columns["label"] = ColumnImage.from_values(Kind.INT64, labels)
+        return drv, prof, bas
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    _err(_config(512, ops, {"c": 3}, filt="age != -12345"), tmp_path, mut)
