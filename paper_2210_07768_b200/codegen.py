@@ -364,11 +364,26 @@ class PlanCodegen:
                             "{" + ",".join(map(str, lens)) + "};")
         self.globals.append(f"__device__ const u8 {tag}_ns[] = "
                             "{" + ",".join(map(str, nseg)) + "};")
+        km = f"{tag}_KM"
+        cases = []
+        for pi, e in enumerate(exts):
+            for si, seg in enumerate(e.path.split(".")):
+                b = seg.encode("utf-8")
+                pre = int.from_bytes(b[:8].ljust(8, b"\0"), "little")
+                cases.append(f"    case {pi * 8 + si}: return len == {len(b)}u && pre == "
+                             f"0x{pre:016X}ull;")
+        nsegs = ", ".join(str(len(e.path.split("."))) for e in exts)
+        self.globals.append(
+            f"struct {km} {{\n"
+            f"  static FBX_DI u32 nseg(int p) {{ const u32 t[{np_}] = {{{nsegs}}}; return t[p]; }}\n"
+            f"  static FBX_DI bool eq(int p, u32 sidx, u64 pre, u32 len) {{\n"
+            f"    switch (p * 8 + (int)sidx) {{\n" + "\n".join(cases) +
+            "\n    default: return false;\n    }\n  }\n};")
         leaf = g.fresh("leaf")
         g(f"fbx::JLeaf {leaf}[{np_}];")
         g(f"bool {leaf}_ok = false;")
         g(f"if (alive && !{src.n}) {{")
-        g(f"u32 js = fbx::json_extract<{np_}>({src.c}, fbx::JPathSet{{{tag}_seg, {tag}_off, "
+        g(f"u32 js = fbx::json_extract<{np_}, {km}>({src.c}, fbx::JPathSet{{{tag}_seg, {tag}_off, "
           f"{tag}_len, {tag}_ns}}, {leaf});")
         g(f"if (js == fbx::JS_OK) {{ {leaf}_ok = true; }}")
         g(f"else if (js == fbx::JS_MALFORMED) {{ {on_malformed} }}")

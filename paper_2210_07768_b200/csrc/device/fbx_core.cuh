@@ -725,7 +725,11 @@ struct JReader {
     return (w >> ((pos & 3u) * 8u)) & 0xFFu;
   }
   FBX_DI u32 skip_ws(u32 i) {
-    while (i < n && j_ws(at(i))) ++i;
+    while (i < n) {
+      const u32 c = at(i);
+      if (c > 0x20u || !j_ws(c)) break;
+      ++i;
+    }
     return i;
   }
 };
@@ -883,7 +887,9 @@ FBX_DI bool j_lit(JReader& r, u32 i, const char* w, u32 wl) {
 
 // Validate the whole document (CPython json.loads, strict) and extract the NP
 // dot paths.  Inlined so the leaves live in registers.  Returns JS_*.
-template <int NP>
+// KM: plan-generated key matcher -- KM::nseg(p) and KM::eq(p, sidx, prefix8, len)
+// with the path segments as immediates (escaped keys use the generic compare).
+template <int NP, class KM>
 FBX_DI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
 #pragma unroll
   for (int p = 0; p < NP; ++p) leaf[p] = JLeaf{0, 0, J_MISSING, 0};
@@ -998,13 +1004,25 @@ FBX_DI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
       u32 lv = (u32)((live >> ((depth - 1) * 8)) & 0xFFull);
       u32 sidx = depth - 1;
       if (lv) {
+        const u32 klen = ke - kb;
+        const u64 kpre = kesc ? 0ull : load_prefix8(doc.p + kb, klen);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           if (!(lv & (1u << p))) continue;
-          u32 ns = ps.nseg[p];
+          const u32 ns = KM::nseg(p);
           if (sidx >= ns) continue;
-          u32 off = ps.seg_off[p * 8 + sidx], sl = ps.seg_len[p * 8 + sidx];
-          if (!j_key_eq(r, doc.p, kb, ke, kesc, ps.seg + off, sl)) continue;
+          bool eq;
+          if (!kesc) {
+            eq = KM::eq(p, sidx, kpre, klen);
+            if (eq && klen > 8u) {
+              u32 off = ps.seg_off[p * 8 + sidx];
+              for (u32 k = 8; k < klen && eq; ++k) eq = r.at(kb + k) == ps.seg[off + k];
+            }
+          } else {
+            u32 off = ps.seg_off[p * 8 + sidx], sl = ps.seg_len[p * 8 + sidx];
+            eq = j_key_eq(r, doc.p, kb, ke, kesc, ps.seg + off, sl);
+          }
+          if (!eq) continue;
           leaf[p] = JLeaf{0, 0, J_MISSING, 0};  // a later duplicate key replaces the value
           if (sidx + 1 == ns) leafm |= (1u << p); else descm |= (1u << p);
         }
