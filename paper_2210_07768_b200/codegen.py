@@ -921,9 +921,9 @@ class PlanCodegen:
         g("} sm;")
         g("// tiles in blockIdx order: the hardware dispatches CTAs in order, so every")
         g("// predecessor a look-back waits on is resident or done (as CUB relies on)")
-        g("const u32 tile = blockIdx.x;")
-        g("const u64 chunk = CHUNK0 + tile;")
-        g(f"const u64 row0 = ROW_LO + (u64)tile * {ir.chunk}ull;")
+        g(f"const u32 tile = (u32){g.p('tile_base')} + blockIdx.x;  // run-global tile id")
+        g("const u64 chunk = CHUNK0 + blockIdx.x;")
+        g(f"const u64 row0 = ROW_LO + (u64)blockIdx.x * {ir.chunk}ull;")
         g(f"const u64 row_end = (row0 + {ir.chunk}ull < ROW_HI) ? row0 + {ir.chunk}ull : ROW_HI;")
         g("const u64 srow = row0 + threadIdx.x;")
         g(f"const bool inrange = threadIdx.x < {ir.chunk}u && srow < row_end;")

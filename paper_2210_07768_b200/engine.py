@@ -474,12 +474,15 @@ class Engine:
         self._set("idset", self.idset.data_ptr())
         self._set("idset_mask", self._idset_cap - 1)
 
-    def _arena(self, rows: int):
-        """Per-launch buffers: look-back status, CSR outputs, bump pool."""
+    def reserve(self, rows: int, launch_rows: int | None = None):
+        """Run-wide buffers: look-back status for every tile of the run (the
+        look-back continues across launches), the CSR for every row, and a
+        bump pool sized for the largest launch."""
         torch = self.torch
+        launch_rows = rows if launch_rows is None else launch_rows
         tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
         k = max(1, len(self.ir.features))
-        need = (tiles, rows, k)
+        need = (tiles, rows, k, launch_rows)
         if getattr(self, "_arena_key", None) != need:
             dev = self.device
             self.status = torch.zeros(tiles + 1, dtype=torch.int64, device=dev)
@@ -490,7 +493,8 @@ class Engine:
             self.o_sign = torch.empty(rows * k + 1, dtype=torch.int64, device=dev)
             pool_cap = 0
             if codegen_pool_sites(self.prog):
-                pool_cap = self.pool_bytes_per_row * rows + 128 * tiles * 8 + (1 << 20)
+                lt = (launch_rows + self.ir.chunk - 1) // self.ir.chunk
+                pool_cap = self.pool_bytes_per_row * launch_rows + 128 * lt * 8 + (1 << 20)
             self.pool = torch.empty(pool_cap + 256, dtype=torch.uint8, device=dev)
             self.pool_cap = pool_cap
             self._arena_key = need
@@ -504,26 +508,40 @@ class Engine:
         self._set("pool_cap", self.pool_cap)
         return tiles
 
+    def _arena(self, rows: int):
+        return self.reserve(rows)
+
     def bind_driver(self, dview: DeviceView):
         for c in dview.tensors:
             for part in ("nulls", "data", "offsets"):
                 self._set(f"drv.{c}.{part}", dview.ptr(c, part))
         self.dview = dview
 
-    def launch(self, row_lo: int, row_hi: int, stream: int | None = None) -> int:
+    def launch(self, row_lo: int, row_hi: int, stream: int | None = None,
+               tile_base: int | None = None) -> int:
         """Enqueue one fused launch over driver rows [row_lo, row_hi) (no sync).
 
         ``row_lo`` must be a multiple of ``batch_size`` (chunk boundaries are
-        the reference's read boundaries, pipeline.py:994)."""
+        the reference's read boundaries, pipeline.py:994).  Without
+        ``tile_base`` the launch is a run of its own (status + CSR from 0);
+        with it the launch continues a reserved run: its tiles are
+        ``tile_base + i`` of the run-wide look-back and its CSR lands at the
+        run-global positions."""
         if row_lo % self.ir.chunk:
             raise ValueError("row_lo must start a driver chunk")
         rows = row_hi - row_lo
-        tiles = self._arena(rows)
         stream = self._stream() if stream is None else stream
+        if tile_base is None:
+            tiles = self._arena(rows)
+            runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(), tiles + 1, stream)
+            tile_base = 0
+        else:
+            tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
+            runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(), 0, stream)
         self._set("row_lo", row_lo)
         self._set("row_hi", row_hi)
         self._set("chunk0", row_lo // self.ir.chunk)
-        runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(), tiles + 1, stream)
+        self._set("tile_base", tile_base)
         self.module.launch("fbx_pipeline", tiles, self.prog.threads, self.prog.smem_bytes,
                            stream, self.params)
         return tiles
@@ -539,6 +557,150 @@ class Engine:
     def run(self, row_lo: int, row_hi: int) -> CsrBatch:
         self.launch(row_lo, row_hi)
         return self.finish()
+
+
+class StreamedRun:
+    """End-to-end run from pinned host column images (the e2e path).
+
+    The driver is cut into slices of whole chunks.  Slice k's column spans
+    are copied H2D on a copy stream into one of two device buffer sets, the
+    fused kernel runs on the compute stream, and the emitted CSR range of
+    slice k-1 is copied D2H on a second copy stream -- so PCIe traffic in both
+    directions overlaps the kernels.  The look-back continues across the
+    launches (run-global tile ids), so the CSR is written at its final
+    positions and slices need no host-side fix-up.
+    """
+
+    PARTS = ("nulls", "data", "offsets")
+
+    def __init__(self, eng: "Engine", host_view: ViewImage, slice_rows: int = 1 << 17):
+        torch = eng.torch
+        self.eng, self.torch = eng, torch
+        chunk = eng.ir.chunk
+        self.slice_rows = max(chunk, slice_rows - slice_rows % chunk)
+        self.n = n = host_view.row_count
+        self.bounds = [(lo, min(lo + self.slice_rows, n)) for lo in range(0, n, self.slice_rows)]
+        used = [c for c in host_view.order if any(f"drv.{c}.{p}" in eng.slots for p in self.PARTS)]
+        # Each slice's column spans packed into ONE pinned region (16-B aligned
+        # pieces) -- the layout a chunk reader produces -- so a slice is one H2D.
+        self.packs, self.layout = [], []
+        self.h2d_bytes = 0
+        cols = {c: host_view.columns[c] for c in used}
+        for lo, hi in self.bounds:
+            pieces, off = [], 0
+            for c, col in cols.items():
+                sp = {"nulls": (lo // 8, (hi + 7) // 8)}
+                if col.kind.var_length:
+                    sp["data"] = (int(col.offsets[lo]) & ~15, (int(col.offsets[hi]) + 15) & ~15)
+                    sp["offsets"] = (lo * 4, (hi + 1) * 4)
+                else:
+                    w = col.kind.fixed_width
+                    sp["data"] = (lo * w, hi * w)
+                for p, (a, b) in sp.items():
+                    pieces.append((c, p, a, b, off))
+                    off += (b - a + 15) & ~15
+            buf = np.zeros(off + 16, dtype=np.uint8)
+            for c, p, a, b, o in pieces:
+                src = getattr(cols[c], p)
+                raw = np.ascontiguousarray(src).view(np.uint8).reshape(-1)
+                seg = raw[a:b]
+                buf[o:o + seg.size] = seg
+            self.packs.append(torch.from_numpy(buf).pin_memory())
+            self.layout.append(pieces)
+            self.h2d_bytes += off
+        cap = max(p.numel() for p in self.packs)
+        self.dev = [torch.empty(cap + 32, dtype=torch.uint8, device=eng.device) for _ in range(2)]
+        self.s_h2d = torch.cuda.Stream(eng.device)
+        self.s_comp = torch.cuda.Stream(eng.device)
+        self.s_d2h = torch.cuda.Stream(eng.device)
+        k = max(1, len(eng.ir.features))
+        self.out = {"ids": torch.empty(n + 1, dtype=torch.int64, pin_memory=True),
+                    "labels": torch.empty(n + 16, dtype=torch.uint8, pin_memory=True),
+                    "offsets": torch.empty(n + 2, dtype=torch.int64, pin_memory=True),
+                    "slots": torch.empty(n * k + 8, dtype=torch.int16, pin_memory=True),
+                    "signs": torch.empty(n * k + 1, dtype=torch.int64, pin_memory=True)}
+        self.states = torch.empty((len(self.bounds), runtime.STATE_BYTES // 8),
+                                  dtype=torch.int64, pin_memory=True)
+
+    def run(self) -> Counters:
+        torch, eng = self.torch, self.eng
+        eng.reserve(self.n, self.slice_rows)
+        cur = torch.cuda.current_stream(eng.device)
+        self.s_comp.wait_stream(cur)
+        self.s_h2d.wait_stream(cur)
+        with torch.cuda.stream(self.s_comp):
+            eng.status.zero_()
+        comp_done = [torch.cuda.Event() for _ in self.bounds]
+        h2d_done = [torch.cuda.Event() for _ in self.bounds]
+        d2h_done = [torch.cuda.Event() for _ in self.bounds]
+        tot = Counters()
+        tiles_before = 0
+        inst_base, sign_base = 0, 0
+        pending = []
+
+        def drain(j):
+            nonlocal inst_base, sign_base
+            comp_done[j].synchronize()
+            st = self.states[j].numpy().view(np.uint64)
+            stt = {f: int(st[i]) for i, f in enumerate(runtime.STATE_FIELDS)}
+            eng._raise_if_error(stt)
+            ni, ms = stt["instances"], stt["signs"]
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(comp_done[j])
+                o = self.out
+                a, b = inst_base, inst_base + ni
+                o["ids"][a:b].copy_(eng.o_ids[a:b], non_blocking=True)
+                o["labels"][a:b].copy_(eng.o_lab[a:b], non_blocking=True)
+                o["offsets"][a:b + 1].copy_(eng.o_off[a:b + 1], non_blocking=True)
+                o["slots"][sign_base:sign_base + ms].copy_(eng.o_slot[sign_base:sign_base + ms],
+                                                           non_blocking=True)
+                o["signs"][sign_base:sign_base + ms].copy_(eng.o_sign[sign_base:sign_base + ms],
+                                                           non_blocking=True)
+                d2h_done[j].record(self.s_d2h)
+            inst_base += ni
+            sign_base += ms
+            tot.digest ^= stt["digest"]
+            tot.instances += ni
+            tot.signs += ms
+            tot.malformed += stt["malformed"]
+            tot.filtered += stt["filtered"]
+            tot.joined += stt["joined"]
+            tot.launches += 1
+
+        for k, (lo, hi) in enumerate(self.bounds):
+            buf = k & 1
+            with torch.cuda.stream(self.s_h2d):
+                if k >= 2:
+                    self.s_h2d.wait_event(comp_done[k - 2])  # buffer set reuse
+                pk = self.packs[k]
+                self.dev[buf][: pk.numel()].copy_(pk, non_blocking=True)
+                h2d_done[k].record(self.s_h2d)
+            base = self.dev[buf].data_ptr()
+            for c, p, a, b, o in self.layout[k]:
+                eng._set(f"drv.{c}.{p}", base + o - a)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(h2d_done[k])
+                eng.launch(lo, hi, self.s_comp.cuda_stream, tile_base=tiles_before)
+                self.states[k].copy_(eng.state, non_blocking=True)
+                comp_done[k].record(self.s_comp)
+            tiles_before += (hi - lo + eng.ir.chunk - 1) // eng.ir.chunk
+            pending.append(k)
+            if len(pending) > 1:
+                drain(pending.pop(0))
+        while pending:
+            drain(pending.pop(0))
+        self.s_d2h.synchronize()
+        self.d2h_bytes = tot.instances * 17 + 8 + tot.signs * 10
+        return tot
+
+    def csr(self, c: Counters) -> dict[str, np.ndarray]:
+        n, m = c.instances, c.signs
+        o = self.out
+        return {"ids": o["ids"][:n].numpy().view(np.uint64),
+                "labels": o["labels"][:n].numpy(),
+                "offsets": o["offsets"][:n + 1].numpy().view(np.uint64),
+                "slots": o["slots"][:m].numpy().view(np.uint16),
+                "signs": o["signs"][:m].numpy().view(np.uint64)}
 
 
 def codegen_pool_sites(prog: codegen.Program) -> bool:
