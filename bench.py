@@ -64,6 +64,11 @@ def parse_args():
     ap.add_argument("--cpu-sample-rows", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shards", type=int, default=0,
+                    help="C5 mode: this many independent 1M-record shards (seeds "
+                         "--shard-seed0 + k), split across ranks; 0 = one log per rank")
+    ap.add_argument("--shard-seed0", type=int, default=1000)
+    ap.add_argument("--launch-rows", type=int, default=1 << 24)
     return ap.parse_args()
 
 
@@ -184,7 +189,7 @@ def main():
     from paper_2210_07768_b200 import engine as E
     from paper_2210_07768_b200 import runtime
     from paper_2210_07768_b200.config import config_from_dict
-    from paper_2210_07768_b200.corpus import make_corpus, write_corpus
+    from paper_2210_07768_b200.corpus import make_corpus_fast as make_corpus, write_corpus
     from paper_2210_07768_b200.workloads import workload_config, write_lookup_tables
 
     torch.cuda.set_device(local)
@@ -193,80 +198,111 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    seed = args.seed + rank
-    t0 = time.time()
-    corpus = make_corpus(args.rows, args.users, seed)
-    gen_s = time.time() - t0
-    tmp = Path(tempfile.mkdtemp(prefix="fbxbench"))
-    write_corpus(corpus, tmp)
+    # what this rank extracts per step: one log (seed 11 + rank, weak scaling)
+    # or, in C5 mode, its share of independent 1M-record shards (seeds 1000+k)
+    if args.shards:
+        seeds = [args.shard_seed0 + k for k in range(args.shards) if k % world == rank]
+    else:
+        seeds = [args.seed + rank]
     raw = workload_config(args.dag)
-    if args.dag == "lookup_heavy":
-        write_lookup_tables(tmp, args.users)
-    cfg = config_from_dict(raw, tmp)
-    views = {"user_events": corpus.driver, "user_profile": corpus.profile}
-    t1 = time.time()
-    prep = E.prepare(cfg, views, corpus.basic)
-    eng = E.Engine(prep, views, corpus.basic, device=str(dev), max_rows_per_launch=args.rows)
-    dview = E.DeviceView(corpus.driver, device=dev)
-    eng.bind_driver(dview)
-    prep_s = time.time() - t1
-    n = corpus.driver.row_count
+    t0 = time.time()
+    shards, gen_s, prep_s = [], 0.0, 0.0
+    for sd in seeds:
+        t0 = time.time()
+        corpus = make_corpus(args.rows, args.users, sd)
+        gen_s += time.time() - t0
+        tmp = Path(tempfile.mkdtemp(prefix="fbxbench"))
+        write_corpus(corpus, tmp)
+        if args.dag == "lookup_heavy":
+            write_lookup_tables(tmp, args.users)
+        cfg = config_from_dict(raw, tmp)
+        views = {"user_events": corpus.driver, "user_profile": corpus.profile}
+        t1 = time.time()
+        prep = E.prepare(cfg, views, corpus.basic)
+        eng = E.Engine(prep, views, corpus.basic, device=str(dev),
+                       max_rows_per_launch=min(args.rows, args.launch_rows))
+        eng.bind_driver(E.DeviceView(corpus.driver, device=dev))
+        eng.reserve(corpus.driver.row_count, eng.max_rows)
+        prep_s += time.time() - t1
+        shards.append((corpus, eng, tmp, cfg))
+    corpus, eng, tmp, cfg = shards[0]
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    launches = [0]
 
-    def step():
+    def run_shard(eng, n, ev=None):
+        """One pass over a shard: clear the run's id set, then launches of at
+        most --launch-rows rows with the look-back continuing across them."""
         eng.begin_run(n)
-        eng.launch(0, n)
+        launches[0] += 1  # fbx_state_reset (k_state_reset)
+        if ev is not None:
+            ev[0].record(stream)
+        for lo in range(0, n, eng.max_rows):
+            eng.launch(lo, min(lo + eng.max_rows, n), tile_base=lo // eng.ir.chunk)
+            launches[0] += 1  # fbx_pipeline
+        if ev is not None:
+            ev[1].record(stream)
 
-    # ---- warmup + correctness of every step --------------------------------
+    # ---- warmup + correctness of every shard ---------------------------------
     for _ in range(max(args.warmup, 3)):
-        step()
-    batch = eng.finish()
-    c = batch.counters
-    if args.rows == 1_000_000 and args.users == 5000 and args.seed == 11 and rank == 0:
+        for corp, e, _, _ in shards:
+            run_shard(e, corp.driver.row_count)
+    results = [e.finish().counters for _, e, _, _ in shards]
+    c = results[0]
+    if (args.rows == 1_000_000 and args.users == 5000 and args.seed == 11 and rank == 0
+            and not args.shards):
         want = GOLDEN_1M.get(args.dag)
         if want and (c.digest, c.instances, c.signs) != want:
             raise SystemExit(f"parity failure: got digest 0x{c.digest:016x} / {c.instances} / "
                              f"{c.signs}, want 0x{want[0]:016x} / {want[1]} / {want[2]}")
-    ab = algorithmic_bytes(corpus, c)
+    ab = None
+    for (corp, _, _, _), cc in zip(shards, results):
+        b = algorithmic_bytes(corp, cc)
+        ab = b if ab is None else {k: ab[k] + b[k] for k in ab}
 
     # ---- timed device-resident steps ---------------------------------------
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in shards] for _ in range(K)]
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(K)]
     clocks = Clocks(local)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     clocks.start()
+    launches[0] = 0
     for k in range(K):
         runtime.l2_flush(flush.data_ptr(), flush.numel(), stream.cuda_stream)  # L2 flush
-        ev[k][0].record(stream)
-        eng.begin_run(n)
-        ev[k][1].record(stream)
-        eng.launch(0, n)
-        ev[k][2].record(stream)
+        step_ev[k][0].record(stream)
+        for (corp, e, _, _), ev in zip(shards, evs[k]):
+            run_shard(e, corp.driver.row_count, ev)
+        step_ev[k][1].record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     if dist:
         dist.barrier()
-    step_ms = [a.elapsed_time(b2) for a, _, b2 in ev]
-    kern_ms = [b1.elapsed_time(b2) for _, b1, b2 in ev]
-    c = eng.finish().counters
-    total_ms = sum(step_ms)
-    tot = torch.tensor([total_ms, sum(kern_ms)], dtype=torch.float64, device=dev)
+    total_ms = sum(a.elapsed_time(b) for a, b in step_ev)
+    kern_total = sum(a.elapsed_time(b) for row in evs for a, b in row)
+    results = [e.finish().counters for _, e, _, _ in shards]
+    tot = torch.tensor([total_ms, kern_total], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     total_ms, kern_total = float(tot[0]), float(tot[1])
     # the one collective: all-gather of per-shard counters (distributed.py)
     from paper_2210_07768_b200.distributed import ShardResult, all_gather_results, combine
-    shard = ShardResult(n, c.instances, c.signs, c.digest, c.malformed, c.filtered)
+    mine = combine([ShardResult(corp.driver.row_count, r.instances, r.signs, r.digest,
+                                r.malformed, r.filtered)
+                    for (corp, _, _, _), r in zip(shards, results)])
+    shard = ShardResult(mine.records, mine.instances, mine.signs, mine.digest, mine.malformed,
+                        mine.filtered)
     totals = all_gather_results(shard, device=dev) if dist else combine([shard])
     run_digest = totals.digest
     records_all = totals.records
     value = records_all * K / (total_ms / 1e3)
     ms_per_step = total_ms / K
     kern_avg_s = kern_total / K / 1e3
+    n = corpus.driver.row_count
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -289,7 +325,7 @@ def main():
 
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and len(shards) == 1:
         e2e = measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist)
 
     cpu = None
@@ -298,23 +334,27 @@ def main():
             cpu = cpu_baseline(corpus, raw, tmp, args.cpu_sample_rows)
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "error": str(exc)[:200]}
-    launches_per_step = 2  # fbx_state_reset + fbx_pipeline (id-set clear is a memset)
     out = {
         "metric": "raw log records/sec extracted (device-resident input)",
         "value": round(value, 1), "unit": "records/s", "n_gpus": world, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (gen_corpus restatement, byte-identical to the reference)",
-        "config": {"workload": f"{args.dag} DAG (SURVEY Appendix B), {args.rows} records/GPU, "
-                               f"users {args.users}, seed {args.seed}+rank, full emit incl. "
-                               "basic merge", "batch_size": cfg.batch_size,
+        "config": {"workload": (f"{args.dag} DAG (SURVEY Appendix B), "
+                                + (f"C5: {len(shards)} of {args.shards} independent "
+                                   f"{args.rows}-record shards (seeds {args.shard_seed0}+k) "
+                                   "on this rank" if args.shards else
+                                   f"{args.rows} records/GPU, seed {args.seed}+rank")
+                                + f", users {args.users}, full emit incl. basic merge"),
+                   "batch_size": cfg.batch_size,
                    "l2": "flushed between steps (512 MiB write, outside the timed events)",
                    "parallelism": f"record-sharded x{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": launches_per_step * K, "clocks": clk,
+        "gpu_launches": launches[0], "clocks": clk,
         "parity": {"digest": f"0x{run_digest:016x}", "instances": totals.instances,
                    "signs": totals.signs},
         "setup_s": {"corpus": round(gen_s, 1), "prepare": round(prep_s, 1)},
+        "records_per_step": records_all,
     }
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -34,6 +34,18 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
 
 
+GEN_LIB = PKG / "libfbxgen.so"
+GEN_SRC = PKG / "csrc" / "corpus_gen.c"
+
+
+def build_corpus_gen(force: bool = False) -> Path:
+    """gcc build of the bulk corpus generator (measurement input)."""
+    if force or not GEN_LIB.exists() or GEN_SRC.stat().st_mtime > GEN_LIB.stat().st_mtime:
+        subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-o", str(GEN_LIB), str(GEN_SRC)],
+                       check=True)
+    return GEN_LIB
+
+
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     if force or stale():
         cmd = nvcc_command()
@@ -45,3 +57,4 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
 
 if __name__ == "__main__":
     build_library(force=True, verbose=True)
+    build_corpus_gen(force=True)

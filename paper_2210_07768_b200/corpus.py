@@ -6,7 +6,7 @@ from one ``random.Random(seed)`` (MT19937, CPython's algorithms) in the
 reference's order -- driver rows (``_driver_batch`` :52-108), then the profile
 side view (:111-123), then basic payloads (:126-143).  The column images are
 built directly (``ViewImage``), so nothing round-trips through files unless
-``write`` is asked for.  ``gen_corpus_fast`` (C, ``csrc/corpus_gen.c``) is the
+``write`` is asked for.  ``make_corpus_fast`` (C, ``csrc/corpus_gen.c``) is the
 bulk path used by the benchmark and is checked against this one in tests.
 """
 
@@ -130,6 +130,74 @@ def make_corpus(rows: int = 20_000, users: int = 2_000, seed: int = 7,
     if views == 2:
         profile = ViewImage.from_pydict(PROFILE_SPEC, _draw_profile(users, rng), ("user_id",))
     basic = ViewImage.from_pydict(BASIC_SPEC, _draw_basic(rows, rng), ("instance_id",))
+    city = {c: fnv1a64(c.encode()) for c in CITIES} if views == 2 else None
+    return Corpus(driver, profile, basic, city, rows, users, seed)
+
+
+def make_corpus_fast(rows: int = 20_000, users: int = 2_000, seed: int = 7,
+                     views: int = 2) -> Corpus:
+    """``make_corpus`` through the C generator (csrc/corpus_gen.c): the same
+    bytes, ~100x faster -- used for the 1M..100M-record benchmark logs."""
+    import ctypes
+
+    from .build import build_corpus_gen
+    if rows < 0 or users < 1 or views not in (1, 2):
+        raise ValueError("bad corpus parameters")
+    lib = ctypes.CDLL(str(build_corpus_gen()))
+
+    class Out(ctypes.Structure):
+        _fields_ = [(n, ctypes.c_void_p) for n in (
+            "id", "label", "user", "age", "id_n", "label_n", "user_n", "query_n", "meta_n",
+            "age_n", "query_off", "meta_off", "query", "meta", "p_user", "p_user_n",
+            "p_city_n", "p_score_n", "p_city_off", "p_city", "p_score", "b_id", "b_a", "b_b",
+            "b_id_n", "b_a_n", "b_b_n", "b_pay_n", "b_pay")] + [("profile_rows", ctypes.c_uint64)]
+
+    nb = (rows + 7) // 8
+    ub = (users + 7) // 8
+    arr = {
+        "id": np.zeros(rows, np.int64), "label": np.zeros(rows, np.int64),
+        "user": np.zeros(rows, np.int64), "age": np.zeros(rows, np.int64),
+        "query_off": np.zeros(rows + 1, np.uint32), "meta_off": np.zeros(rows + 1, np.uint32),
+        "query": np.zeros(rows * 48 + 64, np.uint8), "meta": np.zeros(rows * 64 + 64, np.uint8),
+        "p_user": np.zeros(users, np.int64), "p_city_off": np.zeros(users + 1, np.uint32),
+        "p_city": np.zeros(users * 16 + 16, np.uint8), "p_score": np.zeros(users, np.float32),
+        "b_id": np.zeros(rows, np.int64), "b_a": np.zeros(rows, np.int64),
+        "b_b": np.zeros(rows, np.int64), "b_pay": np.zeros(rows, np.float32)}
+    for k in ("id_n", "label_n", "user_n", "query_n", "meta_n", "age_n", "b_id_n", "b_a_n",
+              "b_b_n", "b_pay_n"):
+        arr[k] = np.zeros(nb, np.uint8)
+    for k in ("p_user_n", "p_city_n", "p_score_n"):
+        arr[k] = np.zeros(ub, np.uint8)
+    out = Out(**{k: a.ctypes.data for k, a in arr.items()})
+    lib.fbxgen_corpus(ctypes.c_uint64(rows), ctypes.c_uint64(users), ctypes.c_uint64(seed),
+                      ctypes.c_int(views), ctypes.byref(out))
+    a = arr
+    C = ColumnImage
+    driver = ViewImage({
+        "instance_id": C(Kind.INT64, rows, a["id_n"], a["id"]),
+        "label": C(Kind.INT64, rows, a["label_n"], a["label"]),
+        "user_id": C(Kind.INT64, rows, a["user_n"], a["user"]),
+        "query": C(Kind.UTF8, rows, a["query_n"], a["query"][: a["query_off"][-1]],
+                   a["query_off"]),
+        "meta": C(Kind.JSON, rows, a["meta_n"], a["meta"][: a["meta_off"][-1]], a["meta_off"]),
+        "age": C(Kind.INT64, rows, a["age_n"], a["age"])},
+        ("user_id",), tuple(n for n, _ in DRIVER_SPEC))
+    profile = None
+    if views == 2:
+        np_ = int(out.profile_rows)
+        pb = (np_ + 7) // 8
+        off = a["p_city_off"][: np_ + 1]
+        profile = ViewImage({
+            "user_id": C(Kind.INT64, np_, a["p_user_n"][:pb].copy(), a["p_user"][:np_]),
+            "city": C(Kind.UTF8, np_, a["p_city_n"][:pb].copy(), a["p_city"][: off[-1]], off),
+            "score": C(Kind.FLOAT32, np_, a["p_score_n"][:pb].copy(), a["p_score"][:np_])},
+            ("user_id",), tuple(n for n, _ in PROFILE_SPEC))
+    basic = ViewImage({
+        "instance_id": C(Kind.INT64, rows, a["b_id_n"], a["b_id"]),
+        "basic_a": C(Kind.INT64, rows, a["b_a_n"], a["b_a"]),
+        "basic_b": C(Kind.INT64, rows, a["b_b_n"], a["b_b"]),
+        "payload": C(Kind.FLOAT32, rows, a["b_pay_n"], a["b_pay"])},
+        ("instance_id",), tuple(n for n, _ in BASIC_SPEC))
     city = {c: fnv1a64(c.encode()) for c in CITIES} if views == 2 else None
     return Corpus(driver, profile, basic, city, rows, users, seed)
 

@@ -463,8 +463,13 @@ class Engine:
         raise StageError(stage, None if stage == "prepare" else chunk, cause)
 
     def begin_run(self, rows_hint: int):
-        """Clear the run-wide instance-id set (check_unique_ids' `seen`)."""
+        """Start a run: clear the run-wide instance-id set (check_unique_ids'
+        `seen`), the counters / error word, and -- for a reserved run -- the
+        look-back status of every tile."""
         torch = self.torch
+        if getattr(self, "status", None) is not None:
+            runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(),
+                                self.status.numel(), self._stream())
         cap = _next_pow2(2 * max(rows_hint, 1))
         if self.idset is None or self._idset_cap < cap:
             self.idset = torch.zeros(cap + 2, dtype=torch.int64, device=self.device)
@@ -536,8 +541,11 @@ class Engine:
             runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(), tiles + 1, stream)
             tile_base = 0
         else:
+            # continuation of a reserved run: counters / digest / error word keep
+            # accumulating across launches; only the bump pool is reset
             tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
-            runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(), 0, stream)
+            with self.torch.cuda.stream(self.torch.cuda.ExternalStream(stream)):
+                self.state[1:2].zero_()
         self._set("row_lo", row_lo)
         self._set("row_hi", row_hi)
         self._set("chunk0", row_lo // self.ir.chunk)
@@ -625,11 +633,10 @@ class StreamedRun:
     def run(self) -> Counters:
         torch, eng = self.torch, self.eng
         eng.reserve(self.n, self.slice_rows)
+        eng.begin_run(self.n)
         cur = torch.cuda.current_stream(eng.device)
         self.s_comp.wait_stream(cur)
         self.s_h2d.wait_stream(cur)
-        with torch.cuda.stream(self.s_comp):
-            eng.status.zero_()
         comp_done = [torch.cuda.Event() for _ in self.bounds]
         h2d_done = [torch.cuda.Event() for _ in self.bounds]
         d2h_done = [torch.cuda.Event() for _ in self.bounds]
@@ -644,7 +651,8 @@ class StreamedRun:
             st = self.states[j].numpy().view(np.uint64)
             stt = {f: int(st[i]) for i, f in enumerate(runtime.STATE_FIELDS)}
             eng._raise_if_error(stt)
-            ni, ms = stt["instances"], stt["signs"]
+            # counters accumulate over the run's launches: this slice's share
+            ni, ms = stt["instances"] - inst_base, stt["signs"] - sign_base
             with torch.cuda.stream(self.s_d2h):
                 self.s_d2h.wait_event(comp_done[j])
                 o = self.out
@@ -659,12 +667,10 @@ class StreamedRun:
                 d2h_done[j].record(self.s_d2h)
             inst_base += ni
             sign_base += ms
-            tot.digest ^= stt["digest"]
-            tot.instances += ni
-            tot.signs += ms
-            tot.malformed += stt["malformed"]
-            tot.filtered += stt["filtered"]
-            tot.joined += stt["joined"]
+            tot.digest = stt["digest"]
+            tot.instances, tot.signs = stt["instances"], stt["signs"]
+            tot.malformed, tot.filtered = stt["malformed"], stt["filtered"]
+            tot.joined = stt["joined"]
             tot.launches += 1
 
         for k, (lo, hi) in enumerate(self.bounds):

@@ -29,6 +29,16 @@ def test_corpus_is_byte_identical_to_reference(goldens, tmp_path):
         assert got == want, key
 
 
+@pytest.mark.parametrize("rows,users,seed,views", [(3000, 300, 7, 2), (1200, 200, 11, 1),
+                                                   (4000, 5000, 2**40 + 3, 2), (0, 5, 1, 2)])
+def test_fast_generator_is_byte_identical(rows, users, seed, views, tmp_path):
+    from paper_2210_07768_b200.corpus import make_corpus, make_corpus_fast, write_corpus
+    fa = write_corpus(make_corpus(rows, users, seed, views), tmp_path / "py")
+    fb = write_corpus(make_corpus_fast(rows, users, seed, views), tmp_path / "c")
+    for k in fa:
+        assert fa[k].read_bytes() == fb[k].read_bytes(), k
+
+
 def test_fbxc_roundtrip_and_crc(tmp_path):
     v = ViewImage.from_pydict([("a", Kind.INT64), ("s", Kind.UTF8), ("f", Kind.FLOAT32)],
                               {"a": [1, None, -3], "s": ["x", "é", None], "f": [0.5, None, 2.0]})
