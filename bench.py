@@ -61,7 +61,7 @@ def parse_args():
     ap.add_argument("--rows", type=int, default=1_000_000)
     ap.add_argument("--users", type=int, default=5000)
     ap.add_argument("--seed", type=int, default=11)
-    ap.add_argument("--cpu-sample-rows", type=int, default=8192)
+    ap.add_argument("--cpu-sample-rows", type=int, default=24576)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--shards", type=int, default=0,
@@ -220,7 +220,7 @@ def main():
         t1 = time.time()
         prep = E.prepare(cfg, views, corpus.basic)
         eng = E.Engine(prep, views, corpus.basic, device=str(dev),
-                       max_rows_per_launch=min(args.rows, args.launch_rows))
+                       max_rows_per_launch=args.launch_rows)
         eng.bind_driver(E.DeviceView(corpus.driver, device=dev))
         eng.reserve(corpus.driver.row_count, eng.max_rows)
         prep_s += time.time() - t1

@@ -313,7 +313,8 @@ class Engine:
         self.prog = prepared.program
         self.slots = self.prog.slots
         self.params = np.zeros(runtime.FBX_MAX_PARAM_SLOTS, dtype=np.uint64)
-        self.max_rows = max_rows_per_launch - max_rows_per_launch % ir.chunk or ir.chunk
+        # launches cover whole chunks; round UP so a run of <= max rows is one launch
+        self.max_rows = -(-max_rows_per_launch // ir.chunk) * ir.chunk
         self.pool_bytes_per_row = pool_bytes_per_row
         with torch.cuda.device(self.device):
             self.module = runtime.Program(prepared.cubin)
