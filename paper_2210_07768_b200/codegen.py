@@ -1148,15 +1148,24 @@ class PlanCodegen:
             g("const u32 tile_signs = sm.scan.sum(m);")
         g("// publish the aggregate now: successors' look-back overlaps our sort")
         g("if (threadIdx.x == 0) fbx::publish_aggregate(STATUS, tile, n_inst, tile_signs);")
-        g("// the staged record spans are dead now: the sort reuses that memory.")
-        g("// Emitted ids are unique (else the run fails), so a row's rank is the")
-        g("// number of sorted keys below its id; dead rows sort last as ~0.")
+        g("// the staged record spans are dead now: the rank pass reuses that memory.")
+        g("// Emitted ids are unique (else the run fails): a row's rank is the number")
+        g("// of live ids below its own.  Adaptive radix buckets; bitonic fallback.")
         g("u64* sbuf = (u64*)dyn_smem;")
+        g("u32 myrank = 0;")
+        g("{")
+        g("u64 kor, kand;")
+        g("fbx::block_or_and<NT>(alive ? skey : 0ull, alive ? skey : ~0ull, sbuf, &kor, &kand);")
+        g("u32* hist = (u32*)(sbuf + NT); u32* bstart = hist + 1024;")
+        g("if (!fbx::radix_rank<NT>(skey, alive, kor ^ kand, hist, bstart, sbuf, sm.scan, &myrank)) {")
         g("const u64 sorted = fbx::bitonic_keys<NT>(skey, sbuf);")
-        g("sm.soff[threadIdx.x] = 0u;")
         g("sbuf[2 * NT + threadIdx.x] = sorted;")
         g("__syncthreads();")
-        g("const u32 myrank = alive ? fbx::lower_rank<NT>(sbuf + 2 * NT, skey) : 0u;")
+        g("myrank = alive ? fbx::lower_rank<NT>(sbuf + 2 * NT, skey) : 0u;")
+        g("}")
+        g("}")
+        g("sm.soff[threadIdx.x] = 0u;")
+        g("__syncthreads();")
         g("if (alive) sm.soff[myrank] = m;")
         g("__syncthreads();")
         g("const u32 s_off = sm.scan.exclusive(sm.soff[threadIdx.x]);")
@@ -1388,9 +1397,10 @@ class PlanCodegen:
         # Sized so MIN_BLOCKS CTAs fit an SM (227 KB); a tile whose CSR does not
         # fit is written directly.
         per_cta = (227 * 1024) // self.min_blocks - STATIC_SMEM_EST - 1024
-        need = max(self.span_cap, 24 * self.nt, self.nt * (17 + 10 * k) + 64)
-        self.dyn_smem = max(self.span_cap, 24 * self.nt,
-                            min(need, per_cta, OUT_BUDGET)) // 16 * 16  # sort: 3*NT u64
+        need = max(self.span_cap, 24 * self.nt, 8 * self.nt + 8192, self.nt * (17 + 10 * k) + 64)
+        rank_bytes = max(24 * self.nt, 8 * self.nt + 8192)  # bitonic 3*NT u64 | radix
+        self.dyn_smem = max(self.span_cap, rank_bytes,
+                            min(need, per_cta, OUT_BUDGET)) // 16 * 16
         self.g.slot("state")  # slot 0
         if ir.mode == "extract":
             kname = self.extract_rows_kernel()

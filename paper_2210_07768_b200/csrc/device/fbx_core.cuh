@@ -167,23 +167,55 @@ FBX_DI Str str_token(Str s, u32 delim, u32 index) {
   return Str{s.p, 0u};
 }
 
-// Up to 4 fields of one split in one pass (codegen groups token calls that
-// share an input and a delimiter).  fields[k] = field number wanted at k.
+// exact per-byte zero test: 0x80 in every byte of x that is 0x00
+FBX_DI u32 zero_bytes(u32 x) { return ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u; }
+
+// 4 bytes of a span starting at byte k (funnel-shifted aligned words; reads
+// only words that hold bytes of the span)
+struct WordCursor {
+  const u32* wp;
+  u32 sh, n;
+  FBX_DI WordCursor(const u8* p, u32 len) : n(len) {
+    const u64 a = (u64)p;
+    sh = (u32)(a & 3u) * 8u;
+    wp = (const u32*)(a & ~3ull);
+  }
+  FBX_DI u32 word(u32 k) const {  // bytes [k, k+4) (k % 4 == 0), bytes past n are garbage
+    const u32 lo = wp[k >> 2];
+    const bool need = sh && (k + 4u - sh / 8u) < n;  // next word holds span bytes
+    const u32 hi = need ? wp[(k >> 2) + 1] : 0u;
+    return __funnelshift_r(lo, hi, sh);
+  }
+};
+
+// Several fields of one single-byte split in one SWAR pass (codegen groups
+// token calls that share an input and a delimiter).  want[k] = field number.
 template <int K>
 FBX_DI void str_tokens(Str s, u32 delim, const u32 (&want)[K], Str (&out)[K]) {
 #pragma unroll
   for (int k = 0; k < K; ++k) out[k] = Str{s.p, 0u};
   u32 field = 0, start = 0;
-  for (u32 i = 0; i <= s.n; ++i) {
-    bool end = (i == s.n);
-    if (end || s.p[i] == delim) {
+  if (s.n) {
+    const WordCursor wc(s.p, s.n);
+    const u32 dm = delim * 0x01010101u;
+    for (u32 b = 0; b < s.n; b += 4u) {
+      u32 z = zero_bytes(wc.word(b) ^ dm);
+      const u32 left = s.n - b;
+      if (left < 4u) z &= (1u << (left * 8u)) - 1u;
+      while (z) {
+        const u32 pos = b + ((u32)(__ffs(z) - 1) >> 3);
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (want[k] == field) out[k] = Str{s.p + start, i - start};
-      ++field;
-      start = i + 1;
+        for (int k = 0; k < K; ++k)
+          if (want[k] == field) out[k] = Str{s.p + start, pos - start};
+        ++field;
+        start = pos + 1u;
+        z &= z - 1u;
+      }
     }
   }
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (want[k] == field) out[k] = Str{s.p + start, s.n - start};
 }
 
 // str.isspace() for a decoded code point (CPython 3.12 / Unicode 15)
@@ -245,13 +277,17 @@ FBX_DI Str str_trim(Str s) {
 // lower (featureops.py:298-299): 0 = unchanged (view ok), 1 = ASCII changes,
 // 2 = non-ASCII present (needs the Unicode tables: not supported on device)
 FBX_DI u32 str_lower_class(Str s) {
-  u32 cls = 0;
-  for (u32 i = 0; i < s.n; ++i) {
-    u32 c = s.p[i];
-    if (c >= 0x80u) return 2;
-    if (c >= 'A' && c <= 'Z') cls = 1;
+  if (s.n == 0) return 0;
+  const WordCursor wc(s.p, s.n);
+  u32 up = 0;
+  for (u32 b = 0; b < s.n; b += 4u) {
+    u32 w = wc.word(b);
+    const u32 left = s.n - b;
+    if (left < 4u) w &= (1u << (left * 8u)) - 1u;  // garbage bytes -> 0 (not upper, ASCII)
+    if (w & 0x80808080u) return 2;
+    up |= (w + 0x3F3F3F3Fu) & ~(w + 0x25252525u);  // 'A'..'Z' -> bit 7
   }
-  return cls;
+  return (up & 0x80808080u) ? 1u : 0u;
 }
 
 FBX_DI void str_lower_copy(u8* dst, Str s) {
@@ -508,6 +544,83 @@ FBX_DI u64 bitonic_keys(u64 key, u64* buf) {
   return key;
 }
 
+
+// Rank of each live key among the tile's live keys (keys unique among live
+// rows): an adaptive radix bucket pass.  `diff` = OR ^ AND of the live keys
+// (the bits that vary); bucket = the 10 bits below the highest varying bit, so
+// random ids and sequential ids alike spread over 1024 buckets; each key's
+// rank = bucket start + number of smaller keys in its (small) bucket.  Returns
+// false (CTA-uniformly) when some bucket holds more than 32 keys -- the caller
+// then uses the bitonic network.  smem: hist u32[1024], start u32[1024],
+// keys u64[NT].
+template <int NT>
+FBX_DI bool radix_rank(u64 key, bool live, u64 diff, u32* hist, u32* start, u64* bkeys,
+                       BlockScanU32<NT>& scan, u32* rank) {
+  constexpr int BPT = 1024 / NT;  // buckets per thread
+  const u32 hb = diff ? 63u - (u32)__clzll((long long)diff) : 0u;
+  const u32 shift = hb >= 9u ? hb - 9u : 0u;
+  const u32 digit = (u32)(key >> shift) & 1023u;
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) hist[threadIdx.x * BPT + b] = 0u;
+  __syncthreads();
+  u32 pos = 0;
+  if (live) pos = atomicAdd(&hist[digit], 1u);
+  __syncthreads();
+  u32 sz[BPT], tot = 0;
+  bool big = false;
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    sz[b] = hist[threadIdx.x * BPT + b];
+    tot += sz[b];
+    big |= sz[b] > 32u;
+  }
+  if (__syncthreads_or(big)) return false;
+  u32 run = scan.exclusive(tot);
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    start[threadIdx.x * BPT + b] = run;
+    run += sz[b];
+  }
+  __syncthreads();
+  u32 b0 = 0, bn = 0;
+  if (live) {
+    b0 = start[digit];
+    bn = hist[digit];
+    bkeys[b0 + pos] = key;
+  }
+  __syncthreads();
+  if (live) {
+    u32 r = b0;
+    for (u32 q = 0; q < bn; ++q) r += bkeys[b0 + q] < key ? 1u : 0u;
+    *rank = r;
+  }
+  return true;
+}
+
+// block-wide OR and AND of a u64 (all threads receive both)
+template <int NT>
+FBX_DI void block_or_and(u64 vo, u64 va, u64* red, u64* o, u64* a) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    vo |= __shfl_xor_sync(0xFFFFFFFFu, vo, d);
+    va &= __shfl_xor_sync(0xFFFFFFFFu, va, d);
+  }
+  if ((threadIdx.x & 31u) == 0) {
+    red[threadIdx.x >> 5] = vo;
+    red[(NT / 32) + (threadIdx.x >> 5)] = va;
+  }
+  __syncthreads();
+  u64 ro = 0, ra = ~0ull;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    ro |= red[w];
+    ra &= red[(NT / 32) + w];
+  }
+  *o = ro;
+  *a = ra;
+  __syncthreads();
+}
+
 // Rank of `key` among the NT sorted keys in buf (number of keys < key).
 template <int NT>
 FBX_DI u32 lower_rank(const u64* sorted, u64 key) {
@@ -619,7 +732,11 @@ FBX_DI void lookback(u64* status, u32 tile, u64 inst, u64 signs, u64* ex_inst, u
     i64 idx = base - (i64)lane;
     u64 w = 0;
     if (idx >= 0) {
-      do { w = ld_acquire(status + idx); } while ((w >> 62) == 0);
+      w = ld_acquire(status + idx);
+      while ((w >> 62) == 0) {  // predecessor not published yet: yield the issue slot
+        __nanosleep(64);
+        w = ld_acquire(status + idx);
+      }
     } else {
       w = pack_status(2, 0, 0);
     }
