@@ -54,7 +54,9 @@ def library_source() -> str:
     """fbx_abi.h + fbx_core.cuh, flattened for NVRTC (no include paths)."""
     abi = (INCLUDE / "fbx_abi.h").read_text()
     core = (CSRC / "device" / "fbx_core.cuh").read_text()
-    return abi + "\n" + core.replace('#include "fbx_abi.h"', "")
+    uni = (CSRC / "device" / "fbx_unicode.cuh").read_text()
+    return abi + "\n" + core.replace('#include "fbx_abi.h"', "").replace(
+        '#include "fbx_unicode.cuh"', uni)
 
 
 # ---------------------------------------------------------------------------
@@ -757,15 +759,24 @@ class PlanCodegen:
         if op == "lower":
             a = self.as_str(args[0], fn.spec)
             if a.lower:
-                return a
+                return a  # str.lower is idempotent (checked over all code points)
             cls = g.fresh("lc")
             cond = f"alive && !{a.n}" if a.nullable else "alive"
             g(f"u32 {cls} = ({cond}) ? fbx::str_lower_class({a.c}) : 0u;")
-            g(f"if ({cls} == 2u) {{")
-            err("unicode_lower")
-            g("}")
-            # ASCII-only from here on: a lazy view, lowercased by its consumers
-            return V("str", a.c, a.nullable, a.lone, lower=True)
+            # non-ASCII rows: full Unicode lower() materialised from the pool;
+            # ASCII rows stay a lazy view, lowercased by their consumers
+            sz = g.fresh("lz")
+            g(f"const u32 {sz} = ({cls} == 2u) ? fbx::unicode_lower({a.c}, nullptr) : 0u;")
+            ptr = self.pool_alloc(sz)
+            out = V("str", g.fresh("n"), a.nullable, a.lone, lower=True)
+            g(f"fbx::Str {out.c} = {a.c};")
+            if a.nullable:
+                g(f"bool {out.c}_n = {a.n};")
+            if a.lone:
+                g(f"bool {out.c}_l = {a.l};")
+            g(f"if ({cls} == 2u && ({ptr} || {sz} == 0u)) {{ fbx::unicode_lower({a.c}, {ptr});"
+              f" {out.c} = fbx::Str{{{ptr}, {sz}}}; }}")
+            return out
         if op == "lookup":
             a = args[0]
             out = V("u64", g.fresh("n"), False)

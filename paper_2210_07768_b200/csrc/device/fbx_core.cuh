@@ -93,9 +93,10 @@ struct Fnv {
   FBX_DI void bytes_lower(const u8* p, u32 n) { bytes_t<true>(p, n); }
   // ASCII lowercase of 4 packed bytes (all < 0x80): 'A'..'Z' -> 'a'..'z'
   static FBX_DI u32 lower_word(u32 w) {
-    u32 ge_a = w + 0x3F3F3F3Fu;  // byte >= 0x41 -> bit 7 set
-    u32 gt_z = w + 0x25252525u;  // byte >= 0x5B -> bit 7 set
-    u32 up = ge_a & ~gt_z & 0x80808080u;
+    const u32 w7 = w & 0x7F7F7F7Fu;      // no carries between bytes
+    u32 ge_a = w7 + 0x3F3F3F3Fu;         // byte >= 0x41 -> bit 7 set
+    u32 gt_z = w7 + 0x25252525u;         // byte >= 0x5B -> bit 7 set
+    u32 up = ge_a & ~gt_z & ~w & 0x80808080u;  // ASCII 'A'..'Z' only
     return w | (up >> 2);
   }
 };
@@ -288,6 +289,103 @@ FBX_DI u32 str_lower_class(Str s) {
     up |= (w + 0x3F3F3F3Fu) & ~(w + 0x25252525u);  // 'A'..'Z' -> bit 7
   }
   return (up & 0x80808080u) ? 1u : 0u;
+}
+
+}  // namespace fbx
+#include "fbx_unicode.cuh"
+namespace fbx {
+
+// ---------------------------------------------------------------------------
+// Full Unicode lower() (CPython 3.12, Unicode 15.0): _PyUnicode_ToLowerFull +
+// Final_Sigma (unicodeobject.c handle_capital_sigma), tables generated from
+// CPython itself (unicode_tables.py).  Only reached for strings with bytes
+// >= 0x80; ASCII strings take the lazy SWAR path.
+// ---------------------------------------------------------------------------
+FBX_DI bool u_in(u32 cp, const u32* lo, const u32* hi, u32 n) {
+  u32 a = 0, b = n;
+  while (a < b) {
+    const u32 m = (a + b) >> 1;
+    if (__ldg(lo + m) <= cp) a = m + 1; else b = m;
+  }
+  return a > 0 && cp <= __ldg(hi + a - 1);
+}
+FBX_DI u32 u_lower_single(u32 cp) {
+  u32 a = 0, b = ULOWER_N;
+  while (a < b) {
+    const u32 m = (a + b) >> 1;
+    const u32 f = __ldg(ULOWER_FROM + m);
+    if (f == cp) return __ldg(ULOWER_TO + m);
+    if (f < cp) a = m + 1; else b = m;
+  }
+  return cp;
+}
+FBX_DI u32 utf8_len(u32 cp) { return cp < 0x80u ? 1u : cp < 0x800u ? 2u : cp < 0x10000u ? 3u : 4u; }
+FBX_DI void utf8_put(u8* d, u32 cp) {  // surrogates encode as WTF-8 3-byte units
+  if (cp < 0x80u) { d[0] = (u8)cp; return; }
+  if (cp < 0x800u) { d[0] = (u8)(0xC0u | (cp >> 6)); d[1] = (u8)(0x80u | (cp & 0x3Fu)); return; }
+  if (cp < 0x10000u) {
+    d[0] = (u8)(0xE0u | (cp >> 12));
+    d[1] = (u8)(0x80u | ((cp >> 6) & 0x3Fu));
+    d[2] = (u8)(0x80u | (cp & 0x3Fu));
+    return;
+  }
+  d[0] = (u8)(0xF0u | (cp >> 18));
+  d[1] = (u8)(0x80u | ((cp >> 12) & 0x3Fu));
+  d[2] = (u8)(0x80u | ((cp >> 6) & 0x3Fu));
+  d[3] = (u8)(0x80u | (cp & 0x3Fu));
+}
+FBX_DI bool u_cased(u32 cp) { return u_in(cp, UCASED_LO, UCASED_HI, UCASED_N); }
+FBX_DI bool u_ignorable(u32 cp) { return u_in(cp, UIGN_LO, UIGN_HI, UIGN_N); }
+
+// U+03A3 at byte `pos` (2 bytes): final sigma when preceded (skipping case-
+// ignorables) by a cased letter and not followed (likewise) by one.
+FBX_DI u32 sigma_lower(Str s, u32 pos) {
+  bool fin = false;
+  u32 j = pos;
+  while (j > 0) {
+    do { --j; } while (j > 0 && (s.p[j] & 0xC0u) == 0x80u);
+    u32 cp;
+    utf8_at(s.p, j, s.n, &cp);
+    if (!u_ignorable(cp)) { fin = u_cased(cp); break; }
+  }
+  if (fin) {
+    u32 k = pos + 2u;
+    while (k < s.n) {
+      u32 cp;
+      const u32 l = utf8_at(s.p, k, s.n, &cp);
+      if (!u_ignorable(cp)) { fin = !u_cased(cp); break; }
+      k += l;
+    }
+  }
+  return fin ? 0x3C2u : 0x3C3u;
+}
+
+// str.lower() of a UTF-8 (or WTF-8) span into dst; returns the byte length
+// (dst == nullptr: length only).
+FBX_DI u32 unicode_lower(Str s, u8* dst) {
+  u32 o = 0;
+  for (u32 i = 0; i < s.n;) {
+    const u32 c = s.p[i];
+    if (c < 0x80u) {
+      if (dst) dst[o] = (u8)((c - 'A' < 26u) ? c + 32u : c);
+      ++o;
+      ++i;
+      continue;
+    }
+    u32 cp;
+    const u32 len = utf8_at(s.p, i, s.n, &cp);
+    if (cp == 0x130u) {  // LATIN CAPITAL I WITH DOT ABOVE -> "i" U+0307
+      if (dst) { dst[o] = 'i'; utf8_put(dst + o + 1, 0x307u); }
+      o += 3;
+      i += len;
+      continue;
+    }
+    const u32 lc = (cp == 0x3A3u) ? sigma_lower(s, i) : u_lower_single(cp);
+    if (dst) utf8_put(dst + o, lc);
+    o += utf8_len(lc);
+    i += len;
+  }
+  return o;
 }
 
 FBX_DI void str_lower_copy(u8* dst, Str s) {

@@ -133,3 +133,22 @@ def test_engine_refuses_cpu():
                        compile_program=False)
     with pytest.raises(RuntimeError):
         engine.Engine(p, {"user_events": c.driver, "user_profile": c.profile}, c.basic)
+
+
+def test_unicode_lower_tables_current_and_exact():
+    """Device lower() tables regenerate identically from this CPython, and the
+    device algorithm (emulated) equals str.lower on fuzzed strings."""
+    import random
+    import unicodedata
+
+    from paper_2210_07768_b200 import unicode_tables as U
+    if unicodedata.unidata_version != "15.0.0":
+        pytest.skip("tables are pinned to Unicode 15.0 (CPython 3.12)")
+    assert U.render() == U.HEADER.read_text()
+    rng = random.Random(5)
+    alphabet = [chr(c) for c in list(range(0x20, 0x7F)) + [
+        0xC0, 0xC9, 0xDF, 0x130, 0x131, 0x3A3, 0x3C3, 0x391, 0x1E9E, 0x10400, 0x345, 0x2126,
+        0x212A, 0x1F88, 0x1FBC, 0x307, 0xAD, 0x2019, 0x1C4, 0x1C5, 0x24B6, 0x10A0, 0xFF21]]
+    for _ in range(3000):
+        s = "".join(rng.choice(alphabet) for _ in range(rng.randint(0, 12)))
+        assert U.emulate_lower(s) == s.lower(), s
