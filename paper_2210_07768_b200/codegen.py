@@ -55,8 +55,9 @@ def library_source() -> str:
     abi = (INCLUDE / "fbx_abi.h").read_text()
     core = (CSRC / "device" / "fbx_core.cuh").read_text()
     uni = (CSRC / "device" / "fbx_unicode.cuh").read_text()
+    p10 = (CSRC / "device" / "fbx_pow10.cuh").read_text()
     return abi + "\n" + core.replace('#include "fbx_abi.h"', "").replace(
-        '#include "fbx_unicode.cuh"', uni)
+        '#include "fbx_unicode.cuh"', uni).replace('#include "fbx_pow10.cuh"', p10)
 
 
 # ---------------------------------------------------------------------------

@@ -1250,69 +1250,125 @@ FBX_DI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
   }
 }
 
+}  // namespace fbx
+#include "fbx_pow10.cuh"
+namespace fbx {
+
+// 192-bit product (p2:p1:p0) times 2^-s rounded to nearest-even binary64.
+// Returns the bits, or ~0ull on overflow (inf).  P > 0.
+FBX_DI u64 round_p192(u64 p2, u64 p1, u64 p0, int s) {
+  int msb = p2 ? 191 - __clzll((long long)p2) : (p1 ? 127 - __clzll((long long)p1) : 63 - __clzll((long long)p0));
+  const int exp = msb - s;
+  if (exp > 1023) return ~0ull;
+  int shift = exp >= -1022 ? msb - 52 : s - 1074;  // right shift to the 53-bit (or subnormal) quantum
+  if (shift > 191) return 0ull;                      // far below half the smallest subnormal
+  // m = P >> shift (fits 64 bits), guard bit and sticky
+  u64 m, guard, sticky;
+  {
+    const int w = shift >> 6, b = shift & 63;
+    const u64 words[4] = {p0, p1, p2, 0ull};
+    m = b ? (words[w] >> b) | (words[w + 1] << (64 - b)) : words[w];
+    if (w + 1 < 3 && b == 0) m = words[w];
+    const int gs = shift - 1;
+    if (gs < 0) {
+      guard = 0; sticky = 0;
+    } else {
+      const int gw = gs >> 6, gb = gs & 63;
+      guard = (words[gw] >> gb) & 1ull;
+      u64 st = words[gw] & ((1ull << gb) - 1ull);
+      for (int k = 0; k < gw; ++k) st |= words[k];
+      sticky = st != 0ull;
+    }
+  }
+  if (guard && (sticky || (m & 1ull))) ++m;
+  int qexp = shift - s;  // value = m * 2^qexp
+  if (m == 0) return 0ull;
+  if (m >> 53) { m >>= 1; ++qexp; }
+  if (m >> 52) {
+    const int be = qexp + 1075;
+    if (be >= 2047) return ~0ull;
+    return ((u64)be << 52) | (m & ((1ull << 52) - 1ull));
+  }
+  return m;  // subnormal
+}
+
+// Correctly rounded w * 10^q (exact=false: the value lies in [w, w+1) * 10^q,
+// i.e. nonzero digits were dropped past the 19th).  Bracketing Eisel-Lemire,
+// the exact model is decimal_tables.to_double.  Returns 0 ok, 1 needs a bignum,
+// 2 overflow (*bits = +inf).
+FBX_DI u32 dec_to_double(u64 w, int q, bool exact, u64* bits) {
+  if (w == 0 || q < P10_QMIN) { *bits = 0ull; return 0; }
+  if (q > P10_QMAX) { *bits = 0x7FF0000000000000ull; return 2; }
+  const int k = q - P10_QMIN;
+  const u64 th = __ldg(P10_HI + k), tl = __ldg(P10_LO + k);
+  const int s = __ldg(P10_S + k);
+  const bool tex = __ldg(P10_EXACT + k) != 0;
+  // lo = w * T
+  u64 a0 = w * tl, a1 = __umul64hi(w, tl);
+  u64 b0 = w * th, b1 = __umul64hi(w, th);
+  u64 p0 = a0, p1 = a1 + b0, p2 = b1 + (p1 < a1 ? 1ull : 0ull);
+  const u64 lo_bits = round_p192(p2, p1, p0, s);
+  if (!(exact && tex)) {
+    // hi = (w + !exact) * (T + !tex) - 1
+    const u64 w2 = w + (exact ? 0ull : 1ull);
+    const u64 t2l = tl + (tex ? 0ull : 1ull), t2h = th + (t2l < tl ? 1ull : 0ull);
+    u64 c0 = w2 * t2l, c1 = __umul64hi(w2, t2l);
+    u64 d0 = w2 * t2h, d1 = __umul64hi(w2, t2h);
+    u64 q0 = c0, q1 = c1 + d0, q2 = d1 + (q1 < c1 ? 1ull : 0ull);
+    // minus one
+    const u64 borrow0 = q0 == 0ull;
+    q0 -= 1ull;
+    if (borrow0) { const u64 borrow1 = q1 == 0ull; q1 -= 1ull; if (borrow1) q2 -= 1ull; }
+    const u64 hi_bits = round_p192(q2, q1, q0, s);
+    if (hi_bits != lo_bits) return 1;
+  }
+  if (lo_bits == ~0ull) { *bits = 0x7FF0000000000000ull; return 2; }
+  *bits = lo_bits;
+  return 0;
+}
+
 // JSON leaf -> Float32 bits (viewpipe.py:278-279: canon_f32(float(value))).
-// 0 = ok, 1 = not a number (-> null), 2 = OverflowError (struct.pack 'f'),
-// 3 = needs a bignum decimal conversion (not implemented on device).
+// 0 = ok, 1 = not a number (-> null), 2 = OverflowError (float(int) or
+// struct.pack 'f'), 3 = needs a bignum decimal conversion (not on device).
 FBX_DI u32 j_to_f32(const u8* s, JLeaf lf, u32* bits) {
-  const double p10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
-                          1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
   if (lf.type == J_NAN) { *bits = 0x7FC00000u; return 0; }
   if (lf.type == J_POSINF) { *bits = 0x7F800000u; return 0; }
   if (lf.type == J_NEGINF) { *bits = 0xFF800000u; return 0; }
   if (lf.type != J_INT && lf.type != J_FLOAT) return 1;
   u32 i = lf.beg;
-  bool neg = s[i] == '-';
+  const bool neg = s[i] == '-';
   if (neg) ++i;
-  u64 m = 0;
-  u32 sig = 0;   // significant digits consumed into m
-  i32 e10 = 0;
-  bool nz = false;
-  for (; i < lf.end && j_digit(s[i]); ++i) {
-    u32 d = s[i] - '0';
-    if (!nz && d == 0) continue;
-    nz = true;
-    if (sig < 19) { m = m * 10u + d; ++sig; } else { ++e10; if (sig < 40) return 3; }
+  u64 w = 0;
+  u32 sig = 0;
+  int e10 = 0;
+  bool exact = true, frac = false;
+  for (; i < lf.end; ++i) {
+    const u32 c = s[i];
+    if (c == '.') { frac = true; continue; }
+    if (c == 'e' || c == 'E') break;
+    const u32 d = c - '0';
+    if (frac) --e10;
+    if (sig == 0 && d == 0) continue;
+    if (sig < 19) { w = w * 10u + d; ++sig; }
+    else { ++e10; if (d) exact = false; }
   }
-  if (lf.type == J_INT) {
-    if (e10 > 0) return 3;  // > 19 digits: float(int) needs exact big-int rounding
-    double d = (double)m;   // u64 -> double, round-to-nearest-even (exact for int())
-    d = __ull2double_rn(m);
-    if (neg && m != 0) d = -d;
-    float f = __double2float_rn(d);
-    *bits = __float_as_uint(f);
-    if (isinf(f) && !isinf(d)) return 2;
-    return 0;
-  }
-  if (i < lf.end && s[i] == '.') {
-    ++i;
-    for (; i < lf.end && j_digit(s[i]); ++i) {
-      u32 d = s[i] - '0';
-      if (!nz && d == 0) { --e10; continue; }
-      nz = true;
-      if (sig < 19) { m = m * 10u + d; ++sig; --e10; } else if (d) { return 3; }
-    }
-  }
-  if (i < lf.end && (s[i] | 0x20u) == 'e') {
+  if (i < lf.end) {  // exponent
     ++i;
     bool eneg = false;
     if (s[i] == '+' || s[i] == '-') { eneg = s[i] == '-'; ++i; }
-    i32 ev = 0;
-    for (; i < lf.end; ++i) {
-      if (ev < 100000) ev = ev * 10 + (i32)(s[i] - '0');
-    }
+    int ev = 0;
+    for (; i < lf.end; ++i)
+      if (ev < 100000) ev = ev * 10 + (int)(s[i] - '0');
     e10 += eneg ? -ev : ev;
   }
-  double d;
-  if (m == 0) {
-    d = 0.0;
-  } else if (m <= (1ull << 53) && e10 >= -22 && e10 <= 22) {
-    d = (double)m;  // exact
-    d = e10 >= 0 ? d * p10[e10] : d / p10[-e10];  // one correctly-rounded op (Clinger)
-  } else {
-    return 3;
-  }
-  if (neg) d = -d;
-  float f = __double2float_rn(d);
+  u64 db;
+  const u32 st = dec_to_double(w, e10, exact, &db);
+  if (st == 1) return 3;
+  if (st == 2 && lf.type == J_INT) return 2;  // float(int): "int too large to convert to float"
+  if (lf.type == J_INT && w == 0) db = 0ull;  // int -0 is 0
+  else if (neg) db |= 0x8000000000000000ull;
+  const double d = __longlong_as_double((long long)db);
+  const float f = __double2float_rn(d);
   *bits = __float_as_uint(f);
   if (isinf(f) && !isinf(d)) return 2;
   return 0;

@@ -234,3 +234,66 @@ def test_bad_labels(label, tmp_path):
         return drv, prof, bas
     ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
     _err(_config(512, ops, {"c": 3}, filt="age != -12345"), tmp_path, mut)
+
+
+def _float_views(n, seed, extra=()):
+    from paper_2210_07768_b200.columns import Kind, ViewImage
+    rng = random.Random(seed)
+    nums = []
+    for _ in range(n):
+        r = rng.random()
+        if r < 0.5:
+            nd = rng.choice([1, 3, 7, 12, 16, 17, 19])
+            d = "".join(rng.choice("0123456789") for _ in range(nd)).lstrip("0") or "0"
+            e = rng.choice([0, rng.randint(-45, 38 - nd)])  # stay inside float32 range
+            t = f"{d}e{e}" if rng.random() < 0.4 else (d[:1] + "." + d[1:] if nd > 1 else d)
+            nums.append(("-" if rng.random() < 0.3 else "") + t)
+        elif r < 0.7:
+            nums.append(str(rng.choice([0, 1, -1, 7, 2**53 + 1, 10**20, -(2**70), 16777217])))
+        else:
+            nums.append(rng.choice(["NaN", "Infinity", "-Infinity", "true", "null", '"1.5"',
+                                    "-0", "-0.0", "0.1", "3.4028235e38", "1e-46", "1.17549435e-38"]))
+    nums += list(extra)
+    docs = ['{"u": {"f": %s, "city": "x"}}' % x for x in nums]
+    m = len(docs)
+    drv = ViewImage.from_pydict(
+        [("instance_id", Kind.INT64), ("label", Kind.INT64), ("user_id", Kind.INT64),
+         ("query", Kind.UTF8), ("meta", Kind.JSON), ("age", Kind.INT64)],
+        {"instance_id": list(range(1, m + 1)), "label": [0] * m, "user_id": [1] * m,
+         "query": ["q"] * m, "meta": docs, "age": [30] * m}, ("user_id",))
+    prof = ViewImage.from_pydict([("user_id", Kind.INT64), ("city", Kind.UTF8),
+                                  ("score", Kind.FLOAT32)],
+                                 {"user_id": [1], "city": ["c"], "score": [0.5]}, ("user_id",))
+    bas = ViewImage.from_pydict([("instance_id", Kind.INT64), ("basic_a", Kind.INT64)],
+                                {"instance_id": list(range(1, m + 1)), "basic_a": [1] * m},
+                                ("instance_id",))
+    return drv, prof, bas
+
+
+def _float_config():
+    raw = _config(512, [{"name": "fs", "inputs": ["fx"], "outputs": ["fs"],
+                         "body": {"fn": "hash:5"}}], {"fs": 5}, filt="age == 30")
+    raw["views"][0]["clean"]["extract"].append(
+        {"source": "meta", "path": "u.f", "output": "fx", "kind": "float32"})
+    return raw
+
+
+def test_json_float32_leaves_match_oracle(tmp_path):
+    """Correctly rounded decimal -> double -> float32 (canon_f32(float(v)))."""
+    drv, prof, bas = _float_views(4000, 21)
+    _write_views(tmp_path, drv, prof, bas)
+    ref, ref_err, got, got_err = _run_both(_float_config(), drv, prof, bas, tmp_path)
+    assert ref_err is None and got_err is None, (ref_err, got_err)
+    assert (got.report.digest, got.report.signs) == (ref.digest, ref.signs)
+    np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
+
+
+@pytest.mark.parametrize("bad", ["3.5e38", "1e40", str(10**400)])
+def test_json_float32_overflow_is_stage_error(bad, tmp_path):
+    drv, prof, bas = _float_views(100, 22, extra=[bad])
+    _write_views(tmp_path, drv, prof, bas)
+    ref, ref_err, got, got_err = _run_both(_float_config(), drv, prof, bas, tmp_path)
+    assert ref_err is not None and got_err is not None
+    assert type(ref_err.cause).__name__ == "OverflowError"
+    assert got_err.stage == ref_err.stage == "clean"
+    assert isinstance(got_err.__cause__, OverflowError)

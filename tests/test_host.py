@@ -152,3 +152,12 @@ def test_unicode_lower_tables_current_and_exact():
     for _ in range(3000):
         s = "".join(rng.choice(alphabet) for _ in range(rng.randint(0, 12)))
         assert U.emulate_lower(s) == s.lower(), s
+
+
+def test_decimal_to_double_model_and_tables():
+    """The device's bracketing Eisel-Lemire (modelled exactly in Python) equals
+    float() on random decimals; the generated power table is current."""
+    from paper_2210_07768_b200 import decimal_tables as Dt
+    assert Dt.render() == Dt.HEADER.read_text()
+    slow = Dt.check_random(30000, 11)  # asserts equality for every non-slow case
+    assert slow < 60
