@@ -69,6 +69,7 @@ def parse_args():
                          "--shard-seed0 + k), split across ranks; 0 = one log per rank")
     ap.add_argument("--shard-seed0", type=int, default=1000)
     ap.add_argument("--launch-rows", type=int, default=1 << 24)
+    ap.add_argument("--e2e-slice-rows", type=int, default=1 << 18)
     return ap.parse_args()
 
 
@@ -326,7 +327,8 @@ def main():
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
     if not args.no_e2e and len(shards) == 1:
-        e2e = measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist)
+        e2e = measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist,
+                          args.e2e_slice_rows)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -362,12 +364,12 @@ def main():
         dist.destroy_process_group()
 
 
-def measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist):
+def measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist, slice_rows=1 << 17):
     """Same metric through the public API from HOST buffers: every step copies
     the driver column images H2D from pinned memory and the emitted CSR D2H,
     overlapped with the fused kernels (engine.StreamedRun)."""
     n = corpus.driver.row_count
-    sr = E.StreamedRun(eng, corpus.driver, slice_rows=1 << 17)
+    sr = E.StreamedRun(eng, corpus.driver, slice_rows=slice_rows)
     times = []
     if dist:
         dist.barrier()

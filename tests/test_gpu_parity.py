@@ -73,8 +73,9 @@ def test_multi_launch_equals_single_launch():
         np.testing.assert_array_equal(a.csr[k], b.csr[k], err_msg=k)
 
 
-@pytest.mark.parametrize("dag", ["sign_heavy", "cross_heavy"])
-def test_streamed_e2e_equals_device_resident(dag, goldens):
+@pytest.mark.parametrize("dag,zero_copy", [("sign_heavy", True), ("cross_heavy", False),
+                                           ("default", True)])
+def test_streamed_e2e_equals_device_resident(dag, zero_copy, goldens):
     """Host buffers -> overlapped H2D / fused kernels / D2H with the look-back
     continuing across launches == the single device-resident launch."""
     from paper_2210_07768_b200 import engine as E
@@ -85,7 +86,7 @@ def test_streamed_e2e_equals_device_resident(dag, goldens):
     prep = E.prepare(config_from_dict(workload_config(dag), d), views, c.basic)
     eng = E.Engine(prep, views, c.basic)
     eng.begin_run(c.driver.row_count)
-    sr = E.StreamedRun(eng, c.driver, slice_rows=3000)
+    sr = E.StreamedRun(eng, c.driver, slice_rows=3000, zero_copy=zero_copy)
     tot = sr.run()
     g = golden_run(goldens, 20000, 7, dag)
     assert f"0x{tot.digest:016x}" == g["digest"]
