@@ -398,7 +398,7 @@ def reference_arm(args, rank, world):
     """The reference's CPU path (oracle port) on the host cores, rank 0 only."""
     if rank != 0:
         return
-    from paper_2210_07768_b200.corpus import make_corpus, write_corpus
+    from paper_2210_07768_b200.corpus import make_corpus_fast as make_corpus, write_corpus
     from paper_2210_07768_b200.workloads import workload_config, write_lookup_tables
     sample = args.cpu_sample_rows
     procs = os.cpu_count() or 1
