@@ -256,19 +256,19 @@ class PlanCodegen:
     def as_str(self, v: V, what: str) -> V:
         if v.t == "str":
             return v
-        if v.t == "f32":
-            raise UnsupportedOnDevice(
-                f"{what}: str() of a Float32 value (Python float repr) is not implemented "
-                "on device")
         g = self.g
         s = V("str", g.fresh("dec"), v.nullable)
         buf = s.c + "_buf"
         g(f"__align__(16) u8 {buf}[24];")
         self.decl(s)
-        signed = "true" if v.t == "i64" else "false"
         cond = f"alive && !{v.n}" if v.nullable else "alive"
         g(f"if ({cond}) {{")
-        g(f"u32 L = fbx::int_dec_len({v.c}, {signed}); fbx::int_dec({buf}, {v.c}, {signed}, L);")
+        if v.t == "f32":  # repr(float) of the widened value
+            g(f"u32 L = fbx::f32_repr({buf}, {v.c});")
+        else:
+            signed = "true" if v.t == "i64" else "false"
+            g(f"u32 L = fbx::int_dec_len({v.c}, {signed}); "
+              f"fbx::int_dec({buf}, {v.c}, {signed}, L);")
         g(f"{s.c} = fbx::Str{{{buf}, L}};")
         if s.nullable:
             g(f"{s.c}_n = false;")

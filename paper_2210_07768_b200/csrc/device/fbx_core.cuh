@@ -1395,4 +1395,140 @@ FBX_DI bool j_to_i64(const u8* s, u32 b, u32 e, i64* out) {
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// str() of a Float32 value (featureops.py:298-299 lower/trim, :318 token, :336
+// lookup, concat): CPython's repr -- the shortest digits that round-trip the
+// value widened to binary64, laid out by format_float_short.  Exact integer
+// algorithm; decimal_tables.f32_repr is its Python model (checked against
+// repr() on CPU, tests/test_host.py).
+// ---------------------------------------------------------------------------
+// floor(x * 2^t / 10^k) (< 10^19 by the choice of k) and whether it is inexact
+FBX_DI u64 repr_window(u64 x, int t, int k, bool* sticky) {
+  if (k >= 0) {
+    if (t < 0) {
+      const u64 ip = -t >= 64 ? 0ull : x >> -t;
+      const bool fr = -t >= 64 ? x != 0ull : (x & ((1ull << -t) - 1ull)) != 0ull;
+      u64 p = 1;
+      for (int i = 0; i < k; ++i) p *= 10u;
+      *sticky = fr || (ip % p) != 0ull;
+      return ip / p;
+    }
+    u32 l[4];  // x << t < 2^128 (x < 2^55, t <= 73)
+    const u64 lo = t >= 64 ? 0ull : x << t;
+    const u64 hi = t == 0 ? 0ull : (t >= 64 ? x << (t - 64) : x >> (64 - t));
+    l[0] = (u32)lo; l[1] = (u32)(lo >> 32); l[2] = (u32)hi; l[3] = (u32)(hi >> 32);
+    bool st = false;
+    for (int kk = k; kk > 0;) {
+      const int d = kk < 9 ? kk : 9;
+      u32 div = 1;
+      for (int i = 0; i < d; ++i) div *= 10u;
+      u64 rem = 0;
+#pragma unroll
+      for (int i = 3; i >= 0; --i) {
+        const u64 cur = (rem << 32) | l[i];
+        l[i] = (u32)(cur / div);
+        rem = cur % div;
+      }
+      st |= rem != 0ull;
+      kk -= d;
+    }
+    *sticky = st;
+    return ((u64)l[1] << 32) | l[0];
+  }
+  // x * 10^-k * 2^t = (x * 5^-k) * 2^(t - k); x * 5^62 < 2^199
+  u32 l[8] = {(u32)x, (u32)(x >> 32), 0u, 0u, 0u, 0u, 0u, 0u};
+  for (int kk = -k; kk > 0;) {
+    const int d = kk < 13 ? kk : 13;
+    u32 mul = 1;
+    for (int i = 0; i < d; ++i) mul *= 5u;
+    u64 carry = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const u64 cur = (u64)l[i] * mul + carry;
+      l[i] = (u32)cur;
+      carry = cur >> 32;
+    }
+    kk -= d;
+  }
+  const int sh = t - k;
+  if (sh >= 0) {
+    *sticky = false;
+    return (((u64)l[1] << 32) | l[0]) << sh;
+  }
+  const int r = -sh, ws = r >> 5, bs = r & 31;
+  bool st = (l[ws] & ((1u << bs) - 1u)) != 0u;
+  for (int i = 0; i < ws; ++i) st |= l[i] != 0u;
+  *sticky = st;
+  const u32 a = l[ws], b = ws + 1 < 8 ? l[ws + 1] : 0u, c = ws + 2 < 8 ? l[ws + 2] : 0u;
+  return ((u64)__funnelshift_r(b, c, bs) << 32) | __funnelshift_r(a, b, bs);
+}
+
+// writes repr(float) of the float32 bits; returns the length (<= 24).  Not
+// inlined: one body per kernel however many operators stringify a Float32.
+__device__ __noinline__ u32 f32_repr(u8* dst, u32 bits) {
+  const u32 sgn = bits >> 31, ex = (bits >> 23) & 0xFFu, m = bits & 0x7FFFFFu;
+  u32 n = 0;
+  if (ex == 255u && m) { dst[0] = 'n'; dst[1] = 'a'; dst[2] = 'n'; return 3u; }
+  if (sgn) dst[n++] = '-';
+  if (ex == 255u) { dst[n] = 'i'; dst[n + 1] = 'n'; dst[n + 2] = 'f'; return n + 3u; }
+  if (ex == 0u && m == 0u) { dst[n] = '0'; dst[n + 1] = '.'; dst[n + 2] = '0'; return n + 3u; }
+  // widened: f * 2^e, f in [2^52, 2^53) and even -> closed rounding interval
+  const u32 mant = ex ? (m | 0x800000u) : m;
+  const int bl = 32 - __clz(mant);
+  const u64 f = (u64)mant << (53 - bl);
+  const int t = (ex ? (int)ex - 150 : -149) - (53 - bl) - 2;  // units of 2^t
+  const u64 v4 = 4ull * f, lo4 = v4 - (f == (1ull << 52) ? 1ull : 2ull), hi4 = v4 + 2ull;
+  const int k = (((54 + t) * 78913) >> 18) - 17;  // floor(log10 hi) - 17
+  bool sl, sv, shh;
+  const u64 wl = repr_window(lo4, t, k, &sl), wv = repr_window(v4, t, k, &sv);
+  const u64 wh = repr_window(hi4, t, k, &shh);
+  // largest p with a multiple of 10^(k+p) in [lo, hi]: monotone, p = 1 always holds
+  int p = 1;
+  u64 p10 = 10u, bot = wl / 10u + ((wl % 10u) != 0u || sl), top = wh / 10u;
+  while (p < 18) {
+    const u64 q10 = p10 * 10u;
+    const u64 nb = wl / q10 + ((wl % q10) != 0u || sl), nt = wh / q10;
+    if (nb > nt) break;
+    p10 = q10; ++p; bot = nb; top = nt;
+  }
+  u64 w = wv / p10;
+  const u64 r = wv % p10, half = p10 >> 1;
+  if (r > half || (r == half && (sv || (w & 1u)))) ++w;
+  w = w < bot ? bot : (w > top ? top : w);
+  u8 dg[20];
+  const u32 nd = u64_dec_len(w);
+  u64_dec(dg, w, nd);
+  const int decpt = (int)nd + k + p;
+  if (decpt <= -4 || decpt > 16) {
+    dst[n++] = dg[0];
+    if (nd > 1u) {
+      dst[n++] = '.';
+      for (u32 i = 1; i < nd; ++i) dst[n++] = dg[i];
+    }
+    int x = decpt - 1;
+    dst[n++] = 'e';
+    dst[n++] = x < 0 ? '-' : '+';
+    x = x < 0 ? -x : x;
+    if (x >= 100) dst[n++] = (u8)('0' + x / 100);
+    dst[n++] = (u8)('0' + (x / 10) % 10);
+    dst[n++] = (u8)('0' + x % 10);
+  } else if (decpt <= 0) {
+    dst[n++] = '0';
+    dst[n++] = '.';
+    for (int i = 0; i < -decpt; ++i) dst[n++] = '0';
+    for (u32 i = 0; i < nd; ++i) dst[n++] = dg[i];
+  } else if ((u32)decpt < nd) {
+    for (u32 i = 0; i < nd; ++i) {
+      if (i == (u32)decpt) dst[n++] = '.';
+      dst[n++] = dg[i];
+    }
+  } else {
+    for (u32 i = 0; i < nd; ++i) dst[n++] = dg[i];
+    for (u32 i = nd; i < (u32)decpt; ++i) dst[n++] = '0';
+    dst[n++] = '.';
+    dst[n++] = '0';
+  }
+  return n;
+}
+
 }  // namespace fbx

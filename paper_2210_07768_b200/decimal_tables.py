@@ -123,6 +123,83 @@ def decimal_parts(text: str):
     return int(digits[:19]), ex, not tail.strip("0")
 
 
+def f32_repr(bits: int) -> str:
+    """Exact Python model of ``fbx::f32_repr``: ``repr(float)`` of a float32 value.
+
+    str() of a Float32 value reaching lower/trim/token/concat/lookup
+    (featureops.py:298-299, 318, 336) is CPython's shortest round-trip repr of
+    the value widened to binary64 (``_Py_dg_dtoa`` mode 0 + ``format_float_short``).
+    Widened, the value is ``f * 2**e`` with ``f`` even, so its round-to-nearest
+    interval ``[L, H]`` is closed.  In units of ``2**t`` (t = e - 2) the interval
+    and the value are the integers L, V, H < 2**55.  With K chosen so that
+    ``H * 2**t / 10**K < 10**19``, the 19-digit windows ``floor(X * 2**t / 10**K)``
+    plus a sticky bit decide exactly, for every p, whether a multiple of
+    ``10**(K+p)`` lies in [L, H]; the largest such p gives the shortest digit
+    string, and the candidate nearest V (ties to even) is the repr digits.
+    """
+    s, ex, m = bits >> 31, (bits >> 23) & 0xFF, bits & 0x7FFFFF
+    if ex == 255:
+        return "nan" if m else ("-inf" if s else "inf")
+    if ex == 0 and m == 0:
+        return "-0.0" if s else "0.0"
+    mant, e2 = ((m | 0x800000), ex - 150) if ex else (m, -149)
+    bl = mant.bit_length()
+    f, e = mant << (53 - bl), e2 - (53 - bl)
+    lo, v, hi, t = 4 * f - (1 if f == 1 << 52 else 2), 4 * f, 4 * f + 2, e - 2
+    k = (((hi.bit_length() - 1 + t) * 78913) >> 18) - 17  # floor(log10 2^x) - 17
+
+    def window(x: int) -> tuple[int, bool]:
+        if k >= 0:
+            if t >= 0:
+                q, r = divmod(x << t, 10 ** k)
+                return q, r != 0
+            q, r = divmod(x >> -t, 10 ** k)
+            return q, r != 0 or (x & ((1 << -t) - 1)) != 0
+        p5, sh = x * 5 ** -k, t - k
+        if sh >= 0:
+            return p5 << sh, False
+        return p5 >> -sh, (p5 & ((1 << -sh) - 1)) != 0
+
+    (wl, sl), (wv, sv), (wh, _) = window(lo), window(v), window(hi)
+    for p in range(19, 0, -1):
+        p10 = 10 ** p
+        top = wh // p10
+        bot = wl // p10 + (1 if (wl % p10 or sl) else 0)
+        if bot <= top:
+            w, r = divmod(wv, p10)
+            if r > p10 // 2 or (r == p10 // 2 and (sv or (w & 1))):
+                w += 1
+            w = min(max(w, bot), top)
+            break
+    digits = str(w)
+    nd = len(digits)
+    decpt = nd + k + p
+    out = "-" if s else ""
+    if decpt <= -4 or decpt > 16:
+        x = decpt - 1
+        return (out + digits[0] + ("." + digits[1:] if nd > 1 else "")
+                + ("e-" if x < 0 else "e+") + f"{abs(x):02d}")
+    if decpt <= 0:
+        return out + "0." + "0" * -decpt + digits
+    if decpt < nd:
+        return out + digits[:decpt] + "." + digits[decpt:]
+    return out + digits + "0" * (decpt - nd) + ".0"
+
+
+def check_f32_repr(n: int = 100000, seed: int = 5) -> int:
+    """Compare ``f32_repr`` with repr() on edge and random float32 bit patterns."""
+    import random
+    rng = random.Random(seed)
+    cases = [0, 1, 0x80000000, 0x7F800000, 0xFF800000, 0x7FC00000, 0xFFC00001, 0x7F7FFFFF]
+    for ex in range(255):
+        cases += [ex << 23, (ex << 23) | 1, (ex << 23) | 0x7FFFFF, (ex << 23) | 0x400000]
+    cases += [rng.getrandbits(32) for _ in range(n)]
+    for b in cases:
+        want = repr(struct.unpack("<f", struct.pack("<I", b))[0])
+        assert f32_repr(b) == want, (hex(b), f32_repr(b), want)
+    return len(cases)
+
+
 def render() -> str:
     rows = table()
     hi = ",".join(f"0x{t >> 64:016X}ull" for t, _ in rows)

@@ -297,3 +297,43 @@ def test_json_float32_overflow_is_stage_error(bad, tmp_path):
     assert type(ref_err.cause).__name__ == "OverflowError"
     assert got_err.stage == ref_err.stage == "clean"
     assert isinstance(got_err.__cause__, OverflowError)
+
+
+def test_float32_str_repr_matches_oracle(tmp_path):
+    """str() of Float32 values (Python repr of the widened double) feeding
+    lower / trim / token / concat / lookup -- JSON leaves and a side-view column."""
+    import struct
+    rng = random.Random(31)
+    extra = []
+    for _ in range(3000):  # random float32 bit patterns, written as their repr
+        x = struct.unpack("<f", struct.pack("<I", rng.getrandbits(32)))[0]
+        if x == x and abs(x) != float("inf"):
+            extra.append(repr(x))
+    extra += ["1e16", "1e15", "0.0001", "0.00001", "123456789", "16777216", "1.5e-7",
+              "1e-45", "3.4028234663852886e+38", "-0.0", "0.1", "100"]
+    drv, prof, bas = _float_views(3000, 23, extra=extra)
+    keys = [repr(struct.unpack("<f", struct.pack("<f", float(x)))[0]) for x in extra[::7]]
+    (tmp_path / "fdict.tsv").write_text("".join(f"{k}\t{i + 1}\n" for i, k in enumerate(keys)))
+    ops = [
+        {"name": "fl", "inputs": ["fx"], "outputs": ["fl"], "pre": [{"fn": "lower"}],
+         "body": {"fn": "hash:3"}},
+        {"name": "ft", "inputs": ["fx"], "outputs": ["ft"], "pre": [{"fn": "trim"}],
+         "body": {"fn": "hash:4"}},
+        {"name": "fk", "inputs": ["fx"], "outputs": ["fk"], "pre": [{"fn": "token:.:1"}],
+         "body": {"fn": "hash:5"}},
+        {"name": "fc", "inputs": ["fx", "score", "cx"], "outputs": ["fc"],
+         "body": {"fn": "concat:|"}},
+        {"name": "fch", "inputs": ["fc"], "outputs": ["fch"], "body": {"fn": "hash:6"}},
+        {"name": "fd", "inputs": ["fx"], "outputs": ["fd"], "pre": [{"fn": "lookup:fdict"}],
+         "body": {"fn": "hash:7"}},
+    ]
+    raw = _config(512, ops, {"fl": 3, "ft": 4, "fk": 5, "fch": 6, "fd": 7}, filt="age == 30",
+                  tables={"fdict": {"path": "fdict.tsv", "default": 0}})
+    raw["views"][0]["clean"]["extract"].append(
+        {"source": "meta", "path": "u.f", "output": "fx", "kind": "float32"})
+    _write_views(tmp_path, drv, prof, bas)
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is None and got_err is None, (ref_err, got_err)
+    assert (got.report.digest, got.report.signs) == (ref.digest, ref.signs)
+    np.testing.assert_array_equal(got.csr["slots"], np.array(ref.slots, np.uint16))
+    np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))

@@ -91,11 +91,24 @@ def test_unsupported_constructs_are_plan_time_errors():
         {"source": "meta", "path": "u", "output": "u_json", "kind": "json"})
     with pytest.raises(UnsupportedOnDevice):
         engine.prepare(config_from_dict(raw, d), compile_program=False)
+
+
+def test_float_repr_plan_compiles():
+    """str(Float32) (Python repr) is generated on device: the plan compiles."""
+    c, d = corpus(2000, 300, 7)
     raw = workload_config("default")
     raw["operators"].append({"name": "sc", "inputs": ["score"], "outputs": ["sc"],
                              "pre": [{"fn": "lower"}], "body": {"fn": "hash:90"}})
-    with pytest.raises(UnsupportedOnDevice):  # str(float) = Python repr
-        engine.prepare(config_from_dict(raw, d), compile_program=False)
+    raw["emit"]["features"]["sc"] = 90
+    p = engine.prepare(config_from_dict(raw, d),
+                       {"user_events": c.driver, "user_profile": c.profile}, c.basic)
+    assert p.cubin[:4] == b"\x7fELF"
+
+
+def test_f32_repr_model_matches_python():
+    """decimal_tables.f32_repr (model of fbx::f32_repr) == repr() of float32 values."""
+    from paper_2210_07768_b200.decimal_tables import check_f32_repr
+    assert check_f32_repr(60000) > 60000
 
 
 @pytest.mark.parametrize("dag", DAGS)
