@@ -86,6 +86,15 @@ int fbx_gather_strings(const unsigned long long* d_ptrs, const unsigned int* d_l
                        const unsigned long long* d_offsets, unsigned long long n,
                        unsigned char* d_out, void* stream);
 
+/* check_unique_ids' failing chunk (viewpipe.py:562-576 as called at
+ * pipeline.py:1071): the chunk of an instance id's SECOND occurrence in chunk
+ * order, minimised over ids.  d_winner_chunk[i] is the chunk of the row that
+ * claimed id-set slot i, d_later_chunks[i] the two smallest chunks (+1, packed
+ * hi|lo, 0 = none) of the rows that found the id already present.  Writes
+ * (chunk << 32 | slot) of the answer to *d_out, ~0 when no id repeats. */
+int fbx_dup_resolve(const unsigned int* d_winner_chunk, const unsigned long long* d_later_chunks,
+                    unsigned long long n_slots, unsigned long long* d_out, void* stream);
+
 /* Write `bytes` of a scratch buffer (an L2 flush between timed steps). */
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream);
 

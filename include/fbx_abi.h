@@ -52,7 +52,12 @@ typedef struct fbx_state {
   unsigned long long filtered;      /* CleanCounters.filtered_rows */
   unsigned long long joined;        /* rows surviving the join(s) */
   unsigned long long side_rows;     /* side-view rows indexed */
-  unsigned long long reserved[4];
+  unsigned long long dup_seen;      /* an instance id was inserted twice (resolved by
+                                       fbx_dup_resolve to the reference's chunk) */
+  unsigned long long emit_key;      /* min (batch | null-before-range | position) of
+                                       the label errors met at emission */
+  unsigned long long emit_detail;   /* the offending label of emit_key */
+  unsigned long long reserved;
 } fbx_state;
 
 /* Kernel parameter block: program-defined u64 slots (device pointers, sizes,

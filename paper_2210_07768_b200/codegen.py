@@ -1079,38 +1079,37 @@ class PlanCodegen:
         # ---- uniqueness check + merge ------------------------------------------------
         g(f"CUR_STAGE = {STAGE['merge']}u;")
         lab = self.col(ir.label_column, node_out)
-        g("// ---- check_unique_ids over the run (pipeline.py:1071) ----")
+        g("// ---- check_unique_ids over the run (pipeline.py:1071, viewpipe.py:562) ----")
+        g("// the winner of an id's slot stores its chunk; a later occurrence notes its")
+        g("// chunk for fbx_dup_resolve and stays live (its rank keeps the emission")
+        g("// positions of the chunks before the reported one exact)")
         g(f"if (alive && !{idv.n}) {{")
         g(f"u64* IDS = {g.p('idset', 'u64*')}; const u64 IMASK = {g.p('idset_mask')};")
         g(f"const u64 key = {idv.c};")
+        g("u64 slot = IMASK + 1; bool dup;")
         g("if (key == 0ull) {")
-        g("if (atomicAdd((unsigned long long*)&IDS[IMASK + 1], 1ull) != 0ull) {")
-        self.row_error("merge", "dup_id", detail="key")
-        g("}")
+        g("dup = atomicAdd((unsigned long long*)&IDS[IMASK + 1], 1ull) != 0ull;")
         g("} else {")
         g("u64 i = (key * 0x9E3779B97F4A7C15ull) >> 20 & IMASK;")
         g("while (true) {")
         g("unsigned long long old = atomicCAS((unsigned long long*)&IDS[i], 0ull, "
           "(unsigned long long)key);")
-        g("if (old == 0ull) break;")
-        g("if (old == key) {")
-        self.row_error("merge", "dup_id", detail="key")
-        g("break;")
-        g("}")
+        g("if (old == 0ull) { dup = false; break; }")
+        g("if (old == key) { dup = true; break; }")
         g("i = (i + 1) & IMASK;")
         g("}")
+        g("slot = i;")
         g("}")
+        g(f"if (dup) fbx::dup_note(ST, {g.p('idset_d', 'u64*')} + slot, (u32)chunk);")
+        g(f"else {g.p('idset_w', 'u32*')}[slot] = (u32)chunk;")
         g("}")
         if ir.basic is not None:
             g(f"if (alive && ({idv.n} || !bhit)) alive = false;  // inner merge drops it")
         # ---- emit ---------------------------------------------------------------------
         g("// ---- emit_minibatch: sorted, de-duplicated (slot, sign) ----")
-        g(f"if (alive && {lab.n}) {{")
-        self.row_error("merge", "null_label")
-        g("}")
-        g(f"if (alive && ({lab.c} > 1ull)) {{")
-        self.row_error("merge", "label_range", detail=lab.c)
-        g("}")
+        g("// null / non-0/1 labels fail when the row's mini-batch is flushed: the row")
+        g("// stays live for its emission position (raised after the look-back)")
+        g(f"const u32 emit_bad = !alive ? 0u : ({lab.n} ? 1u : ({lab.c} > 1ull ? 2u : 0u));")
         fv = []
         for col, slot in feats:
             v = self.col(col, node_out)
@@ -1233,6 +1232,7 @@ class PlanCodegen:
         g(f"u64* O_OFF = {g.p('out.offsets', 'u64*')}; u16* O_SLOT = {g.p('out.slots', 'u16*')};")
         g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
         g("const u64 ei = sm.ex_inst, es = sm.ex_signs;")
+        g(f"if (emit_bad) fbx::raise_emit(ST, ei + myrank, {ir.chunk}u, emit_bad == 2u, {lab.c});")
         g("if (staged_out) {")
         g("for (u32 q = threadIdx.x; q < tile_signs; q += NT) { O_SIGN[es + q] = s_sign[q]; "
           "O_SLOT[es + q] = s_slot[q]; }")

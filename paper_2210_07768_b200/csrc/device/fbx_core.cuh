@@ -448,6 +448,37 @@ FBX_DI void raise_err(fbx_state* st, u64 key, u64 detail) {
   if (key < old) atomicExch((unsigned long long*)&st->error_detail, (unsigned long long)detail);
 }
 
+// Label errors surface when their mini-batch is flushed (pipeline.py:765-777):
+// key = batch(39) | null-before-range(1) | position in batch(12); the host maps
+// the batch to the chunk whose merge flushes it (look-back status).
+FBX_DI void raise_emit(fbx_state* st, u64 pos, u32 batch_size, bool range, u64 detail) {
+  const u64 key = ((pos / batch_size) << 13) | ((u64)range << 12) | (pos % batch_size);
+  u64 old = atomicMin((unsigned long long*)&st->emit_key, (unsigned long long)key);
+  if (key < old) atomicExch((unsigned long long*)&st->emit_detail, (unsigned long long)detail);
+}
+
+// check_unique_ids (viewpipe.py:562-576) raises at the chunk of an id's SECOND
+// occurrence in chunk order.  The id-set winner records its chunk with a plain
+// store; a thread that finds its id already present (rare) folds its chunk into
+// the slot's two smallest "later" chunks (+1, 0 = none) and flags the run;
+// fbx_dup_resolve takes min over slots of the 2nd smallest after the run.
+FBX_DI void dup_note(fbx_state* st, u64* pair, u32 chunk) {
+  const u64 c = (u64)chunk + 1u;
+  u64 cur = *(volatile u64*)pair;
+  while (true) {
+    const u64 a = cur >> 32, b = cur & 0xFFFFFFFFull;
+    u64 nw;
+    if (a == 0u || c < a) nw = (c << 32) | a;
+    else if (b == 0u || c < b) nw = (a << 32) | c;
+    else break;
+    const u64 old = atomicCAS((unsigned long long*)pair, (unsigned long long)cur,
+                              (unsigned long long)nw);
+    if (old == cur) break;
+    cur = old;
+  }
+  atomicExch((unsigned long long*)&st->dup_seen, 1ull);
+}
+
 // ---------------------------------------------------------------------------
 // Block-level primitives (blockDim.x == NT, a multiple of 32, <= 1024)
 // ---------------------------------------------------------------------------

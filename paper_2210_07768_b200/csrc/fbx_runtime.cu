@@ -94,8 +94,24 @@ __global__ void k_state_reset(fbx_state* st, unsigned long long* status, size_t 
   if (i == 0) {
     memset(st, 0, sizeof(fbx_state));
     st->error_key = ~0ull;
+    st->emit_key = ~0ull;
   }
   for (; i < n; i += (size_t)gridDim.x * blockDim.x) status[i] = 0ull;
+}
+
+// second-smallest chunk over {winner, later occurrences} of every repeated id
+__global__ void k_dup_resolve(const unsigned int* w, const unsigned long long* later,
+                              unsigned long long n, unsigned long long* out) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long p = later[i];
+    if (p == 0ull) continue;
+    const unsigned int x = (unsigned int)(p >> 32) - 1u;
+    const unsigned int y = (unsigned int)p ? (unsigned int)p - 1u : 0xFFFFFFFFu;
+    const unsigned int c = w[i];
+    const unsigned int second = max(min(c, x), min(max(c, x), y));
+    atomicMin(out, ((unsigned long long)second << 32) | (i & 0xFFFFFFFFull));
+  }
 }
 
 using fbx::Slot;
@@ -349,6 +365,17 @@ int fbx_gather_strings(const unsigned long long* d_ptrs, const unsigned int* d_l
   k_gather_strings<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_ptrs, d_lens, d_offsets,
                                                                         n, d_out);
   return cuda_check(cudaGetLastError(), "fbx_gather_strings");
+}
+
+int fbx_dup_resolve(const unsigned int* d_winner_chunk, const unsigned long long* d_later_chunks,
+                    unsigned long long n_slots, unsigned long long* d_out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = cuda_check(cudaMemsetAsync(d_out, 0xFF, sizeof(unsigned long long), s), "dup out");
+  if (rc) return rc;
+  const unsigned long long blocks = (n_slots + 255) / 256;
+  k_dup_resolve<<<(unsigned)(blocks < 4096 ? (blocks ? blocks : 1) : 4096), 256, 0, s>>>(
+      d_winner_chunk, d_later_chunks, n_slots, d_out);
+  return cuda_check(cudaGetLastError(), "fbx_dup_resolve");
 }
 
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream) {

@@ -445,7 +445,25 @@ class Engine:
         return {f: int(raw[i]) for i, f in enumerate(runtime.STATE_FIELDS)}
 
     def _raise_if_error(self, st: dict, prepare: bool = False):
+        """Raise the run's first failure in the reference's pipeline order.
+
+        ``error_key`` holds the row-level failures at their own chunk.  Two
+        kinds surface later in the reference and are placed here: a repeated
+        instance id fails the merge of the chunk holding its second occurrence
+        (``fbx_dup_resolve``), and a null / non-0/1 label fails the merge of the
+        chunk whose ``_Emitter.add`` flushes its mini-batch (pipeline.py:748-777)
+        -- or the final flush (stage "emit", no batch index)."""
         key = st["error_key"]
+        detail = st["error_detail"]
+        if not prepare:
+            if st.get("dup_seen"):
+                dk, did = self._dup_key()
+                if dk < key:
+                    key, detail = dk, did
+            if st.get("emit_key", ~0 & ((1 << 64) - 1)) != (1 << 64) - 1:
+                ek = self._emit_error_key(st["emit_key"])
+                if ek < key:
+                    key, detail = ek, st["emit_detail"]
         if key == (1 << 64) - 1:
             if st["pool_overflow"]:
                 req, rem = st["pool_overflow"] >> 32, st["pool_overflow"] & 0xFFFFFFFF
@@ -456,12 +474,50 @@ class Engine:
         layer = (key >> 20) & 0xFF
         rank = (key >> 8) & 0xFFF
         code = ERR_NAMES.get(key & 0xFF, "value")
-        detail = st["error_detail"]
         cause = _cause(code, detail, st)
         if stage == "extract" and layer:
             node = self.prepared.node_names[rank]
             cause = LayerExecutionError(layer, node, cause)
-        raise StageError(stage, None if stage == "prepare" else chunk, cause)
+        raise StageError(stage, None if stage in ("prepare", "emit") else chunk, cause)
+
+    def check_run(self, st: dict):
+        """End of a run: note whether the id set saw a repeat (its pair array
+        then needs clearing) and raise the run's first failure."""
+        self._dup_dirty = bool(st["dup_seen"])
+        self._raise_if_error(st)
+
+    def _dup_key(self) -> tuple[int, int]:
+        """(error key, id) of check_unique_ids' failure: the merge of the chunk
+        holding some id's second occurrence, minimised over ids."""
+        out = self.torch.empty(1, dtype=self.torch.int64, device=self.device)
+        runtime.dup_resolve(self.idset_w.data_ptr(), self.idset_d.data_ptr(),
+                            self._idset_cap + 2, out.data_ptr(), self._stream())
+        v = int(out.cpu().numpy().view(np.uint64)[0])
+        if v == (1 << 64) - 1:
+            return (1 << 64) - 1, 0
+        chunk, slot = v >> 32, v & 0xFFFFFFFF
+        ident = int(self.idset[slot].item()) & ((1 << 64) - 1) if slot <= self._idset_cap else 0
+        if slot == self._idset_cap + 1:
+            ident = 0
+        key = (chunk << 32) | (codegen.STAGE["merge"] << 28) | codegen.ERR["dup_id"]
+        return key, ident
+
+    def _emit_error_key(self, ek: int) -> int:
+        """Map a label error at emission position (batch b) to the chunk whose
+        merge flushes batch b: the first chunk whose inclusive instance count
+        reaches (b + 1) * batch_size (look-back status words), else the final
+        flush."""
+        bs = self.ir.chunk
+        batch, rng, pos = ek >> 13, (ek >> 12) & 1, ek & 0xFFF
+        code = codegen.ERR["label_range" if rng else "null_label"]
+        sub = (((1 + rng) & 0xFF) << 20) | ((pos & 0xFFF) << 8) | code  # after the dup check
+        words = self.status[: self._run_tiles].cpu().numpy().view(np.uint64)
+        incl = (words >> np.uint64(34)) & np.uint64(0xFFFFFFF)
+        hit = np.nonzero(incl >= np.uint64((batch + 1) * bs))[0]
+        if hit.size == 0:
+            return (0xFFFFFFFF << 32) | (codegen.STAGE["emit"] << 28) | sub
+        chunk = int(hit[0]) + self._chunk_minus_tile
+        return (chunk << 32) | (codegen.STAGE["merge"] << 28) | sub
 
     def begin_run(self, rows_hint: int):
         """Start a run: clear the run-wide instance-id set (check_unique_ids'
@@ -474,11 +530,23 @@ class Engine:
         cap = _next_pow2(2 * max(rows_hint, 1))
         if self.idset is None or self._idset_cap < cap:
             self.idset = torch.zeros(cap + 2, dtype=torch.int64, device=self.device)
+            # winner chunk per slot (no reset: read only for claimed slots) and the
+            # later-occurrence chunk pairs (only written when an id repeats)
+            self.idset_w = torch.empty(cap + 2, dtype=torch.int32, device=self.device)
+            self.idset_d = torch.zeros(cap + 2, dtype=torch.int64, device=self.device)
             self._idset_cap = cap
+            self._dup_dirty = False
         else:
             self.idset.zero_()
+            if self._dup_dirty:
+                self.idset_d.zero_()
+        # unknown until finish() reads dup_seen (a run abandoned early stays dirty)
+        self._dup_dirty = True
         self._set("idset", self.idset.data_ptr())
         self._set("idset_mask", self._idset_cap - 1)
+        self._set("idset_w", self.idset_w.data_ptr())
+        self._set("idset_d", self.idset_d.data_ptr())
+        self._run_tiles = 0
 
     def reserve(self, rows: int, launch_rows: int | None = None):
         """Run-wide buffers: look-back status for every tile of the run (the
@@ -551,6 +619,8 @@ class Engine:
         self._set("row_hi", row_hi)
         self._set("chunk0", row_lo // self.ir.chunk)
         self._set("tile_base", tile_base)
+        self._chunk_minus_tile = row_lo // self.ir.chunk - tile_base
+        self._run_tiles = tile_base + tiles
         self.module.launch("fbx_pipeline", tiles, self.prog.threads, self.prog.smem_bytes,
                            stream, self.params)
         return tiles
@@ -558,7 +628,7 @@ class Engine:
     def finish(self) -> CsrBatch:
         """Synchronise, read counters, raise the first error in pipeline order."""
         st = self._read_state()
-        self._raise_if_error(st)
+        self.check_run(st)
         c = Counters(st["digest"], st["instances"], st["signs"], st["malformed"],
                      st["filtered"], st["joined"], 1)
         return CsrBatch(self.o_ids, self.o_lab, self.o_off, self.o_slot, self.o_sign, c)
@@ -659,7 +729,8 @@ class StreamedRun:
             comp_done[j].synchronize()
             st = self.states[j].numpy().view(np.uint64)
             stt = {f: int(st[i]) for i, f in enumerate(runtime.STATE_FIELDS)}
-            eng._raise_if_error(stt)
+            # failures are resolved once at the end of the run: a label error's
+            # flush chunk and a repeated id's second chunk may lie in later slices
             # counters accumulate over the run's launches: this slice's share
             ni, ms = stt["instances"] - inst_base, stt["signs"] - sign_base
             with torch.cuda.stream(self.s_d2h):
@@ -704,6 +775,8 @@ class StreamedRun:
                 drain(pending.pop(0))
         while pending:
             drain(pending.pop(0))
+        self.s_comp.synchronize()
+        eng.check_run(eng._read_state())
         self.s_d2h.synchronize()
         self.d2h_bytes = tot.instances * 17 + 8 + tot.signs * 10
         return tot
@@ -742,7 +815,7 @@ class StreamedRun:
             tiles_before += (hi - lo + eng.ir.chunk - 1) // eng.ir.chunk
         self.s_comp.synchronize()
         st = eng._read_state()
-        eng._raise_if_error(st)
+        eng.check_run(st)
         # restore the device CSR for later device-resident launches
         eng._arena_key = None
         tot = Counters(st["digest"], st["instances"], st["signs"], st["malformed"],
@@ -879,34 +952,23 @@ def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: Vie
     stage["read"] = time.perf_counter() - t1
     eng.bind_driver(dv)
     n = drv.row_count
-    eng.begin_run(n)
-    total = Counters()
-    parts = []
-    t2 = time.perf_counter()
+    # one reserved run: the look-back, the CSR positions and the id set span
+    # every launch, so emission order and error placement are run-global
     step = eng.max_rows
+    eng.reserve(n, min(step, max(n, 1)))
+    eng.begin_run(n)
+    t2 = time.perf_counter()
+    tiles = 0
+    launches = 0
     for lo in range(0, n, step):
         hi = min(lo + step, n)
-        eng.launch(lo, hi)
-        b = eng.finish()
-        c = b.counters
-        total.digest ^= c.digest
-        for f in ("instances", "signs", "malformed", "filtered", "joined", "launches"):
-            setattr(total, f, getattr(total, f) + getattr(c, f))
-        if collect:
-            parts.append((b.to_numpy(), total.signs - c.signs))
+        tiles += eng.launch(lo, hi, tile_base=tiles)
+        launches += 1
+    b = eng.finish()
+    total = b.counters
+    total.launches = launches
     stage["extract"] = time.perf_counter() - t2
-    csr = None
-    if collect:
-        ids = [p["ids"] for p, _ in parts]
-        offs = [p["offsets"][:-1] + base for p, base in parts]
-        csr = {"ids": np.concatenate(ids) if ids else np.zeros(0, np.uint64),
-               "labels": np.concatenate([p["labels"] for p, _ in parts]) if parts else
-               np.zeros(0, np.uint8),
-               "offsets": np.concatenate(offs + [np.array([total.signs], np.uint64)]),
-               "slots": np.concatenate([p["slots"] for p, _ in parts]) if parts else
-               np.zeros(0, np.uint16),
-               "signs": np.concatenate([p["signs"] for p, _ in parts]) if parts else
-               np.zeros(0, np.uint64)}
+    csr = b.to_numpy() if collect else None
     bs = config.batch_size
     rep = RunReport(
         mode="pipelined", digest=total.digest, batches=math.ceil(total.instances / bs),

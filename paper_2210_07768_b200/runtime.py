@@ -24,13 +24,14 @@ _lib = None
 FBX_MAX_PARAM_SLOTS = 384
 STATE_FIELDS = ("tile_ticket", "pool_head", "pool_overflow", "error_key", "error_detail",
                 "digest", "instances", "signs", "malformed", "filtered", "joined", "side_rows",
-                "r0", "r1", "r2", "r3")
+                "dup_seen", "emit_key", "emit_detail", "reserved")
 STATE_BYTES = 8 * len(STATE_FIELDS)
 
 EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_program_load",
            "fbx_program_unload", "fbx_program_kernel", "fbx_kernel_attributes",
            "fbx_kernel_set_max_dynamic_smem", "fbx_launch", "fbx_state_reset",
-           "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings")
+           "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
+           "fbx_dup_resolve")
 
 
 class FbxError(RuntimeError):
@@ -66,6 +67,7 @@ def lib() -> ctypes.CDLL:
             L.fbx_l2_flush.argtypes = [vp, sz, vp]
             L.fbx_exclusive_scan_u32.argtypes = [vp, vp, ctypes.c_ulonglong, vp]
             L.fbx_gather_strings.argtypes = [vp, vp, vp, ctypes.c_ulonglong, vp, vp]
+            L.fbx_dup_resolve.argtypes = [vp, vp, ctypes.c_ulonglong, vp, vp]
             for name in EXPORTS:
                 getattr(L, name).restype = getattr(L, name).restype or c
             L.fbx_version.restype = ctypes.c_char_p
@@ -173,6 +175,12 @@ def dict_build(d_slots: int, capacity: int, d_blob: int, d_offs: int, d_vals: in
 def l2_flush(d_buf: int, nbytes: int, stream: int):
     _check(lib().fbx_l2_flush(ctypes.c_void_p(d_buf), int(nbytes), ctypes.c_void_p(stream)),
            "l2 flush")
+
+
+def dup_resolve(d_winner: int, d_later: int, n_slots: int, d_out: int, stream: int):
+    _check(lib().fbx_dup_resolve(ctypes.c_void_p(d_winner), ctypes.c_void_p(d_later),
+                                 int(n_slots), ctypes.c_void_p(d_out), ctypes.c_void_p(stream)),
+           "dup resolve")
 
 
 def exclusive_scan_u32(d_in: int, d_out: int, n: int, stream: int):

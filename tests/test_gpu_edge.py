@@ -220,6 +220,7 @@ def test_duplicate_instance_ids(tmp_path):
     raw = _config(512, ops, {"c": 3}, filt="age != -12345")
     ref_err, got_err = _err(raw, tmp_path, mut)
     assert got_err.stage == "merge"
+    assert got_err.batch_index == ref_err.chunk
 
 
 @pytest.mark.parametrize("label", [None, 2, -1])
@@ -233,7 +234,85 @@ def test_bad_labels(label, tmp_path):
         drv.columns["label"] = ColumnImage.from_values(Kind.INT64, labels)
         return drv, prof, bas
     ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
-    _err(_config(512, ops, {"c": 3}, filt="age != -12345"), tmp_path, mut)
+    ref_err, got_err = _err(_config(512, ops, {"c": 3}, filt="age != -12345"), tmp_path, mut)
+    assert got_err.batch_index == ref_err.chunk
+
+
+def _set_ids(pairs):
+    """Mutation: ids[dst] = ids[src] for (dst, src) in pairs."""
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+
+    def mut(drv, prof, bas):
+        ids = drv.columns["instance_id"].to_pylist()
+        for dst, src in pairs:
+            ids[dst] = ids[src]
+        drv.columns["instance_id"] = ColumnImage.from_values(Kind.INT64, ids)
+        return drv, prof, bas
+    return mut
+
+
+def _set_labels(rows, value):
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+
+    def mut(drv, prof, bas):
+        labels = drv.columns["label"].to_pylist()
+        for i in rows:
+            labels[i] = value
+        drv.columns["label"] = ColumnImage.from_values(Kind.INT64, labels)
+        return drv, prof, bas
+    return mut
+
+
+def _chain(*muts):
+    def mut(*views):
+        for m in muts:
+            views = m(*views)
+        return views
+    return mut
+
+
+# Placement of failures that surface after their row (SURVEY Appendix A):
+# a repeated id fails the merge of the chunk of its SECOND occurrence; a bad
+# label fails the merge of the chunk that flushes its mini-batch, or the final
+# flush (stage "emit", no batch index); a repeat in the same chunk beats a flush.
+PLACEMENT = {  # rows chosen among those that reach the merge in _views(2000, 5)
+    "dup_far": _set_ids([(1900, 3)]),                        # chunks 0 and 3
+    "dup_three": _set_ids([(1500, 1400), (702, 1400)]),      # 2nd occurrence: row 1400
+    "dup_two_ids": _set_ids([(1993, 12), (1200, 1102)]),     # min over ids
+    "dup_same_chunk": _set_ids([(600, 601)]),
+    "label_straddle": _set_labels([505], None),              # batch completes later
+    "label_tail": _set_labels([1998], 5),                    # final partial batch
+    "label_null_vs_range": _chain(_set_labels([302], 7), _set_labels([505], None)),
+    "label_and_dup": _chain(_set_labels([40], None), _set_ids([(1003, 1000)])),
+    "labels_two": _chain(_set_labels([1030], 3), _set_labels([1021], None)),
+}
+
+
+@pytest.mark.parametrize("case", sorted(PLACEMENT))
+@pytest.mark.parametrize("batch_size", [512, 100])
+def test_failure_placement_matches_reference(case, batch_size, tmp_path):
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    raw = _config(batch_size, ops, {"c": 3}, filt="age != -12345")
+    ref_err, got_err = _err(raw, tmp_path, PLACEMENT[case])
+    assert (got_err.stage, got_err.batch_index) == (ref_err.stage, ref_err.chunk)
+
+
+def test_failure_placement_across_launches(tmp_path):
+    """The same placement when the run is split over several launches."""
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.engine import run_views
+    drv, prof, bas = _views(2000, 5)
+    drv, prof, bas = _chain(_set_labels([1010], None), _set_ids([(1900, 3)]))(drv, prof, bas)
+    _write_views(tmp_path, drv, prof, bas)
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    raw = _config(100, ops, {"c": 3}, filt="age != -12345")
+    ref, ref_err, _, _ = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is not None
+    for rows in (300, 700):
+        with pytest.raises(Exception) as ei:
+            run_views(config_from_dict(raw, tmp_path), {"ev": drv, "pr": prof}, bas,
+                      max_rows_per_launch=rows)
+        assert (ei.value.stage, ei.value.batch_index) == (ref_err.stage, ref_err.chunk)
 
 
 def _float_views(n, seed, extra=()):
