@@ -122,6 +122,7 @@ class Program:
     kernels: list[str]
     side_kernels: list[str]
     notes: list[str]
+    int_keyed: tuple[int, ...] = ()   # tables with 16-B fbx::ISlot slots
 
 
 # ---------------------------------------------------------------------------
@@ -232,6 +233,8 @@ class PlanCodegen:
         default_mb = max(1, min(default_mb, 2048 // self.nt))
         self.min_blocks = int(os.environ.get("FBX_MIN_BLOCKS", str(default_mb)))
         self.pool_sites = 0
+        self._ids_tail: list[str] = []
+        self.pf_slot: dict[int, int] = {}
 
     # -- value helpers ---------------------------------------------------------
     def kind_t(self, kind: Kind) -> str:
@@ -650,6 +653,15 @@ class PlanCodegen:
         g("}")
         g(f"if (alive && !({null_any})) {{")
         self.key_hash(keys, kk, "tag")
+        if self.int_keyed(k):
+            g(f"fbx::islot_insert((fbx::ISlot*)TBL, MASK, tag, (u64){keys[0].c}, (u32)row); ++nidx;")
+            g("}")
+            g("}")
+            g("if (nmal) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)nmal);")
+            g("if (nfilt) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)nfilt);")
+            g("if (nidx) atomicAdd((unsigned long long*)&ST->side_rows, (unsigned long long)nidx);")
+            g("}")
+            return name
         g("u64 i = tag & MASK;")
         g("while (true) {")
         g("unsigned long long old = atomicCAS((unsigned long long*)&TBL[i].tag, 0ull, "
@@ -858,6 +870,27 @@ class PlanCodegen:
 
         With ``pre`` the first slot (tag/ref/aux) was loaded in the prologue."""
         g = self.g
+        if self.int_keyed(k):
+            g(f"const fbx::ISlot* T = {g.p(f'side{k}.table', 'const fbx::ISlot*')};")
+            g(f"const u64 MASK = {g.p(f'side{k}.mask')};")
+            if pre:
+                g(f"u64 tag = {pre}_tag;")
+            else:
+                self.key_hash(keys, kinds, "tag")
+            g("u64 i = tag & MASK;")
+            if pre and k in self.pf_slot:
+                g("fbx::cp_async_wait_all();")
+                g(f"fbx::ISlot s = *(const fbx::ISlot*)(dyn_smem + SPAN_BUDGET + "
+                  f"{16 * self.nt * self.pf_slot[k]}u + 16u * threadIdx.x);")
+            else:
+                g("fbx::ISlot s = fbx::islot_ld(T + i);")
+            g("while (true) {")
+            g("if (s.aux == 0u) break;")
+            g(f"if (s.key == (u64){keys[0].c}) {{ {cnt_var} = s.aux; {row_var} = s.ref; break; }}")
+            g("i = (i + 1) & MASK;")
+            g("s = fbx::islot_ld(T + i);")
+            g("}")
+            return
         g(f"const fbx::Slot* T = {g.p(f'side{k}.table', 'const fbx::Slot*')};")
         g(f"const u64 MASK = {g.p(f'side{k}.mask')};")
         if pre:
@@ -889,14 +922,56 @@ class PlanCodegen:
         g("i = (i + 1) & MASK;")
         g("}")
 
+    def int_keyed(self, k: int) -> bool:
+        """Table k is keyed by one Int64 column on both sides: 16-B ISlot layout
+        (key stored in the slot, no key gather on the probe)."""
+        ir = self.ir
+        if k < len(ir.sides):
+            sv = ir.sides[k]
+            if len(ir.join_keys) != 1 or len(sv.keys) != 1:
+                return False
+            dk = ir.driver.cleaned_kinds()
+            return (dk.get(ir.join_keys[0]) is Kind.INT64
+                    and sv.cleaned_kinds().get(sv.keys[0]) is Kind.INT64)
+        bv = ir.basic
+        return (bv is not None and len(bv.keys) == 1
+                and bv.cleaned_kinds().get(bv.keys[0]) is Kind.INT64)
+
+    def raw_key_cols(self, cols) -> bool:
+        drv = self.ir.driver
+        needed = self.driver_needed()
+        ext_out = {e.output for e in drv.extractions}
+        return all(c in drv.kinds and c in needed and c not in ext_out and c not in drv.fills
+                   for c in cols)
+
+    def smem_prefetch_tables(self) -> list[int]:
+        """Int-keyed tables whose first probe slot is copied to shared memory
+        (cp.async) in the prologue: the probe then never waits on HBM."""
+        ir = self.ir
+        out = [k for k in range(len(ir.sides))
+               if self.int_keyed(k) and self.raw_key_cols(ir.join_keys)]
+        bk = len(ir.sides)
+        if ir.basic is not None and self.int_keyed(bk) and self.raw_key_cols([ir.instance_column]):
+            out.append(bk)
+        return out
+
     def prefetch(self, k: int, keys: list[V], kinds: list[Kind], name: str) -> str:
         """Prologue: hash the raw key and load the first probe slot."""
         g = self.g
-        g(f"u64 {name}_tag = 0, {name}_t = 0; u32 {name}_ref = 0, {name}_aux = 0;")
+        if k in self.pf_slot:
+            g(f"u64 {name}_tag = 0;")
+        else:
+            g(f"u64 {name}_tag = 0, {name}_t = 0; u32 {name}_ref = 0, {name}_aux = 0;")
         nn = " && ".join(f"!{v.n}" for v in keys if v.nullable) or "true"
         g(f"if (inrange && {nn}) {{")
         self.key_hash(keys, kinds, "tg")
         g(f"{name}_tag = tg;")
+        if k in self.pf_slot:
+            g(f"const fbx::ISlot* T = {g.p(f'side{k}.table', 'const fbx::ISlot*')};")
+            g(f"fbx::cp_async16(dyn_smem + SPAN_BUDGET + {16 * self.nt * self.pf_slot[k]}u"
+              " + 16u * threadIdx.x, T + (tg & " + g.p(f'side{k}.mask') + "));")
+            g("}")
+            return name
         g(f"const fbx::Slot* T = {g.p(f'side{k}.table', 'const fbx::Slot*')};")
         g(f"const fbx::Slot* sl = T + (tg & {g.p(f'side{k}.mask')});")
         g(f"{name}_t = __ldg(&sl->tag); {name}_ref = __ldg(&sl->ref); {name}_aux = __ldg(&sl->aux);")
@@ -992,6 +1067,8 @@ class PlanCodegen:
         pre_basic = None
         if ir.basic is not None and raw_key([ir.instance_column]):
             pre_basic = self.prefetch(bk, [raw[ir.instance_column]], [Kind.INT64], "pfb")
+        if self.pf_slot:
+            g("fbx::cp_async_commit();")
         if self.staged:
             g("fbx::mbar_wait(&sm.bar, 0u);")
         # ---- clean ------------------------------------------------------------------
@@ -1083,26 +1160,36 @@ class PlanCodegen:
         g("// the winner of an id's slot stores its chunk; a later occurrence notes its")
         g("// chunk for fbx_dup_resolve and stays live (its rank keeps the emission")
         g("// positions of the chunks before the reported one exact)")
-        g(f"if (alive && !{idv.n}) {{")
+        g("// the first atomic is issued here; its result is only consumed at the very")
+        g("// end of the kernel (collision probing + dup note), off the critical path")
         g(f"u64* IDS = {g.p('idset', 'u64*')}; const u64 IMASK = {g.p('idset_mask')};")
-        g(f"const u64 key = {idv.c};")
-        g("u64 slot = IMASK + 1; bool dup;")
-        g("if (key == 0ull) {")
-        g("dup = atomicAdd((unsigned long long*)&IDS[IMASK + 1], 1ull) != 0ull;")
+        g("u64 ids_slot = IMASK + 1; unsigned long long ids_old = 0ull;")
+        g(f"const bool ids_on = alive && !{idv.n};")
+        g("if (ids_on) {")
+        g(f"if ({idv.c} == 0ull) {{")
+        g("ids_old = atomicAdd((unsigned long long*)&IDS[IMASK + 1], 1ull);")
         g("} else {")
-        g("u64 i = (key * 0x9E3779B97F4A7C15ull) >> 20 & IMASK;")
-        g("while (true) {")
-        g("unsigned long long old = atomicCAS((unsigned long long*)&IDS[i], 0ull, "
-          "(unsigned long long)key);")
-        g("if (old == 0ull) { dup = false; break; }")
-        g("if (old == key) { dup = true; break; }")
-        g("i = (i + 1) & IMASK;")
+        g(f"ids_slot = ({idv.c} * 0x9E3779B97F4A7C15ull) >> 20 & IMASK;")
+        g(f"ids_old = atomicCAS((unsigned long long*)&IDS[ids_slot], 0ull, (unsigned long long){idv.c});")
         g("}")
-        g("slot = i;")
         g("}")
-        g(f"if (dup) fbx::dup_note(ST, {g.p('idset_d', 'u64*')} + slot, (u32)chunk);")
-        g(f"else {g.p('idset_w', 'u32*')}[slot] = (u32)chunk;")
-        g("}")
+        self._ids_tail = [
+            "// ---- check_unique_ids: resolve the id-set insertion issued at the merge ----",
+            "if (ids_on) {",
+            "bool dup;",
+            f"if ({idv.c} == 0ull) {{",
+            "dup = ids_old != 0ull;",
+            "} else {",
+            f"while (ids_old != 0ull && ids_old != (unsigned long long){idv.c}) {{",
+            "ids_slot = (ids_slot + 1) & IMASK;",
+            f"ids_old = atomicCAS((unsigned long long*)&IDS[ids_slot], 0ull, (unsigned long long){idv.c});",
+            "}",
+            "dup = ids_old != 0ull;",
+            "}",
+            f"if (dup) fbx::dup_note(ST, {g.p('idset_d', 'u64*')} + ids_slot, (u32)chunk);",
+            f"else {g.p('idset_w', 'u32*')}[ids_slot] = (u32)chunk;",
+            "}",
+        ]
         if ir.basic is not None:
             g(f"if (alive && ({idv.n} || !bhit)) alive = false;  // inner merge drops it")
         # ---- emit ---------------------------------------------------------------------
@@ -1247,6 +1334,8 @@ class PlanCodegen:
             g(f"if ((fpres >> {q}) & 1u) {{ O_SLOT[so] = (u16){slot}u; O_SIGN[so] = fsg[{q}]; ++so; }}")
         g("}")
         g("if (threadIdx.x == 0) O_OFF[ei + n_inst] = es + tile_signs;")
+        for line in self._ids_tail:
+            g(line)
         g("}")
         return "fbx_pipeline"
 
@@ -1413,6 +1502,14 @@ class PlanCodegen:
         rank_bytes = max(24 * self.nt, 8 * self.nt + 8192)  # bitonic 3*NT u64 | radix
         self.dyn_smem = max(self.span_cap, rank_bytes,
                             min(need, per_cta, OUT_BUDGET)) // 16 * 16
+        # first probe slots of int-keyed tables land behind the staged spans
+        self.pf_slot = {}
+        if ir.mode != "extract":
+            pf = self.smem_prefetch_tables()
+            pf_need = self.span_cap + 16 * self.nt * len(pf)
+            if pf and pf_need <= max(self.dyn_smem, per_cta):
+                self.pf_slot = {k: j for j, k in enumerate(pf)}
+                self.dyn_smem = max(self.dyn_smem, pf_need) // 16 * 16
         self.g.slot("state")  # slot 0
         if ir.mode == "extract":
             kname = self.extract_rows_kernel()
@@ -1439,7 +1536,9 @@ class PlanCodegen:
         src = "\n".join(head + self.g.lines)
         smem = self.dyn_smem
         del body_start
-        return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes)
+        nt_ = len(ir.sides) + (1 if ir.basic is not None else 0)
+        return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes,
+                       tuple(k for k in range(nt_) if self.int_keyed(k)))
 
 
 def _filter_columns(expr) -> set[str]:

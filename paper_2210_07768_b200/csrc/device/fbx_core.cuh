@@ -535,6 +535,34 @@ struct BlockScanU32 {
 template <int NT>
 FBX_DI u8* pool_alloc(BlockScanU32<NT>& scan, u64* base_smem, fbx_state* st, u8* pool,
                       u64 pool_cap, u32 size, bool* exhausted) {
+#ifdef FBX_POOL_WARP
+  // warp-aggregated: one atomicAdd per warp that asks, no CTA barrier
+  __syncwarp();
+  *exhausted = false;
+  if (__ballot_sync(0xFFFFFFFFu, size != 0u) == 0u) return nullptr;
+  const u32 lane = threadIdx.x & 31u;
+  u32 inc = size;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u32 y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= (u32)d) inc += y;
+  }
+  const u32 total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+  u64 b = 0;
+  if (lane == 31u) {
+    const u64 tot = ((u64)total + 15ull) & ~15ull;
+    b = atomicAdd((unsigned long long*)&st->pool_head, (unsigned long long)tot);
+    if (b + tot > pool_cap) {
+      const u64 rem = b < pool_cap ? pool_cap - b : 0ull;
+      atomicMax((unsigned long long*)&st->pool_overflow, (unsigned long long)((tot << 32) | (rem & 0xFFFFFFFFull)));
+      b = ~0ull;
+    }
+  }
+  b = __shfl_sync(0xFFFFFFFFu, b, 31);
+  *exhausted = (b == ~0ull);
+  if (b == ~0ull || size == 0) return nullptr;
+  return pool + b + (inc - size);
+#else
   if (!__syncthreads_or(size != 0u)) {
     *exhausted = false;
     return nullptr;
@@ -558,6 +586,7 @@ FBX_DI u8* pool_alloc(BlockScanU32<NT>& scan, u64* base_smem, fbx_state* st, u8*
   *exhausted = (b == ~0ull);
   if (b == ~0ull || size == 0) return nullptr;
   return pool + b + pre;
+#endif
 }
 
 // Bitonic sort of (key, payload) pairs held in shared memory, N = power of 2.
@@ -818,6 +847,48 @@ FBX_DI void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
+// per-thread async copies (LDGSTS): probe slots prefetched into shared memory
+FBX_DI void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+FBX_DI void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+FBX_DI void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Int64-keyed join tables: 16-B slots {u64 key, u32 ref, u32 aux}, aux = count
+// (0 = empty), so a probe is one 16-B load and no key gather.
+struct ISlot {
+  u64 key;
+  u32 ref;
+  u32 aux;
+};
+FBX_DI ISlot islot_ld(const ISlot* s) {
+  const uint4 v = __ldg((const uint4*)s);
+  return ISlot{((u64)v.y << 32) | v.x, v.z, v.w};
+}
+FBX_DI u32 ld_acquire_u32(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// build-side insert (count duplicates); returns after the key is counted
+FBX_DI void islot_insert(ISlot* T, u64 mask, u64 h, u64 key, u32 row) {
+  u64 i = h & mask;
+  while (true) {
+    unsigned long long* ra = (unsigned long long*)&T[i].ref;  // {ref, aux}
+    const unsigned long long old = atomicCAS(ra, 0ull, (0xFFFFFFFFull << 32) | (unsigned long long)row);
+    if (old == 0ull) {
+      *((volatile u64*)&T[i].key) = key;
+      __threadfence();
+      atomicExch(&T[i].aux, 1u);
+      return;
+    }
+    u32 c;
+    do { c = ld_acquire_u32(&T[i].aux); } while (c == 0xFFFFFFFFu);  // claimed, key not yet visible
+    if (*((volatile u64*)&T[i].key) == key) { atomicAdd(&T[i].aux, 1u); return; }
+    i = (i + 1) & mask;
+  }
+}
+
 FBX_DI void mbar_wait(u64* bar, u32 phase) {
   u32 done = 0;
   while (!done) {
@@ -958,25 +1029,25 @@ FBX_DI bool j_digit(u32 c) { return c - '0' < 10u; }
 FBX_DI bool j_hex(u32 c) { return (c - '0' < 10u) || ((c | 0x20u) - 'a' < 6u); }
 FBX_DI u32 j_hexval(u32 c) { return c <= '9' ? c - '0' : (c | 0x20u) - 'a' + 10u; }
 
-// Forward reader over a byte span: loads each aligned 32-bit word once and
-// never touches a word past the span's last byte.
+// Reader over a document (shared-memory stage or HBM).  Documents of at most
+// 60 bytes with no backslash and no byte < 0x20 (the common case) take the
+// mask mode: one branch-free SWAR pass builds 64-bit quote / space masks
+// (jmask_build), after which whitespace skipping and string scanning are a
+// find-first-set each.  Every other document runs the byte-wise scanner.
+// Both modes accept exactly the same language: with no escapes and no
+// control bytes, a string ends at the next quote and whitespace is ' ' only.
 struct JReader {
-  const u32* wp;
-  u32 off, n, wi, w;
-  FBX_DI void init(const u8* p, u32 len) {
-    u64 a = (u64)p;
-    off = (u32)(a & 3u);
-    wp = (const u32*)(a & ~3ull);
-    n = len;
-    wi = 0;
-    w = len ? wp[0] : 0u;
-  }
-  FBX_DI u32 at(u32 k) {  // byte k, k < n
-    u32 pos = off + k, idx = pos >> 2;
-    if (idx != wi) { wi = idx; w = wp[idx]; }
-    return (w >> ((pos & 3u) * 8u)) & 0xFFu;
-  }
-  FBX_DI u32 skip_ws(u32 i) {
+  const u8* p;
+  u32 n;
+  bool fast;
+  u64 q;    // quote bytes (doc-relative, fast mode)
+  u64 nsp;  // non-space bytes (doc-relative, fast mode)
+  FBX_DI u32 at(u32 k) const { return p[k]; }  // byte k, k < n
+  FBX_DI u32 skip_ws(u32 i) const {
+    if (fast) {
+      const u64 m = i < 64u ? (nsp >> i) : 0ull;
+      return m ? i + (u32)(__ffsll((long long)m) - 1) : (i > n ? i : n);
+    }
     while (i < n) {
       const u32 c = at(i);
       if (c > 0x20u || !j_ws(c)) break;
@@ -986,16 +1057,53 @@ struct JReader {
   }
 };
 
+// 0x80 in every byte of x equal to the byte replicated in c (x7 = x & 0x7F7F7F7F)
+FBX_DI u32 eq_bytes(u32 x, u32 x7, u32 c) { return ~(((x7 ^ c) + 0x7F7F7F7Fu) | x) & 0x80808080u; }
+
+// The mask mode's single pass: false -> the document needs the byte scanner.
+FBX_DI bool jmask_build(const u8* p, u32 n, u64* qm, u64* nspm) {
+  if (n == 0u || n > 60u) return false;
+  const u64 a = (u64)p;
+  const u32 sh = (u32)(a & 3u);
+  const u32* wp = (const u32*)(a & ~3ull);
+  const int nw = (int)((sh + n + 3u) >> 2);  // <= 16 aligned words
+  u32 qlo = 0, qhi = 0, slo = 0, shi = 0, blo = 0, bhi = 0;
+  for (int w = nw - 1; w >= 0; --w) {  // last word first: word 0 lands in bits 0..3
+    const u32 x = wp[w];
+    const u32 x7 = x & 0x7F7F7F7Fu;
+    const u32 zq = eq_bytes(x, x7, 0x22222222u);
+    const u32 zs = eq_bytes(x, x7, 0x20202020u);
+    // bad = byte < 0x20 or a backslash
+    const u32 zb = (~((x7 + 0x60606060u) | x) | eq_bytes(x, x7, 0x5C5C5C5Cu)) & 0x80808080u;
+    // gather the four 0x80 flags into bits 28..31 (products land on distinct bits)
+    const u32 pq = zq * 0x00204081u, ps = zs * 0x00204081u, pb = zb * 0x00204081u;
+    qhi = __funnelshift_l(qlo, qhi, 4); qlo = __funnelshift_l(pq, qlo, 4);
+    shi = __funnelshift_l(slo, shi, 4); slo = __funnelshift_l(ps, slo, 4);
+    bhi = __funnelshift_l(blo, bhi, 4); blo = __funnelshift_l(pb, blo, 4);
+  }
+  const u64 range = (1ull << n) - 1ull;
+  const u64 bad = ((((u64)bhi << 32) | blo) >> sh) & range;
+  if (bad) return false;
+  *qm = ((((u64)qhi << 32) | qlo) >> sh) & range;
+  *nspm = ~((((u64)shi << 32) | slo) >> sh) & range;
+  return true;
+}
+
 // JSON string body starting at i (after the quote): index of the closing quote
-// or ~0 when malformed.  Four bytes at a time until a quote, backslash or
-// control byte shows up (SWAR), then byte-wise escape validation.
-FBX_DI u32 j_string(JReader& r, u32 i, u32* esc) {
+// or ~0 when malformed.  Mask mode: the next quote.  Byte mode: four bytes at
+// a time until a quote, backslash or control byte shows up (SWAR), then
+// byte-wise escape validation.
+FBX_DI u32 j_string(const JReader& r, u32 i, u32* esc) {
+  if (r.fast) {
+    const u64 m = i < 64u ? (r.q >> i) : 0ull;
+    return m ? i + (u32)(__ffsll((long long)m) - 1) : ~0u;
+  }
+  const u64 base = (u64)r.p;
   while (i < r.n) {
-    u32 pos = r.off + i, idx = pos >> 2;
-    if (idx != r.wi) { r.wi = idx; r.w = r.wp[idx]; }
-    u32 sh = (pos & 3u) * 8u;
-    u32 v = r.w >> sh;
-    u32 avail = 4u - (pos & 3u), left = r.n - i;
+    const u64 a = base + i;
+    const u32 sh = (u32)(a & 3u) * 8u;
+    const u32 v = *(const u32*)(a & ~3ull) >> sh;
+    u32 avail = 4u - (u32)(a & 3u), left = r.n - i;
     u32 m = avail < left ? avail : left;
     u32 q = v ^ 0x22222222u, b = v ^ 0x5C5C5C5Cu;
     u32 sp = (((q - 0x01010101u) & ~q) | ((b - 0x01010101u) & ~b) | ((v - 0x20202020u) & ~v)) &
@@ -1080,7 +1188,7 @@ FBX_DI u32 j_unescape(const u8* s, u32 b, u32 e, u8* dst, u32* lone) {
 }
 
 // key comparison against a path segment, decoding escapes when present
-FBX_DI bool j_key_eq(JReader& r, const u8* s, u32 b, u32 e, u32 esc, const u8* seg, u32 slen) {
+FBX_DI bool j_key_eq(const JReader& r, const u8* s, u32 b, u32 e, u32 esc, const u8* seg, u32 slen) {
   if (!esc) {
     if (e - b != slen) return false;
     for (u32 k = 0; k < slen; ++k)
@@ -1100,7 +1208,7 @@ FBX_DI bool j_key_eq(JReader& r, const u8* s, u32 b, u32 e, u32 esc, const u8* s
 
 // number at i; returns end index (or ~0 malformed); *type J_INT / J_FLOAT,
 // *digits = number of integer digits (for the 4300-digit int limit).
-FBX_DI u32 j_number(JReader& r, u32 i, u32* type, u32* digits) {
+FBX_DI u32 j_number(const JReader& r, u32 i, u32* type, u32* digits) {
   const u32 n = r.n;
   u32 st = i;
   bool neg = r.at(i) == '-';
@@ -1130,7 +1238,7 @@ FBX_DI u32 j_number(JReader& r, u32 i, u32* type, u32* digits) {
   return i;
 }
 
-FBX_DI bool j_lit(JReader& r, u32 i, const char* w, u32 wl) {
+FBX_DI bool j_lit(const JReader& r, u32 i, const char* w, u32 wl) {
   if (i + wl > r.n) return false;
   for (u32 k = 0; k < wl; ++k)
     if (r.at(i + k) != (u8)w[k]) return false;
@@ -1146,7 +1254,11 @@ FBX_DI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
 #pragma unroll
   for (int p = 0; p < NP; ++p) leaf[p] = JLeaf{0, 0, J_MISSING, 0};
   JReader r;
-  r.init(doc.p, doc.n);
+  r.p = doc.p;
+  r.n = doc.n;
+  r.q = 0ull;
+  r.nsp = 0ull;
+  r.fast = jmask_build(doc.p, doc.n, &r.q, &r.nsp);
   const u32 n = doc.n;
   u64 kind_stack = 0;  // bit d: container at depth d+1 is an object
   u32 depth = 0;

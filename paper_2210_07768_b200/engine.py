@@ -409,7 +409,8 @@ class Engine:
 
     def _check_basic_unique(self, k: int):
         torch = self.torch
-        aux = self.side_tables[k].view(torch.int32).view(-1, 8)[:, 3]
+        words = 4 if k in self.prog.int_keyed else 8  # 16-B ISlot | 32-B Slot
+        aux = self.side_tables[k].view(torch.int32).view(-1, words)[:, 3]
         mx = int(aux.max().item()) if aux.numel() else 0
         if mx > 1:
             raise StageError("prepare", None,

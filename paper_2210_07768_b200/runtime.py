@@ -88,7 +88,8 @@ _CUBIN_CACHE: dict[str, bytes] = {}
 
 def compile_source(source: str, name: str = "plan.cu", options: tuple[str, ...] = ()) -> bytes:
     """NVRTC -> sm_100a cubin (host-only).  Cached per process and on disk."""
-    opts = ("-arch=sm_100a", "-std=c++17", "-lineinfo", "-diag-suppress=177,550", *options)
+    opts = ("-arch=sm_100a", "-std=c++17", "-lineinfo", "-diag-suppress=177,550", *options,
+            *os.environ.get("FBX_NVRTC_OPTS", "").split())  # A/B experiments only
     dump = os.environ.get("FBX_DUMP_SOURCE")
     if dump:  # profiling aid: keep the generated plan so ncu can import it by name
         Path(dump).write_text(source)

@@ -151,6 +151,50 @@ def test_adversarial_records_match_oracle(batch_size, seed, tmp_path):
     np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
 
 
+FUZZ_ALPHABET = ' "{}[]:,\\0123456789.-+eEtrufalsnNIycity\t\n\x01'
+
+
+def _fuzz_docs(n, seed):
+    """Short JSON-ish documents: random edits of the grammar corpus (covers the
+    mask-mode reader for <= 60-byte docs and its byte-scanner fallback)."""
+    rng = random.Random(seed)
+    base = [d for d in JSON_DOCS if "\\ud8" not in d] + [
+        '{"u": {"city": "a b", "tier": 1}}', '{"u":{"city":" ","tier":-0}}',
+        '{ "u" : { "city" : "k" , "tier" : 12 } }', '{"u": {"tier": 3, "city": "z"}}']
+    out = []
+    for _ in range(n):
+        d = list(rng.choice(base))
+        for _ in range(rng.choice([0, 0, 1, 1, 2, 3])):
+            op = rng.randrange(3)
+            k = rng.randrange(len(d) + 1)
+            if op == 0:
+                d.insert(k, rng.choice(FUZZ_ALPHABET))
+            elif op == 1 and d:
+                del d[min(k, len(d) - 1)]
+            elif d:
+                d[min(k, len(d) - 1)] = rng.choice(FUZZ_ALPHABET)
+        out.append("".join(d))
+    return out
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_json_fuzz_matches_oracle(seed, tmp_path):
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+    drv, prof, bas = _views(4000, seed)
+    docs = _fuzz_docs(4000, seed)
+    drv.columns["meta"] = ColumnImage.from_values(Kind.JSON, docs)
+    _write_views(tmp_path, drv, prof, bas)
+    ops = [{"name": "c", "inputs": ["cx", "tier"], "outputs": ["c"], "body": {"fn": "hash:3"}},
+           {"name": "d", "inputs": ["cx"], "outputs": ["d"], "body": {"fn": "hash:4"}}]
+    raw = _config(256, ops, {"c": 3, "d": 4}, filt="age != -12345")
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is None and got_err is None, (ref_err, got_err)
+    assert (got.report.rows_dropped, got.report.rows_filtered) == (ref.malformed, ref.filtered)
+    assert (got.report.digest, got.report.instances, got.report.signs) == \
+        (ref.digest, ref.instances, ref.signs)
+    np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
+
+
 @pytest.mark.parametrize("filt", ["age < 120.5", "age >= -4611686018427387904", "age == 20.0",
                                   "age != 9999999999999999999999", "age > -1.5 or tier == 2",
                                   "(age < 30 or age > 60) and query != ''", "cx >= 'kyoto'",
