@@ -68,6 +68,16 @@ int fbx_launch(fbx_kernel* k, unsigned grid, unsigned block, unsigned dyn_smem, 
 int fbx_state_reset(fbx_state* d_state, unsigned long long* d_tile_status, size_t n_tiles,
                     void* stream);
 
+/* Reset only the bump-pool head of the run state (ArenaPool.reset, mempool.py:136):
+ * between the launches of one run, whose counters keep accumulating. */
+int fbx_pool_reset(fbx_state* d_state, void* stream);
+
+/* Copy the run state (fbx_state) into host-mapped pinned memory with a kernel on
+ * `stream` (no copy engine: the snapshot never waits behind bulk D2H transfers).
+ * Streamed runs read each slice's emitted counts from it to size the CSR D2H.
+ * Replaces the per-batch counter read of device.py:110-113 / pipeline.py:883-886. */
+int fbx_state_snapshot(const fbx_state* d_state, void* h_mapped_dst, void* stream);
+
 /* Build an HBM open-addressing dictionary table (featureops.py:104-167):
  * n keys given as a byte blob + u32 offsets[n+1] (device), u64 values.
  * slots: capacity * 32 bytes (capacity a power of two >= 2n).  Returns

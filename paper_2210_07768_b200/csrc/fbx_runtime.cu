@@ -99,6 +99,13 @@ __global__ void k_state_reset(fbx_state* st, unsigned long long* status, size_t 
   for (; i < n; i += (size_t)gridDim.x * blockDim.x) status[i] = 0ull;
 }
 
+// run-state snapshot into host-mapped pinned memory: a kernel store, not a
+// copy-engine transfer, so it never queues behind the bulk D2H of a previous slice
+__global__ void k_state_snapshot(const unsigned long long* st, volatile unsigned long long* dst,
+                                 unsigned n) {
+  if (threadIdx.x < n) dst[threadIdx.x] = st[threadIdx.x];
+}
+
 // second-smallest chunk over {winner, later occurrences} of every repeated id
 __global__ void k_dup_resolve(const unsigned int* w, const unsigned long long* later,
                               unsigned long long n, unsigned long long* out) {
@@ -309,6 +316,18 @@ int fbx_state_reset(fbx_state* d_state, unsigned long long* d_status, size_t n_t
   if (blocks > 1184) blocks = 1184;
   k_state_reset<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_state, d_status, n_tiles);
   return cuda_check(cudaGetLastError(), "fbx_state_reset");
+}
+
+int fbx_pool_reset(fbx_state* d_state, void* stream) {
+  return cuda_check(cudaMemsetAsync(&d_state->pool_head, 0, sizeof(d_state->pool_head),
+                                    (cudaStream_t)stream), "fbx_pool_reset");
+}
+
+int fbx_state_snapshot(const fbx_state* d_state, void* h_mapped_dst, void* stream) {
+  const unsigned n = (unsigned)(sizeof(fbx_state) / 8);
+  k_state_snapshot<<<1, 32 * ((n + 31) / 32), 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)d_state, (volatile unsigned long long*)h_mapped_dst, n);
+  return cuda_check(cudaGetLastError(), "fbx_state_snapshot");
 }
 
 int fbx_dict_build(void* d_slots, unsigned long long capacity, const unsigned char* d_keyblob,

@@ -614,8 +614,7 @@ class Engine:
             # continuation of a reserved run: counters / digest / error word keep
             # accumulating across launches; only the bump pool is reset
             tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
-            with self.torch.cuda.stream(self.torch.cuda.ExternalStream(stream)):
-                self.state[1:2].zero_()
+            runtime.pool_reset(self.state.data_ptr(), stream)
         self._set("row_lo", row_lo)
         self._set("row_hi", row_hi)
         self._set("chunk0", row_lo // self.ir.chunk)
@@ -654,13 +653,29 @@ class StreamedRun:
     PARTS = ("nulls", "data", "offsets")
 
     def __init__(self, eng: "Engine", host_view: ViewImage, slice_rows: int = 1 << 17,
-                 zero_copy: bool = False):
+                 zero_copy: bool = False, taper: bool = True):
         torch = eng.torch
         self.eng, self.torch = eng, torch
         chunk = eng.ir.chunk
         self.slice_rows = max(chunk, slice_rows - slice_rows % chunk)
         self.n = n = host_view.row_count
-        self.bounds = [(lo, min(lo + self.slice_rows, n)) for lo in range(0, n, self.slice_rows)]
+        # taper: short first and last slices, so the D2H stream (the bound) starts
+        # early and the tail after the last kernel is short (for a run on its own;
+        # back-to-back runs overlap their fill and drain instead)
+        div = 4 if taper else 1
+        S = self.slice_rows
+        q = max(chunk, (S // div) // chunk * chunk) if div > 1 else S
+        cuts = [0]
+        if n > q:
+            cuts.append(q)
+        while n - cuts[-1] > S + q:
+            cuts.append(cuts[-1] + S)
+        r = n - cuts[-1]
+        if div > 1 and r > 2 * q:
+            cuts.append(cuts[-1] + (r - q) // chunk * chunk)
+        if cuts[-1] < n:
+            cuts.append(n)
+        self.bounds = [(a, b) for a, b in zip(cuts, cuts[1:])]
         used = [c for c in host_view.order if any(f"drv.{c}.{p}" in eng.slots for p in self.PARTS)]
         # Each slice's column spans packed into ONE pinned region (16-B aligned
         # pieces) -- the layout a chunk reader produces -- so a slice is one H2D.
@@ -690,7 +705,8 @@ class StreamedRun:
             self.layout.append(pieces)
             self.h2d_bytes += off
         cap = max(p.numel() for p in self.packs)
-        self.dev = [torch.empty(cap + 32, dtype=torch.uint8, device=eng.device) for _ in range(2)]
+        # three input buffer sets: the H2D of slice k+1 waits only for kernel k-2
+        self.dev = [torch.empty(cap + 32, dtype=torch.uint8, device=eng.device) for _ in range(3)]
         self.s_h2d = torch.cuda.Stream(eng.device)
         self.s_comp = torch.cuda.Stream(eng.device)
         self.s_d2h = torch.cuda.Stream(eng.device)
@@ -707,35 +723,87 @@ class StreamedRun:
         # Correct, but measured slower than DMA copies on B200/PCIe5 (246 vs 278
         # M rec/s, round 1), so off by default.
         self.zero_copy = zero_copy
+        self.trace = None  # set to [] to record a per-slice event timeline (ms)
 
     def run(self) -> Counters:
         if self.zero_copy:
             return self._run_zero_copy()
+        self.start()
+        tot = self.finish()
+        self.wait()
+        return tot
+
+    def start(self):
+        """Enqueue every slice's H2D and fused kernel (no host synchronisation).
+
+        A StreamedRun may be restarted while the previous run's CSR is still
+        draining: the new kernels wait (on the device) for that D2H.  The host
+        output buffers of a run stay valid until the next ``start``."""
         torch, eng = self.torch, self.eng
         eng.reserve(self.n, self.slice_rows)
         eng.begin_run(self.n)
         cur = torch.cuda.current_stream(eng.device)
         self.s_comp.wait_stream(cur)
         self.s_h2d.wait_stream(cur)
-        comp_done = [torch.cuda.Event() for _ in self.bounds]
+        if getattr(self, "_last_d2h", None) is not None:
+            self.s_comp.wait_event(self._last_d2h)   # the CSR arena is still draining
+        self.comp_done = comp_done = [torch.cuda.Event() for _ in self.bounds]
         h2d_done = [torch.cuda.Event() for _ in self.bounds]
-        d2h_done = [torch.cuda.Event() for _ in self.bounds]
-        tot = Counters()
+        self._trace = trace = [] if self.trace is not None else None
         tiles_before = 0
-        inst_base, sign_base = 0, 0
-        pending = []
 
-        def drain(j):
-            nonlocal inst_base, sign_base
+        def mark(name, k, stream):
+            if trace is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                trace.append((name, k, ev, time.perf_counter()))
+        self._mark = mark
+        nb = len(self.dev)
+        # buffer reuse is ordered by events on the copy stream; the host drains
+        # slice by slice in finish(): slice j's D2H is enqueued as soon as its
+        # kernel's state snapshot lands in mapped memory.
+        for k, (lo, hi) in enumerate(self.bounds):
+            buf = k % nb
+            with torch.cuda.stream(self.s_h2d):
+                if k >= nb:
+                    self.s_h2d.wait_event(comp_done[k - nb])  # buffer set reuse
+                pk = self.packs[k]
+                mark("h2d0", k, self.s_h2d)
+                self.dev[buf][: pk.numel()].copy_(pk, non_blocking=True)
+                h2d_done[k].record(self.s_h2d)
+                mark("h2d1", k, self.s_h2d)
+            base = self.dev[buf].data_ptr()
+            for c, p, a, b, o in self.layout[k]:
+                eng._set(f"drv.{c}.{p}", base + o - a)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(h2d_done[k])
+                mark("k0", k, self.s_comp)
+                eng.launch(lo, hi, self.s_comp.cuda_stream, tile_base=tiles_before)
+                runtime.state_snapshot(eng.state.data_ptr(), self.states[k].data_ptr(),
+                                       self.s_comp.cuda_stream)
+                comp_done[k].record(self.s_comp)
+                mark("k1", k, self.s_comp)
+            tiles_before += (hi - lo + eng.ir.chunk - 1) // eng.ir.chunk
+
+    def finish(self) -> Counters:
+        """Drain the run started by ``start``: per slice, wait for its kernel,
+        then enqueue the D2H of its CSR range; check the run's failures."""
+        torch, eng = self.torch, self.eng
+        comp_done, mark, trace = self.comp_done, self._mark, self._trace
+        tot = Counters()
+        inst_base, sign_base = 0, 0
+        last = None
+        for j in range(len(self.bounds)):
             comp_done[j].synchronize()
             st = self.states[j].numpy().view(np.uint64)
             stt = {f: int(st[i]) for i, f in enumerate(runtime.STATE_FIELDS)}
             # failures are resolved once at the end of the run: a label error's
-            # flush chunk and a repeated id's second chunk may lie in later slices
-            # counters accumulate over the run's launches: this slice's share
+            # flush chunk and a repeated id's second chunk may lie in later slices.
+            # Counters accumulate over the run's launches: this slice's share.
             ni, ms = stt["instances"] - inst_base, stt["signs"] - sign_base
             with torch.cuda.stream(self.s_d2h):
                 self.s_d2h.wait_event(comp_done[j])
+                mark("d2h0", j, self.s_d2h)
                 o = self.out
                 a, b = inst_base, inst_base + ni
                 o["ids"][a:b].copy_(eng.o_ids[a:b], non_blocking=True)
@@ -745,42 +813,30 @@ class StreamedRun:
                                                            non_blocking=True)
                 o["signs"][sign_base:sign_base + ms].copy_(eng.o_sign[sign_base:sign_base + ms],
                                                            non_blocking=True)
-                d2h_done[j].record(self.s_d2h)
+                mark("d2h1", j, self.s_d2h)
             inst_base += ni
             sign_base += ms
-            tot.digest = stt["digest"]
-            tot.instances, tot.signs = stt["instances"], stt["signs"]
-            tot.malformed, tot.filtered = stt["malformed"], stt["filtered"]
-            tot.joined = stt["joined"]
-            tot.launches += 1
-
-        for k, (lo, hi) in enumerate(self.bounds):
-            buf = k & 1
-            with torch.cuda.stream(self.s_h2d):
-                if k >= 2:
-                    self.s_h2d.wait_event(comp_done[k - 2])  # buffer set reuse
-                pk = self.packs[k]
-                self.dev[buf][: pk.numel()].copy_(pk, non_blocking=True)
-                h2d_done[k].record(self.s_h2d)
-            base = self.dev[buf].data_ptr()
-            for c, p, a, b, o in self.layout[k]:
-                eng._set(f"drv.{c}.{p}", base + o - a)
-            with torch.cuda.stream(self.s_comp):
-                self.s_comp.wait_event(h2d_done[k])
-                eng.launch(lo, hi, self.s_comp.cuda_stream, tile_base=tiles_before)
-                self.states[k].copy_(eng.state, non_blocking=True)
-                comp_done[k].record(self.s_comp)
-            tiles_before += (hi - lo + eng.ir.chunk - 1) // eng.ir.chunk
-            pending.append(k)
-            if len(pending) > 1:
-                drain(pending.pop(0))
-        while pending:
-            drain(pending.pop(0))
-        self.s_comp.synchronize()
-        eng.check_run(eng._read_state())
-        self.s_d2h.synchronize()
+            last = stt
+        tot.digest = last["digest"]
+        tot.instances, tot.signs = last["instances"], last["signs"]
+        tot.malformed, tot.filtered = last["malformed"], last["filtered"]
+        tot.joined = last["joined"]
+        tot.launches = len(self.bounds)
+        ev = torch.cuda.Event()
+        ev.record(self.s_d2h)
+        self._last_d2h = ev
+        # the last snapshot is the run's final state (no extra D2H read)
+        eng.check_run(last)
         self.d2h_bytes = tot.instances * 17 + 8 + tot.signs * 10
+        if trace:
+            t0e, t0h = trace[0][2], trace[0][3]
+            self.trace = [(nm, k, t0e.elapsed_time(ev), (th - t0h) * 1e3) for nm, k, ev, th in trace]
         return tot
+
+    def wait(self):
+        """Block until the last finished run's CSR is in host memory."""
+        if getattr(self, "_last_d2h", None) is not None:
+            self._last_d2h.synchronize()
 
     def _run_zero_copy(self) -> Counters:
         torch, eng = self.torch, self.eng

@@ -31,7 +31,8 @@ EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_prog
            "fbx_program_unload", "fbx_program_kernel", "fbx_kernel_attributes",
            "fbx_kernel_set_max_dynamic_smem", "fbx_launch", "fbx_state_reset",
            "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
-           "fbx_dup_resolve")
+           "fbx_dup_resolve", "fbx_state_snapshot",
+           "fbx_pool_reset")
 
 
 class FbxError(RuntimeError):
@@ -68,6 +69,8 @@ def lib() -> ctypes.CDLL:
             L.fbx_exclusive_scan_u32.argtypes = [vp, vp, ctypes.c_ulonglong, vp]
             L.fbx_gather_strings.argtypes = [vp, vp, vp, ctypes.c_ulonglong, vp, vp]
             L.fbx_dup_resolve.argtypes = [vp, vp, ctypes.c_ulonglong, vp, vp]
+            L.fbx_state_snapshot.argtypes = [vp, vp, vp]
+            L.fbx_pool_reset.argtypes = [vp, vp]
             for name in EXPORTS:
                 getattr(L, name).restype = getattr(L, name).restype or c
             L.fbx_version.restype = ctypes.c_char_p
@@ -164,6 +167,15 @@ class Program:
 def state_reset(d_state: int, d_status: int, n_tiles: int, stream: int):
     _check(lib().fbx_state_reset(ctypes.c_void_p(d_state), ctypes.c_void_p(d_status),
                                  int(n_tiles), ctypes.c_void_p(stream)), "state reset")
+
+
+def state_snapshot(d_state: int, h_mapped: int, stream: int):
+    _check(lib().fbx_state_snapshot(ctypes.c_void_p(d_state), ctypes.c_void_p(h_mapped),
+                                    ctypes.c_void_p(stream)), "state snapshot")
+
+
+def pool_reset(d_state: int, stream: int):
+    _check(lib().fbx_pool_reset(ctypes.c_void_p(d_state), ctypes.c_void_p(stream)), "pool reset")
 
 
 def dict_build(d_slots: int, capacity: int, d_blob: int, d_offs: int, d_vals: int, n: int,

@@ -38,3 +38,28 @@ def both():
 
 a, b, c = t(h2d), t(d2h), t(both)
 print(f"H2D {n / a / 1e9:.1f} GB/s  D2H {n / b / 1e9:.1f} GB/s  both {2 * n / c / 1e9:.1f} GB/s total")
+
+# the e2e step's transfer pattern alone (no kernels, no dependencies):
+# 102.5 MB H2D in 6 pieces on one stream, 131.3 MB D2H in 6 x 5 pieces on another
+H, D = 102_522_448, 131_291_299
+hs = torch.empty(H, dtype=torch.uint8, pin_memory=True)
+hd = torch.empty(D, dtype=torch.uint8, pin_memory=True)
+dh = torch.empty(H, dtype=torch.uint8, device=dev)
+dd = torch.empty(D, dtype=torch.uint8, device=dev)
+
+
+def pattern(nh=6, nd=30):
+    with torch.cuda.stream(s1):
+        step = H // nh
+        for i in range(nh):
+            dh[i * step:(i + 1) * step].copy_(hs[i * step:(i + 1) * step], non_blocking=True)
+    with torch.cuda.stream(s2):
+        step = D // nd
+        for i in range(nd):
+            hd[i * step:(i + 1) * step].copy_(dd[i * step:(i + 1) * step], non_blocking=True)
+
+
+for nh, nd in ((1, 1), (6, 6), (6, 30)):
+    tt = t(lambda: pattern(nh, nd))
+    print(f"e2e transfer pattern H2D {nh} + D2H {nd} pieces: {tt * 1e3:.3f} ms "
+          f"({(H + D) / tt / 1e9:.1f} GB/s) -> bound {1e6 / tt / 1e6:.0f} M rec/s")
