@@ -1271,33 +1271,21 @@ class PlanCodegen:
         g("__syncthreads();")
         g("const u32 myoff = alive ? sm.rank[myrank] : 0u;")
         g("{")
-        g("u64 r0 = digest, r1 = malformed, r2 = filtered, r3 = joined;")
-        g("#pragma unroll")
-        g("for (int d = 16; d > 0; d >>= 1) {")
-        g("r0 ^= __shfl_xor_sync(0xFFFFFFFFu, r0, d); r1 += __shfl_xor_sync(0xFFFFFFFFu, r1, d);")
-        g("r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, d); r3 += __shfl_xor_sync(0xFFFFFFFFu, r3, d);")
+        g("// warp reductions (redux.sync): the XOR digest and three <=512 counters packed")
+        g("const u32 r0l = __reduce_xor_sync(0xFFFFFFFFu, (u32)digest);")
+        g("const u32 r0h = __reduce_xor_sync(0xFFFFFFFFu, (u32)(digest >> 32));")
+        g("const u32 rc = __reduce_add_sync(0xFFFFFFFFu, malformed | (filtered << 10) | (joined << 20));")
+        g("if ((threadIdx.x & 31u) == 0) { sm.red[threadIdx.x >> 5][0] = ((u64)r0h << 32) | r0l; "
+          "sm.red[threadIdx.x >> 5][1] = rc & 0x3FFu; sm.red[threadIdx.x >> 5][2] = (rc >> 10) & 0x3FFu; "
+          "sm.red[threadIdx.x >> 5][3] = rc >> 20; }")
         g("}")
-        g("if ((threadIdx.x & 31u) == 0) { sm.red[threadIdx.x >> 5][0] = r0; "
-          "sm.red[threadIdx.x >> 5][1] = r1; sm.red[threadIdx.x >> 5][2] = r2; "
-          "sm.red[threadIdx.x >> 5][3] = r3; }")
-        g("}")
-        # stage the tile's CSR in shared memory in final order (coalesced write-out)
-        g("// stage the tile's CSR in emission order in shared memory (reuses the span buffer)")
-        g("const u32 out_bytes = tile_signs * 10u + n_inst * 17u + 64u;")
+        # look-back first; then the tile's CSR is staged in shared memory in final
+        # order, each array at its global address mod 16, and leaves by TMA bulk
+        # stores (ragged 16-B head/tail bytewise)
+        g("// the tile's CSR staged in emission order (reuses the span buffer); each")
+        g("// array at its global address mod 16 so the middle leaves by one TMA store")
+        g("const u32 out_bytes = tile_signs * 10u + n_inst * 17u + 176u;")
         g("const bool staged_out = out_bytes <= DYN_SMEM;")
-        g("u64* s_sign = (u64*)dyn_smem;")
-        g("u64* s_ids = s_sign + tile_signs;")
-        g("u32* st_off = (u32*)(s_ids + n_inst);")
-        g("u16* s_slot = (u16*)(st_off + n_inst);")
-        g("u8* s_lab = (u8*)(s_slot + tile_signs);")
-        g("__syncthreads();")
-        g("if (staged_out && alive) {")
-        g("const u32 r = myrank;")
-        g("u32 so = myoff;")
-        g(f"s_ids[r] = {idv.c}; s_lab[r] = (u8)({lab.c}); st_off[r] = so;")
-        for q, (slot, _) in enumerate(fv):
-            g(f"if ((fpres >> {q}) & 1u) {{ s_slot[so] = (u16){slot}u; s_sign[so] = fsg[{q}]; ++so; }}")
-        g("}")
         g("if (threadIdx.x < 32u) {")
         g("u64 ei = 0, es = 0;")
         g("fbx::lookback(STATUS, tile, n_inst, tile_signs, &ei, &es);")
@@ -1320,11 +1308,28 @@ class PlanCodegen:
         g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
         g("const u64 ei = sm.ex_inst, es = sm.ex_signs;")
         g(f"if (emit_bad) fbx::raise_emit(ST, ei + myrank, {ir.chunk}u, emit_bad == 2u, {lab.c});")
+        g("u8* const st_sign = dyn_smem + ((u64)(O_SIGN + es) & 15u);")
+        g("u8* const st_slot = st_sign + ((8u * tile_signs + 15u) & ~15u) + 16u - ((u64)(O_SIGN + es) & 15u) + ((u64)(O_SLOT + es) & 15u);")
+        g("u8* const st_ids = st_slot + ((2u * tile_signs + 15u) & ~15u) + 16u - ((u64)(O_SLOT + es) & 15u) + ((u64)(O_IDS + ei) & 15u);")
+        g("u8* const st_off = st_ids + ((8u * n_inst + 15u) & ~15u) + 16u - ((u64)(O_IDS + ei) & 15u) + ((u64)(O_OFF + ei) & 15u);")
+        g("u8* const st_lab = st_off + ((8u * n_inst + 15u) & ~15u) + 16u - ((u64)(O_OFF + ei) & 15u) + ((u64)(O_LAB + ei) & 15u);")
         g("if (staged_out) {")
-        g("for (u32 q = threadIdx.x; q < tile_signs; q += NT) { O_SIGN[es + q] = s_sign[q]; "
-          "O_SLOT[es + q] = s_slot[q]; }")
-        g("for (u32 q = threadIdx.x; q < n_inst; q += NT) { O_IDS[ei + q] = s_ids[q]; "
-          "O_OFF[ei + q] = es + st_off[q]; O_LAB[ei + q] = s_lab[q]; }")
+        g("if (alive) {")
+        g("u64* s_sign = (u64*)st_sign; u16* s_slot = (u16*)st_slot;")
+        g("const u32 r = myrank;")
+        g("u32 so = myoff;")
+        g(f"((u64*)st_ids)[r] = {idv.c}; st_lab[r] = (u8)({lab.c}); ((u64*)st_off)[r] = es + so;")
+        for q, (slot, _) in enumerate(fv):
+            g(f"if ((fpres >> {q}) & 1u) {{ s_slot[so] = (u16){slot}u; s_sign[so] = fsg[{q}]; ++so; }}")
+        g("}")
+        g("fbx::fence_async_smem();")
+        g("__syncthreads();")
+        g("fbx::tile_out<NT>((u8*)(O_SIGN + es), st_sign, 8u * tile_signs);")
+        g("fbx::tile_out<NT>((u8*)(O_SLOT + es), st_slot, 2u * tile_signs);")
+        g("fbx::tile_out<NT>((u8*)(O_IDS + ei), st_ids, 8u * n_inst);")
+        g("fbx::tile_out<NT>((u8*)(O_OFF + ei), st_off, 8u * n_inst);")
+        g("fbx::tile_out<NT>(O_LAB + ei, st_lab, n_inst);")
+        g("if (threadIdx.x == 0) fbx::bulk_commit();")
         g("} else if (alive) {")
         g("const u64 pos = ei + myrank;")
         g("u64 so = es + myoff;")
@@ -1336,6 +1341,7 @@ class PlanCodegen:
         g("if (threadIdx.x == 0) O_OFF[ei + n_inst] = es + tile_signs;")
         for line in self._ids_tail:
             g(line)
+        g("if (threadIdx.x == 0 && staged_out) fbx::bulk_wait_read();  // smem lives until read")
         g("}")
         return "fbx_pipeline"
 

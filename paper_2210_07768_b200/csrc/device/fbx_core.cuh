@@ -889,6 +889,29 @@ FBX_DI void islot_insert(ISlot* T, u64 mask, u64 h, u64 key, u32 row) {
   }
 }
 
+// TMA bulk store shared -> global (bulk async-group; 16-B aligned, 16-B multiple)
+FBX_DI void bulk_s2g(void* gdst, const void* ssrc, u32 bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes)
+               : "memory");
+}
+FBX_DI void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+FBX_DI void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+FBX_DI void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Copy n bytes staged at s (s == g mod 16) to global g: the 16-B aligned middle
+// by one TMA bulk store (issued by thread 0), the ragged head / tail bytewise.
+template <int NT>
+FBX_DI void tile_out(u8* g, const u8* s, u32 n) {
+  const u32 head = (u32)((16u - ((u64)g & 15u)) & 15u) < n ? (u32)((16u - ((u64)g & 15u)) & 15u) : n;
+  const u32 mid = (n - head) & ~15u;
+  for (u32 b = threadIdx.x; b < n - mid; b += NT) {
+    const u32 o = b < head ? b : b + mid;
+    g[o] = s[o];
+  }
+  if (threadIdx.x == 0 && mid) bulk_s2g(g + head, s + head, mid);
+}
+
 FBX_DI void mbar_wait(u64* bar, u32 phase) {
   u32 done = 0;
   while (!done) {
@@ -1040,14 +1063,14 @@ struct JReader {
   const u8* p;
   u32 n;
   bool fast;
-  u64 q;    // quote bytes (doc-relative, fast mode)
-  u64 nsp;  // non-space bytes (doc-relative, fast mode)
+  // fast mode, bit-reversed (bit 63 - j = byte j) so "first set bit at or
+  // after i" is a left shift and a count-leading-zeros:
+  u64 q;    // quote bytes | sentinel at byte 63 (no closing quote -> >= n)
+  u64 nsp;  // non-space bytes | sentinel at byte n (all space -> n)
   FBX_DI u32 at(u32 k) const { return p[k]; }  // byte k, k < n
-  FBX_DI u32 skip_ws(u32 i) const {
-    if (fast) {
-      const u64 m = i < 64u ? (nsp >> i) : 0ull;
-      return m ? i + (u32)(__ffsll((long long)m) - 1) : (i > n ? i : n);
-    }
+  FBX_DI u32 skip_ws(u32 i) const {  // i <= n
+    if (fast) return i + (u32)__clzll((long long)(nsp << i));
+
     while (i < n) {
       const u32 c = at(i);
       if (c > 0x20u || !j_ws(c)) break;
@@ -1084,8 +1107,10 @@ FBX_DI bool jmask_build(const u8* p, u32 n, u64* qm, u64* nspm) {
   const u64 range = (1ull << n) - 1ull;
   const u64 bad = ((((u64)bhi << 32) | blo) >> sh) & range;
   if (bad) return false;
-  *qm = ((((u64)qhi << 32) | qlo) >> sh) & range;
-  *nspm = ~((((u64)shi << 32) | slo) >> sh) & range;
+  const u64 qq = ((((u64)qhi << 32) | qlo) >> sh) & range;
+  const u64 ns = ~((((u64)shi << 32) | slo) >> sh) & range;
+  *qm = __brevll(qq | (1ull << 63));
+  *nspm = __brevll(ns | (1ull << n));
   return true;
 }
 
@@ -1094,9 +1119,9 @@ FBX_DI bool jmask_build(const u8* p, u32 n, u64* qm, u64* nspm) {
 // a time until a quote, backslash or control byte shows up (SWAR), then
 // byte-wise escape validation.
 FBX_DI u32 j_string(const JReader& r, u32 i, u32* esc) {
-  if (r.fast) {
-    const u64 m = i < 64u ? (r.q >> i) : 0ull;
-    return m ? i + (u32)(__ffsll((long long)m) - 1) : ~0u;
+  if (r.fast) {  // i <= n
+    const u32 e = i + (u32)__clzll((long long)(r.q << i));
+    return e < r.n ? e : ~0u;
   }
   const u64 base = (u64)r.p;
   while (i < r.n) {
