@@ -71,6 +71,9 @@ def parse_args():
     ap.add_argument("--launch-rows", type=int, default=1 << 24)
     ap.add_argument("--e2e-slice-rows", type=int, default=1 << 18)
     ap.add_argument("--e2e-stream-slice-rows", type=int, default=1 << 20)
+    ap.add_argument("--lookup-fillers", type=int, default=10_000_000,
+                    help="lookup_heavy: never-matching query_dict fillers (SURVEY 8d: >= 1e7 so "
+                         "the HBM table exceeds L2)")
     return ap.parse_args()
 
 
@@ -216,7 +219,7 @@ def main():
         tmp = Path(tempfile.mkdtemp(prefix="fbxbench"))
         write_corpus(corpus, tmp)
         if args.dag == "lookup_heavy":
-            write_lookup_tables(tmp, args.users)
+            write_lookup_tables(tmp, args.users, args.lookup_fillers)
         cfg = config_from_dict(raw, tmp)
         views = {"user_events": corpus.driver, "user_profile": corpus.profile}
         t1 = time.time()

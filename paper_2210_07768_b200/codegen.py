@@ -235,6 +235,8 @@ class PlanCodegen:
         self.pool_sites = 0
         self._ids_tail: list[str] = []
         self.pf_slot: dict[int, int] = {}
+        self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
+        self._pf_tail: list[str] = []
 
     # -- value helpers ---------------------------------------------------------
     def kind_t(self, kind: Kind) -> str:
@@ -1045,6 +1047,32 @@ class PlanCodegen:
                   f"{data} + sm.span_lo[{i}], sm.span_len[{i}], &sm.bar);")
             g("}")
             g("__syncthreads();")
+        # ---- L2 prefetch of the tile PF ahead (the CTA that starts when this one
+        # retires): its fixed columns, bitmaps and offsets now, its string spans
+        # at the end of this tile (their offsets are L2 hits by then)
+        pf_cols = [(c, k) for c, k in drv.kinds.items() if c in needed]
+        pf_dist = 148 * self.min_blocks
+        if self.prefetch_next:
+            g(f"const u32 PF_TILE = blockIdx.x + {pf_dist}u;")
+            g(f"const bool pf_on = threadIdx.x == 0 && PF_TILE + 1u < gridDim.x;")
+            g("if (pf_on) {")
+            g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {ir.chunk}ull, p1 = p0 + {ir.chunk}ull;")
+            for c, k in pf_cols:
+                g(f"fbx::prefetch_span({g.p(f'drv.{c}.nulls', 'const u8*')} + (p0 >> 3), ((p1 - p0) >> 3) + 1);")
+                if k.var_length:
+                    g(f"fbx::prefetch_span({g.p(f'drv.{c}.offsets', 'const u32*')} + p0, (p1 - p0 + 1) * 4);")
+                else:
+                    w = 8 if k is Kind.INT64 else 4
+                    g(f"fbx::prefetch_span({g.p(f'drv.{c}.data', 'const u8*')} + p0 * {w}, (p1 - p0) * {w});")
+            g("}")
+            self._pf_tail = []
+            for c, k in pf_cols:
+                if k.var_length:
+                    offs = g.p(f"drv.{c}.offsets", "const u32*")
+                    data = g.p(f"drv.{c}.data", "const u8*")
+                    self._pf_tail.append(
+                        f"{{ const u32 a = fbx::ldg_u32({offs} + p0), b = fbx::ldg_u32({offs} + p1);"
+                        f" fbx::prefetch_span({data} + a, b - a); }}")
         # ---- prologue loads: every driver column this plan reads ----------------
         g("// ---- prologue: coalesced loads of the row's fixed columns / offsets ----")
         raw: dict[str, V] = {}
@@ -1227,14 +1255,6 @@ class PlanCodegen:
             i = j
         g("if (!alive) fpres = 0u;")
         g("const u32 m = alive ? __popc(fpres) : 0u;")
-        g("u64 digest = 0ull;")
-        g("if (alive) {")
-        g("fbx::Fnv h;")
-        g(f"h.u64_le({idv.c}); h.byte((u32)({lab.c} & 1ull));")
-        for q, (slot, _) in enumerate(fv):
-            g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
-        g("digest = h.value();")
-        g("}")
         # ---- tile: sort by instance id, offsets, look-back, write -----------------------
         g("// ---- chunk emission order: ascending u64 instance id (viewpipe.py:521) ----")
         g(f"u64 skey = alive ? {idv.c} : ~0ull;")
@@ -1270,6 +1290,23 @@ class PlanCodegen:
         g("sm.rank[threadIdx.x] = s_off;  // sign offset by sorted position")
         g("__syncthreads();")
         g("const u32 myoff = alive ? sm.rank[myrank] : 0u;")
+        # look-back by warp 0 while every warp (warp 0 after it) hashes its rows'
+        # instance digests -- the digest is off the path to the aggregate publish
+        g("const u32 out_bytes = tile_signs * 10u + n_inst * 17u + 176u;")
+        g("const bool staged_out = out_bytes <= DYN_SMEM;")
+        g("if (threadIdx.x < 32u) {")
+        g("u64 ei = 0, es = 0;")
+        g("fbx::lookback(STATUS, tile, n_inst, tile_signs, &ei, &es);")
+        g("if (threadIdx.x == 0) { sm.ex_inst = ei; sm.ex_signs = es; }")
+        g("}")
+        g("u64 digest = 0ull;")
+        g("if (alive) {")
+        g("fbx::Fnv h;")
+        g(f"h.u64_le({idv.c}); h.byte((u32)({lab.c} & 1ull));")
+        for q, (slot, _) in enumerate(fv):
+            g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
+        g("digest = h.value();")
+        g("}")
         g("{")
         g("// warp reductions (redux.sync): the XOR digest and three <=512 counters packed")
         g("const u32 r0l = __reduce_xor_sync(0xFFFFFFFFu, (u32)digest);")
@@ -1279,18 +1316,8 @@ class PlanCodegen:
           "sm.red[threadIdx.x >> 5][1] = rc & 0x3FFu; sm.red[threadIdx.x >> 5][2] = (rc >> 10) & 0x3FFu; "
           "sm.red[threadIdx.x >> 5][3] = rc >> 20; }")
         g("}")
-        # look-back first; then the tile's CSR is staged in shared memory in final
-        # order, each array at its global address mod 16, and leaves by TMA bulk
-        # stores (ragged 16-B head/tail bytewise)
-        g("// the tile's CSR staged in emission order (reuses the span buffer); each")
-        g("// array at its global address mod 16 so the middle leaves by one TMA store")
-        g("const u32 out_bytes = tile_signs * 10u + n_inst * 17u + 176u;")
-        g("const bool staged_out = out_bytes <= DYN_SMEM;")
-        g("if (threadIdx.x < 32u) {")
-        g("u64 ei = 0, es = 0;")
-        g("fbx::lookback(STATUS, tile, n_inst, tile_signs, &ei, &es);")
+        g("__syncthreads();")
         g("if (threadIdx.x == 0) {")
-        g("sm.ex_inst = ei; sm.ex_signs = es;")
         g("u64 r0 = 0, r1 = 0, r2 = 0, r3 = 0;")
         g("for (int w = 0; w < NT / 32; ++w) { r0 ^= sm.red[w][0]; r1 += sm.red[w][1]; "
           "r2 += sm.red[w][2]; r3 += sm.red[w][3]; }")
@@ -1301,8 +1328,6 @@ class PlanCodegen:
         g("if (r2) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)r2);")
         g("if (r3) atomicAdd((unsigned long long*)&ST->joined, (unsigned long long)r3);")
         g("}")
-        g("}")
-        g("__syncthreads();")
         g(f"u64* O_IDS = {g.p('out.ids', 'u64*')}; u8* O_LAB = {g.p('out.labels', 'u8*')};")
         g(f"u64* O_OFF = {g.p('out.offsets', 'u64*')}; u16* O_SLOT = {g.p('out.slots', 'u16*')};")
         g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
@@ -1341,6 +1366,12 @@ class PlanCodegen:
         g("if (threadIdx.x == 0) O_OFF[ei + n_inst] = es + tile_signs;")
         for line in self._ids_tail:
             g(line)
+        if self.prefetch_next and self._pf_tail:
+            g("if (pf_on) {")
+            g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {ir.chunk}ull, p1 = p0 + {ir.chunk}ull;")
+            for line in self._pf_tail:
+                g(line)
+            g("}")
         g("if (threadIdx.x == 0 && staged_out) fbx::bulk_wait_read();  // smem lives until read")
         g("}")
         return "fbx_pipeline"

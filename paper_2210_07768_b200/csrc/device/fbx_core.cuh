@@ -889,6 +889,15 @@ FBX_DI void islot_insert(ISlot* T, u64 mask, u64 h, u64 key, u32 row) {
   }
 }
 
+// L2 prefetch of a byte range (TMA bulk prefetch; the range is widened to 16 B)
+FBX_DI void prefetch_span(const void* p, u64 bytes) {
+  const u64 a = (u64)p & ~15ull, e = ((u64)p + bytes + 15ull) & ~15ull;
+  for (u64 x = a; x < e; x += (1u << 20)) {
+    const u32 len = (u32)((e - x) < (1ull << 20) ? (e - x) : (1ull << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x), "r"(len) : "memory");
+  }
+}
+
 // TMA bulk store shared -> global (bulk async-group; 16-B aligned, 16-B multiple)
 FBX_DI void bulk_s2g(void* gdst, const void* ssrc, u32 bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),

@@ -139,6 +139,10 @@ def lookup_table_entries(users: int, fillers: int = 100_000) -> dict[str, dict[s
 
 def write_lookup_tables(dest: str | Path, users: int, fillers: int = 100_000) -> None:
     dest = Path(dest)
-    for name, entries in lookup_table_entries(users, fillers).items():
-        (dest / f"{name}.tsv").write_text("".join(f"{k}\t{v}\n" for k, v in entries.items()),
-                                          encoding="utf-8")
+    for name, entries in lookup_table_entries(users, 0).items():
+        with open(dest / f"{name}.tsv", "w", encoding="utf-8") as fh:
+            fh.write("".join(f"{k}\t{v}\n" for k, v in entries.items()))
+            if name == "query_dict":  # fillers f{i} -> i, streamed (1e7 lines)
+                step = 1 << 20
+                for lo in range(0, fillers, step):
+                    fh.write("".join(f"f{i}\t{i}\n" for i in range(lo, min(lo + step, fillers))))
