@@ -171,16 +171,20 @@ def cpu_baseline(corpus, raw_cfg, tables_dir, sample_rows, procs=None):
 
 # ---------------------------------------------------------------------------
 
-def algorithmic_bytes(corpus, counters) -> dict:
-    """Compulsory HBM bytes of one step (SURVEY.md §8 d)."""
+def algorithmic_bytes(corpus, counters, dict_probes_per_row: int = 0) -> dict:
+    """Compulsory HBM bytes of one step (SURVEY.md §8 d).
+
+    dict_probes_per_row: lookups per live row into dictionaries larger than L2
+    (lookup_heavy: query_dict with 1e7 fillers), one 32-B sector each."""
     d = corpus.driver
     inp = sum(d.columns[c].nbytes() for c in d.order)
     b = corpus.basic
     basic = sum(b.columns[c].nbytes() for c in ("instance_id", "basic_a", "basic_b"))
     probe = 32 * counters.joined  # one 32-B sector of the basic index per merged row
     out = counters.instances * (8 + 1 + 8) + counters.signs * (2 + 8)
-    return {"input": inp, "basic": basic, "basic_probe": probe, "output": out,
-            "total": inp + basic + probe + out}
+    dprobe = 32 * dict_probes_per_row * counters.joined
+    return {"input": inp, "basic": basic, "basic_probe": probe, "dict_probe": dprobe,
+            "output": out, "total": inp + basic + probe + dprobe + out}
 
 
 def main():
@@ -262,7 +266,8 @@ def main():
                              f"{c.signs}, want 0x{want[0]:016x} / {want[1]} / {want[2]}")
     ab = None
     for (corp, _, _, _), cc in zip(shards, results):
-        b = algorithmic_bytes(corp, cc)
+        big = 1 if (args.dag == "lookup_heavy" and args.lookup_fillers * 64 > (126 << 20)) else 0
+        b = algorithmic_bytes(corp, cc, big)
         ab = b if ab is None else {k: ab[k] + b[k] for k in ab}
 
     # ---- timed device-resident steps ---------------------------------------
@@ -356,6 +361,8 @@ def main():
                                    f"{args.rows} records/GPU, seed {args.seed}+rank")
                                 + f", users {args.users}, full emit incl. basic merge"),
                    "batch_size": cfg.batch_size,
+                   **({"query_dict_keys": 47296 + args.lookup_fillers}
+                      if args.dag == "lookup_heavy" else {}),
                    "l2": "flushed between steps (512 MiB write, outside the timed events)",
                    "parallelism": f"record-sharded x{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

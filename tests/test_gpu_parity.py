@@ -95,3 +95,48 @@ def test_streamed_e2e_equals_device_resident(dag, zero_copy, goldens):
     ref = _run(20000, 2000, 7, dag).csr
     for k in ("ids", "labels", "offsets", "slots", "signs"):
         np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+
+
+def test_streamed_runs_back_to_back_two_engines(goldens):
+    """start()/finish() pipelining: run k+1's H2D and kernels are enqueued before
+    run k drains; every run's CSR still equals the device-resident result."""
+    from paper_2210_07768_b200 import engine as E
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.workloads import workload_config
+    c, d = corpus(20000, 2000, 7)
+    views = {"user_events": c.driver, "user_profile": c.profile}
+    cfg = config_from_dict(workload_config("sign_heavy"), d)
+    engs = [E.Engine(E.prepare(cfg, views, c.basic), views, c.basic) for _ in range(2)]
+    for taper in (False, True):
+        srs = [E.StreamedRun(e, c.driver, slice_rows=4096, taper=taper) for e in engs]
+        ref = _run(20000, 2000, 7, "sign_heavy").csr
+        g = golden_run(goldens, 20000, 7, "sign_heavy")
+        srs[0].start()
+        for k in range(5):
+            if k + 1 < 5:
+                srs[(k + 1) % 2].start()
+            tot = srs[k % 2].finish()
+            srs[k % 2].wait()
+            assert f"0x{tot.digest:016x}" == g["digest"]
+            got = srs[k % 2].csr(tot)
+            for key in ("ids", "labels", "offsets", "slots", "signs"):
+                np.testing.assert_array_equal(got[key], ref[key], err_msg=f"{key} run {k}")
+        for r in srs:
+            r.wait()
+
+
+def test_streamed_slice_plan_covers_rows():
+    """Tapered slices: chunk-aligned cuts covering every row exactly once."""
+    from paper_2210_07768_b200 import engine as E
+    c, d = corpus(20000, 2000, 7)
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.workloads import workload_config
+    views = {"user_events": c.driver, "user_profile": c.profile}
+    eng = E.Engine(E.prepare(config_from_dict(workload_config("default"), d), views, c.basic),
+                   views, c.basic)
+    for rows, taper in ((1000, True), (4096, True), (4096, False), (1 << 20, True)):
+        sr = E.StreamedRun(eng, c.driver, slice_rows=rows, taper=taper)
+        cuts = [a for a, _ in sr.bounds] + [sr.bounds[-1][1]]
+        assert cuts[0] == 0 and cuts[-1] == 20000
+        assert all(a < b for a, b in sr.bounds)
+        assert all(x % eng.ir.chunk == 0 for x in cuts[:-1])
