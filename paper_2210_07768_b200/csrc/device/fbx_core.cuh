@@ -197,10 +197,46 @@ struct WordCursor {
 
 // Several fields of one single-byte split in one SWAR pass (codegen groups
 // token calls that share an input and a delimiter).  want[k] = field number.
+// 0x80 in every byte of x equal to the byte replicated in c (x7 = x & 0x7F7F7F7F)
+FBX_DI u32 eq_bytes(u32 x, u32 x7, u32 c) { return ~(((x7 ^ c) + 0x7F7F7F7Fu) | x) & 0x80808080u; }
+
+// bit j = (p[j] == c) for a span of 1..60 bytes: one branch-free pass over its
+// aligned words (flags gathered by one IMAD per word, see jmask_build)
+FBX_DI u64 byte_mask64(const u8* p, u32 n, u32 c) {
+  const u64 a = (u64)p;
+  const u32 sh = (u32)(a & 3u);
+  const u32* wp = (const u32*)(a & ~3ull);
+  const int nw = (int)((sh + n + 3u) >> 2);
+  const u32 cc = c * 0x01010101u;
+  u32 lo = 0, hi = 0;
+  for (int w = nw - 1; w >= 0; --w) {
+    const u32 x = wp[w];
+    const u32 pz = eq_bytes(x, x & 0x7F7F7F7Fu, cc) * 0x00204081u;
+    hi = __funnelshift_l(lo, hi, 4);
+    lo = __funnelshift_l(pz, lo, 4);
+  }
+  return ((((u64)hi << 32) | lo) >> sh) & ((1ull << n) - 1ull);
+}
+
 template <int K>
 FBX_DI void str_tokens(Str s, u32 delim, const u32 (&want)[K], Str (&out)[K]) {
 #pragma unroll
   for (int k = 0; k < K; ++k) out[k] = Str{s.p, 0u};
+  if (s.n != 0u && s.n <= 60u) {
+    // mask mode: field f ends at the f-th set bit of the delimiter mask (or n)
+    u64 m = byte_mask64(s.p, s.n, delim);
+    u32 start = 0;
+#pragma unroll
+    for (u32 f = 0; f <= want[K - 1]; ++f) {
+      const u32 end = m ? (u32)(__ffsll((long long)m) - 1) : s.n;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (want[k] == f && start <= s.n) out[k] = Str{s.p + start, end - start};
+      start = end + 1u;
+      m &= m - 1ull;
+    }
+    return;
+  }
   u32 field = 0, start = 0;
   if (s.n) {
     const WordCursor wc(s.p, s.n);
@@ -1089,8 +1125,6 @@ struct JReader {
   }
 };
 
-// 0x80 in every byte of x equal to the byte replicated in c (x7 = x & 0x7F7F7F7F)
-FBX_DI u32 eq_bytes(u32 x, u32 x7, u32 c) { return ~(((x7 ^ c) + 0x7F7F7F7Fu) | x) & 0x80808080u; }
 
 // The mask mode's single pass: false -> the document needs the byte scanner.
 FBX_DI bool jmask_build(const u8* p, u32 n, u64* qm, u64* nspm) {

@@ -37,6 +37,8 @@ JSON_DOCS = [
 QUERIES = ["running shoes", "Coffee Beans", "  desk  ", "", "a  b", "x", "mechanical keyboard gravel bike",
            "ÉCOLE café", "tab\tsep", None, "ΟΔΟΣ ΑΣ.Σ", "İstanbul", "ΣΑΣ", "Ω\u0345x", "ŉ ǅ ß ẞ",
            "\U0001F600 SMILE", "ПРИВЕТ мир", "Σ", "A\u00adΣ", "x\u2019Σ y"]
+LONG_QUERIES = ["w " * 30, "long query " * 6 + "x", " lead", "trail ", "a  b  c  d  e", "x" * 61,
+                " " * 59 + "y", "q" * 60, "é " * 20 + "z"]
 
 
 def _views(n, seed):
@@ -190,6 +192,26 @@ def test_json_fuzz_matches_oracle(seed, tmp_path):
     ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
     assert ref_err is None and got_err is None, (ref_err, got_err)
     assert (got.report.rows_dropped, got.report.rows_filtered) == (ref.malformed, ref.filtered)
+    assert (got.report.digest, got.report.instances, got.report.signs) == \
+        (ref.digest, ref.instances, ref.signs)
+    np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
+
+
+def test_tokens_long_and_ragged_queries_match_oracle(tmp_path):
+    """token splits over <= 60-byte queries (mask mode) and longer ones (scan)."""
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+    drv, prof, bas = _views(3000, 31)
+    rng = random.Random(31)
+    qs = [rng.choice(LONG_QUERIES + QUERIES) for _ in range(3000)]
+    drv.columns["query"] = ColumnImage.from_values(Kind.UTF8, qs)
+    _write_views(tmp_path, drv, prof, bas)
+    ops = [{"name": f"t{i}", "inputs": ["query"], "outputs": [f"t{i}"],
+            "pre": [{"fn": f"token: :{i}"}], "body": {"fn": f"hash:{10 + i}"}} for i in range(5)]
+    ops.append({"name": "t9", "inputs": ["query"], "outputs": ["t9"],
+                "pre": [{"fn": "token: :9"}], "body": {"fn": "hash:19"}})
+    raw = _config(256, ops, {f"t{i}": 10 + i for i in (0, 1, 2, 3, 4, 9)}, filt="age != -12345")
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is None and got_err is None, (ref_err, got_err)
     assert (got.report.digest, got.report.instances, got.report.signs) == \
         (ref.digest, ref.instances, ref.signs)
     np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
