@@ -724,7 +724,7 @@ class PlanCodegen:
             if gk not in self.token_done:
                 base = g.fresh("tg")
                 kk = len(fields)
-                g(f"fbx::Str {base}[{kk}];")
+                g(f"fbx::Str {base}[{kk}] = {{}};")
                 g(f"{{ const u32 want[{kk}] = {{{', '.join(map(str, fields))}}};")
                 cond = f"alive && !{a.n}" if a.nullable else "alive"
                 g(f"if ({cond}) fbx::str_tokens<{kk}>({a.c}, {ord(delim)}u, want, {base}); }}")
@@ -813,13 +813,16 @@ class PlanCodegen:
             self.decl(out)
             nulls = [a.n for a in args if a.nullable]
             cond = "alive" + "".join(f" && !{x}" for x in nulls)
-            g(f"if ({cond}) {{")
             lones = [a.l for a in args if a.t == "str" and a.lone]
             if lones:
-                g(f"if ({' || '.join(lones)}) {{")
+                g(f"if (({cond}) && ({' || '.join(lones)})) {{")
                 err("encode")
                 g("}")
+            # hashed unconditionally: a dead / null row's value is never read, and
+            # every input is a valid (possibly empty) view -- no reconvergence
+            # scaffolding around the FNV loops
             h0 = fnv1a64(fn.slot.to_bytes(2, "big"))
+            g("{")
             g(f"fbx::Fnv h({_u64(h0)});")
             for i, a in enumerate(args):
                 if i:
@@ -831,9 +834,9 @@ class PlanCodegen:
                 else:
                     g(f"h.u64_be({a.c});")
             g(f"{out.c} = h.value();")
-            if nullable:
-                g(f"{out.c}_n = false;")
             g("}")
+            if nullable:
+                g(f"{out.c}_n = !({cond});")
             return out
         if op == "concat":
             parts = [self.as_str(a, fn.spec) for a in args]
