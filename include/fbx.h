@@ -68,8 +68,9 @@ int fbx_launch(fbx_kernel* k, unsigned grid, unsigned block, unsigned dyn_smem, 
 int fbx_state_reset(fbx_state* d_state, unsigned long long* d_tile_status, size_t n_tiles,
                     void* stream);
 
-/* Reset only the bump-pool head of the run state (ArenaPool.reset, mempool.py:136):
- * between the launches of one run, whose counters keep accumulating. */
+/* Reset the per-launch part of the run state -- the bump-pool head (ArenaPool.reset,
+ * mempool.py:136) and the persistent kernel's tile ticket -- between the launches of
+ * one run, whose counters keep accumulating. */
 int fbx_pool_reset(fbx_state* d_state, void* stream);
 
 /* Copy the run state (fbx_state) into host-mapped pinned memory with a kernel on

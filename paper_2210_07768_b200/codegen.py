@@ -123,6 +123,7 @@ class Program:
     side_kernels: list[str]
     notes: list[str]
     int_keyed: tuple[int, ...] = ()   # tables with 16-B fbx::ISlot slots
+    persistent_ctas_per_sm: int = 0   # >0: fbx_pipeline takes tiles from a ticket
 
 
 # ---------------------------------------------------------------------------
@@ -236,6 +237,7 @@ class PlanCodegen:
         self._ids_tail: list[str] = []
         self.pf_slot: dict[int, int] = {}
         self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
+        self.persistent = os.environ.get("FBX_PERSISTENT", "0") != "0"  # measured slower (r1)
         self._pf_tail: list[str] = []
 
     # -- value helpers ---------------------------------------------------------
@@ -1011,11 +1013,29 @@ class PlanCodegen:
         g("u64 span_lo[16]; u32 span_len[16];")
         g("u64 red[NT / 32][4];")
         g("} sm;")
-        g("// tiles in blockIdx order: the hardware dispatches CTAs in order, so every")
-        g("// predecessor a look-back waits on is resident or done (as CUB relies on)")
-        g(f"const u32 tile = (u32){g.p('tile_base')} + blockIdx.x;  // run-global tile id")
-        g("const u64 chunk = CHUNK0 + blockIdx.x;")
-        g(f"const u64 row0 = ROW_LO + (u64)blockIdx.x * {ir.chunk}ull;")
+        if self.persistent:
+            g("// persistent CTAs (one per resident slot) take tiles in order from a ticket:")
+            g("// every predecessor a look-back waits on is held by a running CTA, no wave")
+            g("// tail, and the shared state is set up once")
+            g("__shared__ u32 sm_ltile;")
+            g(f"const u32 NTILES = (u32)((ROW_HI - ROW_LO + {ir.chunk - 1}ull) / {ir.chunk}ull);")
+            if self.staged:
+                g("if (threadIdx.x == 0) fbx::mbar_init(&sm.bar, 1u);")
+            g("u32 bar_phase = 0u;")
+            g("__syncthreads();")
+            g("for (;;) {")
+            g("if (threadIdx.x == 0) sm_ltile = (u32)atomicAdd((unsigned long long*)&ST->tile_ticket, 1ull);")
+            g("__syncthreads();")
+            g("const u32 LT = sm_ltile;")
+            g("if (LT >= NTILES) break;")
+            bid = "LT"
+        else:
+            g("// tiles in blockIdx order: the hardware dispatches CTAs in order, so every")
+            g("// predecessor a look-back waits on is resident or done (as CUB relies on)")
+            bid = "blockIdx.x"
+        g(f"const u32 tile = (u32){g.p('tile_base')} + {bid};  // run-global tile id")
+        g(f"const u64 chunk = CHUNK0 + {bid};")
+        g(f"const u64 row0 = ROW_LO + (u64){bid} * {ir.chunk}ull;")
         g(f"const u64 row_end = (row0 + {ir.chunk}ull < ROW_HI) ? row0 + {ir.chunk}ull : ROW_HI;")
         g("const u64 srow = row0 + threadIdx.x;")
         g(f"const bool inrange = threadIdx.x < {ir.chunk}u && srow < row_end;")
@@ -1032,7 +1052,8 @@ class PlanCodegen:
             g(f"__shared__ bool sm_span_ok[{ns_}];")
             g("if (threadIdx.x == 0) {")
             g("u32 used = 0;")
-            g("fbx::mbar_init(&sm.bar, 1u);")
+            if not self.persistent:
+                g("fbx::mbar_init(&sm.bar, 1u);")
             for i, c in enumerate(self.staged):
                 offs = g.p(f"drv.{c}.offsets", "const u32*")
                 g("{")
@@ -1056,7 +1077,7 @@ class PlanCodegen:
         pf_cols = [(c, k) for c, k in drv.kinds.items() if c in needed]
         pf_dist = 148 * self.min_blocks
         if self.prefetch_next:
-            g(f"const u32 PF_TILE = blockIdx.x + {pf_dist}u;")
+            g(f"const u32 PF_TILE = {bid} + {pf_dist}u;")
             g(f"const bool pf_on = threadIdx.x == 0 && PF_TILE + 1u < gridDim.x;")
             g("if (pf_on) {")
             g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {ir.chunk}ull, p1 = p0 + {ir.chunk}ull;")
@@ -1101,7 +1122,10 @@ class PlanCodegen:
         if self.pf_slot:
             g("fbx::cp_async_commit();")
         if self.staged:
-            g("fbx::mbar_wait(&sm.bar, 0u);")
+            if self.persistent:
+                g("fbx::mbar_wait(&sm.bar, bar_phase); bar_phase ^= 1u;")
+            else:
+                g("fbx::mbar_wait(&sm.bar, 0u);")
         # ---- clean ------------------------------------------------------------------
         g("// ---- clean (viewpipe.clean_views) ----")
         vals = self.clean_view(drv, "d_", lambda n, k: raw[n], "clean", needed, "")
@@ -1376,6 +1400,9 @@ class PlanCodegen:
                 g(line)
             g("}")
         g("if (threadIdx.x == 0 && staged_out) fbx::bulk_wait_read();  // smem lives until read")
+        if self.persistent:
+            g("__syncthreads();  // the next tile reuses every shared buffer")
+            g("}")
         g("}")
         return "fbx_pipeline"
 
@@ -1578,7 +1605,8 @@ class PlanCodegen:
         del body_start
         nt_ = len(ir.sides) + (1 if ir.basic is not None else 0)
         return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes,
-                       tuple(k for k in range(nt_) if self.int_keyed(k)))
+                       tuple(k for k in range(nt_) if self.int_keyed(k)),
+                       self.min_blocks if self.persistent else 0)
 
 
 def _filter_columns(expr) -> set[str]:

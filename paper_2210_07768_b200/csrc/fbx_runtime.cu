@@ -319,8 +319,10 @@ int fbx_state_reset(fbx_state* d_state, unsigned long long* d_status, size_t n_t
 }
 
 int fbx_pool_reset(fbx_state* d_state, void* stream) {
-  return cuda_check(cudaMemsetAsync(&d_state->pool_head, 0, sizeof(d_state->pool_head),
-                                    (cudaStream_t)stream), "fbx_pool_reset");
+  // tile ticket + pool head (adjacent): the per-launch part of the run state
+  static_assert(offsetof(fbx_state, pool_head) == offsetof(fbx_state, tile_ticket) + 8, "layout");
+  return cuda_check(cudaMemsetAsync(&d_state->tile_ticket, 0, 16, (cudaStream_t)stream),
+                    "fbx_pool_reset");
 }
 
 int fbx_state_snapshot(const fbx_state* d_state, void* h_mapped_dst, void* stream) {

@@ -337,6 +337,11 @@ class Engine:
         if name in self.slots:
             self.params[self.slots[name]] = np.uint64(int(value) & ((1 << 64) - 1))
 
+    def _sm_count(self) -> int:
+        if getattr(self, "_sms", None) is None:
+            self._sms = self.torch.cuda.get_device_properties(self.device).multi_processor_count
+        return self._sms
+
     def _stream(self) -> int:
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
@@ -621,7 +626,10 @@ class Engine:
         self._set("tile_base", tile_base)
         self._chunk_minus_tile = row_lo // self.ir.chunk - tile_base
         self._run_tiles = tile_base + tiles
-        self.module.launch("fbx_pipeline", tiles, self.prog.threads, self.prog.smem_bytes,
+        grid = tiles
+        if self.prog.persistent_ctas_per_sm:
+            grid = max(1, min(tiles, self._sm_count() * self.prog.persistent_ctas_per_sm))
+        self.module.launch("fbx_pipeline", grid, self.prog.threads, self.prog.smem_bytes,
                            stream, self.params)
         return tiles
 
