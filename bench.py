@@ -430,20 +430,43 @@ def measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist, slice_rows=1
         r.wait()
     torch.cuda.synchronize(dev)
     dt = time.perf_counter() - t0
-    tt = torch.tensor([dt, sum(times)], dtype=torch.float64, device=dev)
+    # device sink: the same stream with the CSR left in HBM for a GPU trainer
+    dvs = [E.StreamedRun(r.eng, corpus.driver, slice_rows=stream_slice_rows, taper=False,
+                         sink="device") for r in srs]
+    for r in dvs:
+        r.run()
+    torch.cuda.synchronize(dev)
+    t1 = time.perf_counter()
+    dvs[0].start()
+    for k in range(K):
+        if k + 1 < K:
+            dvs[(k + 1) % len(dvs)].start()
+        dtot = dvs[k % len(dvs)].finish()
+        if len(dvs) == 1 and k + 1 < K:
+            dvs[0].wait()
+        if dtot.digest != want:
+            raise SystemExit("e2e parity failure (device sink)")
+    torch.cuda.synchronize(dev)
+    ddt = time.perf_counter() - t1
+    tt = torch.tensor([dt, sum(times), ddt], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     rate = n * world * K / float(tt[0])
     single = n * world * K / float(tt[1])
+    dev_rate = n * world * K / float(tt[2])
     return {"value": round(rate, 1), "unit": "records/s", "h2d_bytes_per_step": sr.h2d_bytes,
             "d2h_bytes_per_step": sr.d2h_bytes, "digest": f"0x{tot.digest:016x}",
             "single_step_value": round(single, 1),
+            "device_sink_value": round(dev_rate, 1),
+            "device_sink_d2h_bytes_per_step": dvs[0].d2h_bytes,
             "path": f"engine.StreamedRun x{len(srs)} engines alternating over a stream of {K} "
                     f"1M-record steps; {len(srs[0].bounds)} slices per step "
                     f"(<= {srs[0].slice_rows} rows); "
                     "pinned H2D / fused kernel / D2H of the full CSR on three streams per "
                     "engine; wall clock (host perf_counter) over the whole stream. "
-                    "single_step_value: each step synchronised on its own "
+                    "single_step_value: each step synchronised on its own; "
+                    "device_sink_value: same stream, CSR left in HBM for a GPU trainer "
+                    "(D2H = run-state snapshots only); "
                     f"({len(sr.bounds)} tapered slices of <= {sr.slice_rows} rows)"}
 
 

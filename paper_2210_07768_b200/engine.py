@@ -661,7 +661,7 @@ class StreamedRun:
     PARTS = ("nulls", "data", "offsets")
 
     def __init__(self, eng: "Engine", host_view: ViewImage, slice_rows: int = 1 << 17,
-                 zero_copy: bool = False, taper: bool = True):
+                 zero_copy: bool = False, taper: bool = True, sink: str = "host"):
         torch = eng.torch
         self.eng, self.torch = eng, torch
         chunk = eng.ir.chunk
@@ -732,6 +732,12 @@ class StreamedRun:
         # M rec/s, round 1), so off by default.
         self.zero_copy = zero_copy
         self.trace = None  # set to [] to record a per-slice event timeline (ms)
+        # sink "device": the CSR stays in HBM (the engine's torch tensors, for a GPU
+        # trainer -- the paper's FeatureBox hand-off); only the per-slice run-state
+        # snapshots (mapped pinned memory) come back to the host
+        if sink not in ("host", "device"):
+            raise ValueError("sink must be 'host' or 'device'")
+        self.sink = sink
 
     def run(self) -> Counters:
         if self.zero_copy:
@@ -809,6 +815,11 @@ class StreamedRun:
             # flush chunk and a repeated id's second chunk may lie in later slices.
             # Counters accumulate over the run's launches: this slice's share.
             ni, ms = stt["instances"] - inst_base, stt["signs"] - sign_base
+            if self.sink == "device":
+                inst_base += ni
+                sign_base += ms
+                last = stt
+                continue
             with torch.cuda.stream(self.s_d2h):
                 self.s_d2h.wait_event(comp_done[j])
                 mark("d2h0", j, self.s_d2h)
@@ -831,11 +842,12 @@ class StreamedRun:
         tot.joined = last["joined"]
         tot.launches = len(self.bounds)
         ev = torch.cuda.Event()
-        ev.record(self.s_d2h)
+        ev.record(self.s_d2h if self.sink == "host" else self.s_comp)
         self._last_d2h = ev
         # the last snapshot is the run's final state (no extra D2H read)
         eng.check_run(last)
-        self.d2h_bytes = tot.instances * 17 + 8 + tot.signs * 10
+        self.d2h_bytes = (tot.instances * 17 + 8 + tot.signs * 10 if self.sink == "host"
+                          else runtime.STATE_BYTES * len(self.bounds))
         if trace:
             t0e, t0h = trace[0][2], trace[0][3]
             self.trace = [(nm, k, t0e.elapsed_time(ev), (th - t0h) * 1e3) for nm, k, ev, th in trace]
