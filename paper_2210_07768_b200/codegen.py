@@ -238,6 +238,8 @@ class PlanCodegen:
         self.pf_slot: dict[int, int] = {}
         self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
         self.persistent = os.environ.get("FBX_PERSISTENT", "0") != "0"  # measured slower (r1)
+        # profiling aid: per-phase SM cycles (lane 0 of every warp), printed by the last CTA
+        self.phase_timers = os.environ.get("FBX_PHASE_TIMERS", "0") != "0"
         self._pf_tail: list[str] = []
 
     # -- value helpers ---------------------------------------------------------
@@ -1008,11 +1010,14 @@ class PlanCodegen:
         g("extern __shared__ __align__(16) u8 dyn_smem[];")
         g("__shared__ struct {")
         g("fbx::BlockScanU32<NT> scan;")
+        g("fbx::TileReduce<NT> tred;")
         g("u64 pool_base; u32 tile; u64 ex_inst, ex_signs; u64 bar;")
         g("u32 rank[NT]; u32 soff[NT];")
         g("u64 span_lo[16]; u32 span_len[16];")
         g("u64 red[NT / 32][4];")
         g("} sm;")
+        if self.phase_timers:
+            g("u64 ph_t = clock64();")
         if self.persistent:
             g("// persistent CTAs (one per resident slot) take tiles in order from a ticket:")
             g("// every predecessor a look-back waits on is held by a running CTA, no wave")
@@ -1127,9 +1132,13 @@ class PlanCodegen:
             else:
                 g("fbx::mbar_wait(&sm.bar, 0u);")
         # ---- clean ------------------------------------------------------------------
+        if self.phase_timers:
+            g("FBX_PHASE(0);")
         g("// ---- clean (viewpipe.clean_views) ----")
         vals = self.clean_view(drv, "d_", lambda n, k: raw[n], "clean", needed, "")
         # ---- join -------------------------------------------------------------------
+        if self.phase_timers:
+            g("FBX_PHASE(1);")
         g(f"CUR_STAGE = {STAGE['join']}u;")
         env: dict[str, V] = dict(vals)
         side_rows: list[str] = []
@@ -1187,6 +1196,8 @@ class PlanCodegen:
                 self.col(c, {})
         # ---- DAG --------------------------------------------------------------------
         g(f"CUR_STAGE = {STAGE['extract']}u;")
+        if self.phase_timers:
+            g("FBX_PHASE(2);")
         g("// ---- operator DAG: layer order (driver-only nodes first) ----")
         self.token_groups = self.plan_token_groups()
         self.token_done: dict[str, V] = {}
@@ -1209,6 +1220,8 @@ class PlanCodegen:
                 self.row_error("extract", "value")
                 g("}")
         # ---- uniqueness check + merge ------------------------------------------------
+        if self.phase_timers:
+            g("FBX_PHASE(3);")
         g(f"CUR_STAGE = {STAGE['merge']}u;")
         lab = self.col(ir.label_column, node_out)
         g("// ---- check_unique_ids over the run (pipeline.py:1071, viewpipe.py:562) ----")
@@ -1283,32 +1296,38 @@ class PlanCodegen:
         g("if (!alive) fpres = 0u;")
         g("const u32 m = alive ? __popc(fpres) : 0u;")
         # ---- tile: sort by instance id, offsets, look-back, write -----------------------
+        if self.phase_timers:
+            g("FBX_PHASE(4);")
         g("// ---- chunk emission order: ascending u64 instance id (viewpipe.py:521) ----")
         g(f"u64 skey = alive ? {idv.c} : ~0ull;")
-        if self.nt * max(1, len(ir.features)) < 65536:
-            g("const u32 both = sm.scan.sum((alive ? 0x10000u : 0u) + m);  // one reduction")
+        g("u64* sbuf = (u64*)dyn_smem;")
+        g("u32* hist = (u32*)(sbuf + NT); u32* bstart = hist + 1024; u16* bmv = (u16*)(bstart + 1024);")
+        g("u32 myrank = 0, myoff = 0;")
+        fused = self.nt * max(1, len(ir.features)) < 65536
+        if fused:
+            g("// counts, signs and the ids' OR / AND in one reduction; the staged record")
+            g("// spans are dead after its first barrier: the rank pass reuses that memory")
+            g("u32 both; u64 kor, kand;")
+            g("sm.tred.run((alive ? 0x10000u : 0u) + m, alive ? skey : 0ull, alive ? skey : ~0ull, "
+              "&both, &kor, &kand, hist, 1024u);")
             g("const u32 n_inst = both >> 16, tile_signs = both & 0xFFFFu;")
         else:
             g("const u32 n_inst = sm.scan.sum(alive ? 1u : 0u);")
             g("const u32 tile_signs = sm.scan.sum(m);")
         g("// publish the aggregate now: successors' look-back overlaps our sort")
         g("if (threadIdx.x == 0) fbx::publish_aggregate(STATUS, tile, n_inst, tile_signs);")
-        g("// the staged record spans are dead now: the rank pass reuses that memory.")
         g("// Emitted ids are unique (else the run fails): a row's rank is the number")
-        g("// of live ids below its own.  Adaptive radix buckets; bitonic fallback.")
-        g("u64* sbuf = (u64*)dyn_smem;")
-        g("u32 myrank = 0;")
-        g("{")
-        g("u64 kor, kand;")
-        g("fbx::block_or_and<NT>(alive ? skey : 0ull, alive ? skey : ~0ull, sbuf, &kor, &kand);")
-        g("u32* hist = (u32*)(sbuf + NT); u32* bstart = hist + 1024;")
-        g("if (!fbx::radix_rank<NT>(skey, alive, kor ^ kand, hist, bstart, sbuf, sm.scan, &myrank)) {")
+        g("// of live ids below its own.  Adaptive radix buckets carrying the sign counts")
+        g("// (rank and sign offset in one pass); bitonic sort + offset scan fallback.")
+        if fused:
+            g("if (!fbx::radix_rank_off<NT>(skey, alive, m, kor ^ kand, hist, bstart, sbuf, bmv, "
+              "sm.scan, &myrank, &myoff)) {")
+        else:
+            g("{")
         g("const u64 sorted = fbx::bitonic_keys<NT>(skey, sbuf);")
         g("sbuf[2 * NT + threadIdx.x] = sorted;")
         g("__syncthreads();")
         g("myrank = alive ? fbx::lower_rank<NT>(sbuf + 2 * NT, skey) : 0u;")
-        g("}")
-        g("}")
         g("sm.soff[threadIdx.x] = 0u;")
         g("__syncthreads();")
         g("if (alive) sm.soff[myrank] = m;")
@@ -1316,9 +1335,12 @@ class PlanCodegen:
         g("const u32 s_off = sm.scan.exclusive(sm.soff[threadIdx.x]);")
         g("sm.rank[threadIdx.x] = s_off;  // sign offset by sorted position")
         g("__syncthreads();")
-        g("const u32 myoff = alive ? sm.rank[myrank] : 0u;")
+        g("myoff = alive ? sm.rank[myrank] : 0u;")
+        g("}")
         # look-back by warp 0 while every warp (warp 0 after it) hashes its rows'
         # instance digests -- the digest is off the path to the aggregate publish
+        if self.phase_timers:
+            g("FBX_PHASE(5);")
         g("const u32 out_bytes = tile_signs * 10u + n_inst * 17u + 176u;")
         g("const bool staged_out = out_bytes <= DYN_SMEM;")
         g("if (threadIdx.x < 32u) {")
@@ -1376,6 +1398,8 @@ class PlanCodegen:
         g("}")
         g("fbx::fence_async_smem();")
         g("__syncthreads();")
+        if self.phase_timers:
+            g("FBX_PHASE(6);")
         g("fbx::tile_out<NT>((u8*)(O_SIGN + es), st_sign, 8u * tile_signs);")
         g("fbx::tile_out<NT>((u8*)(O_SLOT + es), st_slot, 2u * tile_signs);")
         g("fbx::tile_out<NT>((u8*)(O_IDS + ei), st_ids, 8u * n_inst);")
@@ -1399,10 +1423,17 @@ class PlanCodegen:
             for line in self._pf_tail:
                 g(line)
             g("}")
+        if self.phase_timers:
+            g("FBX_PHASE(7);")
         g("if (threadIdx.x == 0 && staged_out) fbx::bulk_wait_read();  // smem lives until read")
         if self.persistent:
             g("__syncthreads();  // the next tile reuses every shared buffer")
             g("}")
+        if self.phase_timers:
+            g("if (threadIdx.x == 0) { __threadfence(); if (atomicAdd(&fbx_ph_done, 1u) == gridDim.x - 1) {")
+            g("__threadfence(); u64 t = 0; for (int q = 0; q < 8; ++q) t += fbx_ph[q];")
+            g('for (int q = 0; q < 8; ++q) printf("FBX_PHASE %d %llu %.4f\\n", q, fbx_ph[q], (double)fbx_ph[q] / (double)t);')
+            g("fbx_ph_done = 0; for (int q = 0; q < 8; ++q) fbx_ph[q] = 0; } }")
         g("}")
         return "fbx_pipeline"
 
@@ -1565,8 +1596,8 @@ class PlanCodegen:
         # Sized so MIN_BLOCKS CTAs fit an SM (227 KB); a tile whose CSR does not
         # fit is written directly.
         per_cta = (227 * 1024) // self.min_blocks - STATIC_SMEM_EST - 1024
-        need = max(self.span_cap, 24 * self.nt, 8 * self.nt + 8192, self.nt * (17 + 10 * k) + 64)
-        rank_bytes = max(24 * self.nt, 8 * self.nt + 8192)  # bitonic 3*NT u64 | radix
+        need = max(self.span_cap, 24 * self.nt, 10 * self.nt + 8192, self.nt * (17 + 10 * k) + 64)
+        rank_bytes = max(24 * self.nt, 10 * self.nt + 8192)  # bitonic 3*NT u64 | radix
         self.dyn_smem = max(self.span_cap, rank_bytes,
                             min(need, per_cta, OUT_BUDGET)) // 16 * 16
         # first probe slots of int-keyed tables land behind the staged spans

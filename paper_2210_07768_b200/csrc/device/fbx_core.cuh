@@ -26,6 +26,12 @@ typedef long long i64;
 
 #include "fbx_abi.h"
 
+// profiling aid (codegen FBX_PHASE_TIMERS): SM cycles per kernel phase, summed over warps
+__device__ unsigned long long fbx_ph[8];
+__device__ unsigned int fbx_ph_done;
+#define FBX_PHASE(k) do { if ((threadIdx.x & 31u) == 0) { const u64 t_ = clock64(); \
+  atomicAdd(&fbx_ph[(k)], t_ - ph_t); ph_t = t_; } } while (0)
+
 namespace fbx {
 
 // ---------------------------------------------------------------------------
@@ -793,6 +799,92 @@ FBX_DI bool radix_rank(u64 key, bool live, u64 diff, u32* hist, u32* start, u64*
     u32 r = b0;
     for (u32 q = 0; q < bn; ++q) r += bkeys[b0 + q] < key ? 1u : 0u;
     *rank = r;
+  }
+  return true;
+}
+
+// One block reduction of a u32 sum and a u64 OR / AND (redux.sync per warp, warp 0
+// folds the warp partials): two barriers, every thread receives all three.
+template <int NT>
+struct TileReduce {
+  u32 ws[NT / 32];
+  u64 wo[NT / 32], wa[NT / 32];
+  u32 rs;
+  u64 ro, ra;
+  // zero[0..nzero) is cleared between the two barriers (after every thread has
+  // left the phase that may still read that shared memory)
+  FBX_DI void run(u32 v, u64 o, u64 a, u32* sum, u64* vor, u64* vand, u32* zero, u32 nzero) {
+    const u32 lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    v = __reduce_add_sync(0xFFFFFFFFu, v);
+    const u32 olo = __reduce_or_sync(0xFFFFFFFFu, (u32)o), ohi = __reduce_or_sync(0xFFFFFFFFu, (u32)(o >> 32));
+    const u32 alo = __reduce_and_sync(0xFFFFFFFFu, (u32)a), ahi = __reduce_and_sync(0xFFFFFFFFu, (u32)(a >> 32));
+    if (lane == 0) { ws[wid] = v; wo[wid] = ((u64)ohi << 32) | olo; wa[wid] = ((u64)ahi << 32) | alo; }
+    __syncthreads();
+    for (u32 q = threadIdx.x; q < nzero; q += NT) zero[q] = 0u;
+    if (wid == 0) {
+      const bool in = lane < (u32)(NT / 32);
+      const u32 x = in ? ws[lane] : 0u;
+      const u64 xo = in ? wo[lane] : 0ull, xa = in ? wa[lane] : ~0ull;
+      const u32 t = __reduce_add_sync(0xFFFFFFFFu, x);
+      const u32 tol = __reduce_or_sync(0xFFFFFFFFu, (u32)xo), toh = __reduce_or_sync(0xFFFFFFFFu, (u32)(xo >> 32));
+      const u32 tal = __reduce_and_sync(0xFFFFFFFFu, (u32)xa), tah = __reduce_and_sync(0xFFFFFFFFu, (u32)(xa >> 32));
+      if (lane == 0) { rs = t; ro = ((u64)toh << 32) | tol; ra = ((u64)tah << 32) | tal; }
+    }
+    __syncthreads();
+    *sum = rs; *vor = ro; *vand = ra;
+  }
+};
+
+// Rank AND sign offset of a row in ascending-key order in one pass: the radix
+// buckets carry packed (count << 16 | signs) so one scan gives both starts, and
+// within a (small) bucket a row adds the members with smaller keys.  `hist` must
+// be zeroed (1024 words) before the caller's last barrier (TileReduce::run does).  Requires the tile's
+// total signs < 65536.  false: a bucket holds > 32 rows (use the sort fallback).
+template <int NT>
+FBX_DI bool radix_rank_off(u64 key, bool live, u32 m, u64 diff, u32* hist, u32* start, u64* bkeys,
+                           u16* bm, BlockScanU32<NT>& scan, u32* rank, u32* off) {
+  constexpr int BPT = 1024 / NT;  // buckets per thread
+  const u32 hb = diff ? 63u - (u32)__clzll((long long)diff) : 0u;
+  const u32 shift = hb >= 9u ? hb - 9u : 0u;
+  const u32 digit = (u32)(key >> shift) & 1023u;
+  u32 pos = 0;
+  if (live) pos = atomicAdd(&hist[digit], (1u << 16) | m) >> 16;
+  __syncthreads();
+  u32 sz[BPT], tot = 0;
+  bool big = false;
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    sz[b] = hist[threadIdx.x * BPT + b];
+    tot += sz[b];
+    big |= (sz[b] >> 16) > 32u;
+  }
+  if (__syncthreads_or(big)) return false;
+  u32 run = scan.exclusive(tot);
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    start[threadIdx.x * BPT + b] = run;
+    run += sz[b];
+  }
+  __syncthreads();
+  u32 b0 = 0, bn = 0;
+  if (live) {
+    const u32 st = start[digit];
+    b0 = st;
+    bn = hist[digit] >> 16;
+    bkeys[(st >> 16) + pos] = key;
+    bm[(st >> 16) + pos] = (u16)m;
+  }
+  __syncthreads();
+  if (live) {
+    u32 r = b0 >> 16, o = b0 & 0xFFFFu;
+    const u32 j0 = b0 >> 16;
+    for (u32 q = 0; q < bn; ++q) {
+      const bool lt = bkeys[j0 + q] < key;
+      r += lt ? 1u : 0u;
+      o += lt ? (u32)bm[j0 + q] : 0u;
+    }
+    *rank = r;
+    *off = o;
   }
   return true;
 }
