@@ -47,7 +47,7 @@ MASK64 = (1 << 64) - 1
 STAGE = {"prepare": 0, "read": 1, "clean": 2, "join": 3, "extract": 4, "merge": 5, "emit": 6}
 ERR = {"type": 1, "value": 2, "encode": 3, "pool": 4, "null_label": 5, "label_range": 6,
        "dup_id": 7, "multi_match": 8, "json_bigint": 9, "json_deep": 10,
-       "unicode_lower": 11, "float_overflow": 12, "float_slow": 13}
+       "unicode_lower": 11, "float_overflow": 12, "float_slow": 13, "internal": 14}
 
 
 def library_source() -> str:
@@ -238,6 +238,8 @@ class PlanCodegen:
         self.pf_slot: dict[int, int] = {}
         self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
         self.persistent = os.environ.get("FBX_PERSISTENT", "0") != "0"  # measured slower (r1)
+        self.early_order = os.environ.get("FBX_EARLY_ORDER", "0") != "0"  # measured ~1% slower (r1)
+        self.early = False
         # profiling aid: per-phase SM cycles (lane 0 of every warp), printed by the last CTA
         self.phase_timers = os.environ.get("FBX_PHASE_TIMERS", "0") != "0"
         self._pf_tail: list[str] = []
@@ -1194,6 +1196,32 @@ class PlanCodegen:
         for c in sorted(used_cols):
             if isinstance(env.get(c), tuple):
                 self.col(c, {})
+        # ---- emission order decided BEFORE the DAG ----------------------------------
+        feats_early = sorted(ir.features.items(), key=lambda kv: (kv[1], kv[0]))
+        pnulls = (self.predict_feature_nulls(feats_early)
+                  if self.early_order and self.nt * max(1, len(ir.features)) < 65536 else None)
+        self.early = pnulls is not None
+        if self.early:
+            # which rows emit and how many signs each is known from null-ness alone:
+            # counts, the tile aggregate and the rank / sign offsets are settled now,
+            # so the aggregate is published a whole DAG earlier (successors' look-backs
+            # rarely wait) and the rank pass runs on shared memory behind the spans
+            g("// ---- emission order, decided before the DAG (exact for every run that")
+            g("// succeeds; a mismatch after the DAG is an internal error) ----")
+            if ir.basic is not None:
+                g(f"const bool palive = alive && !{idv.n} && bhit;")
+            else:
+                g("const bool palive = alive;")
+            g("u32 pfpres = 0u;")
+            for q, x in enumerate(pnulls):
+                g(f"if (!({x})) pfpres |= {1 << q}u;")
+            g("if (!palive) pfpres = 0u;")
+            g("const u32 pm = __popc(pfpres);")
+            self.emission_order(idv, "palive", "pm", f"dyn_smem + {self.span_cap}u")
+            # the look-back right away: warp 0 resolves (and publishes) the inclusive
+            # prefix while the other warps start the DAG; inclusive prefixes then
+            # trail the tile frontier by little, so look-backs walk back few tiles
+            self.emit_lookback()
         # ---- DAG --------------------------------------------------------------------
         g(f"CUR_STAGE = {STAGE['extract']}u;")
         if self.phase_timers:
@@ -1298,56 +1326,20 @@ class PlanCodegen:
         # ---- tile: sort by instance id, offsets, look-back, write -----------------------
         if self.phase_timers:
             g("FBX_PHASE(4);")
-        g("// ---- chunk emission order: ascending u64 instance id (viewpipe.py:521) ----")
-        g(f"u64 skey = alive ? {idv.c} : ~0ull;")
-        g("u64* sbuf = (u64*)dyn_smem;")
-        g("u32* hist = (u32*)(sbuf + NT); u32* bstart = hist + 1024; u16* bmv = (u16*)(bstart + 1024);")
-        g("u32 myrank = 0, myoff = 0;")
-        fused = self.nt * max(1, len(ir.features)) < 65536
-        if fused:
-            g("// counts, signs and the ids' OR / AND in one reduction; the staged record")
-            g("// spans are dead after its first barrier: the rank pass reuses that memory")
-            g("u32 both; u64 kor, kand;")
-            g("sm.tred.run((alive ? 0x10000u : 0u) + m, alive ? skey : 0ull, alive ? skey : ~0ull, "
-              "&both, &kor, &kand, hist, 1024u);")
-            g("const u32 n_inst = both >> 16, tile_signs = both & 0xFFFFu;")
+        if self.early:
+            g("if (alive && fpres != pfpres) {  // the pre-DAG prediction must hold")
+            self.row_error("merge", "internal")
+            g("}")
         else:
-            g("const u32 n_inst = sm.scan.sum(alive ? 1u : 0u);")
-            g("const u32 tile_signs = sm.scan.sum(m);")
-        g("// publish the aggregate now: successors' look-back overlaps our sort")
-        g("if (threadIdx.x == 0) fbx::publish_aggregate(STATUS, tile, n_inst, tile_signs);")
-        g("// Emitted ids are unique (else the run fails): a row's rank is the number")
-        g("// of live ids below its own.  Adaptive radix buckets carrying the sign counts")
-        g("// (rank and sign offset in one pass); bitonic sort + offset scan fallback.")
-        if fused:
-            g("if (!fbx::radix_rank_off<NT>(skey, alive, m, kor ^ kand, hist, bstart, sbuf, bmv, "
-              "sm.scan, &myrank, &myoff)) {")
-        else:
-            g("{")
-        g("const u64 sorted = fbx::bitonic_keys<NT>(skey, sbuf);")
-        g("sbuf[2 * NT + threadIdx.x] = sorted;")
-        g("__syncthreads();")
-        g("myrank = alive ? fbx::lower_rank<NT>(sbuf + 2 * NT, skey) : 0u;")
-        g("sm.soff[threadIdx.x] = 0u;")
-        g("__syncthreads();")
-        g("if (alive) sm.soff[myrank] = m;")
-        g("__syncthreads();")
-        g("const u32 s_off = sm.scan.exclusive(sm.soff[threadIdx.x]);")
-        g("sm.rank[threadIdx.x] = s_off;  // sign offset by sorted position")
-        g("__syncthreads();")
-        g("myoff = alive ? sm.rank[myrank] : 0u;")
-        g("}")
+            self.emission_order(idv, "alive", "m", "dyn_smem")
         # look-back by warp 0 while every warp (warp 0 after it) hashes its rows'
         # instance digests -- the digest is off the path to the aggregate publish
         if self.phase_timers:
             g("FBX_PHASE(5);")
         g("const u32 out_bytes = tile_signs * 10u + n_inst * 17u + 176u;")
         g("const bool staged_out = out_bytes <= DYN_SMEM;")
-        g("if (threadIdx.x < 32u) {")
-        g("u64 ei = 0, es = 0;")
-        g("fbx::lookback(STATUS, tile, n_inst, tile_signs, &ei, &es);")
-        g("if (threadIdx.x == 0) { sm.ex_inst = ei; sm.ex_signs = es; }")
-        g("}")
+        if not self.early:
+            self.emit_lookback()
         g("u64 digest = 0ull;")
         g("if (alive) {")
         g("fbx::Fnv h;")
@@ -1356,6 +1348,8 @@ class PlanCodegen:
             g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
         g("digest = h.value();")
         g("}")
+        if self.phase_timers:
+            g("FBX_PHASE(9);  // instance digests")
         g("{")
         g("// warp reductions (redux.sync): the XOR digest and three <=512 counters packed")
         g("const u32 r0l = __reduce_xor_sync(0xFFFFFFFFu, (u32)digest);")
@@ -1431,9 +1425,9 @@ class PlanCodegen:
             g("}")
         if self.phase_timers:
             g("if (threadIdx.x == 0) { __threadfence(); if (atomicAdd(&fbx_ph_done, 1u) == gridDim.x - 1) {")
-            g("__threadfence(); u64 t = 0; for (int q = 0; q < 8; ++q) t += fbx_ph[q];")
-            g('for (int q = 0; q < 8; ++q) printf("FBX_PHASE %d %llu %.4f\\n", q, fbx_ph[q], (double)fbx_ph[q] / (double)t);')
-            g("fbx_ph_done = 0; for (int q = 0; q < 8; ++q) fbx_ph[q] = 0; } }")
+            g("__threadfence(); u64 t = 0; for (int q = 0; q < 10; ++q) t += fbx_ph[q];")
+            g('for (int q = 0; q < 10; ++q) printf("FBX_PHASE %d %llu %.4f\\n", q, fbx_ph[q], (double)fbx_ph[q] / (double)t);')
+            g("fbx_ph_done = 0; for (int q = 0; q < 10; ++q) fbx_ph[q] = 0; } }")
         g("}")
         return "fbx_pipeline"
 
@@ -1512,6 +1506,110 @@ class PlanCodegen:
         g("}")
         g("}")
         return "fbx_extract_rows"
+
+    def emit_lookback(self):
+        g = self.g
+        g("if (threadIdx.x < 32u) {")
+        g("u64 ei = 0, es = 0;")
+        g("fbx::lookback(STATUS, tile, n_inst, tile_signs, &ei, &es);")
+        g("if (threadIdx.x == 0) { sm.ex_inst = ei; sm.ex_signs = es; }")
+        g("}")
+        if self.phase_timers:
+            g("FBX_PHASE(8);  // look-back (warp 0 only)")
+
+    def emission_order(self, idv: V, live: str, mm: str, scratch: str):
+        """Tile counts + aggregate publish + rank / sign offset of every row (by
+        ascending u64 instance id, viewpipe.py:521).  `live` / `mm`: which rows emit
+        and their sign counts; `scratch`: shared memory for the rank pass."""
+        g = self.g
+        g("// ---- chunk emission order: ascending u64 instance id (viewpipe.py:521) ----")
+        g(f"u64 skey = {live} ? {idv.c} : ~0ull;")
+        g(f"u64* sbuf = (u64*)({scratch});")
+        g("u32* hist = (u32*)(sbuf + NT); u32* bstart = hist + 1024; u16* bmv = (u16*)(bstart + 1024);")
+        g("u32 myrank = 0, myoff = 0;")
+        ir = self.ir
+        fused = self.nt * max(1, len(ir.features)) < 65536
+        if fused:
+            g("// counts, signs and the ids' OR / AND in one reduction; the staged record")
+            g("// spans are dead after its first barrier: the rank pass reuses that memory")
+            g("u32 both; u64 kor, kand;")
+            g(f"sm.tred.run(({live} ? 0x10000u : 0u) + {mm}, {live} ? skey : 0ull, {live} ? skey : ~0ull, "
+              "&both, &kor, &kand, hist, 1024u);")
+            g("const u32 n_inst = both >> 16, tile_signs = both & 0xFFFFu;")
+        else:
+            g(f"const u32 n_inst = sm.scan.sum({live} ? 1u : 0u);")
+            g(f"const u32 tile_signs = sm.scan.sum({mm});")
+        g("// publish the aggregate now: successors' look-back overlaps our sort")
+        g("if (threadIdx.x == 0) fbx::publish_aggregate(STATUS, tile, n_inst, tile_signs);")
+        g("// Emitted ids are unique (else the run fails): a row's rank is the number")
+        g("// of live ids below its own.  Adaptive radix buckets carrying the sign counts")
+        g("// (rank and sign offset in one pass); bitonic sort + offset scan fallback.")
+        if fused:
+            g(f"if (!fbx::radix_rank_off<NT>(skey, {live}, {mm}, kor ^ kand, hist, bstart, sbuf, bmv, "
+              "sm.scan, &myrank, &myoff)) {")
+        else:
+            g("{")
+        g("const u64 sorted = fbx::bitonic_keys<NT>(skey, sbuf);")
+        g("sbuf[2 * NT + threadIdx.x] = sorted;")
+        g("__syncthreads();")
+        g(f"myrank = {live} ? fbx::lower_rank<NT>(sbuf + 2 * NT, skey) : 0u;")
+        g("sm.soff[threadIdx.x] = 0u;")
+        g("__syncthreads();")
+        g(f"if ({live}) sm.soff[myrank] = {mm};")
+        g("__syncthreads();")
+        g("const u32 s_off = sm.scan.exclusive(sm.soff[threadIdx.x]);")
+        g("sm.rank[threadIdx.x] = s_off;  // sign offset by sorted position")
+        g("__syncthreads();")
+        g(f"myoff = {live} ? sm.rank[myrank] : 0u;")
+        g("}")
+
+    NULL_PROPAGATING = ("hash", "concat", "token", "lower", "trim", "id", "mix", "fold")
+
+    def predict_feature_nulls(self, feats) -> list[str] | None:
+        """Null expression of every emitted feature, evaluated BEFORE the DAG.
+
+        An operator output is null iff an input is null (hash, concat, token,
+        lower, trim, id, mix, fold) or never (lookup); a row whose operators
+        raise fails the run, so for every run that succeeds the prediction is
+        exact.  None when some operator is outside that set or two features
+        share a slot (the (slot, sign) dedup then depends on values)."""
+        ir = self.ir
+        if len({slot for _, slot in feats}) != len(feats):
+            return None
+        pn: dict[str, str] = {}
+
+        def colnull(c):
+            if c in ir.producer:
+                return pn.get(ir.producer[c])
+            v = self.env.get(c)
+            if v is None or isinstance(v, tuple):
+                return None
+            return v.n if v.nullable else "false"
+        for nd in self.node_schedule():
+            if nd.role == "pre":
+                ins = [colnull(nd.inputs[0])]
+            elif nd.role == "post":
+                ins = [pn.get(nd.op)]
+            else:
+                pre = ir.pre_of.get(nd.op, {})
+                ins = [pn.get(pre[i]) if i in pre else colnull(c) for i, c in enumerate(nd.inputs)]
+            if any(x is None for x in ins):
+                return None
+            op = nd.fn.op
+            if op == "lookup":
+                pn[nd.name] = "false"
+            elif op in self.NULL_PROPAGATING:
+                xs = [x for x in ins if x != "false"]
+                pn[nd.name] = "(" + " || ".join(xs) + ")" if xs else "false"
+            else:
+                return None
+        out = []
+        for col, _ in feats:
+            x = colnull(col)
+            if x is None:
+                return None
+            out.append(x)
+        return out
 
     def node_schedule(self) -> list[NodeIR]:
         """Layer order, with nodes that need no joined column first (their work
@@ -1600,6 +1698,8 @@ class PlanCodegen:
         rank_bytes = max(24 * self.nt, 10 * self.nt + 8192)  # bitonic 3*NT u64 | radix
         self.dyn_smem = max(self.span_cap, rank_bytes,
                             min(need, per_cta, OUT_BUDGET)) // 16 * 16
+        if self.early_order:  # the pre-DAG rank pass lives behind the staged spans
+            self.dyn_smem = max(self.dyn_smem, (self.span_cap + rank_bytes + 15) // 16 * 16)
         # first probe slots of int-keyed tables land behind the staged spans
         self.pf_slot = {}
         if ir.mode != "extract":

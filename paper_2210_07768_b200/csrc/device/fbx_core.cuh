@@ -27,7 +27,7 @@ typedef long long i64;
 #include "fbx_abi.h"
 
 // profiling aid (codegen FBX_PHASE_TIMERS): SM cycles per kernel phase, summed over warps
-__device__ unsigned long long fbx_ph[8];
+__device__ unsigned long long fbx_ph[10];
 __device__ unsigned int fbx_ph_done;
 #define FBX_PHASE(k) do { if ((threadIdx.x & 31u) == 0) { const u64 t_ = clock64(); \
   atomicAdd(&fbx_ph[(k)], t_ - ph_t); ph_t = t_; } } while (0)
