@@ -140,3 +140,21 @@ def test_streamed_slice_plan_covers_rows():
         assert cuts[0] == 0 and cuts[-1] == 20000
         assert all(a < b for a, b in sr.bounds)
         assert all(x % eng.ir.chunk == 0 for x in cuts[:-1])
+
+
+@pytest.mark.parametrize("knob", ["FBX_EARLY_ORDER=1", "FBX_PERSISTENT=1",
+                                  "FBX_NVRTC_OPTS=-DFBX_POOL_WARP", "FBX_L2_PREFETCH=1",
+                                  "FBX_EARLY_ORDER=1 FBX_PERSISTENT=1"])
+@pytest.mark.parametrize("dag", ["sign_heavy", "cross_heavy"])
+def test_codegen_knobs_keep_parity(knob, dag, goldens, monkeypatch):
+    """The measured-and-rejected kernel variants stay bit-exact."""
+    for kv in knob.split():
+        k, v = kv.split("=", 1)
+        monkeypatch.setenv(k, v)
+    res = _run(20000, 2000, 7, dag, max_rows_per_launch=8192)
+    g = golden_run(goldens, 20000, 7, dag)
+    assert f"0x{res.report.digest:016x}" == g["digest"]
+    assert (res.report.instances, res.report.signs) == (g["instances"], g["signs"])
+    ref = _run(20000, 2000, 7, dag).csr
+    for k in ("ids", "labels", "offsets", "slots", "signs"):
+        np.testing.assert_array_equal(res.csr[k], ref[k], err_msg=k)
