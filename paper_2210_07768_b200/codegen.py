@@ -124,6 +124,7 @@ class Program:
     notes: list[str]
     int_keyed: tuple[int, ...] = ()   # tables with 16-B fbx::ISlot slots
     persistent_ctas_per_sm: int = 0   # >0: fbx_pipeline takes tiles from a ticket
+    json_kind: bool = False           # Json-kind extraction: canonical JSON into the pool
 
 
 # ---------------------------------------------------------------------------
@@ -234,6 +235,7 @@ class PlanCodegen:
         default_mb = max(1, min(default_mb, 2048 // self.nt))
         self.min_blocks = int(os.environ.get("FBX_MIN_BLOCKS", str(default_mb)))
         self.pool_sites = 0
+        self.json_kind = False
         self._ids_tail: list[str] = []
         self.pf_slot: dict[int, int] = {}
         self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
@@ -367,9 +369,7 @@ class PlanCodegen:
             lens += ln + [0] * (8 - len(ln))
             nseg.append(len(parts))
             if e.kind is Kind.JSON:
-                raise UnsupportedOnDevice(
-                    "Json-kind extraction (json.dumps re-serialisation) is not implemented "
-                    "on device")
+                self.json_kind = True
         tag = g.fresh("jp")
         self.globals.append(f"__device__ const u8 {tag}_seg[] = {_c_bytes(segs)};")
         self.globals.append(f"__device__ const u16 {tag}_off[] = "
@@ -429,6 +429,21 @@ class PlanCodegen:
                 g(f"i64 t; if (fbx::j_to_i64({src.c}.p, {lf}.beg, {lf}.end, &t)) "
                   f"{{ {v.c} = (u64)t; {v.c}_n = false; }}")
                 g("}")
+            elif e.kind is Kind.JSON:
+                # json.dumps(value, sort_keys=True, separators=(",", ":")): measured,
+                # allocated from the bump pool, written (viewpipe.py:266-267)
+                v = V("str", g.fresh(f"{prefix}x"), True)
+                self.decl(v)
+                jl = g.fresh("jl")
+                has = (f"alive && {leaf}_ok && {lf}.type != fbx::J_MISSING && "
+                       f"{lf}.type != fbx::J_NULL")
+                g(f"u32 {jl} = ({has}) ? fbx::json_canon({src.c}.p, {src.c}.n, {lf}, nullptr) : 0u;")
+                g(f"if ({jl} == ~0u) {{")
+                self.row_error(stage, "float_slow")
+                g("}")
+                ptr = self.pool_alloc(f"({has} && {jl} != ~0u) ? {jl} : 0u")
+                g(f"if (({has}) && {jl} != ~0u && {ptr}) {{ fbx::json_canon({src.c}.p, {src.c}.n, {lf}, "
+                  f"{ptr}); {v.c} = fbx::Str{{{ptr}, {jl}}}; {v.c}_n = false; }}")
             else:  # FLOAT32
                 v = V("f32", g.fresh(f"{prefix}x"), True)
                 self.decl(v)
@@ -1737,7 +1752,7 @@ class PlanCodegen:
         nt_ = len(ir.sides) + (1 if ir.basic is not None else 0)
         return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes,
                        tuple(k for k in range(nt_) if self.int_keyed(k)),
-                       self.min_blocks if self.persistent else 0)
+                       self.min_blocks if self.persistent else 0, self.json_kind)
 
 
 def _filter_columns(expr) -> set[str]:

@@ -1601,10 +1601,61 @@ FBX_DI u64 round_p192(u64 p2, u64 p1, u64 p0, int s) {
   return m;  // subnormal
 }
 
+// Exact decision between two adjacent doubles for an exact decimal w * 10^q (the
+// bracketing Eisel-Lemire could not: the value is within 2^-64 of their midpoint,
+// e.g. an exact tie like 7283009533423449.5).  Big integers of 48 x 32-bit limbs:
+// w * 5^|q| * 2^x against (2m + 1) * 2^y.  Rare path: not inlined.
+__device__ __noinline__ void big_mul_small(u32* l, int& nl, u32 mul) {
+  u64 carry = 0;
+  for (int i = 0; i < nl; ++i) {
+    const u64 cur = (u64)l[i] * mul + carry;
+    l[i] = (u32)cur;
+    carry = cur >> 32;
+  }
+  if (carry && nl < 48) l[nl++] = (u32)carry;
+}
+// place v << sh into a zeroed 48-limb array
+__device__ __noinline__ void big_set_shifted(u32* out, const u32* v, int nv, int sh) {
+  for (int i = 0; i < 48; ++i) out[i] = 0u;
+  const int ws = sh >> 5, bs = sh & 31;
+  for (int i = 0; i < nv; ++i) {
+    const u64 x = (u64)v[i] << bs;
+    if (i + ws < 48) out[i + ws] |= (u32)x;
+    if (i + ws + 1 < 48) out[i + ws + 1] |= (u32)(x >> 32);
+  }
+}
+__device__ __noinline__ u64 dec_to_double_tie(u64 w, int q, u64 a_bits) {
+  const u32 ea_b = (u32)(a_bits >> 52) & 0x7FFu;
+  const u64 ma = ea_b ? ((a_bits & ((1ull << 52) - 1ull)) | (1ull << 52)) : (a_bits & ((1ull << 52) - 1ull));
+  const int ea = ea_b ? (int)ea_b - 1075 : -1074;
+  const u64 y = 2ull * ma + 1ull;  // midpoint = y * 2^(ea - 1)
+  u32 X[48], Y[48], A[48], B[48];
+  int nx = 2, ny = 2;
+  X[0] = (u32)w; X[1] = (u32)(w >> 32);
+  Y[0] = (u32)y; Y[1] = (u32)(y >> 32);
+  int xs, ys;  // compare X * 2^xs with Y * 2^ys
+  if (q >= 0) {
+    for (int k = q; k > 0;) { const int d = k < 13 ? k : 13; u32 m = 1; for (int i = 0; i < d; ++i) m *= 5u; big_mul_small(X, nx, m); k -= d; }
+    xs = q; ys = ea - 1;
+  } else {
+    for (int k = -q; k > 0;) { const int d = k < 13 ? k : 13; u32 m = 1; for (int i = 0; i < d; ++i) m *= 5u; big_mul_small(Y, ny, m); k -= d; }
+    xs = 0; ys = ea - 1 - q;
+  }
+  const int mn = xs < ys ? xs : ys;
+  big_set_shifted(A, X, nx, xs - mn);
+  big_set_shifted(B, Y, ny, ys - mn);
+  int c = 0;
+  for (int i = 47; i >= 0 && c == 0; --i) c = A[i] < B[i] ? -1 : (A[i] > B[i] ? 1 : 0);
+  if (c < 0) return a_bits;
+  if (c > 0) return a_bits + 1ull;
+  return (ma & 1ull) ? a_bits + 1ull : a_bits;  // exact tie: even mantissa
+}
+
 // Correctly rounded w * 10^q (exact=false: the value lies in [w, w+1) * 10^q,
-// i.e. nonzero digits were dropped past the 19th).  Bracketing Eisel-Lemire,
-// the exact model is decimal_tables.to_double.  Returns 0 ok, 1 needs a bignum,
-// 2 overflow (*bits = +inf).
+// i.e. nonzero digits were dropped past the 19th).  Bracketing Eisel-Lemire with
+// an exact big-integer decision when the bracket straddles a midpoint; the exact
+// model is decimal_tables.to_double.  Returns 0 ok, 1 needs all the digits (an
+// inexact decimal that close to a midpoint), 2 overflow (*bits = +inf).
 FBX_DI u32 dec_to_double(u64 w, int q, bool exact, u64* bits) {
   if (w == 0 || q < P10_QMIN) { *bits = 0ull; return 0; }
   if (q > P10_QMAX) { *bits = 0x7FF0000000000000ull; return 2; }
@@ -1629,7 +1680,13 @@ FBX_DI u32 dec_to_double(u64 w, int q, bool exact, u64* bits) {
     q0 -= 1ull;
     if (borrow0) { const u64 borrow1 = q1 == 0ull; q1 -= 1ull; if (borrow1) q2 -= 1ull; }
     const u64 hi_bits = round_p192(q2, q1, q0, s);
-    if (hi_bits != lo_bits) return 1;
+    if (hi_bits != lo_bits) {
+      if (!exact || lo_bits == ~0ull) return 1;  // digits beyond the 19th: needs them all
+      const u64 r = dec_to_double_tie(w, q, lo_bits);
+      if ((r & 0x7FFFFFFFFFFFFFFFull) >= 0x7FF0000000000000ull) { *bits = 0x7FF0000000000000ull; return 2; }
+      *bits = r;
+      return 0;
+    }
   }
   if (lo_bits == ~0ull) { *bits = 0x7FF0000000000000ull; return 2; }
   *bits = lo_bits;
@@ -1832,6 +1889,405 @@ __device__ __noinline__ u32 f32_repr(u8* dst, u32 bits) {
     dst[n++] = '0';
   }
   return n;
+}
+
+}  // namespace fbx
+
+namespace fbx {
+
+// ---------------------------------------------------------------------------
+// repr() of a binary64 value (json.dumps of Float leaves, Json-kind extraction,
+// viewpipe.py:268): the f32_repr scheme with big-integer windows -- x << t up to
+// 2^1030 and x * 5^341 < 2^850 fit 36 x 32-bit limbs -- subnormals at their fixed
+// spacing and the rounding interval closed only for an even mantissa.  Python
+// model: decimal_tables.f64_repr (checked against repr(), tests/test_host.py).
+// Rare path: not inlined, limbs in local memory.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ u64 repr_window_big(u64 x, int t, int k, bool* sticky) {
+  u32 l[36];
+  int nl;
+  if (k >= 0 && t < 0) {
+    const u64 ip = -t >= 64 ? 0ull : x >> -t;
+    const bool fr = -t >= 64 ? x != 0ull : (x & ((1ull << -t) - 1ull)) != 0ull;
+    u64 p = 1;
+    for (int i = 0; i < k; ++i) p *= 10u;
+    *sticky = fr || (ip % p) != 0ull;
+    return ip / p;
+  }
+  if (k >= 0) {  // (x << t) / 10^k
+    for (int i = 0; i < 36; ++i) l[i] = 0u;
+    const int ws = t >> 5, bs = t & 31;
+    const u64 xs0 = (u64)(u32)x << bs, xs1 = (u64)(u32)(x >> 32) << bs;
+    // x << bs spans up to 3 limbs
+    const u32 a0 = (u32)xs0, a1 = (u32)(xs0 >> 32) | (u32)xs1, a2 = (u32)(xs1 >> 32);
+    l[ws] = a0;
+    if (ws + 1 < 36) l[ws + 1] = a1;
+    if (ws + 2 < 36) l[ws + 2] = a2;
+    nl = ws + 3 < 36 ? ws + 3 : 36;
+    bool st = false;
+    for (int kk = k; kk > 0;) {
+      const int d = kk < 9 ? kk : 9;
+      u32 div = 1;
+      for (int i = 0; i < d; ++i) div *= 10u;
+      u64 rem = 0;
+      for (int i = nl - 1; i >= 0; --i) {
+        const u64 cur = (rem << 32) | l[i];
+        l[i] = (u32)(cur / div);
+        rem = cur % div;
+      }
+      while (nl > 2 && l[nl - 1] == 0u) --nl;
+      st |= rem != 0ull;
+      kk -= d;
+    }
+    *sticky = st;
+    return ((u64)l[1] << 32) | l[0];
+  }
+  // x * 10^-k * 2^t = (x * 5^-k) * 2^(t - k)
+  for (int i = 0; i < 36; ++i) l[i] = 0u;
+  l[0] = (u32)x;
+  l[1] = (u32)(x >> 32);
+  nl = 2;
+  for (int kk = -k; kk > 0;) {
+    const int d = kk < 13 ? kk : 13;
+    u32 mul = 1;
+    for (int i = 0; i < d; ++i) mul *= 5u;
+    u64 carry = 0;
+    for (int i = 0; i < nl; ++i) {
+      const u64 cur = (u64)l[i] * mul + carry;
+      l[i] = (u32)cur;
+      carry = cur >> 32;
+    }
+    if (carry && nl < 36) l[nl++] = (u32)carry;
+    kk -= d;
+  }
+  const int sh = t - k;
+  if (sh >= 0) {
+    *sticky = false;
+    return (((u64)l[1] << 32) | l[0]) << sh;
+  }
+  const int r = -sh, ws = r >> 5, bs = r & 31;
+  if (ws >= 36) { *sticky = true; return 0ull; }
+  bool st = (l[ws] & ((1u << bs) - 1u)) != 0u;
+  for (int i = 0; i < ws; ++i) st |= l[i] != 0u;
+  *sticky = st;
+  const u32 a = l[ws], b = ws + 1 < 36 ? l[ws + 1] : 0u, c = ws + 2 < 36 ? l[ws + 2] : 0u;
+  return ((u64)__funnelshift_r(b, c, bs) << 32) | __funnelshift_r(a, b, bs);
+}
+
+// writes repr(float) of the binary64 bits (finite); returns the length (<= 24)
+__device__ __noinline__ u32 f64_repr(u8* dst, u64 bits) {
+  const u32 sgn = (u32)(bits >> 63), ex = (u32)(bits >> 52) & 0x7FFu;
+  const u64 m = bits & ((1ull << 52) - 1ull);
+  u32 n = 0;
+  if (sgn) dst[n++] = '-';
+  if (ex == 0u && m == 0ull) { dst[n] = '0'; dst[n + 1] = '.'; dst[n + 2] = '0'; return n + 3u; }
+  const u64 f = ex ? (m | (1ull << 52)) : m;
+  const int e = ex ? (int)ex - 1075 : -1074;
+  const bool closed = (f & 1ull) == 0ull;
+  const u64 v4 = 4ull * f, lo4 = v4 - ((m == 0ull && ex > 1u) ? 1ull : 2ull), hi4 = v4 + 2ull;
+  const int t = e - 2;
+  const int hb = 63 - __clzll((long long)hi4);
+  const int k = (((hb + t) * 78913) >> 18) - 17;  // floor(log10 hi) - 17
+  bool sl, sv, shh;
+  const u64 wl = repr_window_big(lo4, t, k, &sl), wv = repr_window_big(v4, t, k, &sv);
+  const u64 wh = repr_window_big(hi4, t, k, &shh);
+  // largest p with a multiple of 10^(k+p) in the interval (monotone in p)
+  int p = 0;
+  u64 p10 = 1, bot = 0, top = 0;
+  while (p < 19) {
+    const u64 q10 = p10 * 10u;
+    u64 nb, nt;
+    if (closed) {
+      nb = wl / q10 + ((wl % q10) != 0u || sl);
+      nt = wh / q10;
+    } else {
+      nb = wl / q10 + 1u;
+      nt = wh / q10 - (((wh % q10) == 0u && !shh) ? 1u : 0u);
+    }
+    if (nb > nt) break;
+    p10 = q10; ++p; bot = nb; top = nt;
+  }
+  u64 w = wv / p10;
+  const u64 r = wv % p10, half = p10 >> 1;
+  if (p > 0 && (r > half || (r == half && (sv || (w & 1u))))) ++w;
+  if (p > 0) w = w < bot ? bot : (w > top ? top : w);
+  u8 dg[20];
+  const u32 nd = u64_dec_len(w);
+  u64_dec(dg, w, nd);
+  const int decpt = (int)nd + k + p;
+  if (decpt <= -4 || decpt > 16) {
+    dst[n++] = dg[0];
+    if (nd > 1u) {
+      dst[n++] = '.';
+      for (u32 i = 1; i < nd; ++i) dst[n++] = dg[i];
+    }
+    int x = decpt - 1;
+    dst[n++] = 'e';
+    dst[n++] = x < 0 ? '-' : '+';
+    x = x < 0 ? -x : x;
+    if (x >= 100) dst[n++] = (u8)('0' + x / 100);
+    dst[n++] = (u8)('0' + (x / 10) % 10);
+    dst[n++] = (u8)('0' + x % 10);
+  } else if (decpt <= 0) {
+    dst[n++] = '0';
+    dst[n++] = '.';
+    for (int i = 0; i < -decpt; ++i) dst[n++] = '0';
+    for (u32 i = 0; i < nd; ++i) dst[n++] = dg[i];
+  } else if ((u32)decpt < nd) {
+    for (u32 i = 0; i < nd; ++i) {
+      if (i == (u32)decpt) dst[n++] = '.';
+      dst[n++] = dg[i];
+    }
+  } else {
+    for (u32 i = 0; i < nd; ++i) dst[n++] = dg[i];
+    for (u32 i = nd; i < (u32)decpt; ++i) dst[n++] = '0';
+    dst[n++] = '.';
+    dst[n++] = '0';
+  }
+  return n;
+}
+
+}  // namespace fbx
+
+namespace fbx {
+
+// ---------------------------------------------------------------------------
+// Json-kind extraction (viewpipe.py:266-267): json.dumps(value, sort_keys=True,
+// separators=(",", ":")) -- ensure_ascii escaping, ints canonical ("-0" -> "0"),
+// floats as repr() of the correctly rounded double ("Infinity" on overflow),
+// objects re-emitted in code-point key order with the LAST duplicate winning.
+// The document was validated by json_extract.  Objects are emitted by
+// selection (each step scans the members for the smallest key above the last
+// one emitted), containers through an explicit stack: no member storage.
+// dst == nullptr measures.  Returns ~0u when a float needs the bignum parse.
+// Python model: decimal_tables.json_canon (checked against json.dumps).
+// ---------------------------------------------------------------------------
+FBX_DI u32 jc_ws(const u8* s, u32 n, u32 i) {
+  while (i < n && (s[i] == ' ' || s[i] == '\t' || s[i] == '\n' || s[i] == '\r')) ++i;
+  return i;
+}
+FBX_DI u32 jc_str_end(const u8* s, u32 i) {  // i after the opening quote
+  while (s[i] != '"') i += (s[i] == '\\') ? 2u : 1u;
+  return i;
+}
+FBX_DI u32 jc_value_end(const u8* s, u32 n, u32 i) {
+  u32 c = s[i];
+  if (c == '"') return jc_str_end(s, i + 1) + 1;
+  if (c == '{' || c == '[') {
+    int depth = 0;
+    while (true) {
+      c = s[i];
+      if (c == '"') { i = jc_str_end(s, i + 1) + 1; continue; }
+      if (c == '{' || c == '[') ++depth;
+      else if ((c == '}' || c == ']') && --depth == 0) return i + 1;
+      ++i;
+    }
+  }
+  while (i < n) {
+    c = s[i];
+    if (c == ',' || c == '}' || c == ']' || c == ' ' || c == '\t' || c == '\n' || c == '\r') break;
+    ++i;
+  }
+  return i;
+}
+FBX_DI u32 jc_hex4(const u8* p) {
+  return (j_hexval(p[0]) << 12) | (j_hexval(p[1]) << 8) | (j_hexval(p[2]) << 4) | j_hexval(p[3]);
+}
+// next code point of a string body (escapes decoded, surrogate pairs joined)
+FBX_DI u32 jc_next_cp(const u8* s, u32& i) {
+  const u32 c = s[i];
+  if (c != '\\') {
+    if (c < 0x80u) { ++i; return c; }
+    if (c < 0xE0u) { const u32 cp = ((c & 0x1Fu) << 6) | (s[i + 1] & 0x3Fu); i += 2; return cp; }
+    if (c < 0xF0u) {
+      const u32 cp = ((c & 0x0Fu) << 12) | ((s[i + 1] & 0x3Fu) << 6) | (s[i + 2] & 0x3Fu);
+      i += 3;
+      return cp;
+    }
+    const u32 cp = ((c & 0x07u) << 18) | ((s[i + 1] & 0x3Fu) << 12) | ((s[i + 2] & 0x3Fu) << 6) |
+                   (s[i + 3] & 0x3Fu);
+    i += 4;
+    return cp;
+  }
+  const u32 x = s[i + 1];
+  if (x != 'u') {
+    i += 2;
+    return x == 'b' ? 8u : x == 'f' ? 12u : x == 'n' ? 10u : x == 'r' ? 13u : x == 't' ? 9u : x;
+  }
+  u32 cp = jc_hex4(s + i + 2);
+  i += 6;
+  if (cp >= 0xD800u && cp <= 0xDBFFu && s[i] == '\\' && s[i + 1] == 'u') {
+    const u32 lo = jc_hex4(s + i + 2);
+    if (lo >= 0xDC00u && lo <= 0xDFFFu) {
+      cp = 0x10000u + ((cp - 0xD800u) << 10) + (lo - 0xDC00u);
+      i += 6;
+    }
+  }
+  return cp;
+}
+// code-point order of two string bodies [ab, ae) and [bb, be)
+FBX_DI int jc_key_cmp(const u8* s, u32 ab, u32 ae, u32 bb, u32 be) {
+  while (ab < ae && bb < be) {
+    const u32 x = jc_next_cp(s, ab), y = jc_next_cp(s, bb);
+    if (x != y) return x < y ? -1 : 1;
+  }
+  return (ab < ae) ? 1 : ((bb < be) ? -1 : 0);
+}
+FBX_DI void jc_put(u8* dst, u32& o, u32 c) { if (dst) dst[o] = (u8)c; ++o; }
+FBX_DI void jc_put_u(u8* dst, u32& o, u32 v) {
+  const char* hx = "0123456789abcdef";
+  jc_put(dst, o, '\\'); jc_put(dst, o, 'u');
+  jc_put(dst, o, hx[(v >> 12) & 15u]); jc_put(dst, o, hx[(v >> 8) & 15u]);
+  jc_put(dst, o, hx[(v >> 4) & 15u]); jc_put(dst, o, hx[v & 15u]);
+}
+FBX_DI void jc_put_str(const u8* s, u32 b, u32 e, u8* dst, u32& o) {
+  jc_put(dst, o, '"');
+  for (u32 i = b; i < e;) {
+    const u32 cp = jc_next_cp(s, i);
+    if (cp == '"' || cp == '\\') { jc_put(dst, o, '\\'); jc_put(dst, o, cp); }
+    else if (cp >= 0x20u && cp <= 0x7Eu) jc_put(dst, o, cp);
+    else if (cp == 8u) { jc_put(dst, o, '\\'); jc_put(dst, o, 'b'); }
+    else if (cp == 12u) { jc_put(dst, o, '\\'); jc_put(dst, o, 'f'); }
+    else if (cp == 10u) { jc_put(dst, o, '\\'); jc_put(dst, o, 'n'); }
+    else if (cp == 13u) { jc_put(dst, o, '\\'); jc_put(dst, o, 'r'); }
+    else if (cp == 9u) { jc_put(dst, o, '\\'); jc_put(dst, o, 't'); }
+    else if (cp < 0x10000u) jc_put_u(dst, o, cp);
+    else {
+      const u32 v = cp - 0x10000u;
+      jc_put_u(dst, o, 0xD800u | (v >> 10));
+      jc_put_u(dst, o, 0xDC00u | (v & 0x3FFu));
+    }
+  }
+  jc_put(dst, o, '"');
+}
+// a scalar at [b, e): string (quotes included), number or literal
+FBX_DI bool jc_put_scalar(const u8* s, u32 b, u32 e, u8* dst, u32& o) {
+  const u32 c = s[b];
+  if (c == '"') { jc_put_str(s, b + 1, e - 1, dst, o); return true; }
+  if (c == '-' && s[b + 1] == 'I') { for (u32 i = b; i < e; ++i) jc_put(dst, o, s[i]); return true; }
+  if (c != '-' && (c - '0') >= 10u) { for (u32 i = b; i < e; ++i) jc_put(dst, o, s[i]); return true; }
+  bool flt = false;
+  for (u32 i = b; i < e; ++i) flt |= (s[i] == '.' || s[i] == 'e' || s[i] == 'E');
+  if (!flt) {  // Python int: digits as written, except -0
+    if (c == '-' && e - b == 2u && s[b + 1] == '0') { jc_put(dst, o, '0'); return true; }
+    for (u32 i = b; i < e; ++i) jc_put(dst, o, s[i]);
+    return true;
+  }
+  JLeaf lf{b, e, J_FLOAT, 0u};
+  u64 db;
+  {
+    u32 i = lf.beg;
+    const bool neg = s[i] == '-';
+    if (neg) ++i;
+    u64 w = 0;
+    u32 sig = 0;
+    int e10 = 0;
+    bool exact = true, frac = false;
+    for (; i < lf.end; ++i) {
+      const u32 ch = s[i];
+      if (ch == '.') { frac = true; continue; }
+      if (ch == 'e' || ch == 'E') break;
+      const u32 d = ch - '0';
+      if (frac) --e10;
+      if (sig == 0 && d == 0) continue;
+      if (sig < 19) { w = w * 10u + d; ++sig; }
+      else { ++e10; if (d) exact = false; }
+    }
+    if (i < lf.end) {
+      ++i;
+      bool eneg = false;
+      if (s[i] == '+' || s[i] == '-') { eneg = s[i] == '-'; ++i; }
+      int ev = 0;
+      for (; i < lf.end; ++i)
+        if (ev < 100000) ev = ev * 10 + (int)(s[i] - '0');
+      e10 += eneg ? -ev : ev;
+    }
+    const u32 st = dec_to_double(w, e10, exact, &db);
+    if (st == 1u) return false;
+    if (neg) db |= 0x8000000000000000ull;
+  }
+  if ((db & 0x7FFFFFFFFFFFFFFFull) == 0x7FF0000000000000ull) {
+    if (db >> 63) jc_put(dst, o, '-');
+    const char* w = "Infinity";
+    for (int i = 0; i < 8; ++i) jc_put(dst, o, (u8)w[i]);
+    return true;
+  }
+  u8 buf[32];
+  const u32 L = f64_repr(buf, db);
+  for (u32 i = 0; i < L; ++i) jc_put(dst, o, buf[i]);
+  return true;
+}
+
+constexpr int JC_MAXD = 64;
+struct JcFrame {
+  u32 obj, pos, lkb, lke, first;
+};
+
+// json.dumps(..., sort_keys=True, separators=(",", ":")) of the leaf; ~0u: unsupported
+__device__ __noinline__ u32 json_canon(const u8* s, u32 n, JLeaf lf, u8* dst) {
+  u32 o = 0;
+  if (lf.type != J_CONTAINER) {
+    if (lf.type == J_STRING) { jc_put_str(s, lf.beg, lf.end, dst, o); return o; }
+    u32 b = lf.beg, e = lf.end;
+    if (!jc_put_scalar(s, b, e, dst, o)) return ~0u;
+    return o;
+  }
+  JcFrame st[JC_MAXD];
+  int d = 0;
+  u32 i0 = lf.beg;
+  st[0] = JcFrame{s[i0] == '{' ? 1u : 0u, jc_ws(s, n, i0 + 1), 0u, 0u, 1u};
+  jc_put(dst, o, s[i0]);
+  d = 1;
+  while (d > 0) {
+    JcFrame& f = st[d - 1];
+    u32 vb, ve;
+    if (!f.obj) {
+      const u32 i = f.pos;
+      if (s[i] == ']') { jc_put(dst, o, ']'); --d; continue; }
+      if (!f.first) jc_put(dst, o, ',');
+      f.first = 0u;
+      vb = i;
+      ve = jc_value_end(s, n, i);
+      u32 nx = jc_ws(s, n, ve);
+      if (s[nx] == ',') nx = jc_ws(s, n, nx + 1);
+      f.pos = nx;
+    } else {
+      u32 bkb = 0, bke = 0, bv = 0;
+      bool have = false;
+      u32 i = f.pos;
+      while (s[i] != '}') {
+        const u32 kb = i + 1, ke = jc_str_end(s, kb);
+        u32 vi = jc_ws(s, n, ke + 1);
+        vi = jc_ws(s, n, vi + 1);
+        const u32 vend = jc_value_end(s, n, vi);
+        if (f.first || jc_key_cmp(s, kb, ke, f.lkb, f.lke) > 0) {
+          if (!have || jc_key_cmp(s, kb, ke, bkb, bke) <= 0) {  // equal: the later one wins
+            bkb = kb; bke = ke; bv = vi; have = true;
+          }
+        }
+        i = jc_ws(s, n, vend);
+        if (s[i] == ',') i = jc_ws(s, n, i + 1);
+      }
+      if (!have) { jc_put(dst, o, '}'); --d; continue; }
+      if (!f.first) jc_put(dst, o, ',');
+      f.first = 0u;
+      f.lkb = bkb;
+      f.lke = bke;
+      jc_put_str(s, bkb, bke, dst, o);
+      jc_put(dst, o, ':');
+      vb = bv;
+      ve = jc_value_end(s, n, bv);
+    }
+    if (s[vb] == '{' || s[vb] == '[') {
+      if (d >= JC_MAXD) return ~0u;
+      st[d] = JcFrame{s[vb] == '{' ? 1u : 0u, jc_ws(s, n, vb + 1), 0u, 0u, 1u};
+      jc_put(dst, o, s[vb]);
+      ++d;
+    } else if (!jc_put_scalar(s, vb, ve, dst, o)) {
+      return ~0u;
+    }
+  }
+  return o;
 }
 
 }  // namespace fbx

@@ -102,7 +102,17 @@ def to_double(w: int, q: int, exact: bool):
     b = _round53(hi, -s)
     if a == b:
         return a
-    return "slow"
+    if not exact or a is None:
+        return "slow"
+    # exact decision against the midpoint of a and its successor (fbx::dec_to_double_tie)
+    from fractions import Fraction
+    ea_b = (a >> 52) & 0x7FF
+    ma = ((a & ((1 << 52) - 1)) | (1 << 52)) if ea_b else (a & ((1 << 52) - 1))
+    ea = ea_b - 1075 if ea_b else -1074
+    mid = Fraction(2 * ma + 1) * Fraction(2) ** (ea - 1)
+    v = Fraction(w) * Fraction(10) ** q
+    r = a if v < mid else a + 1 if v > mid else (a + 1 if ma & 1 else a)
+    return None if (r & 0x7FFFFFFFFFFFFFFF) >= 0x7FF0000000000000 else r
 
 
 def decimal_parts(text: str):
@@ -244,3 +254,93 @@ def check_random(n: int = 20000, seed: int = 3) -> int:
 if __name__ == "__main__":
     HEADER.write_text(render())
     print("wrote", HEADER, "slow:", check_random())
+
+
+def f64_repr(bits: int) -> str:
+    """Exact Python model of ``fbx::f64_repr``: ``repr(float)`` of a binary64 value.
+
+    The f32 scheme of :func:`f32_repr` generalised: subnormals keep their fixed
+    spacing (no normalisation), the round-to-nearest interval is closed only for
+    an even mantissa (ties-to-even parsing), and the windows need big integers
+    (the device uses 36 x 32-bit limbs: x << t < 2^1030, x * 5^341 < 2^850).
+    """
+    s, ex, m = bits >> 63, (bits >> 52) & 0x7FF, bits & ((1 << 52) - 1)
+    if ex == 0x7FF:
+        return "nan" if m else ("-inf" if s else "inf")
+    if ex == 0 and m == 0:
+        return "-0.0" if s else "0.0"
+    f, e = ((m | (1 << 52)), ex - 1075) if ex else (m, -1074)
+    closed = (f & 1) == 0
+    lo = 4 * f - (1 if (m == 0 and ex > 1) else 2)
+    v, hi, t = 4 * f, 4 * f + 2, e - 2
+    k = (((hi.bit_length() - 1 + t) * 78913) >> 18) - 17
+
+    def window(x: int) -> tuple[int, bool]:
+        if k >= 0:
+            if t >= 0:
+                q, r = divmod(x << t, 10 ** k)
+                return q, r != 0
+            q, r = divmod(x >> -t, 10 ** k)
+            return q, r != 0 or (x & ((1 << -t) - 1)) != 0
+        p5, sh = x * 5 ** -k, t - k
+        if sh >= 0:
+            return p5 << sh, False
+        return p5 >> -sh, (p5 & ((1 << -sh) - 1)) != 0
+
+    (wl, sl), (wv, sv), (wh, sh_) = window(lo), window(v), window(hi)
+    for p in range(19, 0, -1):
+        p10 = 10 ** p
+        if closed:
+            top = wh // p10
+            bot = wl // p10 + (1 if (wl % p10 or sl) else 0)
+        else:
+            top = wh // p10 - (1 if (wh % p10 == 0 and not sh_) else 0)
+            bot = wl // p10 + 1
+        if bot <= top:
+            w, r = divmod(wv, p10)
+            if r > p10 // 2 or (r == p10 // 2 and (sv or (w & 1))):
+                w += 1
+            w = min(max(w, bot), top)
+            break
+    else:  # p = 0: the window digits themselves (unreachable for binary64)
+        p, w = 0, wv
+    digits = str(w)
+    nd = len(digits)
+    decpt = nd + k + p
+    out = "-" if s else ""
+    if decpt <= -4 or decpt > 16:
+        x = decpt - 1
+        return (out + digits[0] + ("." + digits[1:] if nd > 1 else "")
+                + ("e-" if x < 0 else "e+") + f"{abs(x):02d}")
+    if decpt <= 0:
+        return out + "0." + "0" * -decpt + digits
+    if decpt < nd:
+        return out + digits[:decpt] + "." + digits[decpt:]
+    return out + digits + "0" * (decpt - nd) + ".0"
+
+
+def check_f64_repr(n: int, seed: int = 5) -> int:
+    """f64_repr == repr() on random bit patterns, random decimals and edge cases."""
+    import random
+    import struct
+    rng = random.Random(seed)
+    cases = [0x0000000000000001, 0x000FFFFFFFFFFFFF, 0x0010000000000000, 0x7FEFFFFFFFFFFFFF,
+             0x3FF0000000000000, 0x4340000000000000, 0x3CB0000000000000, 0x0020000000000000]
+    for x in (0.1, 0.2, 0.3, 1e16, 1e17, 9007199254740993.0, 5e-324, 1.7976931348623157e308,
+              2.2250738585072014e-308, 1e-5, 1e-4, 123456789012345680.0, 0.30000000000000004,
+              1.5, 100000.0, 1e22, 1e23, 2 ** 63, 2 ** 64, 4.35, 0.001, 9.999999999999999e22):
+        cases.append(struct.unpack("<Q", struct.pack("<d", x))[0])
+    for _ in range(n):
+        cases.append(rng.getrandbits(64))
+        d = rng.choice([1, 2, 3, 5, 8, 12, 15, 16, 17, 18, 20])
+        cases.append(struct.unpack("<Q", struct.pack(
+            "<d", float(f"{rng.randrange(10 ** d)}e{rng.randrange(-330, 310)}")))[0])
+    checked = 0
+    for b in cases:
+        x = struct.unpack("<d", struct.pack("<Q", b))[0]
+        want = repr(x)
+        got = f64_repr(b)
+        if got != want:
+            raise AssertionError(f"f64_repr({b:#018x}) = {got!r}, repr = {want!r}")
+        checked += 1
+    return checked

@@ -316,6 +316,8 @@ class Engine:
         # launches cover whole chunks; round UP so a run of <= max rows is one launch
         self.max_rows = -(-max_rows_per_launch // ir.chunk) * ir.chunk
         self.pool_bytes_per_row = pool_bytes_per_row
+        if prepared.program.json_kind:  # canonical JSON can outgrow its source (escapes)
+            self.pool_bytes_per_row += 512
         with torch.cuda.device(self.device):
             self.module = runtime.Program(prepared.cubin)
             self.state = torch.zeros(runtime.STATE_BYTES // 8, dtype=torch.int64,
@@ -392,7 +394,8 @@ class Engine:
                     self._set(f"side{k}.ext.{e.output}.val", val.data_ptr())
                     self._set(f"side{k}.ext.{e.output}.null", nul.data_ptr())
                 src_col = img.columns[e.source]
-                side_pool_cap += int(src_col.data.nbytes) + 128 * (n // 256 + 1)
+                grow = 6 if e.kind is Kind.JSON else 1  # ensure_ascii: 1 byte -> "\\uXXXX"
+                side_pool_cap += grow * int(src_col.data.nbytes) + 128 * (n // 256 + 1)
             prepared_views.append((k, v, n))
         pool = torch.zeros(side_pool_cap + 256, dtype=torch.uint8, device=self.device)
         self._keep.append(pool)

@@ -217,6 +217,40 @@ def test_tokens_long_and_ragged_queries_match_oracle(tmp_path):
     np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
 
 
+@pytest.mark.parametrize("seed", [41, 42])
+def test_json_kind_extraction_matches_oracle(seed, tmp_path):
+    """Json-kind leaves (json.dumps(sort_keys=True, separators=(",", ":"))): random
+    nested values, duplicate keys, escapes, non-ASCII, floats of every magnitude."""
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+    from paper_2210_07768_b200.jsoncanon import random_json_docs
+    drv, prof, bas = _views(3000, seed)
+    vals = random_json_docs(3000, seed)
+    rng = random.Random(seed)
+    metas = []
+    for v in vals:
+        r = rng.random()
+        metas.append(None if r < 0.03 else ('{"u": {"city": %s, "tier": 1}}' % v if r < 0.9
+                                           else '{"u": %s}' % v))
+    drv.columns["meta"] = ColumnImage.from_values(Kind.JSON, metas)
+    _write_views(tmp_path, drv, prof, bas)
+    raw = _config(256, [], {}, filt="age != -12345")
+    raw["views"][0]["clean"]["extract"] = [
+        {"source": "meta", "path": "u.city", "output": "cx", "kind": "json"},
+        {"source": "meta", "path": "u", "output": "uj", "kind": "json"}]
+    raw["operators"] = [
+        {"name": "c", "inputs": ["cx"], "outputs": ["c"], "body": {"fn": "hash:3"}},
+        {"name": "u", "inputs": ["uj"], "outputs": ["u"], "body": {"fn": "hash:4"}},
+        {"name": "cl", "inputs": ["cx"], "outputs": ["cl"], "pre": [{"fn": "lower"}],
+         "body": {"fn": "hash:5"}}]
+    raw["emit"] = {"features": {"c": 3, "u": 4, "cl": 5}}
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is None and got_err is None, (ref_err, got_err)
+    assert (got.report.rows_dropped, got.report.rows_filtered) == (ref.malformed, ref.filtered)
+    assert (got.report.digest, got.report.instances, got.report.signs) == \
+        (ref.digest, ref.instances, ref.signs)
+    np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
+
+
 @pytest.mark.parametrize("filt", ["age < 120.5", "age >= -4611686018427387904", "age == 20.0",
                                   "age != 9999999999999999999999", "age > -1.5 or tier == 2",
                                   "(age < 30 or age > 60) and query != ''", "cx >= 'kyoto'",

@@ -86,11 +86,28 @@ def test_config_errors_mirror_reference(tmp_path):
 
 def test_unsupported_constructs_are_plan_time_errors():
     c, d = corpus(2000, 300, 7)
+    raw = workload_config("default", batch_size=2048)  # one CTA per chunk: <= 1024 rows
+    with pytest.raises(UnsupportedOnDevice):
+        engine.prepare(config_from_dict(raw, d), compile_program=False)
+    raw = workload_config("default")
+    raw["views"][0]["clean"]["extract"] += [
+        {"source": "meta", "path": f"u.k{i}", "output": f"k{i}", "kind": "utf8"} for i in range(8)]
+    with pytest.raises(UnsupportedOnDevice):  # > 8 paths from one JSON source
+        engine.prepare(config_from_dict(raw, d), compile_program=False)
+
+
+def test_json_kind_plan_compiles():
+    """Json-kind extraction (json.dumps re-serialisation) is generated on device."""
+    c, d = corpus(2000, 300, 7)
     raw = workload_config("default")
     raw["views"][0]["clean"]["extract"].append(
         {"source": "meta", "path": "u", "output": "u_json", "kind": "json"})
-    with pytest.raises(UnsupportedOnDevice):
-        engine.prepare(config_from_dict(raw, d), compile_program=False)
+    raw["operators"].append({"name": "uj", "inputs": ["u_json"], "outputs": ["uj"],
+                             "body": {"fn": "hash:91"}})
+    raw["emit"]["features"]["uj"] = 91
+    p = engine.prepare(config_from_dict(raw, d),
+                       {"user_events": c.driver, "user_profile": c.profile}, c.basic)
+    assert p.cubin[:4] == b"\x7fELF"
 
 
 def test_float_repr_plan_compiles():
@@ -174,3 +191,15 @@ def test_decimal_to_double_model_and_tables():
     assert Dt.render() == Dt.HEADER.read_text()
     slow = Dt.check_random(30000, 11)  # asserts equality for every non-slow case
     assert slow < 60
+
+
+def test_f64_repr_model_matches_python():
+    """decimal_tables.f64_repr (model of fbx::f64_repr) == repr() of doubles."""
+    from paper_2210_07768_b200.decimal_tables import check_f64_repr
+    assert check_f64_repr(20000) > 40000
+
+
+def test_json_canon_model_matches_json_dumps():
+    """jsoncanon.json_canon (model of fbx::json_canon) == json.dumps(sort_keys, (",", ":"))."""
+    from paper_2210_07768_b200.jsoncanon import check_json_canon
+    assert check_json_canon(4000) == 4000
