@@ -107,6 +107,13 @@ int fbx_dup_resolve(const unsigned int* d_winner_chunk, const unsigned long long
                     unsigned long long n_slots, unsigned long long* d_out, void* stream);
 
 /* Write `bytes` of a scratch buffer (an L2 flush between timed steps). */
+/* zlib CRC-32 of n device bytes into *d_out (columnstore.py:554-562: the FBXC body
+ * check of a full read, done where the body already is -- in HBM).  d_scratch holds
+ * fbx_crc32_scratch_words(n) words.  Two launches on `stream`, no host sync. */
+int fbx_crc32(const void* d_buf, unsigned long long n, unsigned* d_scratch, unsigned* d_out,
+              void* stream);
+unsigned long long fbx_crc32_scratch_words(unsigned long long n);
+
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream);
 
 #ifdef __cplusplus

@@ -190,6 +190,117 @@ __global__ void k_flush(unsigned int* buf, size_t n) {
     buf[i] = buf[i] + 1u;
 }
 
+// ---- CRC-32 (zlib: reflected 0xEDB88320, init / xorout 0xFFFFFFFF) -----------
+// FBXC full-read check (columnstore.py:554-562).  The message is read as
+// 0^pad || M with the pad in FRONT: leading zeros leave a zero-initialised
+// ("raw") CRC unchanged, so every thread handles an equal 256-byte piece and the
+// pieces combine by GF(2) shifts of fixed lengths:
+//   raw(A || B) = raw(A) * x^(8|B|) mod P  xor  raw(B);
+//   crc(M) = raw(M) xor (0xFFFFFFFF * x^(8|M|) mod P) xor 0xFFFFFFFF.
+constexpr unsigned CRC_POLY = 0xEDB88320u;
+constexpr unsigned CRC_PIECE = 256u;                 // bytes per thread
+constexpr unsigned CRC_BLOCK = 256u * CRC_PIECE;     // bytes per CTA (64 KB)
+
+__device__ __host__ unsigned crc_mulmodp(unsigned a, unsigned b) {  // a*b mod P (reflected)
+  unsigned m = 1u << 31, p = 0u;
+  for (;;) {
+    if (a & m) {
+      p ^= b;
+      if ((a & (m - 1u)) == 0u) break;
+    }
+    m >>= 1;
+    b = (b & 1u) ? (b >> 1) ^ CRC_POLY : b >> 1;
+  }
+  return p;
+}
+__device__ __host__ unsigned crc_xpow8n(unsigned long long n) {  // x^(8n) mod P
+  unsigned p = 1u << 31, x2k = 1u << 30;  // x^0, x^1
+  for (int k = 0; k < 3; ++k) x2k = crc_mulmodp(x2k, x2k);  // x^8
+  while (n) {
+    if (n & 1ull) p = crc_mulmodp(x2k, p);
+    x2k = crc_mulmodp(x2k, x2k);
+    n >>= 1;
+  }
+  return p;
+}
+
+// per CTA: raw CRC of its 64 KB of the front-padded message
+__global__ void __launch_bounds__(256) k_crc_blocks(const unsigned char* buf, unsigned long long n,
+                                                    unsigned long long pad, unsigned* out) {
+  __shared__ unsigned T[8][256];
+  __shared__ unsigned part[256];
+  for (unsigned i = threadIdx.x; i < 256u; i += blockDim.x) {
+    unsigned c = i;
+    for (int k = 0; k < 8; ++k) c = (c & 1u) ? (c >> 1) ^ CRC_POLY : c >> 1;
+    T[0][i] = c;
+  }
+  __syncthreads();
+  for (int t = 1; t < 8; ++t) {
+    for (unsigned i = threadIdx.x; i < 256u; i += blockDim.x)
+      T[t][i] = (T[t - 1][i] >> 8) ^ T[0][T[t - 1][i] & 0xFFu];
+    __syncthreads();
+  }
+  const unsigned long long lo = (unsigned long long)blockIdx.x * CRC_BLOCK + threadIdx.x * CRC_PIECE;
+  unsigned c = 0u;
+  const unsigned long long a = (unsigned long long)(buf + (lo - pad));
+  const unsigned sh = (unsigned)(a & 7u) * 8u;
+  // whole piece inside the message; an unaligned piece reads one aligned word past
+  // its end, so the message's last piece then takes the byte loop
+  if (lo >= pad && lo - pad + CRC_PIECE <= n && (sh == 0u || lo - pad + CRC_PIECE + 8u <= n)) {
+    const unsigned long long* p8 = (const unsigned long long*)(a & ~7ull);
+    unsigned long long w0 = __ldg(p8);
+    for (unsigned k = 0; k < CRC_PIECE / 8u; ++k) {  // slice-by-8 over realigned words
+      const unsigned long long w1 = sh ? __ldg(p8 + k + 1) : 0ull;
+      const unsigned long long v = sh ? (w0 >> sh) | (w1 << (64u - sh)) : __ldg(p8 + k);
+      w0 = w1;
+      const unsigned a = (unsigned)v ^ c, b = (unsigned)(v >> 32);
+      c = T[7][a & 0xFFu] ^ T[6][(a >> 8) & 0xFFu] ^ T[5][(a >> 16) & 0xFFu] ^ T[4][a >> 24] ^
+          T[3][b & 0xFFu] ^ T[2][(b >> 8) & 0xFFu] ^ T[1][(b >> 16) & 0xFFu] ^ T[0][b >> 24];
+    }
+  } else {
+    for (unsigned k = 0; k < CRC_PIECE; ++k) {  // bytes of the pad are zero
+      const unsigned long long j = lo + k;
+      const unsigned byte = j >= pad && j - pad < n ? buf[j - pad] : 0u;
+      c = (c >> 8) ^ T[0][(c ^ byte) & 0xFFu];
+    }
+  }
+  // combine the 256 pieces: level s joins pairs 2^s apart (right part 2^s pieces)
+  part[threadIdx.x] = c;
+  __syncthreads();
+  unsigned xs = crc_xpow8n(CRC_PIECE);
+  for (unsigned s = 1; s < 256u; s <<= 1) {
+    if ((threadIdx.x & (2u * s - 1u)) == 0u)
+      part[threadIdx.x] = crc_mulmodp(xs, part[threadIdx.x]) ^ part[threadIdx.x + s];
+    xs = crc_mulmodp(xs, xs);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = part[0];
+}
+
+// one CTA folds the block CRCs (front-padded to 1024 * R blocks) and finishes
+__global__ void __launch_bounds__(1024) k_crc_finish(const unsigned* blk, unsigned long long nb,
+                                                     unsigned long long n, unsigned* out) {
+  __shared__ unsigned part[1024];
+  const unsigned long long R = (nb + 1023ull) / 1024ull, padb = 1024ull * R - nb;
+  const unsigned xb = crc_xpow8n(CRC_BLOCK);
+  unsigned acc = 0u;
+  for (unsigned long long k = 0; k < R; ++k) {
+    const unsigned long long i = threadIdx.x * R + k;
+    const unsigned v = i >= padb ? blk[i - padb] : 0u;
+    acc = crc_mulmodp(xb, acc) ^ v;
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  unsigned xs = crc_xpow8n(R * CRC_BLOCK);
+  for (unsigned s = 1; s < 1024u; s <<= 1) {
+    if ((threadIdx.x & (2u * s - 1u)) == 0u)
+      part[threadIdx.x] = crc_mulmodp(xs, part[threadIdx.x]) ^ part[threadIdx.x + s];
+    xs = crc_mulmodp(xs, xs);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = part[0] ^ crc_mulmodp(crc_xpow8n(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+}
+
 }  // namespace
 
 struct fbx_program {
@@ -397,6 +508,21 @@ int fbx_dup_resolve(const unsigned int* d_winner_chunk, const unsigned long long
   k_dup_resolve<<<(unsigned)(blocks < 4096 ? (blocks ? blocks : 1) : 4096), 256, 0, s>>>(
       d_winner_chunk, d_later_chunks, n_slots, d_out);
   return cuda_check(cudaGetLastError(), "fbx_dup_resolve");
+}
+
+int fbx_crc32(const void* d_buf, unsigned long long n, unsigned* d_scratch, unsigned* d_out,
+              void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned long long nb = n ? (n + CRC_BLOCK - 1ull) / CRC_BLOCK : 1ull;
+  if (nb > 0x7FFFFFFFull) return fail(FBX_E_ARG, "fbx_crc32: buffer too large");
+  const unsigned long long pad = nb * CRC_BLOCK - n;
+  k_crc_blocks<<<(unsigned)nb, 256, 0, st>>>((const unsigned char*)d_buf, n, pad, d_scratch);
+  k_crc_finish<<<1, 1024, 0, st>>>(d_scratch, nb, n, d_out);
+  return cuda_check(cudaGetLastError(), "fbx_crc32");
+}
+
+unsigned long long fbx_crc32_scratch_words(unsigned long long n) {
+  return n ? (n + CRC_BLOCK - 1ull) / CRC_BLOCK : 1ull;
 }
 
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream) {

@@ -257,6 +257,63 @@ class DeviceView:
         t = self.tensors[name].get(part)
         return 0 if t is None else t.data_ptr()
 
+    @classmethod
+    def from_fbxc(cls, path, columns=None, device="cuda", verify: bool = True) -> "DeviceView":
+        """FBXC ingest with no decode (columnstore.py:499-608): the
+        file body goes to HBM in one copy and the columns are views of it.  A full
+        read checks the body's CRC-32 on the device (columnstore.py:554-562)."""
+        from .columns import ChecksumError, open_view
+        torch = _torch()
+        vf = open_view(path)
+        dev = torch.device(device)
+        mm = np.memmap(vf.path, dtype=np.uint8, mode="r")
+        body = torch.zeros(vf.body_bytes + 64, dtype=torch.uint8, device=dev)
+        host = torch.from_numpy(np.array(mm[vf.body_offset:vf.body_offset + vf.body_bytes]))
+        body[:vf.body_bytes].copy_(host)
+        del mm
+        names = [n for n, _ in vf.schema]
+        if verify and (columns is None or set(columns) >= set(names)):
+            crc = crc32_device(body[:vf.body_bytes])
+            if crc != vf.checksum:
+                raise ChecksumError(f"{vf.path}: body CRC {crc:#010x} != {vf.checksum:#010x}")
+        self = cls.__new__(cls)
+        self.n = vf.row_count
+        self.kinds = {n: k for n, k in vf.schema}
+        self.tensors, self.bytes, self.torch = {}, 0, torch
+        # FBXC segments are packed (byte-identical to the reference writer); the
+        # kernels want 16-B aligned segments with 16 B of slack: one device-side
+        # copy per segment into an aligned arena
+        want = [(name, part) for name, _ in vf.schema
+                if columns is None or name in columns
+                for part in ("nulls", "data", "offsets") if (name, part) in vf.segments]
+        place, cur = {}, 0
+        for key in want:
+            place[key] = cur
+            cur += (vf.segments[key][1] + 31) // 16 * 16
+        arena = torch.zeros(cur + 16, dtype=torch.uint8, device=dev)
+        for (name, part), dst in place.items():
+            o, ln = vf.segments[(name, part)]
+            a = o - vf.body_offset
+            if ln:
+                arena[dst:dst + ln].copy_(body[a:a + ln])
+            self.tensors.setdefault(name, {})[part] = arena[dst:dst + ln]
+            self.bytes += ln
+        self._arena = arena
+        return self
+
+
+def crc32_device(t) -> int:
+    """zlib CRC-32 of a contiguous device tensor's bytes (fbx_crc32)."""
+    torch = _torch()
+    t = t.contiguous().view(torch.uint8)
+    n = t.numel()
+    scratch = torch.empty(runtime.crc32_scratch_words(n) + 1, dtype=torch.int32, device=t.device)
+    out = torch.zeros(1, dtype=torch.int32, device=t.device)
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    runtime.crc32(t.data_ptr() if n else out.data_ptr(), n, scratch.data_ptr(), out.data_ptr(),
+                  stream)
+    return int(out.cpu().numpy().view(np.uint32)[0])
+
 
 # ---------------------------------------------------------------------------
 # results

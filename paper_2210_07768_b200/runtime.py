@@ -32,7 +32,7 @@ EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_prog
            "fbx_kernel_set_max_dynamic_smem", "fbx_launch", "fbx_state_reset",
            "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
            "fbx_dup_resolve", "fbx_state_snapshot",
-           "fbx_pool_reset")
+           "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words")
 
 
 class FbxError(RuntimeError):
@@ -71,6 +71,9 @@ def lib() -> ctypes.CDLL:
             L.fbx_dup_resolve.argtypes = [vp, vp, ctypes.c_ulonglong, vp, vp]
             L.fbx_state_snapshot.argtypes = [vp, vp, vp]
             L.fbx_pool_reset.argtypes = [vp, vp]
+            L.fbx_crc32.argtypes = [vp, ctypes.c_ulonglong, vp, vp, vp]
+            L.fbx_crc32_scratch_words.argtypes = [ctypes.c_ulonglong]
+            L.fbx_crc32_scratch_words.restype = ctypes.c_ulonglong
             for name in EXPORTS:
                 getattr(L, name).restype = getattr(L, name).restype or c
             L.fbx_version.restype = ctypes.c_char_p
@@ -176,6 +179,15 @@ def state_snapshot(d_state: int, h_mapped: int, stream: int):
 
 def pool_reset(d_state: int, stream: int):
     _check(lib().fbx_pool_reset(ctypes.c_void_p(d_state), ctypes.c_void_p(stream)), "pool reset")
+
+
+def crc32(d_buf: int, n: int, d_scratch: int, d_out: int, stream: int):
+    _check(lib().fbx_crc32(ctypes.c_void_p(d_buf), n, ctypes.c_void_p(d_scratch),
+                           ctypes.c_void_p(d_out), ctypes.c_void_p(stream)), "crc32")
+
+
+def crc32_scratch_words(n: int) -> int:
+    return int(lib().fbx_crc32_scratch_words(n))
 
 
 def dict_build(d_slots: int, capacity: int, d_blob: int, d_offs: int, d_vals: int, n: int,

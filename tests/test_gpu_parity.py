@@ -158,3 +158,56 @@ def test_codegen_knobs_keep_parity(knob, dag, goldens, monkeypatch):
     ref = _run(20000, 2000, 7, dag).csr
     for k in ("ids", "labels", "offsets", "slots", "signs"):
         np.testing.assert_array_equal(res.csr[k], ref[k], err_msg=k)
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 255, 256, 257, 65535, 65536, 65537, 1_000_003,
+                               1024 * 65536 + 4097, 3 * 1024 * 65536 + 5])
+def test_crc32_device_matches_zlib(n):
+    import zlib
+    import torch
+    from paper_2210_07768_b200.engine import crc32_device
+    rng = np.random.default_rng(n)
+    host = rng.integers(0, 256, size=n + 11, dtype=np.uint8)
+    dev = torch.from_numpy(host).cuda()
+    for off in (0, 3) if n else (0,):  # aligned and unaligned starts
+        got = crc32_device(dev[off:off + n])
+        assert got == zlib.crc32(host[off:off + n].tobytes()) & 0xFFFFFFFF, (n, off)
+
+
+def test_fbxc_ingest_device_view_and_crc(tmp_path):
+    """DeviceView.from_fbxc: one body copy, column views, device CRC (and the
+    engine runs on it bit-exactly)."""
+    from paper_2210_07768_b200 import engine as E
+    from paper_2210_07768_b200.columns import ChecksumError, read_view
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.workloads import workload_config
+    c, d = corpus(20000, 2000, 7)
+    path = d / "user_events.fbxc"
+    dv = E.DeviceView.from_fbxc(path)
+    ref = E.DeviceView(read_view(path))
+    for name, parts in ref.tensors.items():
+        for part, t in parts.items():
+            got = dv.tensors[name][part]
+            assert torch_equal_prefix(got, t), (name, part)
+    views = {"user_events": c.driver, "user_profile": c.profile}
+    eng = E.Engine(E.prepare(config_from_dict(workload_config("sign_heavy"), d), views, c.basic),
+                   views, c.basic)
+    eng.bind_driver(dv)
+    eng.reserve(c.driver.row_count)
+    eng.begin_run(c.driver.row_count)
+    eng.launch(0, c.driver.row_count, tile_base=0)
+    res = eng.finish()
+    want = _run(20000, 2000, 7, "sign_heavy").report.digest
+    assert res.counters.digest == want
+    raw = bytearray(path.read_bytes())
+    raw[len(raw) // 2] ^= 0x40
+    bad = tmp_path / "bad.fbxc"
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(ChecksumError):
+        E.DeviceView.from_fbxc(bad)
+
+
+def torch_equal_prefix(a, b):
+    n = min(a.numel(), b.numel())
+    la = a.numel() if a.numel() < b.numel() else n
+    return bool((a[:la] == b[:la]).all())
