@@ -342,6 +342,19 @@ class CsrBatch:
     signs: object    # torch int64 (u64 bits) [m]
     counters: Counters
 
+    def minibatches(self, batch_size: int):
+        """The trainer hand-off (TrainingSink.consume, pipeline.py:436-455): mini-batch
+        b is instances [b*batch_size, (b+1)*batch_size) of the run -- the _Emitter's
+        cut (pipeline.py:765-777) -- as device tensor views (offsets rebased to the
+        batch's own sign range).  No host round trip."""
+        n = self.counters.instances
+        for b0 in range(0, n, batch_size):
+            b1 = min(n, b0 + batch_size)
+            off = self.offsets[b0:b1 + 1]
+            s0, s1 = int(off[0].item()), int(off[-1].item())
+            yield DeviceMiniBatch(self.ids[b0:b1], self.labels[b0:b1], off - s0,
+                                  self.slots[s0:s1], self.signs[s0:s1])
+
     def to_numpy(self) -> dict[str, np.ndarray]:
         n, m = self.counters.instances, self.counters.signs
         return {"ids": self.ids[:n].cpu().numpy().view(np.uint64),
@@ -349,6 +362,18 @@ class CsrBatch:
                 "offsets": self.offsets[: n + 1].cpu().numpy().view(np.uint64),
                 "slots": self.slots[:m].cpu().numpy().view(np.uint16),
                 "signs": self.signs[:m].cpu().numpy().view(np.uint64)}
+
+
+@dataclass
+class DeviceMiniBatch:
+    """One emitted mini-batch in HBM (MiniBatch, pipeline.py:357-369): CSR of
+    (slot u16, sign u64) per instance, rows in emission order."""
+
+    ids: object      # torch int64 (u64 bits) [b]
+    labels: object   # torch uint8 [b]
+    offsets: object  # torch int64 [b + 1], offsets[0] == 0
+    slots: object    # torch int16 (u16 bits)
+    signs: object    # torch int64 (u64 bits)
 
 
 def _next_pow2(n: int) -> int:
@@ -704,6 +729,25 @@ class Engine:
     def run(self, row_lo: int, row_hi: int) -> CsrBatch:
         self.launch(row_lo, row_hi)
         return self.finish()
+
+    def capture_run(self, n_rows: int):
+        """A whole device-resident run -- the run-state reset, the id-set clear
+        and every launch over rows [0, n_rows) of the bound driver -- captured
+        into one CUDA graph (the serving loop replays it; the stage chain of
+        run_pipelined, pipeline.py:901-1094, becomes one graph launch).
+        Replay with ``g.replay()``, then ``finish()``."""
+        torch = self.torch
+        self.reserve(n_rows, self.max_rows)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            self.begin_run(n_rows)
+            for lo in range(0, n_rows, self.max_rows):
+                self.launch(lo, min(lo + self.max_rows, n_rows),
+                            stream=side.cuda_stream, tile_base=lo // self.ir.chunk)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        return g
 
 
 class StreamedRun:

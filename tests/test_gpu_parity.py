@@ -211,3 +211,55 @@ def torch_equal_prefix(a, b):
     n = min(a.numel(), b.numel())
     la = a.numel() if a.numel() < b.numel() else n
     return bool((a[:la] == b[:la]).all())
+
+
+def test_device_minibatches_match_reference_batches(goldens):
+    """CsrBatch.minibatches: the _Emitter's cut (every batch_size instances across
+    chunks), as device views; concatenated they are the run's CSR."""
+    from paper_2210_07768_b200 import engine as E
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.workloads import workload_config
+    c, d = corpus(20000, 2000, 7)
+    views = {"user_events": c.driver, "user_profile": c.profile}
+    cfg = config_from_dict(workload_config("default"), d)
+    eng = E.Engine(E.prepare(cfg, views, c.basic), views, c.basic)
+    eng.bind_driver(E.DeviceView(c.driver))
+    eng.reserve(c.driver.row_count)
+    eng.begin_run(c.driver.row_count)
+    eng.launch(0, c.driver.row_count, tile_base=0)
+    batch = eng.finish()
+    full = batch.to_numpy()
+    mbs = list(batch.minibatches(cfg.batch_size))
+    n = batch.counters.instances
+    assert len(mbs) == -(-n // cfg.batch_size)
+    assert sum(int(mb.ids.numel()) for mb in mbs) == n
+    signs = np.concatenate([mb.signs.cpu().numpy().view(np.uint64) for mb in mbs])
+    np.testing.assert_array_equal(signs, full["signs"])
+    for k, mb in enumerate(mbs[:5]):
+        o = mb.offsets.cpu().numpy()
+        b0 = k * cfg.batch_size
+        np.testing.assert_array_equal(o, full["offsets"][b0:b0 + len(o)].astype(np.int64)
+                                      - int(full["offsets"][b0]))
+
+
+def test_captured_run_graph_replays_bit_exact(goldens):
+    """Engine.capture_run: reset + launches as one CUDA graph; every replay
+    reproduces the reference digest and CSR."""
+    from paper_2210_07768_b200 import engine as E
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.workloads import workload_config
+    c, d = corpus(20000, 2000, 7)
+    views = {"user_events": c.driver, "user_profile": c.profile}
+    cfg = config_from_dict(workload_config("sign_heavy"), d)
+    eng = E.Engine(E.prepare(cfg, views, c.basic), views, c.basic, max_rows_per_launch=8192)
+    eng.bind_driver(E.DeviceView(c.driver))
+    g = eng.capture_run(c.driver.row_count)
+    gold = golden_run(goldens, 20000, 7, "sign_heavy")
+    ref = _run(20000, 2000, 7, "sign_heavy").csr
+    for _ in range(3):
+        g.replay()
+        res = eng.finish()
+        assert f"0x{res.counters.digest:016x}" == gold["digest"]
+        got = res.to_numpy()
+        for k in ("ids", "offsets", "signs"):
+            np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
