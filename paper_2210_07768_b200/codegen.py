@@ -238,6 +238,8 @@ class PlanCodegen:
         self.json_kind = False
         self._ids_tail: list[str] = []
         self.pf_slot: dict[int, int] = {}
+        self.prefetched: dict[tuple, str] = {}
+        self.defer_gathers = os.environ.get("FBX_DEFER_GATHERS", "1") != "0"
         self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
         self.persistent = os.environ.get("FBX_PERSISTENT", "0") != "0"  # measured slower (r1)
         self.early_order = os.environ.get("FBX_EARLY_ORDER", "0") != "0"  # measured ~1% slower (r1)
@@ -592,6 +594,17 @@ class PlanCodegen:
             v = V(t, g.fresh(f"s{k}_{name}_"), True)
             self.decl(v)
             nul = g.p(f"side{k}.{name}.nulls", "const u8*")
+            pre = self.prefetched.pop((k, name, row), None)
+            if pre is not None:  # raw words loaded before the DAG: only the arithmetic here
+                g(f"{v.c}_n = ({pre}_nb >> ({row} & 7u)) & 1u;")
+                if kind is Kind.INT64:
+                    g(f"{v.c} = {pre}_v;")
+                elif kind is Kind.FLOAT32:
+                    g(f"{v.c} = fbx::f32_canon_bits({pre}_v);")
+                else:
+                    data = g.p(f"side{k}.{name}.data", "const u8*")
+                    g(f"{v.c} = fbx::Str{{{data} + {pre}_o0, {pre}_o1 - {pre}_o0}};")
+                return v
             g(f"{v.c}_n = fbx::null_bit({nul}, {row});")
             if kind is Kind.INT64:
                 g(f"{v.c} = fbx::ldg_u64({g.p(f'side{k}.{name}.data', 'const u64*')} + {row});")
@@ -605,6 +618,27 @@ class PlanCodegen:
                   f" {v.c} = fbx::Str{{{data} + o0, o1 - o0}}; }}")
             return v
         return load
+
+    def prefetch_side_column(self, k: int, view: ViewIR, name: str, row: str):
+        """Issue the raw loads of a joined column before the DAG (no arithmetic on
+        them, so no warp waits here); the first reader does the rest."""
+        g = self.g
+        ext = {e.output for e in view.extractions}
+        if name in ext or name not in view.kinds or (k, name, row) in self.prefetched:
+            return
+        kind = view.kinds[name]
+        pre = g.fresh(f"pg{k}_")
+        nul = g.p(f"side{k}.{name}.nulls", "const u8*")
+        g(f"const u32 {pre}_nb = fbx::ldg_u8({nul} + ({row} >> 3));")
+        if kind is Kind.INT64:
+            g(f"const u64 {pre}_v = fbx::ldg_u64({g.p(f'side{k}.{name}.data', 'const u64*')} + {row});")
+        elif kind is Kind.FLOAT32:
+            g(f"const u32 {pre}_v = fbx::ldg_u32({g.p(f'side{k}.{name}.data', 'const u32*')} + {row});")
+        else:
+            offs = g.p(f"side{k}.{name}.offsets", "const u32*")
+            g(f"const u32 {pre}_o0 = fbx::ldg_u32({offs} + {row}), {pre}_o1 = "
+              f"fbx::ldg_u32({offs} + {row} + 1);")
+        self.prefetched[(k, name, row)] = pre
 
     def side_value(self, k: int, view: ViewIR, name: str, row: str) -> V:
         """Cleaned value of side column `name` at side row `row` (gather)."""
@@ -1207,10 +1241,17 @@ class PlanCodegen:
         used_cols = set(ir.features)
         for nd in ir.nodes:
             used_cols |= set(nd.inputs)
-        g("// ---- gathers of joined side / basic columns (issued before the DAG) ----")
+        g("// ---- gathers of joined side / basic columns: loads issued before the DAG,")
+        g("// their arithmetic at the first reader (driver-only nodes hide the latency)")
         for c in sorted(used_cols):
             if isinstance(env.get(c), tuple):
-                self.col(c, {})
+                if self.defer_gathers:
+                    _, k, cc = env[c]
+                    view = ir.sides[k] if k < len(ir.sides) else ir.basic
+                    row = self.side_rows[k] if k < len(self.side_rows) else f"sr{k}"
+                    self.prefetch_side_column(k, view, cc, row)
+                else:
+                    self.col(c, {})
         # ---- emission order decided BEFORE the DAG ----------------------------------
         feats_early = sorted(ir.features.items(), key=lambda kv: (kv[1], kv[0]))
         pnulls = (self.predict_feature_nulls(feats_early)
