@@ -226,13 +226,10 @@ class PlanCodegen:
         if len(ir.features) > 64:
             raise UnsupportedOnDevice("more than 64 emitted features")
         import os
-        # CTAs per SM (sets the register budget): 3 x 512 threads (<= 40 regs)
-        # when the tile's CSR staging fits a third of the SM's shared memory,
-        # else 2 (64 regs) -- both measured on B200 (profiles/r1_*.md)
-        k = max(1, len(ir.features))
-        need = self.nt * (17 + 10 * k) + 64
-        default_mb = 3 if need <= (227 * 1024) // 3 - STATIC_SMEM_EST - 1024 else 2
-        default_mb = max(1, min(default_mb, 2048 // self.nt))
+        # CTAs per SM (sets the register budget): 2 x 512 threads at 64 registers.
+        # 3 (<= 40 registers) spills 160-340 B/thread and measured 2-4 % slower on
+        # every Appendix-B DAG (round 1), so it is only reachable via the knob.
+        default_mb = max(1, min(2, 2048 // self.nt))
         self.min_blocks = int(os.environ.get("FBX_MIN_BLOCKS", str(default_mb)))
         self.pool_sites = 0
         self.json_kind = False
@@ -240,6 +237,11 @@ class PlanCodegen:
         self.pf_slot: dict[int, int] = {}
         self.prefetched: dict[tuple, str] = {}
         self.defer_gathers = os.environ.get("FBX_DEFER_GATHERS", "1") != "0"
+        # work-balanced warps (rows sorted by string bytes): measured 1-3 % faster on
+        # sign_heavy / default / fig4 / cross_heavy, 10 % slower on lookup_heavy
+        # (latency-bound dictionary probes, scattered rows) -> off for lookup plans
+        has_lookup = any(nd.fn.op == "lookup" for nd in ir.nodes)
+        self.sort_rows = os.environ.get("FBX_SORT_ROWS", "0" if has_lookup else "1") != "0"
         self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
         self.persistent = os.environ.get("FBX_PERSISTENT", "0") != "0"  # measured slower (r1)
         self.early_order = os.environ.get("FBX_EARLY_ORDER", "0") != "0"  # measured ~1% slower (r1)
@@ -1093,8 +1095,46 @@ class PlanCodegen:
         g(f"const u64 chunk = CHUNK0 + {bid};")
         g(f"const u64 row0 = ROW_LO + (u64){bid} * {ir.chunk}ull;")
         g(f"const u64 row_end = (row0 + {ir.chunk}ull < ROW_HI) ? row0 + {ir.chunk}ull : ROW_HI;")
-        g("const u64 srow = row0 + threadIdx.x;")
-        g(f"const bool inrange = threadIdx.x < {ir.chunk}u && srow < row_end;")
+        if self.sort_rows and self.staged:
+            # work-balanced warps: threads take the chunk's rows in order of their
+            # string bytes (a 128-bucket counting sort), so the lanes of a warp run
+            # the per-byte loops (JSON, tokens, FNV) for similar trip counts.  The
+            # emission order is by instance id, independent of this mapping.
+            g("u32 RT;  // the chunk row this thread works on")
+            g("{")
+            g("__shared__ u32 srt_h[128]; __shared__ u16 srt_p[NT];")
+            g("for (u32 q = threadIdx.x; q < 128u; q += NT) srt_h[q] = 0u;")
+            g("u32 L = 0u;")
+            g(f"const bool in0 = threadIdx.x < {ir.chunk}u && row0 + threadIdx.x < row_end;")
+            g("if (in0) {")
+            for c in self.staged:
+                offs = g.p(f"drv.{c}.offsets", "const u32*")
+                g(f"L += fbx::ldg_u32({offs} + row0 + threadIdx.x + 1) - fbx::ldg_u32({offs} + row0 + threadIdx.x);")
+            g("}")
+            g("const u32 key = in0 ? (L >> 1 < 126u ? L >> 1 : 126u) : 127u;")
+            g("__syncthreads();")
+            g("const u32 pos = atomicAdd(&srt_h[key], 1u);")
+            g("__syncthreads();")
+            g("if (threadIdx.x < 32u) {  // exclusive scan of the 128 buckets")
+            g("const u32 a0 = srt_h[4 * threadIdx.x], a1 = srt_h[4 * threadIdx.x + 1], "
+              "a2 = srt_h[4 * threadIdx.x + 2], a3 = srt_h[4 * threadIdx.x + 3];")
+            g("u32 t = a0 + a1 + a2 + a3, x = t;")
+            g("#pragma unroll")
+            g("for (int d = 1; d < 32; d <<= 1) { const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, d); "
+              "if (threadIdx.x >= (u32)d) x += y; }")
+            g("x -= t;")
+            g("srt_h[4 * threadIdx.x] = x; srt_h[4 * threadIdx.x + 1] = x + a0; "
+              "srt_h[4 * threadIdx.x + 2] = x + a0 + a1; srt_h[4 * threadIdx.x + 3] = x + a0 + a1 + a2;")
+            g("}")
+            g("__syncthreads();")
+            g("srt_p[srt_h[key] + pos] = (u16)threadIdx.x;")
+            g("__syncthreads();")
+            g("RT = srt_p[threadIdx.x];")
+            g("}")
+        else:
+            g("const u32 RT = threadIdx.x;")
+        g("const u64 srow = row0 + RT;")
+        g(f"const bool inrange = RT < {ir.chunk}u && srow < row_end;")
         g("const u64 row = inrange ? srow : row0;")
         g("bool alive = inrange;")
         g("u32 malformed = 0, filtered = 0;")
