@@ -1794,6 +1794,7 @@ class PlanCodegen:
         rank_bytes = max(24 * self.nt, 10 * self.nt + 8192)  # bitonic 3*NT u64 | radix
         self.dyn_smem = max(self.span_cap, rank_bytes,
                             min(need, per_cta, OUT_BUDGET)) // 16 * 16
+        self.dyn_smem = max(self.dyn_smem, (self.span_cap + 16 + 15) // 16 * 16)  # read slack
         if self.early_order:  # the pre-DAG rank pass lives behind the staged spans
             self.dyn_smem = max(self.dyn_smem, (self.span_cap + rank_bytes + 15) // 16 * 16)
         # first probe slots of int-keyed tables land behind the staged spans

@@ -73,8 +73,9 @@ struct Fnv {
   FBX_DI void u64_le(u64 v) { word_le((u32)v); word_le((u32)(v >> 32)); }
   FBX_DI void u16_le(u32 v) { mul(lo ^ (v & 0xFFu)); mul(lo ^ ((v >> 8) & 0xFFu)); }
   // arbitrary byte span.  Reads whole aligned 32-bit words and funnel-shifts
-  // them into place; a word past the last byte is only touched when the span
-  // really extends into it, so staged shared-memory spans are never overrun.
+  // them into place.  The word after the last byte may be read: every span the
+  // kernels hash (staged shared-memory spans, padded HBM segments, the pool,
+  // constants) has >= 16 readable bytes of slack (FBX_EXACT_READS: never).
   template <bool LOWER>
   FBX_DI void bytes_t(const u8* p, u32 n) {
     if (n == 0) return;
@@ -85,15 +86,23 @@ struct Fnv {
     u32 lo_w = wp[0];
     for (u32 k = 0; k < nw; ++k) {
       // the next word is needed when the span continues into it
+#ifdef FBX_EXACT_READS
       const bool need = sh || (4u * (k + 1u) < n);
       u32 nxt = need ? wp[k + 1] : 0u;
+#else
+      u32 nxt = wp[k + 1];  // may be one word past the span: every span has >= 16 B slack
+#endif
       u32 w = __funnelshift_r(lo_w, nxt, sh);
       if (LOWER) w = lower_word(w);
       word_le(w);
       lo_w = nxt;
     }
     if (r) {
+#ifdef FBX_EXACT_READS
       u32 hi_w = (sh + r * 8u > 32u) ? wp[nw + 1] : 0u;
+#else
+      u32 hi_w = wp[nw + 1];
+#endif
       u32 w = __funnelshift_r(lo_w, hi_w, sh);
       if (LOWER) w = lower_word(w);
       mul(lo ^ (w & 0xFFu));
@@ -195,8 +204,12 @@ struct WordCursor {
   }
   FBX_DI u32 word(u32 k) const {  // bytes [k, k+4) (k % 4 == 0), bytes past n are garbage
     const u32 lo = wp[k >> 2];
+#ifdef FBX_EXACT_READS
     const bool need = sh && (k + 4u - sh / 8u) < n;  // next word holds span bytes
     const u32 hi = need ? wp[(k >> 2) + 1] : 0u;
+#else
+    const u32 hi = wp[(k >> 2) + 1];  // every span has >= 16 B of readable slack
+#endif
     return __funnelshift_r(lo, hi, sh);
   }
 };
