@@ -107,8 +107,9 @@ def compile_source(source: str, name: str = "plan.cu", options: tuple[str, ...] 
     cpath = cache_dir / f"{key}.cubin"
     if cpath.exists():
         data = cpath.read_bytes()
-        _CUBIN_CACHE[key] = data
-        return data
+        if data[:4] == b"\x7fELF":  # else a damaged entry: recompile
+            _CUBIN_CACHE[key] = data
+            return data
     L = lib()
     arr = (ctypes.c_char_p * len(opts))(*[o.encode() for o in opts])
     img = ctypes.c_void_p()
@@ -123,7 +124,7 @@ def compile_source(source: str, name: str = "plan.cu", options: tuple[str, ...] 
     _CUBIN_CACHE[key] = data
     try:
         cache_dir.mkdir(parents=True, exist_ok=True)
-        tmp = cpath.with_suffix(".tmp")
+        tmp = cpath.with_suffix(f".{os.getpid()}.tmp")  # ranks compile concurrently
         tmp.write_bytes(data)
         tmp.replace(cpath)
     except OSError:
