@@ -58,6 +58,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--dag", default="sign_heavy")
+    ap.add_argument("--batch-size", type=int, default=512,
+                    help="driver chunk (the reference's batch_size); the goldens are for 512")
     ap.add_argument("--rows", type=int, default=1_000_000)
     ap.add_argument("--users", type=int, default=5000)
     ap.add_argument("--seed", type=int, default=11)
@@ -213,7 +215,7 @@ def main():
         seeds = [args.shard_seed0 + k for k in range(args.shards) if k % world == rank]
     else:
         seeds = [args.seed + rank]
-    raw = workload_config(args.dag)
+    raw = workload_config(args.dag, batch_size=args.batch_size)
     t0 = time.time()
     shards, gen_s, prep_s = [], 0.0, 0.0
     for sd in seeds:
@@ -259,6 +261,7 @@ def main():
     results = [e.finish().counters for _, e, _, _ in shards]
     c = results[0]
     if (args.rows == 1_000_000 and args.users == 5000 and args.seed == 11 and rank == 0
+            and args.batch_size == 512
             and not args.shards):
         want = GOLDEN_1M.get(args.dag)
         if want and (c.digest, c.instances, c.signs) != want:
@@ -482,7 +485,7 @@ def reference_arm(args, rank, world):
     corpus = make_corpus(min(rows, args.rows), args.users, args.seed)
     tmp = Path(tempfile.mkdtemp(prefix="fbxref"))
     write_corpus(corpus, tmp)
-    raw = workload_config(args.dag)
+    raw = workload_config(args.dag, batch_size=args.batch_size)
     if args.dag == "lookup_heavy":
         write_lookup_tables(tmp, args.users)
     rates = []

@@ -226,10 +226,11 @@ class PlanCodegen:
         if len(ir.features) > 64:
             raise UnsupportedOnDevice("more than 64 emitted features")
         import os
-        # CTAs per SM (sets the register budget): 2 x 512 threads at 64 registers.
+        # CTAs per SM (sets the register budget): 1024 threads per SM at 64 registers
+        # (2 x 512 for the reference's batch_size 512).
         # 3 (<= 40 registers) spills 160-340 B/thread and measured 2-4 % slower on
         # every Appendix-B DAG (round 1), so it is only reachable via the knob.
-        default_mb = max(1, min(2, 2048 // self.nt))
+        default_mb = max(1, min(32, 1024 // self.nt))  # 1024 threads / SM at 64 registers
         self.min_blocks = int(os.environ.get("FBX_MIN_BLOCKS", str(default_mb)))
         self.pool_sites = 0
         self.json_kind = False
