@@ -263,3 +263,18 @@ def test_captured_run_graph_replays_bit_exact(goldens):
         got = res.to_numpy()
         for k in ("ids", "offsets", "signs"):
             np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+
+
+def test_reproduces_the_reference_published_100k_run(tmp_path):
+    """The reference's own acceptance run (tests/test_acceptance.py: gen_corpus(rows=100_000,
+    users=5_000, seed=11), its default pipeline.json, run_pipelined) published digest
+    0xb2bcd7004cff26a0, 90,326 instances, 177 batches, 517,976 signs
+    (pkg/test_output.txt:19, 25): reproduced end to end on the device."""
+    from paper_2210_07768_b200 import load_config, run_pipelined
+    from paper_2210_07768_b200.corpus import gen_corpus
+    paths = gen_corpus(tmp_path, rows=100_000, users=5_000, seed=11)
+    report = run_pipelined(load_config(paths["config"]))
+    assert report.digest == 0xB2BCD7004CFF26A0
+    assert report.instances == 90326
+    assert report.signs == 517976
+    assert report.batches == 177
