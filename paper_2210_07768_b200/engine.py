@@ -644,7 +644,8 @@ class Engine:
         look-back continues across launches), the CSR for every row, and a
         bump pool sized for the largest launch."""
         torch = self.torch
-        launch_rows = rows if launch_rows is None else launch_rows
+        # no launch of this run covers more than its rows: size the pool for that
+        launch_rows = rows if launch_rows is None else max(1, min(launch_rows, rows))
         tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
         k = max(1, len(self.ir.features))
         need = (tiles, rows, k, launch_rows)
