@@ -1358,14 +1358,12 @@ class PlanCodegen:
         g(f"u64* IDS = {g.p('idset', 'u64*')}; const u64 IMASK = {g.p('idset_mask')};")
         g("u64 ids_slot = IMASK + 1; unsigned long long ids_old = 0ull;")
         g(f"const bool ids_on = alive && !{idv.n};")
-        g("if (ids_on) {")
-        g(f"if ({idv.c} == 0ull) {{")
-        g("ids_old = atomicAdd((unsigned long long*)&IDS[IMASK + 1], 1ull);")
-        g("} else {")
-        g(f"ids_slot = ({idv.c} * 0x9E3779B97F4A7C15ull) >> 20 & IMASK;")
-        g(f"ids_old = atomicCAS((unsigned long long*)&IDS[ids_slot], 0ull, (unsigned long long){idv.c});")
-        g("}")
-        g("}")
+        g("// one CAS for every id (id 0 -> its own slot, set 0 -> 1); no result copy")
+        g(f"if ({idv.c} != 0ull) ids_slot = ({idv.c} * 0x9E3779B97F4A7C15ull) >> 20 & IMASK;")
+        g("// rows that do not take part CAS a private dummy word (0 -> 0): no branch, so")
+        g("// the result is never merged / copied right after the atomic")
+        g(f"ids_old = atomicCAS((unsigned long long*)&IDS[ids_on ? ids_slot : IMASK + 2 + (row & 1023u)], "
+          f"0ull, !ids_on ? 0ull : ({idv.c} == 0ull ? 1ull : (unsigned long long){idv.c}));")
         self._ids_tail = [
             "// ---- check_unique_ids: resolve the id-set insertion issued at the merge ----",
             "if (ids_on) {",

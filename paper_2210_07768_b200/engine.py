@@ -620,7 +620,8 @@ class Engine:
                                 self.status.numel(), self._stream())
         cap = _next_pow2(2 * max(rows_hint, 1))
         if self.idset is None or self._idset_cap < cap:
-            self.idset = torch.zeros(cap + 2, dtype=torch.int64, device=self.device)
+            # + 2: the id-0 slot; + 1024: the dummy words of rows that do not insert
+            self.idset = torch.zeros(cap + 2 + 1024, dtype=torch.int64, device=self.device)
             # winner chunk per slot (no reset: read only for claimed slots) and the
             # later-occurrence chunk pairs (only written when an id repeats)
             self.idset_w = torch.empty(cap + 2, dtype=torch.int32, device=self.device)
