@@ -243,6 +243,8 @@ class PlanCodegen:
         # (latency-bound dictionary probes, scattered rows) -> off for lookup plans
         has_lookup = any(nd.fn.op == "lookup" for nd in ir.nodes)
         self.sort_rows = os.environ.get("FBX_SORT_ROWS", "0" if has_lookup else "1") != "0"
+        self.dict_prefetch = os.environ.get("FBX_DICT_PREFETCH", "1") != "0"
+        self.dict_pf: dict[str, tuple] = {}
         self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
         self.persistent = os.environ.get("FBX_PERSISTENT", "0") != "0"  # measured slower (r1)
         self.early_order = os.environ.get("FBX_EARLY_ORDER", "0") != "0"  # measured ~1% slower (r1)
@@ -860,9 +862,17 @@ class PlanCodegen:
             cond = f"alive && !{s.n}" if s.nullable else "alive"
             lone = f" && !{s.l}" if s.lone else ""
             g(f"if ({cond}{lone}) {{")
-            g(f"{out.c} = fbx::dict_lookup({g.p(f'dict{ti}.slots', 'const fbx::Slot*')}, "
-              f"{g.p(f'dict{ti}.mask')}, {g.p(f'dict{ti}.keys', 'const u8*')}, {s.c}, "
-              f"{_u64(dflt)});")
+            if nd.name in self.dict_pf:
+                _, _, off = self.dict_pf[nd.name]
+                tag = f"dpf_{nd.name.replace('.', '_')}"
+                g("fbx::cp_async_wait_all();")
+                g(f"{out.c} = fbx::dict_lookup_pf({g.p(f'dict{ti}.slots', 'const fbx::Slot*')}, "
+                  f"{g.p(f'dict{ti}.mask')}, {g.p(f'dict{ti}.keys', 'const u8*')}, {s.c}, "
+                  f"{_u64(dflt)}, {tag}, (const fbx::Slot*)(dyn_smem + {off}u + 32u * threadIdx.x));")
+            else:
+                g(f"{out.c} = fbx::dict_lookup({g.p(f'dict{ti}.slots', 'const fbx::Slot*')}, "
+                  f"{g.p(f'dict{ti}.mask')}, {g.p(f'dict{ti}.keys', 'const u8*')}, {s.c}, "
+                  f"{_u64(dflt)});")
             g("}")
             return out
         if op == "hash":
@@ -1018,6 +1028,32 @@ class PlanCodegen:
             out.append(bk)
         return out
 
+    def staged_columns(self) -> list[str]:
+        ir = self.ir
+        drv = ir.driver
+        needed = self.driver_needed()
+        return ([c for c, k in drv.kinds.items() if k.var_length and c in needed]
+                if ir.stage_strings else [])[:16]
+
+    def dict_prefetch_nodes(self) -> list[tuple[str, str, int]]:
+        """lookup pre-ops keyed directly by a (filled) driver string column: their
+        first dictionary slot is copied to shared memory right after the span
+        staging lands, so the probe does not wait on HBM (query_dict: 1e7 keys)."""
+        ir = self.ir
+        drv = ir.driver
+        ext_out = {e.output for e in drv.extractions}
+        out = []
+        for nd in ir.nodes:
+            if nd.role != "pre" or nd.fn.op != "lookup" or len(nd.inputs) != 1:
+                continue
+            c = nd.inputs[0]
+            k = drv.kinds.get(c)
+            if (k not in (Kind.UTF8, Kind.JSON) or c in ext_out or c in ir.producer
+                    or c not in self.staged):
+                continue
+            out.append((nd.name, c, ir.tables[nd.fn.table]))
+        return out
+
     def prefetch(self, k: int, keys: list[V], kinds: list[Kind], name: str) -> str:
         """Prologue: hash the raw key and load the first probe slot."""
         g = self.g
@@ -1047,8 +1083,7 @@ class PlanCodegen:
         drv = ir.driver
         dk = drv.cleaned_kinds()
         needed = self.driver_needed()
-        self.staged = ([c for c, k in drv.kinds.items() if k.var_length and c in needed]
-                       if ir.stage_strings else [])[:16]
+        self.staged = self.staged_columns()
         feats = sorted(ir.features.items(), key=lambda kv: (kv[1], kv[0]))
         K = max(1, len(feats))
         g(f"constexpr int NT = {nt};")
@@ -1223,6 +1258,31 @@ class PlanCodegen:
                 g("fbx::mbar_wait(&sm.bar, bar_phase); bar_phase ^= 1u;")
             else:
                 g("fbx::mbar_wait(&sm.bar, 0u);")
+        if self.dict_pf:
+            g("// first dictionary slot of every lookup keyed by a driver string column,")
+            g("// fetched now (cp.async) so the probe after the JSON finds it in smem")
+            for name, (c, t, off) in self.dict_pf.items():
+                v = raw[c]
+                tag = f"dpf_{name.replace('.', '_')}"
+                g(f"u64 {tag} = 0ull;")
+                fills = self.ir.driver.fills
+                if c in fills:
+                    b = str(fills[c]).encode("utf-8", "surrogatepass")
+                    kc = g.const(b)
+                    key = f"({v.n} ? fbx::Str{{{kc}, {len(b)}u}} : {v.c})"
+                    cond = "inrange"
+                else:
+                    key = v.c
+                    cond = f"inrange && !{v.n}"
+                g(f"if ({cond}) {{")
+                g(f"const fbx::Str kk = {key};")
+                g(f"{tag} = fbx::table_tag(fbx::tbl_hash_bytes(0x5DB2CEB4C16A9E87ull, kk.p, kk.n));")
+                g(f"const fbx::Slot* sl = {g.p(f'dict{t}.slots', 'const fbx::Slot*')} + "
+                  f"({tag} & {g.p(f'dict{t}.mask')});")
+                g(f"u8* dst = dyn_smem + {off}u + 32u * threadIdx.x;")
+                g("fbx::cp_async16(dst, sl); fbx::cp_async16(dst + 16, (const u8*)sl + 16);")
+                g("}")
+            g("fbx::cp_async_commit();")
         # ---- clean ------------------------------------------------------------------
         if self.phase_timers:
             g("FBX_PHASE(0);")
@@ -1804,6 +1864,14 @@ class PlanCodegen:
             if pf and pf_need <= max(self.dyn_smem, per_cta):
                 self.pf_slot = {k: j for j, k in enumerate(pf)}
                 self.dyn_smem = max(self.dyn_smem, pf_need) // 16 * 16
+            self.staged = self.staged_columns()
+            dpf = self.dict_prefetch_nodes() if self.dict_prefetch else []
+            base = self.span_cap + 16 * self.nt * len(self.pf_slot)
+            d_need = base + 32 * self.nt * len(dpf)
+            if dpf and d_need <= max(self.dyn_smem, per_cta):
+                self.dict_pf = {name: (c, t, base + 32 * self.nt * j)
+                                for j, (name, c, t) in enumerate(dpf)}
+                self.dyn_smem = max(self.dyn_smem, d_need) // 16 * 16
         self.g.slot("state")  # slot 0
         if ir.mode == "extract":
             kname = self.extract_rows_kernel()

@@ -1174,6 +1174,28 @@ FBX_DI u64 dict_lookup(const Slot* slots, u64 mask, const u8* keyblob, Str key, 
   }
 }
 
+// dict_lookup whose first slot (tag already computed) was copied into shared
+// memory by cp.async in the prologue (raw driver-column keys)
+FBX_DI u64 dict_lookup_pf(const Slot* slots, u64 mask, const u8* keyblob, Str key, u64 dflt,
+                          u64 tag, const Slot* first) {
+  const u64 pre = load_prefix8(key.p, key.n);
+  u64 i = tag & mask;
+  const Slot* s = first;
+  while (true) {
+    const u64 t = s->tag;
+    if (t == 0) return dflt;
+    if (t == tag && s->aux == key.n && s->pad == pre) {
+      bool eq = true;
+      const u32 ref = s->ref;
+      for (u32 k = 8; k < key.n; ++k)
+        if (__ldg(keyblob + ref + k) != key.p[k]) { eq = false; break; }
+      if (eq) return s->value;
+    }
+    i = (i + 1) & mask;
+    s = slots + i;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // JSON (CPython json.loads, strict=True) validation + dot-path extraction.
 // Leaves are reported for up to NP paths of up to 8 segments each.
