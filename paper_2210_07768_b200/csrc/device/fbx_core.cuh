@@ -953,18 +953,27 @@ FBX_DI u64 load_prefix8(const u8* p, u32 n) {
   const u32 sh = (u32)(a & 3u) * 8u;
   const u32* wp = (const u32*)(a & ~3ull);
   const u32 m = n < 8u ? n : 8u;
+#ifdef FBX_EXACT_READS
   const u32 last = ((u32)(a & 3u) + m - 1u) >> 2;  // last word index touched
   u32 w0 = wp[0];
   u32 w1 = last >= 1u ? wp[1] : 0u;
   u32 w2 = last >= 2u ? wp[2] : 0u;
+#else
+  const u32 w0 = wp[0], w1 = wp[1], w2 = wp[2];  // spans keep >= 16 B of readable slack
+#endif
   u32 lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
   u64 v = ((u64)hi << 32) | lo;
   return m == 8u ? v : (v & ((1ull << (m * 8u)) - 1ull));
 }
+// table hash of a byte key: one multiply-xorshift per 8-byte word, one full
+// avalanche at the end (the same function builds and probes every table)
 FBX_DI u64 tbl_hash_bytes(u64 h, const u8* p, u32 n) {
-  h = mix64(h ^ ((u64)n * 0x9E3779B97F4A7C15ull));
-  for (u32 k = 0; k < n; k += 8u) h = mix64(h ^ load_prefix8(p + k, n - k));
-  return h;
+  h ^= (u64)n * 0x9E3779B97F4A7C15ull;
+  for (u32 k = 0; k < n; k += 8u) {
+    h = (h ^ load_prefix8(p + k, n - k)) * 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 31;
+  }
+  return mix64(h);
 }
 FBX_DI u64 tbl_hash_u64(u64 h, u64 v) { return mix64(h ^ mix64(v)); }
 
@@ -1166,8 +1175,8 @@ FBX_DI u64 dict_lookup(const Slot* slots, u64 mask, const u8* keyblob, Str key, 
     if (t == tag && __ldg(&s->aux) == key.n && __ldg(&s->pad) == pre) {
       bool eq = true;
       u32 ref = __ldg(&s->ref);
-      for (u32 k = 8; k < key.n; ++k)
-        if (__ldg(keyblob + ref + k) != key.p[k]) { eq = false; break; }
+      for (u32 k = 8; k < key.n && eq; k += 8u)
+        eq = load_prefix8(keyblob + ref + k, key.n - k) == load_prefix8(key.p + k, key.n - k);
       if (eq) return __ldg(&s->value);
     }
     i = (i + 1) & mask;
@@ -1187,8 +1196,8 @@ FBX_DI u64 dict_lookup_pf(const Slot* slots, u64 mask, const u8* keyblob, Str ke
     if (t == tag && s->aux == key.n && s->pad == pre) {
       bool eq = true;
       const u32 ref = s->ref;
-      for (u32 k = 8; k < key.n; ++k)
-        if (__ldg(keyblob + ref + k) != key.p[k]) { eq = false; break; }
+      for (u32 k = 8; k < key.n && eq; k += 8u)
+        eq = load_prefix8(keyblob + ref + k, key.n - k) == load_prefix8(key.p + k, key.n - k);
       if (eq) return s->value;
     }
     i = (i + 1) & mask;
