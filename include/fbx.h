@@ -68,6 +68,12 @@ int fbx_launch(fbx_kernel* k, unsigned grid, unsigned block, unsigned dyn_smem, 
 int fbx_state_reset(fbx_state* d_state, unsigned long long* d_tile_status, size_t n_tiles,
                     void* stream);
 
+/* Clear check_unique_ids' run-wide id set (viewpipe.py:562-576 `seen`, pipeline.py:
+ * 1071) for a new run, and its later-occurrence pairs only when the previous run's
+ * state says an id repeated (decided on the device; call BEFORE fbx_state_reset). */
+int fbx_idset_clear(unsigned long long* d_ids, size_t n_words, unsigned long long* d_pairs,
+                    size_t n_pair_words, const fbx_state* d_state, void* stream);
+
 /* Reset the per-launch part of the run state -- the bump-pool head (ArenaPool.reset,
  * mempool.py:136) and the persistent kernel's tile ticket -- between the launches of
  * one run, whose counters keep accumulating. */

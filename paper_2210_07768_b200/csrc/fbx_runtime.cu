@@ -99,6 +99,20 @@ __global__ void k_state_reset(fbx_state* st, unsigned long long* status, size_t 
   for (; i < n; i += (size_t)gridDim.x * blockDim.x) status[i] = 0ull;
 }
 
+// id set of check_unique_ids cleared for a new run; the later-occurrence pairs
+// only if the previous run saw a repeated id (read on the device: no host sync)
+__global__ void k_idset_clear(unsigned long long* ids, size_t n, unsigned long long* pairs,
+                              size_t np, const fbx_state* st) {
+  const bool dirty = st->dup_seen != 0ull;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    ids[i] = 0ull;
+  if (dirty)
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np;
+         i += (size_t)gridDim.x * blockDim.x)
+      pairs[i] = 0ull;
+}
+
 // run-state snapshot into host-mapped pinned memory: a kernel store, not a
 // copy-engine transfer, so it never queues behind the bulk D2H of a previous slice
 __global__ void k_state_snapshot(const unsigned long long* st, volatile unsigned long long* dst,
@@ -427,6 +441,13 @@ int fbx_state_reset(fbx_state* d_state, unsigned long long* d_status, size_t n_t
   if (blocks > 1184) blocks = 1184;
   k_state_reset<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_state, d_status, n_tiles);
   return cuda_check(cudaGetLastError(), "fbx_state_reset");
+}
+
+int fbx_idset_clear(unsigned long long* d_ids, size_t n_words, unsigned long long* d_pairs,
+                    size_t n_pair_words, const fbx_state* d_state, void* stream) {
+  k_idset_clear<<<1184, 256, 0, (cudaStream_t)stream>>>(d_ids, n_words, d_pairs, n_pair_words,
+                                                        d_state);
+  return cuda_check(cudaGetLastError(), "fbx_idset_clear");
 }
 
 int fbx_pool_reset(fbx_state* d_state, void* stream) {

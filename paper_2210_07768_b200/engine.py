@@ -615,9 +615,6 @@ class Engine:
         `seen`), the counters / error word, and -- for a reserved run -- the
         look-back status of every tile."""
         torch = self.torch
-        if getattr(self, "status", None) is not None:
-            runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(),
-                                self.status.numel(), self._stream())
         cap = _next_pow2(2 * max(rows_hint, 1))
         if self.idset is None or self._idset_cap < cap:
             # + 2: the id-0 slot; + 1024: the dummy words of rows that do not insert
@@ -627,13 +624,16 @@ class Engine:
             self.idset_w = torch.empty(cap + 2, dtype=torch.int32, device=self.device)
             self.idset_d = torch.zeros(cap + 2, dtype=torch.int64, device=self.device)
             self._idset_cap = cap
-            self._dup_dirty = False
         else:
-            self.idset.zero_()
-            if self._dup_dirty:
-                self.idset_d.zero_()
-        # unknown until finish() reads dup_seen (a run abandoned early stays dirty)
-        self._dup_dirty = True
+            # one launch: the id set, and the pairs only if the previous run's state
+            # (still in place: cleared just below) recorded a repeated id
+            runtime.idset_clear(self.idset.data_ptr(), self.idset.numel(),
+                                self.idset_d.data_ptr(), self.idset_d.numel(),
+                                self.state.data_ptr(), self._stream())
+        if getattr(self, "status", None) is not None:
+            runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(),
+                                self.status.numel(), self._stream())
+        self._dup_dirty = False
         self._set("idset", self.idset.data_ptr())
         self._set("idset_mask", self._idset_cap - 1)
         self._set("idset_w", self.idset_w.data_ptr())

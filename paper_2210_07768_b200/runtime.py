@@ -32,7 +32,7 @@ EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_prog
            "fbx_kernel_set_max_dynamic_smem", "fbx_launch", "fbx_state_reset",
            "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
            "fbx_dup_resolve", "fbx_state_snapshot",
-           "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words")
+           "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words", "fbx_idset_clear")
 
 
 class FbxError(RuntimeError):
@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
             L.fbx_dup_resolve.argtypes = [vp, vp, ctypes.c_ulonglong, vp, vp]
             L.fbx_state_snapshot.argtypes = [vp, vp, vp]
             L.fbx_pool_reset.argtypes = [vp, vp]
+            L.fbx_idset_clear.argtypes = [vp, sz, vp, sz, vp, vp]
             L.fbx_crc32.argtypes = [vp, ctypes.c_ulonglong, vp, vp, vp]
             L.fbx_crc32_scratch_words.argtypes = [ctypes.c_ulonglong]
             L.fbx_crc32_scratch_words.restype = ctypes.c_ulonglong
@@ -176,6 +177,12 @@ def state_reset(d_state: int, d_status: int, n_tiles: int, stream: int):
 def state_snapshot(d_state: int, h_mapped: int, stream: int):
     _check(lib().fbx_state_snapshot(ctypes.c_void_p(d_state), ctypes.c_void_p(h_mapped),
                                     ctypes.c_void_p(stream)), "state snapshot")
+
+
+def idset_clear(d_ids: int, n: int, d_pairs: int, npairs: int, d_state: int, stream: int):
+    _check(lib().fbx_idset_clear(ctypes.c_void_p(d_ids), int(n), ctypes.c_void_p(d_pairs),
+                                 int(npairs), ctypes.c_void_p(d_state), ctypes.c_void_p(stream)),
+           "id-set clear")
 
 
 def pool_reset(d_state: int, stream: int):

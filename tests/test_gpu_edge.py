@@ -516,3 +516,39 @@ def test_float32_str_repr_matches_oracle(tmp_path):
     assert (got.report.digest, got.report.signs) == (ref.digest, ref.signs)
     np.testing.assert_array_equal(got.csr["slots"], np.array(ref.slots, np.uint16))
     np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
+
+
+def test_engine_reused_after_a_duplicate_id_run(tmp_path):
+    """A run that fails on a repeated instance id leaves its later-occurrence pairs
+    dirty; the next run on the same engine clears them on the device
+    (fbx_idset_clear reads the previous run's dup flag) and is exact."""
+    from paper_2210_07768_b200 import engine as E
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+    from paper_2210_07768_b200.config import StageError, config_from_dict
+    drv, prof, bas = _views(2000, 5)
+    ids = drv.columns["instance_id"].to_pylist()
+    bad_ids = list(ids)
+    for i in range(1000, 1100):
+        bad_ids[i] = bad_ids[999]
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    raw = _config(512, ops, {"c": 3}, filt="age != -12345")
+    _write_views(tmp_path, drv, prof, bas)
+    cfg = config_from_dict(raw, tmp_path)
+    views = {"ev": drv, "pr": prof}
+    eng = E.Engine(E.prepare(cfg, views, bas), views, bas)
+    bad = drv.project(list(drv.order))
+    bad.columns["instance_id"] = ColumnImage.from_values(Kind.INT64, bad_ids)
+    for view, expect_fail in ((bad, True), (drv, False), (bad, True), (drv, False)):
+        eng.bind_driver(E.DeviceView(view))
+        eng.reserve(view.row_count)
+        eng.begin_run(view.row_count)
+        eng.launch(0, view.row_count, tile_base=0)
+        if expect_fail:
+            with pytest.raises(StageError):
+                eng.finish()
+        else:
+            got = eng.finish().counters
+            tables, sizes = O.load_tables(raw.get("tables", {}), tmp_path)
+            ref = O.run_pipelined(raw, views, bas, tables, sizes)
+            assert (got.digest, got.instances, got.signs) == (ref.digest, ref.instances,
+                                                              ref.signs)
