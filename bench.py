@@ -244,8 +244,7 @@ def main():
     def run_shard(eng, n, ev=None):
         """One pass over a shard: clear the run's id set, then launches of at
         most --launch-rows rows with the look-back continuing across them."""
-        eng.begin_run(n)
-        launches[0] += 1  # fbx_state_reset (k_state_reset)
+        launches[0] += eng.begin_run(n)  # k_idset_clear + k_state_reset
         if ev is not None:
             ev[0].record(stream)
         for lo in range(0, n, eng.max_rows):

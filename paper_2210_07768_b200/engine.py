@@ -610,11 +610,13 @@ class Engine:
         chunk = int(hit[0]) + self._chunk_minus_tile
         return (chunk << 32) | (codegen.STAGE["merge"] << 28) | sub
 
-    def begin_run(self, rows_hint: int):
+    def begin_run(self, rows_hint: int) -> int:
         """Start a run: clear the run-wide instance-id set (check_unique_ids'
         `seen`), the counters / error word, and -- for a reserved run -- the
-        look-back status of every tile."""
+        look-back status of every tile.  Returns the number of libfbx kernels
+        it launched."""
         torch = self.torch
+        nk = 0
         cap = _next_pow2(2 * max(rows_hint, 1))
         if self.idset is None or self._idset_cap < cap:
             # + 2: the id-0 slot; + 1024: the dummy words of rows that do not insert
@@ -630,15 +632,18 @@ class Engine:
             runtime.idset_clear(self.idset.data_ptr(), self.idset.numel(),
                                 self.idset_d.data_ptr(), self.idset_d.numel(),
                                 self.state.data_ptr(), self._stream())
+            nk += 1
         if getattr(self, "status", None) is not None:
             runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(),
                                 self.status.numel(), self._stream())
+            nk += 1
         self._dup_dirty = False
         self._set("idset", self.idset.data_ptr())
         self._set("idset_mask", self._idset_cap - 1)
         self._set("idset_w", self.idset_w.data_ptr())
         self._set("idset_d", self.idset_d.data_ptr())
         self._run_tiles = 0
+        return nk
 
     def reserve(self, rows: int, launch_rows: int | None = None):
         """Run-wide buffers: look-back status for every tile of the run (the
