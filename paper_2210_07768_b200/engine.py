@@ -711,7 +711,8 @@ class Engine:
             # continuation of a reserved run: counters / digest / error word keep
             # accumulating across launches; only the bump pool is reset
             tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
-            runtime.pool_reset(self.state.data_ptr(), stream)
+            if tile_base > 0:  # the run's first launch follows begin_run's full reset
+                runtime.pool_reset(self.state.data_ptr(), stream)
         self._set("row_lo", row_lo)
         self._set("row_hi", row_hi)
         self._set("chunk0", row_lo // self.ir.chunk)
