@@ -128,3 +128,40 @@ def test_random_dag_matches_oracle(seed):
     np.testing.assert_array_equal(got.csr["offsets"], np.array(ref.offsets, np.uint64))
     np.testing.assert_array_equal(got.csr["slots"], np.array(ref.slots, np.uint16))
     np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FBX_RANDOM_DAGS", "24")) // 2))
+def test_random_dag_on_adversarial_records(seed, tmp_path):
+    """Random DAGs over the adversarial records of test_gpu_edge (Unicode / ragged
+    queries, escaped and malformed JSON, nulls, int / float corner values)."""
+    import test_gpu_edge as E
+    from paper_2210_07768_b200.config import ConfigError
+    global STR_COLS, INT_COLS, F32_COLS
+    saved = (STR_COLS, INT_COLS, F32_COLS)
+    STR_COLS, INT_COLS, F32_COLS = ["query", "cx", "city"], ["age", "user_id", "tier"], ["score"]
+    try:
+        ops, feats = random_dag(1000 + seed)
+    finally:
+        STR_COLS, INT_COLS, F32_COLS = saved
+    feats.pop("basic_b", None)
+    feats = {k: (9 if k == "basic_a" else v) for k, v in feats.items()}
+    drv, prof, bas = E._views(2500, 50 + seed)
+    E._write_views(tmp_path, drv, prof, bas)
+    raw = E._config([512, 64, 7][seed % 3], ops, feats, filt="age != -12345")
+    raw["tables"] = {}
+    for op in ops:  # the adversarial corpus has no dictionaries: lookups become trims
+        for p in op.get("pre", []):
+            if p["fn"].startswith("lookup:"):
+                p["fn"] = "trim"
+    try:
+        ref, ref_err, got, got_err = E._run_both(raw, drv, prof, bas, tmp_path)
+    except ConfigError:
+        pytest.skip("generated config rejected")
+    if ref_err is not None:
+        assert got_err is not None, f"oracle failed ({ref_err}), engine did not"
+        assert getattr(got_err, "stage", None) == ref_err.stage, (got_err, ref_err)
+        return
+    assert got_err is None, got_err
+    assert (got.report.digest, got.report.instances, got.report.signs) == \
+        (ref.digest, ref.instances, ref.signs)
+    np.testing.assert_array_equal(got.csr["signs"], np.array(ref.values, np.uint64))
