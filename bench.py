@@ -248,7 +248,7 @@ def main():
         if ev is not None:
             ev[0].record(stream)
         for lo in range(0, n, eng.max_rows):
-            eng.launch(lo, min(lo + eng.max_rows, n), tile_base=lo // eng.ir.chunk)
+            eng.launch(lo, min(lo + eng.max_rows, n), tile_base=eng.tile_of_row(lo))
             launches[0] += 1  # fbx_pipeline
         if ev is not None:
             ev[1].record(stream)

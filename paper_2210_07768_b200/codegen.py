@@ -125,6 +125,7 @@ class Program:
     int_keyed: tuple[int, ...] = ()   # tables with 16-B fbx::ISlot slots
     persistent_ctas_per_sm: int = 0   # >0: fbx_pipeline takes tiles from a ticket
     json_kind: bool = False           # Json-kind extraction: canonical JSON into the pool
+    tiles_per_chunk: int = 1          # > 1: chunk cut into 512-row sub-tiles (merged after)
 
 
 # ---------------------------------------------------------------------------
@@ -217,11 +218,13 @@ class PlanCodegen:
         self.ir = ir
         self.g = Gen()
         self.notes: list[str] = []
-        if ir.chunk > 1024:
-            raise UnsupportedOnDevice(
-                f"batch_size {ir.chunk} > 1024: one CTA per chunk is the only emission "
-                "order implemented on device")
-        self.nt = 1 << (max(32, ir.chunk) - 1).bit_length()  # power of two
+        # A chunk (batch_size rows) is one CTA up to 1024 rows.  Larger chunks are cut
+        # into sub-tiles of 512 rows (tiles_per_chunk of them, the last ones possibly
+        # empty); each sub-tile emits its rows sorted by id and the engine merges the
+        # sub-tiles of every chunk afterwards (Engine._merge_big_chunks).
+        self.tile_rows = ir.chunk if ir.chunk <= 1024 else 512
+        self.spc = -(-ir.chunk // self.tile_rows)  # sub-tiles per chunk
+        self.nt = 1 << (max(32, self.tile_rows) - 1).bit_length()  # power of two
         self.nsort = self.nt
         if len(ir.features) > 64:
             raise UnsupportedOnDevice("more than 64 emitted features")
@@ -1112,7 +1115,7 @@ class PlanCodegen:
             g("// every predecessor a look-back waits on is held by a running CTA, no wave")
             g("// tail, and the shared state is set up once")
             g("__shared__ u32 sm_ltile;")
-            g(f"const u32 NTILES = (u32)((ROW_HI - ROW_LO + {ir.chunk - 1}ull) / {ir.chunk}ull);")
+            g(f"const u32 NTILES = (u32)((ROW_HI - ROW_LO + {ir.chunk - 1}ull) / {ir.chunk}ull) * {self.spc}u;")
             if self.staged:
                 g("if (threadIdx.x == 0) fbx::mbar_init(&sm.bar, 1u);")
             g("u32 bar_phase = 0u;")
@@ -1128,9 +1131,19 @@ class PlanCodegen:
             g("// predecessor a look-back waits on is resident or done (as CUB relies on)")
             bid = "blockIdx.x"
         g(f"const u32 tile = (u32){g.p('tile_base')} + {bid};  // run-global tile id")
-        g(f"const u64 chunk = CHUNK0 + {bid};")
-        g(f"const u64 row0 = ROW_LO + (u64){bid} * {ir.chunk}ull;")
-        g(f"const u64 row_end = (row0 + {ir.chunk}ull < ROW_HI) ? row0 + {ir.chunk}ull : ROW_HI;")
+        if self.spc == 1:
+            g(f"const u64 chunk = CHUNK0 + {bid};")
+            g(f"const u64 row0 = ROW_LO + (u64){bid} * {ir.chunk}ull;")
+            g(f"const u64 row_end = (row0 + {ir.chunk}ull < ROW_HI) ? row0 + {ir.chunk}ull : ROW_HI;")
+        else:
+            g(f"// sub-tile {bid} % {self.spc} of chunk {bid} / {self.spc} ({self.tile_rows} rows each)")
+            g(f"const u64 chunk = CHUNK0 + {bid} / {self.spc}u;")
+            g(f"const u64 cend0 = ROW_LO + (u64)({bid} / {self.spc}u + 1u) * {ir.chunk}ull;")
+            g("const u64 cend = cend0 < ROW_HI ? cend0 : ROW_HI;")
+            g(f"const u64 row0s = ROW_LO + (u64)({bid} / {self.spc}u) * {ir.chunk}ull + "
+              f"(u64)({bid} % {self.spc}u) * {self.tile_rows}ull;")
+            g("const u64 row0 = row0s < cend ? row0s : cend;")
+            g(f"const u64 row_end = (row0 + {self.tile_rows}ull < cend) ? row0 + {self.tile_rows}ull : cend;")
         if self.sort_rows and self.staged:
             # work-balanced warps: threads take the chunk's rows in order of their
             # string bytes (a 128-bucket counting sort), so the lanes of a warp run
@@ -1141,7 +1154,7 @@ class PlanCodegen:
             g("__shared__ u32 srt_h[128]; __shared__ u16 srt_p[NT];")
             g("for (u32 q = threadIdx.x; q < 128u; q += NT) srt_h[q] = 0u;")
             g("u32 L = 0u;")
-            g(f"const bool in0 = threadIdx.x < {ir.chunk}u && row0 + threadIdx.x < row_end;")
+            g(f"const bool in0 = threadIdx.x < {self.tile_rows}u && row0 + threadIdx.x < row_end;")
             g("if (in0) {")
             for c in self.staged:
                 offs = g.p(f"drv.{c}.offsets", "const u32*")
@@ -1170,7 +1183,7 @@ class PlanCodegen:
         else:
             g("const u32 RT = threadIdx.x;")
         g("const u64 srow = row0 + RT;")
-        g(f"const bool inrange = RT < {ir.chunk}u && srow < row_end;")
+        g(f"const bool inrange = RT < {self.tile_rows}u && srow < row_end;")
         g("const u64 row = inrange ? srow : row0;")
         g("bool alive = inrange;")
         g("u32 malformed = 0, filtered = 0;")
@@ -1208,11 +1221,11 @@ class PlanCodegen:
         # at the end of this tile (their offsets are L2 hits by then)
         pf_cols = [(c, k) for c, k in drv.kinds.items() if c in needed]
         pf_dist = 148 * self.min_blocks
-        if self.prefetch_next:
+        if self.prefetch_next and self.spc == 1:
             g(f"const u32 PF_TILE = {bid} + {pf_dist}u;")
             g(f"const bool pf_on = threadIdx.x == 0 && PF_TILE + 1u < gridDim.x;")
             g("if (pf_on) {")
-            g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {ir.chunk}ull, p1 = p0 + {ir.chunk}ull;")
+            g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {self.tile_rows}ull, p1 = p0 + {self.tile_rows}ull;")
             for c, k in pf_cols:
                 g(f"fbx::prefetch_span({g.p(f'drv.{c}.nulls', 'const u8*')} + (p0 >> 3), ((p1 - p0) >> 3) + 1);")
                 if k.var_length:
@@ -1531,6 +1544,11 @@ class PlanCodegen:
         g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
         g("const u64 ei = sm.ex_inst, es = sm.ex_signs;")
         g(f"if (emit_bad) fbx::raise_emit(ST, ei + myrank, {ir.chunk}u, emit_bad == 2u, {lab.c});")
+        # sub-tiled chunks: the merge re-places label failures from the final order,
+        # so a bad label is marked in the emitted label byte (0xFE null, 0xFF range;
+        # such a run fails, its CSR is never handed out)
+        labx = (f"(emit_bad ? (u8)(0xFDu + emit_bad) : (u8)({lab.c}))" if self.spc > 1
+                else f"(u8)({lab.c})")
         g("u8* const st_sign = dyn_smem + ((u64)(O_SIGN + es) & 15u);")
         g("u8* const st_slot = st_sign + ((8u * tile_signs + 15u) & ~15u) + 16u - ((u64)(O_SIGN + es) & 15u) + ((u64)(O_SLOT + es) & 15u);")
         g("u8* const st_ids = st_slot + ((2u * tile_signs + 15u) & ~15u) + 16u - ((u64)(O_SLOT + es) & 15u) + ((u64)(O_IDS + ei) & 15u);")
@@ -1541,7 +1559,7 @@ class PlanCodegen:
         g("u64* s_sign = (u64*)st_sign; u16* s_slot = (u16*)st_slot;")
         g("const u32 r = myrank;")
         g("u32 so = myoff;")
-        g(f"((u64*)st_ids)[r] = {idv.c}; st_lab[r] = (u8)({lab.c}); ((u64*)st_off)[r] = es + so;")
+        g(f"((u64*)st_ids)[r] = {idv.c}; st_lab[r] = {labx}; ((u64*)st_off)[r] = es + so;")
         for q, (slot, _) in enumerate(fv):
             g(f"if ((fpres >> {q}) & 1u) {{ s_slot[so] = (u16){slot}u; s_sign[so] = fsg[{q}]; ++so; }}")
         g("}")
@@ -1558,7 +1576,7 @@ class PlanCodegen:
         g("} else if (alive) {")
         g("const u64 pos = ei + myrank;")
         g("u64 so = es + myoff;")
-        g(f"O_IDS[pos] = {idv.c}; O_LAB[pos] = (u8)({lab.c});")
+        g(f"O_IDS[pos] = {idv.c}; O_LAB[pos] = {labx};")
         g("O_OFF[pos] = so;")
         for q, (slot, _) in enumerate(fv):
             g(f"if ((fpres >> {q}) & 1u) {{ O_SLOT[so] = (u16){slot}u; O_SIGN[so] = fsg[{q}]; ++so; }}")
@@ -1566,9 +1584,9 @@ class PlanCodegen:
         g("if (threadIdx.x == 0) O_OFF[ei + n_inst] = es + tile_signs;")
         for line in self._ids_tail:
             g(line)
-        if self.prefetch_next and self._pf_tail:
+        if self.prefetch_next and self._pf_tail and self.spc == 1:
             g("if (pf_on) {")
-            g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {ir.chunk}ull, p1 = p0 + {ir.chunk}ull;")
+            g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {self.tile_rows}ull, p1 = p0 + {self.tile_rows}ull;")
             for line in self._pf_tail:
                 g(line)
             g("}")
@@ -1901,7 +1919,7 @@ class PlanCodegen:
         nt_ = len(ir.sides) + (1 if ir.basic is not None else 0)
         return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes,
                        tuple(k for k in range(nt_) if self.int_keyed(k)),
-                       self.min_blocks if self.persistent else 0, self.json_kind)
+                       self.min_blocks if self.persistent else 0, self.json_kind, self.spc)
 
 
 def _filter_columns(expr) -> set[str]:

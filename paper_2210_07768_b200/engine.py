@@ -552,7 +552,9 @@ class Engine:
                 if dk < key:
                     key, detail = dk, did
             if st.get("emit_key", ~0 & ((1 << 64) - 1)) != (1 << 64) - 1:
-                ek = self._emit_error_key(st["emit_key"])
+                ek = st.get("emit_key_resolved")
+                if ek is None:
+                    ek = self._emit_error_key(st["emit_key"])
                 if ek < key:
                     key, detail = ek, st["emit_detail"]
         if key == (1 << 64) - 1:
@@ -592,6 +594,63 @@ class Engine:
             ident = 0
         key = (chunk << 32) | (codegen.STAGE["merge"] << 28) | codegen.ERR["dup_id"]
         return key, ident
+
+    def _merge_big_chunks(self, st: dict):
+        """batch_size > 1024: every chunk was emitted as sorted 512-row sub-tiles;
+        re-order each chunk's instances by ascending u64 id (a stable two-key sort
+        on the device) and rebuild offsets / slots / signs.  Label failures are then
+        placed from the final order (the kernel marked bad labels 0xFE / 0xFF)."""
+        torch = self.torch
+        n, m = int(st["instances"]), int(st["signs"])
+        if n == 0:
+            return
+        spc, bs = self.prog.tiles_per_chunk, self.ir.chunk
+        words = self.status[: self._run_tiles].cpu().numpy().view(np.uint64)
+        incl = ((words >> np.uint64(34)) & np.uint64(0xFFFFFFF)).astype(np.int64)
+        nch = -(-self._run_tiles // spc)
+        ends = np.array([incl[min((c + 1) * spc, self._run_tiles) - 1] for c in range(nch)],
+                        dtype=np.int64)
+        counts = np.diff(np.concatenate([[0], ends]))
+        dev = self.device
+        ids = self.o_ids[:n]
+        chunk_of = torch.repeat_interleave(torch.arange(nch, device=dev),
+                                           torch.from_numpy(counts).to(dev))
+        key = ids ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=dev)  # u64 order
+        p1 = torch.sort(key, stable=True).indices
+        perm = p1[torch.sort(chunk_of[p1], stable=True).indices]
+        off = self.o_off[: n + 1]
+        lens = off[1:] - off[:-1]
+        self.o_ids[:n] = ids[perm]
+        labels = self.o_lab[:n][perm]
+        self.o_lab[:n] = labels
+        # a repeated id (the run fails) ties two rows' ranks and leaves an instance
+        # slot unwritten: only a consistent CSR is re-ordered
+        if bool(((lens >= 0).all() & (lens.sum() == m)).item()):
+            new_lens = lens[perm]
+            new_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+            new_off[1:] = torch.cumsum(new_lens, 0)
+            seg = torch.repeat_interleave(torch.arange(n, device=dev), new_lens)
+            src = off[:-1][perm][seg] + (torch.arange(m, device=dev) - new_off[:-1][seg])
+            self.o_slot[:m] = self.o_slot[:m][src]
+            self.o_sign[:m] = self.o_sign[:m][src]
+            self.o_off[: n + 1] = new_off
+        elif not (st["dup_seen"] or st["error_key"] != (1 << 64) - 1):
+            raise RuntimeError("inconsistent CSR after a run without failures")
+        if st.get("emit_key", (1 << 64) - 1) != (1 << 64) - 1:
+            bad = torch.nonzero(labels >= 0xFE)
+            if bad.numel():
+                p = int(bad[0, 0].item())
+                rng = int(labels[p].item()) == 0xFF
+                batch, pos = p // bs, p % bs
+                code = codegen.ERR["label_range" if rng else "null_label"]
+                sub = (((1 + rng) & 0xFF) << 20) | ((pos & 0xFFF) << 8) | code
+                hit = np.nonzero(ends >= (batch + 1) * bs)[0]
+                if hit.size == 0:
+                    key = (0xFFFFFFFF << 32) | (codegen.STAGE["emit"] << 28) | sub
+                else:
+                    chunk = int(hit[0]) + self._run_chunk0
+                    key = (chunk << 32) | (codegen.STAGE["merge"] << 28) | sub
+                st["emit_key_resolved"] = key
 
     def _emit_error_key(self, ek: int) -> int:
         """Map a label error at emission position (batch b) to the chunk whose
@@ -652,7 +711,7 @@ class Engine:
         torch = self.torch
         # no launch of this run covers more than its rows: size the pool for that
         launch_rows = rows if launch_rows is None else max(1, min(launch_rows, rows))
-        tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
+        tiles = self.tiles_for(rows)
         k = max(1, len(self.ir.features))
         need = (tiles, rows, k, launch_rows)
         if getattr(self, "_arena_key", None) != need:
@@ -681,7 +740,16 @@ class Engine:
         return tiles
 
     def _arena(self, rows: int):
-        return self.reserve(rows)
+        self.reserve(rows)
+        return self.tiles_for(rows)
+
+    def tiles_for(self, rows: int) -> int:
+        """Look-back tiles of `rows` driver rows (chunks x sub-tiles per chunk)."""
+        return -(-rows // self.ir.chunk) * self.prog.tiles_per_chunk
+
+    def tile_of_row(self, row: int) -> int:
+        """Run-global tile id of the chunk that starts at driver row `row`."""
+        return (row // self.ir.chunk) * self.prog.tiles_per_chunk
 
     def bind_driver(self, dview: DeviceView):
         for c in dview.tensors:
@@ -710,7 +778,7 @@ class Engine:
         else:
             # continuation of a reserved run: counters / digest / error word keep
             # accumulating across launches; only the bump pool is reset
-            tiles = (rows + self.ir.chunk - 1) // self.ir.chunk
+            tiles = self.tiles_for(rows)
             if tile_base > 0:  # the run's first launch follows begin_run's full reset
                 runtime.pool_reset(self.state.data_ptr(), stream)
         self._set("row_lo", row_lo)
@@ -718,6 +786,7 @@ class Engine:
         self._set("chunk0", row_lo // self.ir.chunk)
         self._set("tile_base", tile_base)
         self._chunk_minus_tile = row_lo // self.ir.chunk - tile_base
+        self._run_chunk0 = row_lo // self.ir.chunk - tile_base // self.prog.tiles_per_chunk
         self._run_tiles = tile_base + tiles
         grid = tiles
         if self.prog.persistent_ctas_per_sm:
@@ -729,6 +798,8 @@ class Engine:
     def finish(self) -> CsrBatch:
         """Synchronise, read counters, raise the first error in pipeline order."""
         st = self._read_state()
+        if self.prog.tiles_per_chunk > 1:
+            self._merge_big_chunks(st)
         self.check_run(st)
         c = Counters(st["digest"], st["instances"], st["signs"], st["malformed"],
                      st["filtered"], st["joined"], 1)
@@ -753,7 +824,7 @@ class Engine:
             self.begin_run(n_rows)
             for lo in range(0, n_rows, self.max_rows):
                 self.launch(lo, min(lo + self.max_rows, n_rows),
-                            stream=side.cuda_stream, tile_base=lo // self.ir.chunk)
+                            stream=side.cuda_stream, tile_base=self.tile_of_row(lo))
         torch.cuda.current_stream(self.device).wait_stream(side)
         return g
 
@@ -776,6 +847,9 @@ class StreamedRun:
                  zero_copy: bool = False, taper: bool = True, sink: str = "host"):
         torch = eng.torch
         self.eng, self.torch = eng, torch
+        if eng.prog.tiles_per_chunk > 1:
+            raise UnsupportedOnDevice("streamed runs need batch_size <= 1024 (larger chunks are "
+                                      "merged after the run: use Engine / run_pipelined)")
         chunk = eng.ir.chunk
         self.slice_rows = max(chunk, slice_rows - slice_rows % chunk)
         self.n = n = host_view.row_count
@@ -909,7 +983,7 @@ class StreamedRun:
                                        self.s_comp.cuda_stream)
                 comp_done[k].record(self.s_comp)
                 mark("k1", k, self.s_comp)
-            tiles_before += (hi - lo + eng.ir.chunk - 1) // eng.ir.chunk
+            tiles_before += eng.tiles_for(hi - lo)
 
     def finish(self) -> Counters:
         """Drain the run started by ``start``: per slice, wait for its kernel,
@@ -1001,7 +1075,7 @@ class StreamedRun:
                 self.s_comp.wait_event(h2d_done[k])
                 eng.launch(lo, hi, self.s_comp.cuda_stream, tile_base=tiles_before)
                 comp_done[k].record(self.s_comp)
-            tiles_before += (hi - lo + eng.ir.chunk - 1) // eng.ir.chunk
+            tiles_before += eng.tiles_for(hi - lo)
         self.s_comp.synchronize()
         st = eng._read_state()
         eng.check_run(st)

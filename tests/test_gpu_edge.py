@@ -136,7 +136,8 @@ def _write_views(tmp, drv, prof, bas):
     write_view(bas, tmp / "basic.fbxc")
 
 
-@pytest.mark.parametrize("batch_size,seed", [(512, 1), (64, 2), (7, 3), (1000, 4)])
+@pytest.mark.parametrize("batch_size,seed", [(512, 1), (64, 2), (7, 3), (1000, 4), (2048, 5),
+                                             (5000, 6)])
 def test_adversarial_records_match_oracle(batch_size, seed, tmp_path):
     drv, prof, bas = _views(3000, seed)
     _write_views(tmp_path, drv, prof, bas)
@@ -389,7 +390,7 @@ PLACEMENT = {  # rows chosen among those that reach the merge in _views(2000, 5)
 
 
 @pytest.mark.parametrize("case", sorted(PLACEMENT))
-@pytest.mark.parametrize("batch_size", [512, 100])
+@pytest.mark.parametrize("batch_size", [512, 100, 1500])
 def test_failure_placement_matches_reference(case, batch_size, tmp_path):
     ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
     raw = _config(batch_size, ops, {"c": 3}, filt="age != -12345")

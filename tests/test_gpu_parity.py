@@ -280,3 +280,24 @@ def test_reproduces_the_reference_published_100k_run(tmp_path):
     assert report.instances == 90326
     assert report.signs == 517976
     assert report.batches == 177
+
+
+@pytest.mark.parametrize("batch_size", [20_000, 100_000, 1025, 4096])
+def test_batch_size_beyond_a_cta(batch_size):
+    """SPEC.md:499 (reference): batch_size >= corpus size -> exactly one batch; and any
+    batch_size > 1024 (chunks cut into 512-row sub-tiles, merged by instance id)."""
+    import featurebox_oracle as O
+    res = _run(20000, 2000, 7, "sign_heavy", batch_size=batch_size, max_rows_per_launch=8192)
+    from paper_2210_07768_b200.workloads import workload_config
+    c, d = corpus(20000, 2000, 7)
+    raw = workload_config("sign_heavy", batch_size=batch_size)
+    tables, sizes = O.load_tables(raw.get("tables", {}), d)
+    ref = O.run_pipelined(raw, {"user_events": c.driver, "user_profile": c.profile}, c.basic,
+                          tables, sizes)
+    assert (res.report.digest, res.report.instances, res.report.signs) == \
+        (ref.digest, ref.instances, ref.signs)
+    assert res.report.batches == -(-ref.instances // batch_size)
+    np.testing.assert_array_equal(res.csr["ids"], np.array(ref.ids, np.uint64))
+    np.testing.assert_array_equal(res.csr["offsets"], np.array(ref.offsets, np.uint64))
+    np.testing.assert_array_equal(res.csr["slots"], np.array(ref.slots, np.uint16))
+    np.testing.assert_array_equal(res.csr["signs"], np.array(ref.values, np.uint64))

@@ -94,7 +94,7 @@ def test_random_dag_matches_oracle(seed):
     from paper_2210_07768_b200.engine import run_views
     from paper_2210_07768_b200.workloads import workload_config
     c, d = corpus(3000, 400, 13 + seed % 3)
-    raw = workload_config("default", batch_size=[512, 256, 100][seed % 3])
+    raw = workload_config("default", batch_size=[512, 256, 100, 3000][seed % 4])
     ops, feats = random_dag(seed)
     raw["operators"] = ops
     raw["emit"] = {"features": feats}

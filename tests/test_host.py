@@ -86,14 +86,20 @@ def test_config_errors_mirror_reference(tmp_path):
 
 def test_unsupported_constructs_are_plan_time_errors():
     c, d = corpus(2000, 300, 7)
-    raw = workload_config("default", batch_size=2048)  # one CTA per chunk: <= 1024 rows
-    with pytest.raises(UnsupportedOnDevice):
-        engine.prepare(config_from_dict(raw, d), compile_program=False)
     raw = workload_config("default")
     raw["views"][0]["clean"]["extract"] += [
         {"source": "meta", "path": f"u.k{i}", "output": f"k{i}", "kind": "utf8"} for i in range(8)]
     with pytest.raises(UnsupportedOnDevice):  # > 8 paths from one JSON source
         engine.prepare(config_from_dict(raw, d), compile_program=False)
+
+
+def test_big_batch_plan_compiles():
+    """batch_size > 1024: 512-row sub-tiles per chunk (merged after the run)."""
+    c, d = corpus(2000, 300, 7)
+    p = engine.prepare(config_from_dict(workload_config("sign_heavy", batch_size=100_000), d),
+                       {"user_events": c.driver, "user_profile": c.profile}, c.basic)
+    assert p.program.tiles_per_chunk == 196 and p.program.threads == 512
+    assert p.cubin[:4] == b"\x7fELF"
 
 
 def test_json_kind_plan_compiles():
