@@ -595,34 +595,39 @@ class Engine:
         key = (chunk << 32) | (codegen.STAGE["merge"] << 28) | codegen.ERR["dup_id"]
         return key, ident
 
-    def _merge_big_chunks(self, st: dict):
-        """batch_size > 1024: every chunk was emitted as sorted 512-row sub-tiles;
-        re-order each chunk's instances by ascending u64 id (a stable two-key sort
-        on the device) and rebuild offsets / slots / signs.  Label failures are then
-        placed from the final order (the kernel marked bad labels 0xFE / 0xFF)."""
-        torch = self.torch
-        n, m = int(st["instances"]), int(st["signs"])
-        if n == 0:
-            return
-        spc, bs = self.prog.tiles_per_chunk, self.ir.chunk
-        words = self.status[: self._run_tiles].cpu().numpy().view(np.uint64)
+    def _chunk_ends(self, t0: int, t1: int) -> np.ndarray:
+        """Run-global inclusive instance counts at the end of every chunk whose
+        sub-tiles are [t0, t1) (look-back status words)."""
+        spc = self.prog.tiles_per_chunk
+        words = self.status[t0:t1].cpu().numpy().view(np.uint64)
         incl = ((words >> np.uint64(34)) & np.uint64(0xFFFFFFF)).astype(np.int64)
-        nch = -(-self._run_tiles // spc)
-        ends = np.array([incl[min((c + 1) * spc, self._run_tiles) - 1] for c in range(nch)],
+        nch = -(-(t1 - t0) // spc)
+        return np.array([incl[min((c + 1) * spc, t1 - t0) - 1] for c in range(nch)],
                         dtype=np.int64)
-        counts = np.diff(np.concatenate([[0], ends]))
+
+    def _merge_range(self, i0: int, i1: int, s0: int, s1: int, t0: int, t1: int,
+                     st: dict, stream=None):
+        """batch_size > 1024: the chunks of tiles [t0, t1) hold instances [i0, i1)
+        and signs [s0, s1), each chunk emitted as sorted 512-row sub-tiles; re-order
+        every chunk's instances by ascending u64 id (a stable two-key sort on the
+        device) and rebuild its offsets / slots / signs in place."""
+        torch = self.torch
+        n, m = i1 - i0, s1 - s0
+        if n <= 0:
+            return
+        ends = self._chunk_ends(t0, t1)
+        counts = np.diff(np.concatenate([[i0], ends]))
         dev = self.device
-        ids = self.o_ids[:n]
-        chunk_of = torch.repeat_interleave(torch.arange(nch, device=dev),
+        ids = self.o_ids[i0:i1]
+        chunk_of = torch.repeat_interleave(torch.arange(len(ends), device=dev),
                                            torch.from_numpy(counts).to(dev))
         key = ids ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=dev)  # u64 order
         p1 = torch.sort(key, stable=True).indices
         perm = p1[torch.sort(chunk_of[p1], stable=True).indices]
-        off = self.o_off[: n + 1]
+        off = self.o_off[i0:i1 + 1] - s0
         lens = off[1:] - off[:-1]
-        self.o_ids[:n] = ids[perm]
-        labels = self.o_lab[:n][perm]
-        self.o_lab[:n] = labels
+        self.o_ids[i0:i1] = ids[perm]
+        self.o_lab[i0:i1] = self.o_lab[i0:i1][perm]
         # a repeated id (the run fails) ties two rows' ranks and leaves an instance
         # slot unwritten: only a consistent CSR is re-ordered
         if bool(((lens >= 0).all() & (lens.sum() == m)).item()):
@@ -631,26 +636,37 @@ class Engine:
             new_off[1:] = torch.cumsum(new_lens, 0)
             seg = torch.repeat_interleave(torch.arange(n, device=dev), new_lens)
             src = off[:-1][perm][seg] + (torch.arange(m, device=dev) - new_off[:-1][seg])
-            self.o_slot[:m] = self.o_slot[:m][src]
-            self.o_sign[:m] = self.o_sign[:m][src]
-            self.o_off[: n + 1] = new_off
+            self.o_slot[s0:s1] = self.o_slot[s0:s1][src]
+            self.o_sign[s0:s1] = self.o_sign[s0:s1][src]
+            self.o_off[i0:i1 + 1] = new_off + s0
         elif not (st["dup_seen"] or st["error_key"] != (1 << 64) - 1):
             raise RuntimeError("inconsistent CSR after a run without failures")
-        if st.get("emit_key", (1 << 64) - 1) != (1 << 64) - 1:
-            bad = torch.nonzero(labels >= 0xFE)
-            if bad.numel():
-                p = int(bad[0, 0].item())
-                rng = int(labels[p].item()) == 0xFF
-                batch, pos = p // bs, p % bs
-                code = codegen.ERR["label_range" if rng else "null_label"]
-                sub = (((1 + rng) & 0xFF) << 20) | ((pos & 0xFFF) << 8) | code
-                hit = np.nonzero(ends >= (batch + 1) * bs)[0]
-                if hit.size == 0:
-                    key = (0xFFFFFFFF << 32) | (codegen.STAGE["emit"] << 28) | sub
-                else:
-                    chunk = int(hit[0]) + self._run_chunk0
-                    key = (chunk << 32) | (codegen.STAGE["merge"] << 28) | sub
-                st["emit_key_resolved"] = key
+
+    def _resolve_big_label_error(self, st: dict):
+        """Place a label failure from the final (merged) order: the kernel marked
+        bad labels 0xFE (null) / 0xFF (not 0/1) in the emitted label byte."""
+        if st.get("emit_key", (1 << 64) - 1) == (1 << 64) - 1:
+            return
+        n, bs = int(st["instances"]), self.ir.chunk
+        bad = self.torch.nonzero(self.o_lab[:n] >= 0xFE)
+        if not bad.numel():
+            return
+        p = int(bad[0, 0].item())
+        rng = int(self.o_lab[p].item()) == 0xFF
+        batch, pos = p // bs, p % bs
+        code = codegen.ERR["label_range" if rng else "null_label"]
+        sub = (((1 + rng) & 0xFF) << 20) | ((pos & 0xFFF) << 8) | code
+        ends = self._chunk_ends(0, self._run_tiles)
+        hit = np.nonzero(ends >= (batch + 1) * bs)[0]
+        if hit.size == 0:
+            key = (0xFFFFFFFF << 32) | (codegen.STAGE["emit"] << 28) | sub
+        else:
+            key = ((int(hit[0]) + self._run_chunk0) << 32) | (codegen.STAGE["merge"] << 28) | sub
+        st["emit_key_resolved"] = key
+
+    def _merge_big_chunks(self, st: dict):
+        self._merge_range(0, int(st["instances"]), 0, int(st["signs"]), 0, self._run_tiles, st)
+        self._resolve_big_label_error(st)
 
     def _emit_error_key(self, ek: int) -> int:
         """Map a label error at emission position (batch b) to the chunk whose
@@ -847,9 +863,6 @@ class StreamedRun:
                  zero_copy: bool = False, taper: bool = True, sink: str = "host"):
         torch = eng.torch
         self.eng, self.torch = eng, torch
-        if eng.prog.tiles_per_chunk > 1:
-            raise UnsupportedOnDevice("streamed runs need batch_size <= 1024 (larger chunks are "
-                                      "merged after the run: use Engine / run_pipelined)")
         chunk = eng.ir.chunk
         self.slice_rows = max(chunk, slice_rows - slice_rows % chunk)
         self.n = n = host_view.row_count
@@ -924,6 +937,9 @@ class StreamedRun:
         if sink not in ("host", "device"):
             raise ValueError("sink must be 'host' or 'device'")
         self.sink = sink
+        if zero_copy and eng.prog.tiles_per_chunk > 1:
+            raise UnsupportedOnDevice("zero-copy streamed runs need batch_size <= 1024 (larger "
+                                      "chunks are merged on the device before their D2H)")
 
     def run(self) -> Counters:
         if self.zero_copy:
@@ -951,6 +967,7 @@ class StreamedRun:
         h2d_done = [torch.cuda.Event() for _ in self.bounds]
         self._trace = trace = [] if self.trace is not None else None
         tiles_before = 0
+        self._slice_tiles = []
 
         def mark(name, k, stream):
             if trace is not None:
@@ -983,6 +1000,7 @@ class StreamedRun:
                                        self.s_comp.cuda_stream)
                 comp_done[k].record(self.s_comp)
                 mark("k1", k, self.s_comp)
+            self._slice_tiles.append((tiles_before, tiles_before + eng.tiles_for(hi - lo)))
             tiles_before += eng.tiles_for(hi - lo)
 
     def finish(self) -> Counters:
@@ -1001,13 +1019,21 @@ class StreamedRun:
             # flush chunk and a repeated id's second chunk may lie in later slices.
             # Counters accumulate over the run's launches: this slice's share.
             ni, ms = stt["instances"] - inst_base, stt["signs"] - sign_base
+            merged = None
+            if eng.prog.tiles_per_chunk > 1:  # batch_size > 1024: merge this slice's chunks
+                t0, t1 = self._slice_tiles[j]
+                with torch.cuda.stream(self.s_comp):
+                    eng._merge_range(inst_base, inst_base + ni, sign_base, sign_base + ms,
+                                     t0, t1, stt)
+                    merged = torch.cuda.Event()
+                    merged.record(self.s_comp)
             if self.sink == "device":
                 inst_base += ni
                 sign_base += ms
                 last = stt
                 continue
             with torch.cuda.stream(self.s_d2h):
-                self.s_d2h.wait_event(comp_done[j])
+                self.s_d2h.wait_event(merged if merged is not None else comp_done[j])
                 mark("d2h0", j, self.s_d2h)
                 o = self.out
                 a, b = inst_base, inst_base + ni
@@ -1031,6 +1057,9 @@ class StreamedRun:
         ev.record(self.s_d2h if self.sink == "host" else self.s_comp)
         self._last_d2h = ev
         # the last snapshot is the run's final state (no extra D2H read)
+        if eng.prog.tiles_per_chunk > 1:
+            self.s_comp.synchronize()
+            eng._resolve_big_label_error(last)
         eng.check_run(last)
         self.d2h_bytes = (tot.instances * 17 + 8 + tot.signs * 10 if self.sink == "host"
                           else runtime.STATE_BYTES * len(self.bounds))

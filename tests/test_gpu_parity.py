@@ -301,3 +301,22 @@ def test_batch_size_beyond_a_cta(batch_size):
     np.testing.assert_array_equal(res.csr["offsets"], np.array(ref.offsets, np.uint64))
     np.testing.assert_array_equal(res.csr["slots"], np.array(ref.slots, np.uint16))
     np.testing.assert_array_equal(res.csr["signs"], np.array(ref.values, np.uint64))
+
+
+@pytest.mark.parametrize("batch_size,slice_rows", [(2048, 4096), (3000, 9000)])
+def test_streamed_run_big_batches(batch_size, slice_rows):
+    """StreamedRun with batch_size > 1024: each slice's chunks are merged on the
+    device before their D2H; equals the device-resident run and the oracle digest."""
+    from paper_2210_07768_b200 import engine as E
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.workloads import workload_config
+    c, d = corpus(20000, 2000, 7)
+    views = {"user_events": c.driver, "user_profile": c.profile}
+    raw = workload_config("cross_heavy", batch_size=batch_size)
+    eng = E.Engine(E.prepare(config_from_dict(raw, d), views, c.basic), views, c.basic)
+    sr = E.StreamedRun(eng, c.driver, slice_rows=slice_rows)
+    tot = sr.run()
+    got = sr.csr(tot)
+    ref = _run(20000, 2000, 7, "cross_heavy", batch_size=batch_size).csr
+    for k in ("ids", "labels", "offsets", "slots", "signs"):
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
