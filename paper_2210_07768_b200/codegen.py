@@ -234,7 +234,7 @@ class PlanCodegen:
         # 3 (<= 40 registers) spills 160-340 B/thread and measured 2-4 % slower on
         # every Appendix-B DAG (round 1), so it is only reachable via the knob.
         default_mb = max(1, min(32, 1024 // self.nt))  # 1024 threads / SM at 64 registers
-        self.min_blocks = int(os.environ.get("FBX_MIN_BLOCKS", str(default_mb)))
+        self.min_blocks = int(os.environ.get("FBX_MIN_BLOCKS") or default_mb)
         self.pool_sites = 0
         self.json_kind = False
         self._ids_tail: list[str] = []
