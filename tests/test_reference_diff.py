@@ -11,6 +11,7 @@ import json
 import os
 import sys
 
+import numpy as np
 import pytest
 
 import featurebox_oracle as O
@@ -21,27 +22,42 @@ pytestmark = pytest.mark.skipif(not reference_available(), reason="reference not
 N = int(os.environ.get("FBX_REFDIFF_DAGS", "16"))
 
 
-def _reference_run(raw: dict, where):
-    """run_pipelined(load_config(cfg.json)) of the reference; (report, None) or (None, stage)."""
+def _ref_modules():
     if str(REFERENCE) not in sys.path:
         sys.path.insert(0, str(REFERENCE))
-    from featurebox.pipeline import StageError, load_config, run_pipelined
+    import featurebox.pipeline as P
     from featurebox.featureops import FeatureConfigError
-    from featurebox.pipeline import ConfigError as RefConfigError
+    return P, FeatureConfigError
+
+
+def _reference_call(raw: dict, where, batches=None):
+    """run_pipelined(load_config(cfg.json)) of the reference (its emitted
+    mini-batches appended to `batches`); raises what the reference raises."""
+    P, _ = _ref_modules()
     path = where / f"refdiff_{os.getpid()}.json"
     path.write_text(json.dumps(raw))
+    orig = P.TrainingSink.consume
+    if batches is not None:
+        def consume(self, batch):
+            batches.append(batch)
+            return orig(self, batch)
+        P.TrainingSink.consume = consume
     try:
-        cfg = load_config(path)
-    except (RefConfigError, FeatureConfigError):
-        return None, "config"
-    try:
-        return run_pipelined(cfg), None
-    except StageError as e:
-        return None, e.stage
-    except (RefConfigError, FeatureConfigError):
-        return None, "config"
+        return P.run_pipelined(P.load_config(path))
     finally:
+        P.TrainingSink.consume = orig
         path.unlink()
+
+
+def _reference_run(raw: dict, where):
+    """(report, None) or (None, failing stage | "config")."""
+    P, FeatureConfigError = _ref_modules()
+    try:
+        return _reference_call(raw, where), None
+    except P.StageError as e:
+        return None, e.stage
+    except (P.ConfigError, FeatureConfigError):
+        return None, "config"
 
 
 def _oracle_run(raw, views, basic, where):
@@ -111,3 +127,87 @@ def test_adversarial_records_oracle_equals_reference(batch_size, seed, tmp_path)
     ref, ref_stage = _reference_run(raw, tmp_path)
     mine, my_stage = _oracle_run(raw, {"ev": drv, "pr": prof}, bas, tmp_path)
     _compare(ref, ref_stage, mine, my_stage)
+
+
+# ---- the GPU edge tests, with the reference in the engine's seat ------------------------
+
+class _RefRun:
+    """The reference's run shaped like engine.run_views(..., collect=True)."""
+
+    def __init__(self, report, batches):
+        ids, labels, offs, slots, signs = [], [], [0], [], []
+        for b in batches:
+            for i in range(len(b)):
+                ids.append(b.ids[i])
+                labels.append(b.labels[i])
+                for sl, sg in b.features[i]:
+                    slots.append(sl)
+                    signs.append(sg)
+                offs.append(len(slots))
+        self.report = report
+        self.csr = {"ids": np.array(ids, np.uint64), "labels": np.array(labels, np.uint8),
+                    "offsets": np.array(offs, np.uint64), "slots": np.array(slots, np.uint16),
+                    "signs": np.array(signs, np.uint64)}
+
+
+def _oracle_vs_reference(raw, drv, prof, bas, tmp):
+    """test_gpu_edge._run_both with the unmodified reference instead of the engine."""
+    tables, sizes = O.load_tables(raw.get("tables", {}), tmp)
+    try:
+        ref, ref_err = O.run_pipelined(raw, {"ev": drv, "pr": prof}, bas, tables, sizes), None
+    except O.OracleError as e:
+        ref, ref_err = None, e
+    P, _ = _ref_modules()
+    batches = []
+    try:
+        got, got_err = _RefRun(_reference_call(raw, tmp, batches), batches), None
+    except P.StageError as e:
+        got, got_err = None, e
+    return ref, ref_err, got, got_err
+
+
+EDGE_TESTS = [  # (test function name, parameter sets)
+    ("test_adversarial_records_match_oracle", [{"batch_size": b, "seed": s} for b, s in
+                                               [(2048, 5), (5000, 6)]]),
+    ("test_json_fuzz_matches_oracle", [{"seed": 21}, {"seed": 22}]),
+    ("test_tokens_long_and_ragged_queries_match_oracle", [{}]),
+    ("test_json_kind_extraction_matches_oracle", [{"seed": 41}, {"seed": 42}]),
+    ("test_filters_match_oracle", "filt"),
+    ("test_type_error_mix_of_str", [{}]),
+    ("test_lone_surrogate_hash_is_encode_error", [{}]),
+    ("test_duplicate_instance_ids", [{}]),
+    ("test_bad_labels", "label"),
+    ("test_failure_placement_matches_reference", "case,batch_size"),
+    ("test_json_float32_leaves_match_oracle", [{}]),
+    ("test_json_float32_overflow_is_stage_error", "bad"),
+    ("test_float32_str_repr_matches_oracle", [{}]),
+]
+
+
+def _edge_cases():
+    import test_gpu_edge as E
+    out = []
+    for name, params in EDGE_TESTS:
+        fn = getattr(E, name)
+        if isinstance(params, str):  # the test's own parametrize marks
+            keys = params.split(",")
+            grids = {m.args[0]: m.args[1] for m in fn.pytestmark if m.name == "parametrize"}
+            combos = [{}]
+            for k in keys:
+                combos = [dict(c, **{k: v}) for c in combos for v in grids[k]]
+            params = combos
+        out += [pytest.param(name, p, id=f"{name[5:]}-{'-'.join(str(v)[:12] for v in p.values())}")
+                for p in params]
+    return out
+
+
+@pytest.mark.parametrize("name,params", _edge_cases())
+def test_edge_case_oracle_equals_reference(name, params, tmp_path, monkeypatch):
+    """Every success / failure assertion of test_gpu_edge evaluated with the oracle
+    as the expectation and the reference as the implementation."""
+    import test_gpu_edge as E
+    import paper_2210_07768_b200.config as C
+    P, _ = _ref_modules()
+    monkeypatch.setattr(E, "_run_both", _oracle_vs_reference)
+    monkeypatch.setattr(C, "StageError", P.StageError)
+    getattr(E, name)(tmp_path=tmp_path, **params)
