@@ -1087,6 +1087,9 @@ FBX_DI void mbar_wait(u64* bar, u32 phase) {
 // status word: flag(2) | instances(28) | signs(34); flag 1 = aggregate,
 // 2 = inclusive prefix.
 // ---------------------------------------------------------------------------
+#ifndef FBX_LB_SLEEP
+#define FBX_LB_SLEEP 64  // ns between polls of an unpublished predecessor
+#endif
 FBX_DI u64 ld_acquire(const u64* p) {
   u64 v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1122,7 +1125,9 @@ FBX_DI void lookback(u64* status, u32 tile, u64 inst, u64 signs, u64* ex_inst, u
     if (idx >= 0) {
       w = ld_acquire(status + idx);
       while ((w >> 62) == 0) {  // predecessor not published yet: yield the issue slot
-        __nanosleep(64);
+#if FBX_LB_SLEEP > 0
+        __nanosleep(FBX_LB_SLEEP);
+#endif
         w = ld_acquire(status + idx);
       }
     } else {
