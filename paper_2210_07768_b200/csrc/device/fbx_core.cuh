@@ -967,13 +967,40 @@ FBX_DI u64 load_prefix8(const u8* p, u32 n) {
 }
 // table hash of a byte key: one multiply-xorshift per 8-byte word, one full
 // avalanche at the end (the same function builds and probes every table)
-FBX_DI u64 tbl_hash_bytes(u64 h, const u8* p, u32 n) {
+// (*pre: the first min(n, 8) bytes, zero padded -- the slots' prefix field)
+FBX_DI u64 tbl_hash_bytes_pre(u64 h, const u8* p, u32 n, u64* pre) {
   h ^= (u64)n * 0x9E3779B97F4A7C15ull;
+#ifdef FBX_EXACT_READS
+  *pre = load_prefix8(p, n);
   for (u32 k = 0; k < n; k += 8u) {
     h = (h ^ load_prefix8(p + k, n - k)) * 0xBF58476D1CE4E5B9ull;
     h ^= h >> 31;
   }
+#else
+  // the same 8-byte words, streamed: two aligned word loads per word
+  u64 first = 0ull;
+  if (n) {
+    const u64 a = (u64)p;
+    const u32 sh = (u32)(a & 3u) * 8u;
+    const u32* wp = (const u32*)(a & ~3ull);
+    u32 w0 = wp[0];
+    for (u32 k = 0; k < n; k += 8u, wp += 2) {
+      const u32 w1 = wp[1], w2 = wp[2];  // spans keep >= 16 B of readable slack
+      u64 v = ((u64)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
+      if (n - k < 8u) v &= (1ull << ((n - k) * 8u)) - 1ull;
+      if (k == 0u) first = v;
+      h = (h ^ v) * 0xBF58476D1CE4E5B9ull;
+      h ^= h >> 31;
+      w0 = w2;
+    }
+  }
+  *pre = first;
+#endif
   return mix64(h);
+}
+FBX_DI u64 tbl_hash_bytes(u64 h, const u8* p, u32 n) {
+  u64 pre;
+  return tbl_hash_bytes_pre(h, p, n, &pre);
 }
 FBX_DI u64 tbl_hash_u64(u64 h, u64 v) { return mix64(h ^ mix64(v)); }
 
@@ -1170,8 +1197,8 @@ FBX_DI u64 table_tag(u64 h) { return h | 1ull; }  // never 0
 // dictionary lookup (featureops.py:104-167): key bytes -> u64, default on miss.
 // Slot.pad holds the key's first 8 bytes, so short keys compare in one word.
 FBX_DI u64 dict_lookup(const Slot* slots, u64 mask, const u8* keyblob, Str key, u64 dflt) {
-  u64 tag = table_tag(tbl_hash_bytes(0x5DB2CEB4C16A9E87ull, key.p, key.n));
-  u64 pre = load_prefix8(key.p, key.n);
+  u64 pre;
+  const u64 tag = table_tag(tbl_hash_bytes_pre(0x5DB2CEB4C16A9E87ull, key.p, key.n, &pre));
   u64 i = tag & mask;
   while (true) {
     const Slot* s = slots + i;
