@@ -33,9 +33,10 @@
 #define FBX_ERR_MULTI_MATCH 8     /* side view key matched >1 rows (dup ids after merge) */
 #define FBX_ERR_JSON_BIGINT 9     /* ValueError: int literal > 4300 digits */
 #define FBX_ERR_JSON_DEEP 10      /* unsupported: JSON nesting deeper than 64 */
-#define FBX_ERR_UNICODE_LOWER 11  /* unsupported: non-ASCII lower() */
+#define FBX_ERR_UNICODE_LOWER 11  /* reserved: lower() is exact on device (Unicode 15 tables) */
 #define FBX_ERR_FLOAT_OVERFLOW 12 /* OverflowError: float32 pack of a too-large value */
-#define FBX_ERR_FLOAT_SLOWPATH 13 /* unsupported: decimal->double needs a bignum */
+#define FBX_ERR_FLOAT_SLOWPATH 13 /* unsupported: inexact (>19 digit) decimal at a rounding tie */
+#define FBX_ERR_INTERNAL 14       /* a plan invariant failed (never expected) */
 
 /* Device-resident run state: counters, the pool head, the error word.
  * One per engine, zeroed (error_key = ~0) before a launch. */
