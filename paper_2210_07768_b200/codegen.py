@@ -141,6 +141,9 @@ class V:
     nullable: bool = True
     lone: bool = False
     lower: bool = False   # str view whose (ASCII) bytes are lowercased on read
+    # unmaterialised concat: the string is these items back to back (V str views and
+    # literal separator bytes); hashes read the pieces, other consumers materialise
+    rope: tuple = ()
 
     @property
     def n(self) -> str:
@@ -254,6 +257,8 @@ class PlanCodegen:
         self.early = False
         # profiling aid: per-phase SM cycles (lane 0 of every warp), printed by the last CTA
         self.phase_timers = os.environ.get("FBX_PHASE_TIMERS", "0") != "0"
+        self.lazy_concat = os.environ.get("FBX_LAZY_CONCAT", "0") != "0"  # measured slower (r1)
+        self._ropes: dict[str, V] = {}
         self._pf_tail: list[str] = []
 
     # -- value helpers ---------------------------------------------------------
@@ -301,6 +306,8 @@ class PlanCodegen:
     def materialize(self, v: V) -> V:
         """Copy a lazily-lowered view into the pool (consumers that compare
         or store bytes)."""
+        if v.rope:
+            return self.materialize_rope(v)
         if v.t != "str" or not v.lower:
             return v
         g = self.g
@@ -312,6 +319,34 @@ class PlanCodegen:
           f" {out.c} = fbx::Str{{{ptr} ? {ptr} : {v.c}.p, {v.c}.n}};"
           + (f" {out.c}_n = false;" if out.nullable else "")
           + (f" {out.c}_l = {v.l};" if out.lone else "") + " }")
+        return out
+
+    def materialize_rope(self, v: V) -> V:
+        """sep.join(parts) copied into the pool (once per rope)."""
+        if v.c in self._ropes:
+            return self._ropes[v.c]
+        g = self.g
+        out = V("str", g.fresh("n"), v.nullable, v.lone)
+        self.decl(out)
+        ok = g.fresh("ok")
+        g(f"bool {ok} = alive" + (f" && !{v.n}" if v.nullable else "") + ";")
+        total = " + ".join(f"{p.c}.n" if isinstance(p, V) else f"{len(p)}u" for p in v.rope)
+        ptr = self.pool_alloc(f"{ok} ? ({total}) : 0u")
+        g(f"if ({ok} && {ptr}) {{")
+        g(f"u8* d = {ptr};")
+        for p in v.rope:
+            if isinstance(p, V):
+                g(f"fbx::str_copy{'_lower' if p.lower else ''}(d, {p.c}); d += {p.c}.n;")
+            else:
+                k = g.const(p)
+                g(f"for (u32 q = 0; q < {len(p)}u; ++q) d[q] = {k}[q]; d += {len(p)}u;")
+        g(f"{out.c} = fbx::Str{{{ptr}, {total}}};")
+        if out.nullable:
+            g(f"{out.c}_n = false;")
+        if out.lone:
+            g(f"{out.c}_l = {v.l};")
+        g("}")
+        self._ropes[v.c] = out
         return out
 
     def pool_alloc(self, size_expr: str) -> str:
@@ -758,6 +793,8 @@ class PlanCodegen:
         g(stage_ctx)
         err = lambda code: self.row_error("extract", code, nd.layer, nd.rank)  # noqa: E731
         op = fn.op
+        if op not in ("hash", "concat", "id"):
+            args = [self.materialize_rope(a) if a.rope else a for a in args]
         if op == "id":
             return args[0]
         if op in ("mix", "fold"):
@@ -898,7 +935,13 @@ class PlanCodegen:
             for i, a in enumerate(args):
                 if i:
                     g("h.byte(0u);")
-                if a.t == "str":
+                if a.rope:
+                    for p in a.rope:
+                        if isinstance(p, V):
+                            g(f"h.bytes{'_lower' if p.lower else ''}({p.c}.p, {p.c}.n);")
+                        else:
+                            g(" ".join(f"h.byte({b}u);" for b in p))
+                elif a.t == "str":
                     g(f"h.bytes{'_lower' if a.lower else ''}({a.c}.p, {a.c}.n);")
                 elif a.t == "f32":
                     g(f"h.word_be({a.c});")
@@ -915,6 +958,19 @@ class PlanCodegen:
             lone = any(p.lone for p in parts)
             if len(parts) == 1:
                 return parts[0]  # sep.join([s]) == s: a view
+            if self.lazy_concat:
+                sep = fn.sep.encode("utf-8", "surrogatepass")
+                items: list = []
+                for i, p in enumerate(parts):
+                    if i and sep:
+                        items.append(sep)
+                    items.extend(p.rope if p.rope else (p,))
+                out = V("str", g.fresh("n"), nullable, lone, rope=tuple(items))
+                if nullable:
+                    g(f"const bool {out.c}_n = " + " || ".join(p.n for p in parts if p.nullable) + ";")
+                if lone:
+                    g(f"const bool {out.c}_l = " + " || ".join(p.l for p in parts if p.lone) + ";")
+                return out
             out = V("str", g.fresh("n"), nullable, lone)
             self.decl(out)
             sep = fn.sep.encode("utf-8", "surrogatepass")
@@ -1653,6 +1709,8 @@ class PlanCodegen:
         g("// ---- outputs, row-aligned ----")
         for j, (col, domain) in enumerate(ir.extract_outputs):
             v = node_out[ir.producer[col]]
+            if v.rope:
+                v = self.materialize_rope(v)
             nn = f"(!alive || {v.n})"
             if domain == "u64":
                 if v.t == "i64":
