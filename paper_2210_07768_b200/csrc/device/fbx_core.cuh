@@ -459,7 +459,30 @@ FBX_DI void str_lower_copy(u8* dst, Str s) {
 FBX_DI void str_copy_lower(u8* dst, Str s) { str_lower_copy(dst, s); }
 
 FBX_DI void str_copy(u8* dst, Str s) {
+#ifdef FBX_EXACT_READS
   for (u32 i = 0; i < s.n; ++i) dst[i] = s.p[i];
+#else
+  // bytewise until dst is 4-B aligned, then one aligned source-word pair, a funnel
+  // shift and one 4-B store per word (the source keeps >= 16 B of readable slack)
+  u32 i = 0;
+  const u32 head = (u32)(-(i64)(u64)dst & 3);
+  for (; i < head && i < s.n; ++i) dst[i] = s.p[i];
+  if (i + 4u <= s.n) {
+    const u64 a = (u64)(s.p + i);
+    const u32 sh = (u32)(a & 3u) * 8u;
+    const u32* wp = (const u32*)(a & ~3ull);
+    u32* dw = (u32*)(dst + i);
+    u32 lo = wp[0];
+    const u32 nw = (s.n - i) >> 2;
+    for (u32 k = 0; k < nw; ++k) {
+      const u32 nx = wp[k + 1];
+      dw[k] = __funnelshift_r(lo, nx, sh);
+      lo = nx;
+    }
+    i += nw * 4u;
+  }
+  for (; i < s.n; ++i) dst[i] = s.p[i];
+#endif
 }
 
 // decimal text of a Python int (str(v)); buf >= 20 bytes (+1 for '-')
