@@ -487,8 +487,17 @@ FBX_DI void str_copy(u8* dst, Str s) {
 
 // decimal text of a Python int (str(v)); buf >= 20 bytes (+1 for '-')
 FBX_DI u32 u64_dec_len(u64 v) {
-  u32 n = 1;
-  while (v >= 10u) { v /= 10u; ++n; }
+  if (v < 10000000000ull) {  // < 10^10: 32-bit-sized compares, no division
+    u32 n = 1;
+    u64 p = 10ull;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) { n += v >= p ? 1u : 0u; p *= 10ull; }
+    return n;
+  }
+  u32 n = 11;
+  u64 p = 100000000000ull;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) { n += v >= p ? 1u : 0u; p *= 10ull; }  // up to 10^19
   return n;
 }
 FBX_DI u32 int_dec_len(u64 bits, bool is_signed) {
@@ -496,7 +505,10 @@ FBX_DI u32 int_dec_len(u64 bits, bool is_signed) {
   return u64_dec_len(bits);
 }
 FBX_DI void u64_dec(u8* dst, u64 v, u32 len) {
-  for (u32 i = len; i > 0; --i) { dst[i - 1] = (u8)('0' + v % 10u); v /= 10u; }
+  u32 i = len;
+  while (v > 0xFFFFFFFFull) { dst[--i] = (u8)('0' + v % 10u); v /= 10u; }
+  u32 x = (u32)v;  // 32-bit divisions (a multiply-high each) for the rest
+  while (i > 0) { dst[--i] = (u8)('0' + x % 10u); x /= 10u; }
 }
 FBX_DI void int_dec(u8* dst, u64 bits, bool is_signed, u32 len) {
   if (is_signed && (i64)bits < 0) {
