@@ -22,6 +22,18 @@ typedef int i32;
 typedef long long i64;
 
 #define FBX_DI __device__ __forceinline__
+#define FBX_STR_(x) #x
+#define FBX_XSTR_(x) FBX_STR_(x)
+// variable-trip loops of helpers inlined at many sites stay rolled: the unrolled
+// copies cost more in instruction-cache misses than they save (measured)
+#ifdef FBX_LOOPS_UNROLLED
+#define FBX_ROLLED
+#else
+#define FBX_ROLLED _Pragma("unroll 1")
+#endif
+#ifndef FBX_FNV_UNROLL
+#define FBX_FNV_UNROLL 1  // unroll factor of the FNV word loop
+#endif
 #define FBX_NI __device__ __noinline__
 
 #include "fbx_abi.h"
@@ -84,6 +96,7 @@ struct Fnv {
     const u32* wp = (const u32*)(a & ~3ull);
     const u32 nw = n >> 2, r = n & 3u;
     u32 lo_w = wp[0];
+    _Pragma(FBX_XSTR_(unroll FBX_FNV_UNROLL))
     for (u32 k = 0; k < nw; ++k) {
       // the next word is needed when the span continues into it
 #ifdef FBX_EXACT_READS
@@ -150,6 +163,7 @@ FBX_DI u32 str_byte(const u8* p, u32 i) { return p[i]; }
 
 FBX_DI bool str_eq(Str a, Str b) {
   if (a.n != b.n) return false;
+  FBX_ROLLED
   for (u32 i = 0; i < a.n; ++i)
     if (a.p[i] != b.p[i]) return false;
   return true;
@@ -157,6 +171,7 @@ FBX_DI bool str_eq(Str a, Str b) {
 
 FBX_DI bool str_eq_const(Str a, const u8* c, u32 cn) {
   if (a.n != cn) return false;
+  FBX_ROLLED
   for (u32 i = 0; i < cn; ++i)
     if (a.p[i] != c[i]) return false;
   return true;
@@ -165,6 +180,7 @@ FBX_DI bool str_eq_const(Str a, const u8* c, u32 cn) {
 // Python str ordering == UTF-8 byte order (code points are order-preserving)
 FBX_DI int str_cmp(Str a, const u8* c, u32 cn) {
   u32 m = a.n < cn ? a.n : cn;
+  FBX_ROLLED
   for (u32 i = 0; i < m; ++i) {
     u32 x = a.p[i], y = c[i];
     if (x != y) return x < y ? -1 : 1;
@@ -178,6 +194,7 @@ FBX_DI int str_cmp(Str a, const u8* c, u32 cn) {
 // ---------------------------------------------------------------------------
 FBX_DI Str str_token(Str s, u32 delim, u32 index) {
   u32 field = 0, start = 0;
+  FBX_ROLLED
   for (u32 i = 0; i < s.n; ++i) {
     if (s.p[i] == delim) {
       if (field == index) return Str{s.p + start, i - start};
@@ -260,10 +277,12 @@ FBX_DI void str_tokens(Str s, u32 delim, const u32 (&want)[K], Str (&out)[K]) {
   if (s.n) {
     const WordCursor wc(s.p, s.n);
     const u32 dm = delim * 0x01010101u;
+    FBX_ROLLED
     for (u32 b = 0; b < s.n; b += 4u) {
       u32 z = zero_bytes(wc.word(b) ^ dm);
       const u32 left = s.n - b;
       if (left < 4u) z &= (1u << (left * 8u)) - 1u;
+      FBX_ROLLED
       while (z) {
         const u32 pos = b + ((u32)(__ffs(z) - 1) >> 3);
 #pragma unroll
@@ -308,6 +327,7 @@ FBX_DI u32 utf8_at(const u8* p, u32 i, u32 n, u32* cp) {
 // trim = str.strip() (featureops.py:302-303): a view narrowing
 FBX_DI Str str_trim(Str s) {
   u32 b = 0, e = s.n;
+  FBX_ROLLED
   while (b < e) {
     u32 c = s.p[b];
     if (c < 0x80u) {
@@ -319,6 +339,7 @@ FBX_DI Str str_trim(Str s) {
       b += l;
     }
   }
+  FBX_ROLLED
   while (e > b) {
     u32 c = s.p[e - 1];
     if (c < 0x80u) {
@@ -326,6 +347,7 @@ FBX_DI Str str_trim(Str s) {
       --e;
     } else {
       u32 k = e - 1;  // walk back to the lead byte
+      FBX_ROLLED
       while (k > b && (s.p[k] & 0xC0u) == 0x80u) --k;
       u32 cp;
       utf8_at(s.p, k, e, &cp);
@@ -342,6 +364,7 @@ FBX_DI u32 str_lower_class(Str s) {
   if (s.n == 0) return 0;
   const WordCursor wc(s.p, s.n);
   u32 up = 0;
+  FBX_ROLLED
   for (u32 b = 0; b < s.n; b += 4u) {
     u32 w = wc.word(b);
     const u32 left = s.n - b;
@@ -364,6 +387,7 @@ namespace fbx {
 // ---------------------------------------------------------------------------
 FBX_DI bool u_in(u32 cp, const u32* lo, const u32* hi, u32 n) {
   u32 a = 0, b = n;
+  FBX_ROLLED
   while (a < b) {
     const u32 m = (a + b) >> 1;
     if (__ldg(lo + m) <= cp) a = m + 1; else b = m;
@@ -372,6 +396,7 @@ FBX_DI bool u_in(u32 cp, const u32* lo, const u32* hi, u32 n) {
 }
 FBX_DI u32 u_lower_single(u32 cp) {
   u32 a = 0, b = ULOWER_N;
+  FBX_ROLLED
   while (a < b) {
     const u32 m = (a + b) >> 1;
     const u32 f = __ldg(ULOWER_FROM + m);
@@ -450,6 +475,7 @@ FBX_DI u32 unicode_lower(Str s, u8* dst) {
 }
 
 FBX_DI void str_lower_copy(u8* dst, Str s) {
+  FBX_ROLLED
   for (u32 i = 0; i < s.n; ++i) {
     u32 c = s.p[i];
     dst[i] = (u8)((c >= 'A' && c <= 'Z') ? c + 32u : c);
@@ -460,12 +486,14 @@ FBX_DI void str_copy_lower(u8* dst, Str s) { str_lower_copy(dst, s); }
 
 FBX_DI void str_copy(u8* dst, Str s) {
 #ifdef FBX_EXACT_READS
+  FBX_ROLLED
   for (u32 i = 0; i < s.n; ++i) dst[i] = s.p[i];
 #else
   // bytewise until dst is 4-B aligned, then one aligned source-word pair, a funnel
   // shift and one 4-B store per word (the source keeps >= 16 B of readable slack)
   u32 i = 0;
   const u32 head = (u32)(-(i64)(u64)dst & 3);
+  FBX_ROLLED
   for (; i < head && i < s.n; ++i) dst[i] = s.p[i];
   if (i + 4u <= s.n) {
     const u64 a = (u64)(s.p + i);
@@ -474,6 +502,7 @@ FBX_DI void str_copy(u8* dst, Str s) {
     u32* dw = (u32*)(dst + i);
     u32 lo = wp[0];
     const u32 nw = (s.n - i) >> 2;
+    FBX_ROLLED
     for (u32 k = 0; k < nw; ++k) {
       const u32 nx = wp[k + 1];
       dw[k] = __funnelshift_r(lo, nx, sh);
@@ -481,6 +510,7 @@ FBX_DI void str_copy(u8* dst, Str s) {
     }
     i += nw * 4u;
   }
+  FBX_ROLLED
   for (; i < s.n; ++i) dst[i] = s.p[i];
 #endif
 }
@@ -506,8 +536,10 @@ FBX_DI u32 int_dec_len(u64 bits, bool is_signed) {
 }
 FBX_DI void u64_dec(u8* dst, u64 v, u32 len) {
   u32 i = len;
+  FBX_ROLLED
   while (v > 0xFFFFFFFFull) { dst[--i] = (u8)('0' + v % 10u); v /= 10u; }
   u32 x = (u32)v;  // 32-bit divisions (a multiply-high each) for the rest
+  FBX_ROLLED
   while (i > 0) { dst[--i] = (u8)('0' + x % 10u); x /= 10u; }
 }
 FBX_DI void int_dec(u8* dst, u64 bits, bool is_signed, u32 len) {
@@ -845,6 +877,7 @@ FBX_DI bool radix_rank(u64 key, bool live, u64 diff, u32* hist, u32* start, u64*
   __syncthreads();
   if (live) {
     u32 r = b0;
+    FBX_ROLLED
     for (u32 q = 0; q < bn; ++q) r += bkeys[b0 + q] < key ? 1u : 0u;
     *rank = r;
   }
@@ -926,6 +959,7 @@ FBX_DI bool radix_rank_off(u64 key, bool live, u32 m, u64 diff, u32* hist, u32* 
   if (live) {
     u32 r = b0 >> 16, o = b0 & 0xFFFFu;
     const u32 j0 = b0 >> 16;
+    FBX_ROLLED
     for (u32 q = 0; q < bn; ++q) {
       const bool lt = bkeys[j0 + q] < key;
       r += lt ? 1u : 0u;
@@ -1007,6 +1041,7 @@ FBX_DI u64 tbl_hash_bytes_pre(u64 h, const u8* p, u32 n, u64* pre) {
   h ^= (u64)n * 0x9E3779B97F4A7C15ull;
 #ifdef FBX_EXACT_READS
   *pre = load_prefix8(p, n);
+  FBX_ROLLED
   for (u32 k = 0; k < n; k += 8u) {
     h = (h ^ load_prefix8(p + k, n - k)) * 0xBF58476D1CE4E5B9ull;
     h ^= h >> 31;
@@ -1019,6 +1054,7 @@ FBX_DI u64 tbl_hash_bytes_pre(u64 h, const u8* p, u32 n, u64* pre) {
     const u32 sh = (u32)(a & 3u) * 8u;
     const u32* wp = (const u32*)(a & ~3ull);
     u32 w0 = wp[0];
+    FBX_ROLLED
     for (u32 k = 0; k < n; k += 8u, wp += 2) {
       const u32 w1 = wp[1], w2 = wp[2];  // spans keep >= 16 B of readable slack
       u64 v = ((u64)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
@@ -1235,6 +1271,7 @@ FBX_DI u64 dict_lookup(const Slot* slots, u64 mask, const u8* keyblob, Str key, 
   u64 pre;
   const u64 tag = table_tag(tbl_hash_bytes_pre(0x5DB2CEB4C16A9E87ull, key.p, key.n, &pre));
   u64 i = tag & mask;
+  FBX_ROLLED
   while (true) {
     const Slot* s = slots + i;
     u64 t = __ldg(&s->tag);
@@ -1242,6 +1279,7 @@ FBX_DI u64 dict_lookup(const Slot* slots, u64 mask, const u8* keyblob, Str key, 
     if (t == tag && __ldg(&s->aux) == key.n && __ldg(&s->pad) == pre) {
       bool eq = true;
       u32 ref = __ldg(&s->ref);
+      FBX_ROLLED
       for (u32 k = 8; k < key.n && eq; k += 8u)
         eq = load_prefix8(keyblob + ref + k, key.n - k) == load_prefix8(key.p + k, key.n - k);
       if (eq) return __ldg(&s->value);
@@ -1257,12 +1295,14 @@ FBX_DI u64 dict_lookup_pf(const Slot* slots, u64 mask, const u8* keyblob, Str ke
   const u64 pre = load_prefix8(key.p, key.n);
   u64 i = tag & mask;
   const Slot* s = first;
+  FBX_ROLLED
   while (true) {
     const u64 t = s->tag;
     if (t == 0) return dflt;
     if (t == tag && s->aux == key.n && s->pad == pre) {
       bool eq = true;
       const u32 ref = s->ref;
+      FBX_ROLLED
       for (u32 k = 8; k < key.n && eq; k += 8u)
         eq = load_prefix8(keyblob + ref + k, key.n - k) == load_prefix8(key.p + k, key.n - k);
       if (eq) return s->value;
@@ -1319,6 +1359,7 @@ struct JReader {
   FBX_DI u32 skip_ws(u32 i) const {  // i <= n
     if (fast) return i + (u32)__clzll((long long)(nsp << i));
 
+    FBX_ROLLED
     while (i < n) {
       const u32 c = at(i);
       if (c > 0x20u || !j_ws(c)) break;
@@ -1337,6 +1378,7 @@ FBX_DI bool jmask_build(const u8* p, u32 n, u64* qm, u64* nspm) {
   const u32* wp = (const u32*)(a & ~3ull);
   const int nw = (int)((sh + n + 3u) >> 2);  // <= 16 aligned words
   u32 qlo = 0, qhi = 0, slo = 0, shi = 0, blo = 0, bhi = 0;
+  FBX_ROLLED
   for (int w = nw - 1; w >= 0; --w) {  // last word first: word 0 lands in bits 0..3
     const u32 x = wp[w];
     const u32 x7 = x & 0x7F7F7F7Fu;
@@ -1370,6 +1412,7 @@ FBX_DI u32 j_string(const JReader& r, u32 i, u32* esc) {
     return e < r.n ? e : ~0u;
   }
   const u64 base = (u64)r.p;
+  FBX_ROLLED
   while (i < r.n) {
     const u64 a = base + i;
     const u32 sh = (u32)(a & 3u) * 8u;
@@ -1409,6 +1452,7 @@ FBX_DI u32 j_string(const JReader& r, u32 i, u32* esc) {
 FBX_DI u32 j_unescape(const u8* s, u32 b, u32 e, u8* dst, u32* lone) {
   u32 o = 0;
   u32 i = b;
+  FBX_ROLLED
   while (i < e) {
     u32 c = s[i];
     if (c != '\\') { if (dst) dst[o] = (u8)c; ++o; ++i; continue; }
@@ -1462,6 +1506,7 @@ FBX_DI u32 j_unescape(const u8* s, u32 b, u32 e, u8* dst, u32* lone) {
 FBX_DI bool j_key_eq(const JReader& r, const u8* s, u32 b, u32 e, u32 esc, const u8* seg, u32 slen) {
   if (!esc) {
     if (e - b != slen) return false;
+    FBX_ROLLED
     for (u32 k = 0; k < slen; ++k)
       if (r.at(b + k) != seg[k]) return false;
     return true;
@@ -1472,6 +1517,7 @@ FBX_DI bool j_key_eq(const JReader& r, const u8* s, u32 b, u32 e, u32 esc, const
   if (dl != slen || dl > 64u) return false;
   j_unescape(s, b, e, tmp, &lone);
   if (lone) return false;
+  FBX_ROLLED
   for (u32 k = 0; k < slen; ++k)
     if (tmp[k] != seg[k]) return false;
   return true;
@@ -1488,12 +1534,14 @@ FBX_DI u32 j_number(const JReader& r, u32 i, u32* type, u32* digits) {
   if (r.at(i) == '0') {
     ++i;
   } else {
+    FBX_ROLLED
     while (i < n && j_digit(r.at(i))) ++i;
   }
   *digits = i - st - (neg ? 1u : 0u);
   *type = J_INT;
   if (i + 1 < n && r.at(i) == '.' && j_digit(r.at(i + 1))) {
     i += 2;
+    FBX_ROLLED
     while (i < n && j_digit(r.at(i))) ++i;
     *type = J_FLOAT;
   }
@@ -1501,6 +1549,7 @@ FBX_DI u32 j_number(const JReader& r, u32 i, u32* type, u32* digits) {
     u32 k = i + 1;
     if (k < n && (r.at(k) == '+' || r.at(k) == '-')) ++k;
     if (k < n && j_digit(r.at(k))) {
+      FBX_ROLLED
       while (k < n && j_digit(r.at(k))) ++k;
       i = k;
       *type = J_FLOAT;
@@ -1511,6 +1560,7 @@ FBX_DI u32 j_number(const JReader& r, u32 i, u32* type, u32* digits) {
 
 FBX_DI bool j_lit(const JReader& r, u32 i, const char* w, u32 wl) {
   if (i + wl > r.n) return false;
+  FBX_ROLLED
   for (u32 k = 0; k < wl; ++k)
     if (r.at(i + k) != (u8)w[k]) return false;
   return true;
@@ -1651,6 +1701,7 @@ FBX_DI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
             eq = KM::eq(p, sidx, kpre, klen);
             if (eq && klen > 8u) {
               u32 off = ps.seg_off[p * 8 + sidx];
+              FBX_ROLLED
               for (u32 k = 8; k < klen && eq; ++k) eq = r.at(kb + k) == ps.seg[off + k];
             }
           } else {
