@@ -258,6 +258,7 @@ class PlanCodegen:
         # profiling aid: per-phase SM cycles (lane 0 of every warp), printed by the last CTA
         self.phase_timers = os.environ.get("FBX_PHASE_TIMERS", "0") != "0"
         self.lazy_concat = os.environ.get("FBX_LAZY_CONCAT", "0") != "0"  # measured slower (r1)
+        self.digest_loop = os.environ.get("FBX_DIGEST_LOOP", "0") != "0"  # measured slower (r1)
         self._ropes: dict[str, V] = {}
         self._pf_tail: list[str] = []
 
@@ -1564,37 +1565,11 @@ class PlanCodegen:
         g("const bool staged_out = out_bytes <= DYN_SMEM;")
         if not self.early:
             self.emit_lookback()
-        g("u64 digest = 0ull;")
-        g("if (alive) {")
-        g("fbx::Fnv h;")
-        g(f"h.u64_le({idv.c}); h.byte((u32)({lab.c} & 1ull));")
-        for q, (slot, _) in enumerate(fv):
-            g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
-        g("digest = h.value();")
-        g("}")
-        if self.phase_timers:
-            g("FBX_PHASE(9);  // instance digests")
-        g("{")
-        g("// warp reductions (redux.sync): the XOR digest and three <=512 counters packed")
-        g("const u32 r0l = __reduce_xor_sync(0xFFFFFFFFu, (u32)digest);")
-        g("const u32 r0h = __reduce_xor_sync(0xFFFFFFFFu, (u32)(digest >> 32));")
-        g("const u32 rc = __reduce_add_sync(0xFFFFFFFFu, malformed | (filtered << 10) | (joined << 20));")
-        g("if ((threadIdx.x & 31u) == 0) { sm.red[threadIdx.x >> 5][0] = ((u64)r0h << 32) | r0l; "
-          "sm.red[threadIdx.x >> 5][1] = rc & 0x3FFu; sm.red[threadIdx.x >> 5][2] = (rc >> 10) & 0x3FFu; "
-          "sm.red[threadIdx.x >> 5][3] = rc >> 20; }")
-        g("}")
-        g("__syncthreads();")
-        g("if (threadIdx.x == 0) {")
-        g("u64 r0 = 0, r1 = 0, r2 = 0, r3 = 0;")
-        g("for (int w = 0; w < NT / 32; ++w) { r0 ^= sm.red[w][0]; r1 += sm.red[w][1]; "
-          "r2 += sm.red[w][2]; r3 += sm.red[w][3]; }")
-        g("if (r0) atomicXor((unsigned long long*)&ST->digest, (unsigned long long)r0);")
-        g("atomicAdd((unsigned long long*)&ST->instances, (unsigned long long)n_inst);")
-        g("atomicAdd((unsigned long long*)&ST->signs, (unsigned long long)tile_signs);")
-        g("if (r1) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)r1);")
-        g("if (r2) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)r2);")
-        g("if (r3) atomicAdd((unsigned long long*)&ST->joined, (unsigned long long)r3);")
-        g("}")
+        digest_loop = self.digest_loop and not self.early
+        if digest_loop:
+            g("__syncthreads();  // the look-back's offsets; every rank-scratch read is done")
+        else:
+            self.emit_digest(idv, lab, fv, None)
         g(f"u64* O_IDS = {g.p('out.ids', 'u64*')}; u8* O_LAB = {g.p('out.labels', 'u8*')};")
         g(f"u64* O_OFF = {g.p('out.offsets', 'u64*')}; u16* O_SLOT = {g.p('out.slots', 'u16*')};")
         g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
@@ -1637,6 +1612,8 @@ class PlanCodegen:
         for q, (slot, _) in enumerate(fv):
             g(f"if ((fpres >> {q}) & 1u) {{ O_SLOT[so] = (u16){slot}u; O_SIGN[so] = fsg[{q}]; ++so; }}")
         g("}")
+        if digest_loop:
+            self.emit_digest(idv, lab, fv, "pairs")
         g("if (threadIdx.x == 0) O_OFF[ei + n_inst] = es + tile_signs;")
         for line in self._ids_tail:
             g(line)
@@ -1737,6 +1714,51 @@ class PlanCodegen:
         g("}")
         g("}")
         return "fbx_extract_rows"
+
+
+    def emit_digest(self, idv: V, lab: V, fv, source):
+        """Instance digests (pipeline.py:375-382) + the block's counter reduction.
+        source None: straight-line over the row's features (registers); "pairs":
+        one rolled loop over the row's emitted (slot, sign) pairs, read back from
+        the staged tile (or the CSR in HBM) -- a much smaller kernel."""
+        g = self.g
+        g("u64 digest = 0ull;")
+        g("if (alive) {")
+        g("fbx::Fnv h;")
+        g(f"h.u64_le({idv.c}); h.byte((u32)({lab.c} & 1ull));")
+        if source is None:
+            for q, (slot, _) in enumerate(fv):
+                g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
+        else:
+            g("const u16* dsl = staged_out ? (const u16*)st_slot + myoff : O_SLOT + es + myoff;")
+            g("const u64* dsg = staged_out ? (const u64*)st_sign + myoff : O_SIGN + es + myoff;")
+            g("FBX_ROLLED")
+            g("for (u32 k = 0; k < m; ++k) { h.u16_le(dsl[k]); h.u64_le(dsg[k]); }")
+        g("digest = h.value();")
+        g("}")
+        if self.phase_timers:
+            g("FBX_PHASE(9);  // instance digests")
+        g("{")
+        g("// warp reductions (redux.sync): the XOR digest and three <=512 counters packed")
+        g("const u32 r0l = __reduce_xor_sync(0xFFFFFFFFu, (u32)digest);")
+        g("const u32 r0h = __reduce_xor_sync(0xFFFFFFFFu, (u32)(digest >> 32));")
+        g("const u32 rc = __reduce_add_sync(0xFFFFFFFFu, malformed | (filtered << 10) | (joined << 20));")
+        g("if ((threadIdx.x & 31u) == 0) { sm.red[threadIdx.x >> 5][0] = ((u64)r0h << 32) | r0l; "
+          "sm.red[threadIdx.x >> 5][1] = rc & 0x3FFu; sm.red[threadIdx.x >> 5][2] = (rc >> 10) & 0x3FFu; "
+          "sm.red[threadIdx.x >> 5][3] = rc >> 20; }")
+        g("}")
+        g("__syncthreads();")
+        g("if (threadIdx.x == 0) {")
+        g("u64 r0 = 0, r1 = 0, r2 = 0, r3 = 0;")
+        g("for (int w = 0; w < NT / 32; ++w) { r0 ^= sm.red[w][0]; r1 += sm.red[w][1]; "
+          "r2 += sm.red[w][2]; r3 += sm.red[w][3]; }")
+        g("if (r0) atomicXor((unsigned long long*)&ST->digest, (unsigned long long)r0);")
+        g("atomicAdd((unsigned long long*)&ST->instances, (unsigned long long)n_inst);")
+        g("atomicAdd((unsigned long long*)&ST->signs, (unsigned long long)tile_signs);")
+        g("if (r1) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)r1);")
+        g("if (r2) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)r2);")
+        g("if (r3) atomicAdd((unsigned long long*)&ST->joined, (unsigned long long)r3);")
+        g("}")
 
     def emit_lookback(self):
         g = self.g
