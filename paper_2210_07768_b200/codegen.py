@@ -248,7 +248,11 @@ class PlanCodegen:
         # sign_heavy / default / fig4 / cross_heavy, 10 % slower on lookup_heavy
         # (latency-bound dictionary probes, scattered rows) -> off for lookup plans
         has_lookup = any(nd.fn.op == "lookup" for nd in ir.nodes)
-        self.sort_rows = os.environ.get("FBX_SORT_ROWS", "0" if has_lookup else "1") != "0"
+        # row sort: on for every plan (end of r1: lookup_heavy 0.330 -> 0.325 ms with it)
+        self.sort_rows = os.environ.get("FBX_SORT_ROWS", "1") != "0"
+        # warp-aggregated pool grants (no CTA barrier): cross_heavy 0.306 -> 0.296 ms,
+        # sign_heavy / default -0.5 %; lookup plans +4 % -> off there
+        self.pool_warp = os.environ.get("FBX_POOL_WARP_GRANTS", "0" if has_lookup else "1") != "0"
         self.dict_prefetch = os.environ.get("FBX_DICT_PREFETCH", "1") != "0"
         self.dict_pf: dict[str, tuple] = {}
         self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
@@ -1989,7 +1993,7 @@ class PlanCodegen:
         body_start = len(self.g.lines)
         kname = self.pipeline_kernel()
         consts = b"".join(self.g.consts)
-        head = [library_source(), "",
+        head = (["#ifndef FBX_POOL_WARP", "#define FBX_POOL_WARP", "#endif"] if self.pool_warp else []) + [library_source(), "",
                 "// ===== generated plan =====",
                 f"__device__ const __align__(16) u8 K_STR[] = {_c_bytes(consts + bytes(16))};",
                 *self.globals, ""]
