@@ -123,7 +123,6 @@ class Program:
     side_kernels: list[str]
     notes: list[str]
     int_keyed: tuple[int, ...] = ()   # tables with 16-B fbx::ISlot slots
-    persistent_ctas_per_sm: int = 0   # >0: fbx_pipeline takes tiles from a ticket
     json_kind: bool = False           # Json-kind extraction: canonical JSON into the pool
     tiles_per_chunk: int = 1          # > 1: chunk cut into 512-row sub-tiles (merged after)
 
@@ -141,9 +140,6 @@ class V:
     nullable: bool = True
     lone: bool = False
     lower: bool = False   # str view whose (ASCII) bytes are lowercased on read
-    # unmaterialised concat: the string is these items back to back (V str views and
-    # literal separator bytes); hashes read the pieces, other consumers materialise
-    rope: tuple = ()
 
     @property
     def n(self) -> str:
@@ -255,16 +251,8 @@ class PlanCodegen:
         self.pool_warp = os.environ.get("FBX_POOL_WARP_GRANTS", "0" if has_lookup else "1") != "0"
         self.dict_prefetch = os.environ.get("FBX_DICT_PREFETCH", "1") != "0"
         self.dict_pf: dict[str, tuple] = {}
-        self.prefetch_next = os.environ.get("FBX_L2_PREFETCH", "0") != "0"  # measured slower (r1)
-        self.persistent = os.environ.get("FBX_PERSISTENT", "0") != "0"  # measured slower (r1)
-        self.early_order = os.environ.get("FBX_EARLY_ORDER", "0") != "0"  # measured ~1% slower (r1)
-        self.early = False
         # profiling aid: per-phase SM cycles (lane 0 of every warp), printed by the last CTA
         self.phase_timers = os.environ.get("FBX_PHASE_TIMERS", "0") != "0"
-        self.lazy_concat = os.environ.get("FBX_LAZY_CONCAT", "0") != "0"  # measured slower (r1)
-        self.digest_loop = os.environ.get("FBX_DIGEST_LOOP", "0") != "0"  # measured slower (r1)
-        self._ropes: dict[str, V] = {}
-        self._pf_tail: list[str] = []
 
     # -- value helpers ---------------------------------------------------------
     def kind_t(self, kind: Kind) -> str:
@@ -311,8 +299,6 @@ class PlanCodegen:
     def materialize(self, v: V) -> V:
         """Copy a lazily-lowered view into the pool (consumers that compare
         or store bytes)."""
-        if v.rope:
-            return self.materialize_rope(v)
         if v.t != "str" or not v.lower:
             return v
         g = self.g
@@ -324,34 +310,6 @@ class PlanCodegen:
           f" {out.c} = fbx::Str{{{ptr} ? {ptr} : {v.c}.p, {v.c}.n}};"
           + (f" {out.c}_n = false;" if out.nullable else "")
           + (f" {out.c}_l = {v.l};" if out.lone else "") + " }")
-        return out
-
-    def materialize_rope(self, v: V) -> V:
-        """sep.join(parts) copied into the pool (once per rope)."""
-        if v.c in self._ropes:
-            return self._ropes[v.c]
-        g = self.g
-        out = V("str", g.fresh("n"), v.nullable, v.lone)
-        self.decl(out)
-        ok = g.fresh("ok")
-        g(f"bool {ok} = alive" + (f" && !{v.n}" if v.nullable else "") + ";")
-        total = " + ".join(f"{p.c}.n" if isinstance(p, V) else f"{len(p)}u" for p in v.rope)
-        ptr = self.pool_alloc(f"{ok} ? ({total}) : 0u")
-        g(f"if ({ok} && {ptr}) {{")
-        g(f"u8* d = {ptr};")
-        for p in v.rope:
-            if isinstance(p, V):
-                g(f"fbx::str_copy{'_lower' if p.lower else ''}(d, {p.c}); d += {p.c}.n;")
-            else:
-                k = g.const(p)
-                g(f"for (u32 q = 0; q < {len(p)}u; ++q) d[q] = {k}[q]; d += {len(p)}u;")
-        g(f"{out.c} = fbx::Str{{{ptr}, {total}}};")
-        if out.nullable:
-            g(f"{out.c}_n = false;")
-        if out.lone:
-            g(f"{out.c}_l = {v.l};")
-        g("}")
-        self._ropes[v.c] = out
         return out
 
     def pool_alloc(self, size_expr: str) -> str:
@@ -798,8 +756,6 @@ class PlanCodegen:
         g(stage_ctx)
         err = lambda code: self.row_error("extract", code, nd.layer, nd.rank)  # noqa: E731
         op = fn.op
-        if op not in ("hash", "concat", "id"):
-            args = [self.materialize_rope(a) if a.rope else a for a in args]
         if op == "id":
             return args[0]
         if op in ("mix", "fold"):
@@ -940,13 +896,7 @@ class PlanCodegen:
             for i, a in enumerate(args):
                 if i:
                     g("h.byte(0u);")
-                if a.rope:
-                    for p in a.rope:
-                        if isinstance(p, V):
-                            g(f"h.bytes{'_lower' if p.lower else ''}({p.c}.p, {p.c}.n);")
-                        else:
-                            g(" ".join(f"h.byte({b}u);" for b in p))
-                elif a.t == "str":
+                if a.t == "str":
                     g(f"h.bytes{'_lower' if a.lower else ''}({a.c}.p, {a.c}.n);")
                 elif a.t == "f32":
                     g(f"h.word_be({a.c});")
@@ -963,19 +913,6 @@ class PlanCodegen:
             lone = any(p.lone for p in parts)
             if len(parts) == 1:
                 return parts[0]  # sep.join([s]) == s: a view
-            if self.lazy_concat:
-                sep = fn.sep.encode("utf-8", "surrogatepass")
-                items: list = []
-                for i, p in enumerate(parts):
-                    if i and sep:
-                        items.append(sep)
-                    items.extend(p.rope if p.rope else (p,))
-                out = V("str", g.fresh("n"), nullable, lone, rope=tuple(items))
-                if nullable:
-                    g(f"const bool {out.c}_n = " + " || ".join(p.n for p in parts if p.nullable) + ";")
-                if lone:
-                    g(f"const bool {out.c}_l = " + " || ".join(p.l for p in parts if p.lone) + ";")
-                return out
             out = V("str", g.fresh("n"), nullable, lone)
             self.decl(out)
             sep = fn.sep.encode("utf-8", "surrogatepass")
@@ -1171,26 +1108,9 @@ class PlanCodegen:
         g("} sm;")
         if self.phase_timers:
             g("u64 ph_t = clock64();")
-        if self.persistent:
-            g("// persistent CTAs (one per resident slot) take tiles in order from a ticket:")
-            g("// every predecessor a look-back waits on is held by a running CTA, no wave")
-            g("// tail, and the shared state is set up once")
-            g("__shared__ u32 sm_ltile;")
-            g(f"const u32 NTILES = (u32)((ROW_HI - ROW_LO + {ir.chunk - 1}ull) / {ir.chunk}ull) * {self.spc}u;")
-            if self.staged:
-                g("if (threadIdx.x == 0) fbx::mbar_init(&sm.bar, 1u);")
-            g("u32 bar_phase = 0u;")
-            g("__syncthreads();")
-            g("for (;;) {")
-            g("if (threadIdx.x == 0) sm_ltile = (u32)atomicAdd((unsigned long long*)&ST->tile_ticket, 1ull);")
-            g("__syncthreads();")
-            g("const u32 LT = sm_ltile;")
-            g("if (LT >= NTILES) break;")
-            bid = "LT"
-        else:
-            g("// tiles in blockIdx order: the hardware dispatches CTAs in order, so every")
-            g("// predecessor a look-back waits on is resident or done (as CUB relies on)")
-            bid = "blockIdx.x"
+        g("// tiles in blockIdx order: the hardware dispatches CTAs in order, so every")
+        g("// predecessor a look-back waits on is resident or done (as CUB relies on)")
+        bid = "blockIdx.x"
         g(f"const u32 tile = (u32){g.p('tile_base')} + {bid};  // run-global tile id")
         if self.spc == 1:
             g(f"const u64 chunk = CHUNK0 + {bid};")
@@ -1258,8 +1178,7 @@ class PlanCodegen:
             g(f"__shared__ bool sm_span_ok[{ns_}];")
             g("if (threadIdx.x == 0) {")
             g("u32 used = 0;")
-            if not self.persistent:
-                g("fbx::mbar_init(&sm.bar, 1u);")
+            g("fbx::mbar_init(&sm.bar, 1u);")
             for i, c in enumerate(self.staged):
                 offs = g.p(f"drv.{c}.offsets", "const u32*")
                 g("{")
@@ -1277,32 +1196,6 @@ class PlanCodegen:
                   f"{data} + sm.span_lo[{i}], sm.span_len[{i}], &sm.bar);")
             g("}")
             g("__syncthreads();")
-        # ---- L2 prefetch of the tile PF ahead (the CTA that starts when this one
-        # retires): its fixed columns, bitmaps and offsets now, its string spans
-        # at the end of this tile (their offsets are L2 hits by then)
-        pf_cols = [(c, k) for c, k in drv.kinds.items() if c in needed]
-        pf_dist = 148 * self.min_blocks
-        if self.prefetch_next and self.spc == 1:
-            g(f"const u32 PF_TILE = {bid} + {pf_dist}u;")
-            g(f"const bool pf_on = threadIdx.x == 0 && PF_TILE + 1u < gridDim.x;")
-            g("if (pf_on) {")
-            g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {self.tile_rows}ull, p1 = p0 + {self.tile_rows}ull;")
-            for c, k in pf_cols:
-                g(f"fbx::prefetch_span({g.p(f'drv.{c}.nulls', 'const u8*')} + (p0 >> 3), ((p1 - p0) >> 3) + 1);")
-                if k.var_length:
-                    g(f"fbx::prefetch_span({g.p(f'drv.{c}.offsets', 'const u32*')} + p0, (p1 - p0 + 1) * 4);")
-                else:
-                    w = 8 if k is Kind.INT64 else 4
-                    g(f"fbx::prefetch_span({g.p(f'drv.{c}.data', 'const u8*')} + p0 * {w}, (p1 - p0) * {w});")
-            g("}")
-            self._pf_tail = []
-            for c, k in pf_cols:
-                if k.var_length:
-                    offs = g.p(f"drv.{c}.offsets", "const u32*")
-                    data = g.p(f"drv.{c}.data", "const u8*")
-                    self._pf_tail.append(
-                        f"{{ const u32 a = fbx::ldg_u32({offs} + p0), b = fbx::ldg_u32({offs} + p1);"
-                        f" fbx::prefetch_span({data} + a, b - a); }}")
         # ---- prologue loads: every driver column this plan reads ----------------
         g("// ---- prologue: coalesced loads of the row's fixed columns / offsets ----")
         raw: dict[str, V] = {}
@@ -1328,10 +1221,7 @@ class PlanCodegen:
         if self.pf_slot:
             g("fbx::cp_async_commit();")
         if self.staged:
-            if self.persistent:
-                g("fbx::mbar_wait(&sm.bar, bar_phase); bar_phase ^= 1u;")
-            else:
-                g("fbx::mbar_wait(&sm.bar, 0u);")
+            g("fbx::mbar_wait(&sm.bar, 0u);")
         if self.dict_pf:
             g("// first dictionary slot of every lookup keyed by a driver string column,")
             g("// fetched now (cp.async) so the probe after the JSON finds it in smem")
@@ -1427,32 +1317,6 @@ class PlanCodegen:
                     self.prefetch_side_column(k, view, cc, row)
                 else:
                     self.col(c, {})
-        # ---- emission order decided BEFORE the DAG ----------------------------------
-        feats_early = sorted(ir.features.items(), key=lambda kv: (kv[1], kv[0]))
-        pnulls = (self.predict_feature_nulls(feats_early)
-                  if self.early_order and self.nt * max(1, len(ir.features)) < 65536 else None)
-        self.early = pnulls is not None
-        if self.early:
-            # which rows emit and how many signs each is known from null-ness alone:
-            # counts, the tile aggregate and the rank / sign offsets are settled now,
-            # so the aggregate is published a whole DAG earlier (successors' look-backs
-            # rarely wait) and the rank pass runs on shared memory behind the spans
-            g("// ---- emission order, decided before the DAG (exact for every run that")
-            g("// succeeds; a mismatch after the DAG is an internal error) ----")
-            if ir.basic is not None:
-                g(f"const bool palive = alive && !{idv.n} && bhit;")
-            else:
-                g("const bool palive = alive;")
-            g("u32 pfpres = 0u;")
-            for q, x in enumerate(pnulls):
-                g(f"if (!({x})) pfpres |= {1 << q}u;")
-            g("if (!palive) pfpres = 0u;")
-            g("const u32 pm = __popc(pfpres);")
-            self.emission_order(idv, "palive", "pm", f"dyn_smem + {self.span_cap}u")
-            # the look-back right away: warp 0 resolves (and publishes) the inclusive
-            # prefix while the other warps start the DAG; inclusive prefixes then
-            # trail the tile frontier by little, so look-backs walk back few tiles
-            self.emit_lookback()
         # ---- DAG --------------------------------------------------------------------
         g(f"CUR_STAGE = {STAGE['extract']}u;")
         if self.phase_timers:
@@ -1555,25 +1419,15 @@ class PlanCodegen:
         # ---- tile: sort by instance id, offsets, look-back, write -----------------------
         if self.phase_timers:
             g("FBX_PHASE(4);")
-        if self.early:
-            g("if (alive && fpres != pfpres) {  // the pre-DAG prediction must hold")
-            self.row_error("merge", "internal")
-            g("}")
-        else:
-            self.emission_order(idv, "alive", "m", "dyn_smem")
+        self.emission_order(idv, "alive", "m", "dyn_smem")
         # look-back by warp 0 while every warp (warp 0 after it) hashes its rows'
         # instance digests -- the digest is off the path to the aggregate publish
         if self.phase_timers:
             g("FBX_PHASE(5);")
         g("const u32 out_bytes = tile_signs * 10u + n_inst * 17u + 176u;")
         g("const bool staged_out = out_bytes <= DYN_SMEM;")
-        if not self.early:
-            self.emit_lookback()
-        digest_loop = self.digest_loop and not self.early
-        if digest_loop:
-            g("__syncthreads();  // the look-back's offsets; every rank-scratch read is done")
-        else:
-            self.emit_digest(idv, lab, fv, None)
+        self.emit_lookback()
+        self.emit_digest(idv, lab, fv)
         g(f"u64* O_IDS = {g.p('out.ids', 'u64*')}; u8* O_LAB = {g.p('out.labels', 'u8*')};")
         g(f"u64* O_OFF = {g.p('out.offsets', 'u64*')}; u16* O_SLOT = {g.p('out.slots', 'u16*')};")
         g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
@@ -1616,23 +1470,12 @@ class PlanCodegen:
         for q, (slot, _) in enumerate(fv):
             g(f"if ((fpres >> {q}) & 1u) {{ O_SLOT[so] = (u16){slot}u; O_SIGN[so] = fsg[{q}]; ++so; }}")
         g("}")
-        if digest_loop:
-            self.emit_digest(idv, lab, fv, "pairs")
         g("if (threadIdx.x == 0) O_OFF[ei + n_inst] = es + tile_signs;")
         for line in self._ids_tail:
             g(line)
-        if self.prefetch_next and self._pf_tail and self.spc == 1:
-            g("if (pf_on) {")
-            g(f"const u64 p0 = ROW_LO + (u64)PF_TILE * {self.tile_rows}ull, p1 = p0 + {self.tile_rows}ull;")
-            for line in self._pf_tail:
-                g(line)
-            g("}")
         if self.phase_timers:
             g("FBX_PHASE(7);")
         g("if (threadIdx.x == 0 && staged_out) fbx::bulk_wait_read();  // smem lives until read")
-        if self.persistent:
-            g("__syncthreads();  // the next tile reuses every shared buffer")
-            g("}")
         if self.phase_timers:
             g("if (threadIdx.x == 0) { __threadfence(); if (atomicAdd(&fbx_ph_done, 1u) == gridDim.x - 1) {")
             g("__threadfence(); u64 t = 0; for (int q = 0; q < 10; ++q) t += fbx_ph[q];")
@@ -1690,8 +1533,6 @@ class PlanCodegen:
         g("// ---- outputs, row-aligned ----")
         for j, (col, domain) in enumerate(ir.extract_outputs):
             v = node_out[ir.producer[col]]
-            if v.rope:
-                v = self.materialize_rope(v)
             nn = f"(!alive || {v.n})"
             if domain == "u64":
                 if v.t == "i64":
@@ -1720,24 +1561,16 @@ class PlanCodegen:
         return "fbx_extract_rows"
 
 
-    def emit_digest(self, idv: V, lab: V, fv, source):
-        """Instance digests (pipeline.py:375-382) + the block's counter reduction.
-        source None: straight-line over the row's features (registers); "pairs":
-        one rolled loop over the row's emitted (slot, sign) pairs, read back from
-        the staged tile (or the CSR in HBM) -- a much smaller kernel."""
+    def emit_digest(self, idv: V, lab: V, fv):
+        """Instance digests (pipeline.py:375-382) + the block's counter reduction,
+        straight-line over the row's features (registers)."""
         g = self.g
         g("u64 digest = 0ull;")
         g("if (alive) {")
         g("fbx::Fnv h;")
         g(f"h.u64_le({idv.c}); h.byte((u32)({lab.c} & 1ull));")
-        if source is None:
-            for q, (slot, _) in enumerate(fv):
-                g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
-        else:
-            g("const u16* dsl = staged_out ? (const u16*)st_slot + myoff : O_SLOT + es + myoff;")
-            g("const u64* dsg = staged_out ? (const u64*)st_sign + myoff : O_SIGN + es + myoff;")
-            g("FBX_ROLLED")
-            g("for (u32 k = 0; k < m; ++k) { h.u16_le(dsl[k]); h.u64_le(dsg[k]); }")
+        for q, (slot, _) in enumerate(fv):
+            g(f"if ((fpres >> {q}) & 1u) {{ h.u16_le({slot}u); h.u64_le(fsg[{q}]); }}")
         g("digest = h.value();")
         g("}")
         if self.phase_timers:
@@ -1819,54 +1652,6 @@ class PlanCodegen:
         g("__syncthreads();")
         g(f"myoff = {live} ? sm.rank[myrank] : 0u;")
         g("}")
-
-    NULL_PROPAGATING = ("hash", "concat", "token", "lower", "trim", "id", "mix", "fold")
-
-    def predict_feature_nulls(self, feats) -> list[str] | None:
-        """Null expression of every emitted feature, evaluated BEFORE the DAG.
-
-        An operator output is null iff an input is null (hash, concat, token,
-        lower, trim, id, mix, fold) or never (lookup); a row whose operators
-        raise fails the run, so for every run that succeeds the prediction is
-        exact.  None when some operator is outside that set or two features
-        share a slot (the (slot, sign) dedup then depends on values)."""
-        ir = self.ir
-        if len({slot for _, slot in feats}) != len(feats):
-            return None
-        pn: dict[str, str] = {}
-
-        def colnull(c):
-            if c in ir.producer:
-                return pn.get(ir.producer[c])
-            v = self.env.get(c)
-            if v is None or isinstance(v, tuple):
-                return None
-            return v.n if v.nullable else "false"
-        for nd in self.node_schedule():
-            if nd.role == "pre":
-                ins = [colnull(nd.inputs[0])]
-            elif nd.role == "post":
-                ins = [pn.get(nd.op)]
-            else:
-                pre = ir.pre_of.get(nd.op, {})
-                ins = [pn.get(pre[i]) if i in pre else colnull(c) for i, c in enumerate(nd.inputs)]
-            if any(x is None for x in ins):
-                return None
-            op = nd.fn.op
-            if op == "lookup":
-                pn[nd.name] = "false"
-            elif op in self.NULL_PROPAGATING:
-                xs = [x for x in ins if x != "false"]
-                pn[nd.name] = "(" + " || ".join(xs) + ")" if xs else "false"
-            else:
-                return None
-        out = []
-        for col, _ in feats:
-            x = colnull(col)
-            if x is None:
-                return None
-            out.append(x)
-        return out
 
     def node_schedule(self) -> list[NodeIR]:
         """Layer order, with nodes that need no joined column first (their work
@@ -1956,8 +1741,6 @@ class PlanCodegen:
         self.dyn_smem = max(self.span_cap, rank_bytes,
                             min(need, per_cta, OUT_BUDGET)) // 16 * 16
         self.dyn_smem = max(self.dyn_smem, (self.span_cap + 16 + 15) // 16 * 16)  # read slack
-        if self.early_order:  # the pre-DAG rank pass lives behind the staged spans
-            self.dyn_smem = max(self.dyn_smem, (self.span_cap + rank_bytes + 15) // 16 * 16)
         # first probe slots of int-keyed tables land behind the staged spans
         self.pf_slot = {}
         if ir.mode != "extract":
@@ -2003,7 +1786,7 @@ class PlanCodegen:
         nt_ = len(ir.sides) + (1 if ir.basic is not None else 0)
         return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes,
                        tuple(k for k in range(nt_) if self.int_keyed(k)),
-                       self.min_blocks if self.persistent else 0, self.json_kind, self.spc)
+                       self.json_kind, self.spc)
 
 
 def _filter_columns(expr) -> set[str]:

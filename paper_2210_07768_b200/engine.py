@@ -804,10 +804,7 @@ class Engine:
         self._chunk_minus_tile = row_lo // self.ir.chunk - tile_base
         self._run_chunk0 = row_lo // self.ir.chunk - tile_base // self.prog.tiles_per_chunk
         self._run_tiles = tile_base + tiles
-        grid = tiles
-        if self.prog.persistent_ctas_per_sm:
-            grid = max(1, min(tiles, self._sm_count() * self.prog.persistent_ctas_per_sm))
-        self.module.launch("fbx_pipeline", grid, self.prog.threads, self.prog.smem_bytes,
+        self.module.launch("fbx_pipeline", tiles, self.prog.threads, self.prog.smem_bytes,
                            stream, self.params)
         return tiles
 

@@ -142,16 +142,12 @@ def test_streamed_slice_plan_covers_rows():
         assert all(x % eng.ir.chunk == 0 for x in cuts[:-1])
 
 
-@pytest.mark.parametrize("knob", ["FBX_EARLY_ORDER=1", "FBX_PERSISTENT=1",
-                                  "FBX_NVRTC_OPTS=-DFBX_POOL_WARP", "FBX_L2_PREFETCH=1",
-                                  "FBX_EARLY_ORDER=1 FBX_PERSISTENT=1", "FBX_STAGE=0",
-                                  "FBX_SORT_ROWS=0", "FBX_DEFER_GATHERS=0",
-                                  "FBX_NVRTC_OPTS=-DFBX_EXACT_READS", "FBX_MIN_BLOCKS=3",
-                                  "FBX_LAZY_CONCAT=1", "FBX_DIGEST_LOOP=1",
-                                  "FBX_POOL_WARP_GRANTS=0"])
+@pytest.mark.parametrize("knob", ["FBX_NVRTC_OPTS=-DFBX_POOL_WARP", "FBX_STAGE=0",
+                                  "FBX_SORT_ROWS=0", "FBX_POOL_WARP_GRANTS=0"])
 @pytest.mark.parametrize("dag", ["sign_heavy", "cross_heavy"])
 def test_codegen_knobs_keep_parity(knob, dag, goldens, monkeypatch):
-    """The measured-and-rejected kernel variants stay bit-exact."""
+    """The remaining generator switches (fallback paths the kernel takes for other
+    shapes: HBM-resident spans, unsorted rows, CTA-scan pool grants) stay bit-exact."""
     for kv in knob.split():
         k, v = kv.split("=", 1)
         monkeypatch.setenv(k, v)
