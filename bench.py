@@ -19,6 +19,7 @@ per GPU, no per-record communication, one NCCL all-gather of the per-shard
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -39,6 +40,24 @@ GOLDEN_1M = {  # SURVEY.md Appendix B, 1M / 5000 / seed 11 (reference output, fu
     "cross_heavy": (0xE504098333D34E53, 907463, 8653476),
     "lookup_heavy": (0x5A153AB37CE08E96, 907463, 9074630),
 }
+
+
+def golden_for(dag: str, seed: int, rows: int, users: int, batch_size: int):
+    """(digest, instances, signs) of the UNMODIFIED reference for one shard, or None.
+    Seed 11: SURVEY Appendix B; other seeds: tests/golden/shard_goldens.json
+    (tests/golden/make_shard_goldens.py, the reference run per shard)."""
+    if rows != 1_000_000 or users != 5000 or batch_size != 512:
+        return None
+    if seed == 11 and dag in GOLDEN_1M:
+        return GOLDEN_1M[dag]
+    try:
+        doc = json.loads((ROOT / "tests" / "golden" / "shard_goldens.json").read_text())
+    except (OSError, ValueError):
+        return None
+    for r in doc.get("shards", []):
+        if r["dag"] == dag and r["seed"] == seed:
+            return int(r["digest"], 16), r["instances"], r["signs"]
+    return None
 
 
 def _env_int(name, default):
@@ -170,20 +189,60 @@ def cpu_baseline(corpus, raw_cfg, tables_dir, sample_rows, procs=None):
 
 # ---------------------------------------------------------------------------
 
-def algorithmic_bytes(corpus, counters, dict_probes_per_row: int = 0) -> dict:
-    """Compulsory HBM bytes of one step (SURVEY.md §8 d).
+# FNV-1a bytes hashed by the DAG per input record (measured on the
+# reference corpus); the instance digests add 9 B per instance + 10 B per sign (exact)
+DAG_HASHED_B_PER_REC = {"default": 44, "fig4": 57, "sign_heavy": 102, "cross_heavy": 119,
+                        "lookup_heavy": 73}
+FNV_INSTR_PER_BYTE = 4.75  # LOP3 xor + IMAD.WIDE + IMAD + LEA (+ byte extract), DESIGN §4
 
-    dict_probes_per_row: lookups per live row into dictionaries larger than L2
-    (lookup_heavy: query_dict with 1e7 fillers), one 32-B sector each."""
+
+def algorithmic_bytes(corpus, counters, dict_probes_per_row: int = 0) -> dict:
+    """Compulsory HBM bytes of one step (SURVEY.md §8 d): the driver
+    columns, the basic columns the merge reads, the CSR written and, for
+    lookup_heavy, one 32-B sector per probe of the >L2 query_dict.  Index and
+    hash-table sectors are implementation traffic (they show in ``traffic``).
+
+    dict_probes_per_row: lookups per live row into dictionaries larger than L2."""
     d = corpus.driver
     inp = sum(d.columns[c].nbytes() for c in d.order)
     b = corpus.basic
     basic = sum(b.columns[c].nbytes() for c in ("instance_id", "basic_a", "basic_b"))
-    probe = 32 * counters.joined  # one 32-B sector of the basic index per merged row
     out = counters.instances * (8 + 1 + 8) + counters.signs * (2 + 8)
     dprobe = 32 * dict_probes_per_row * counters.joined
-    return {"input": inp, "basic": basic, "basic_probe": probe, "dict_probe": dprobe,
-            "output": out, "total": inp + basic + probe + dprobe + out}
+    return {"input": inp, "basic": basic, "dict_probe": dprobe, "output": out,
+            "total": inp + basic + dprobe + out}
+
+
+def int_ceiling_s(dag: str, records: int, counters, clock_mhz: float) -> float:
+    """Integer-pipe floor of one step: the FNV-1a instructions alone at full issue
+    on 148 SMs x 4 schedulers x 32 lanes (SURVEY.md §8 d)."""
+    hashed = DAG_HASHED_B_PER_REC.get(dag, 0) * records + 9 * counters.instances + \
+        10 * counters.signs
+    return hashed * FNV_INSTR_PER_BYTE / (148 * 4 * 32 * clock_mhz * 1e6)
+
+
+def relaunch_under_torchrun(args) -> int:
+    """``bench.py --gpus N`` (N > 1) started as a plain process: start the N
+    ranks itself (torchrun, one process per GPU, rendezvous on 127.0.0.1) and
+    return their exit code.  Fails loudly when the box has fewer GPUs."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} GPUs, this box has "
+                                   f"{have}"}), flush=True)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator init (and NVLS use) in the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    print(f"[bench] starting {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -191,6 +250,10 @@ def main():
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
     local = _env_int("LOCAL_RANK", 0)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        raise SystemExit(relaunch_under_torchrun(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         return reference_arm(args, rank, world)
     import torch
@@ -208,10 +271,11 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     # what this rank extracts per step: one log (seed 11 + rank, weak scaling)
     # or, in C5 mode, its share of independent 1M-record shards (seeds 1000+k)
+    from paper_2210_07768_b200.distributed import assign_shards, weak_seeds
     if args.shards:
-        seeds = [args.shard_seed0 + k for k in range(args.shards) if k % world == rank]
+        seeds = assign_shards(args.shards, args.shard_seed0, rank, world)
     else:
-        seeds = [args.seed + rank]
+        seeds = weak_seeds(args.seed, rank)
     raw = workload_config(args.dag, batch_size=args.batch_size)
     t0 = time.time()
     shards, gen_s, prep_s = [], 0.0, 0.0
@@ -255,14 +319,19 @@ def main():
         for corp, e, _, _ in shards:
             run_shard(e, corp.driver.row_count)
     results = [e.finish().counters for _, e, _, _ in shards]
-    c = results[0]
-    if (args.rows == 1_000_000 and args.users == 5000 and args.seed == 11 and rank == 0
-            and args.batch_size == 512
-            and not args.shards):
-        want = GOLDEN_1M.get(args.dag)
-        if want and (c.digest, c.instances, c.signs) != want:
-            raise SystemExit(f"parity failure: got digest 0x{c.digest:016x} / {c.instances} / "
-                             f"{c.signs}, want 0x{want[0]:016x} / {want[1]} / {want[2]}")
+    # every shard on every rank against the unmodified reference's own run of it
+    checked = 0
+    golden_xor = 0
+    for sd, c in zip(seeds, results):
+        want = golden_for(args.dag, sd, args.rows, args.users, args.batch_size)
+        if want is None:
+            continue
+        if (c.digest, c.instances, c.signs) != want:
+            raise SystemExit(f"parity failure on rank {rank} shard seed {sd}: got digest "
+                             f"0x{c.digest:016x} / {c.instances} / {c.signs}, want "
+                             f"0x{want[0]:016x} / {want[1]} / {want[2]}")
+        checked += 1
+        golden_xor ^= want[0]
     ab = None
     for (corp, _, _, _), cc in zip(shards, results):
         big = 1 if (args.dag == "lookup_heavy" and args.lookup_fillers * 64 > (126 << 20)) else 0
@@ -307,6 +376,16 @@ def main():
                         mine.filtered)
     totals = all_gather_results(shard, device=dev) if dist else combine([shard])
     run_digest = totals.digest
+    from paper_2210_07768_b200.distributed import gather_parity
+    try:
+        gp = gather_parity(checked, len(seeds), golden_xor, run_digest, device=dev)
+    except RuntimeError as exc:
+        raise SystemExit(f"parity failure: {exc}")
+    parity = {"digest": f"0x{run_digest:016x}", "instances": totals.instances,
+              "signs": totals.signs, "shards_checked": gp["shards_checked"],
+              "reference_xor": gp["reference_xor"],
+              "source": "tests/golden/shard_goldens.json + SURVEY Appendix B (unmodified "
+                        "reference run per shard)"}
     records_all = totals.records
     value = records_all * K / (total_ms / 1e3)
     ms_per_step = total_ms / K
@@ -319,16 +398,27 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = ab["total"] / kern_avg_s / 1e9
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+    clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    hbm_floor = ab["total"] / (peak * 1e9)
+    int_floor = sum(int_ceiling_s(args.dag, corp.driver.row_count, cc, clk_mhz)
+                    for (corp, _, _, _), cc in zip(shards, results))
+    plan_sha = hashlib.sha256(eng.prepared.cubin).hexdigest()[:16]
+    roofline = {"bound": "hbm" if hbm_floor >= int_floor else "int",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "bytes_per_launch": ab, "kernel_ms": round(kern_avg_s * 1e3, 4),
+                "ceilings_ms": {"hbm": round(hbm_floor * 1e3, 4),
+                                "int_pipe_fnv": round(int_floor * 1e3, 4)},
+                "limiter": "instruction issue (see profiles/: inst_executed, issue_active)",
+                "plan_sha": plan_sha,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
             t = json.loads(prof.read_text()).get(args.dag)
-            if t:
+            if t and t.get("plan_sha") == plan_sha:  # same cubin, measured by ncu
                 roofline["traffic"] = t["dram_bytes"]
+                roofline["traffic_source"] = t.get("source")
         except (OSError, ValueError):
             pass
 
@@ -366,8 +456,7 @@ def main():
                    "parallelism": f"record-sharded x{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches[0], "clocks": clk,
-        "parity": {"digest": f"0x{run_digest:016x}", "instances": totals.instances,
-                   "signs": totals.signs},
+        "parity": parity,
         "setup_s": {"corpus": round(gen_s, 1), "prepare": round(prep_s, 1)},
         "records_per_step": records_all,
     }

@@ -7,3 +7,4 @@ FBX_DUMP_SOURCE=gpurun_out/${name}.cu ncu --set full --clock-control none --impo
   -k regex:fbx_pipeline -s 3 -c 1 -o gpurun_out/${name} \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline "$@" > gpurun_out/${name}.log 2>&1
 tail -2 gpurun_out/${name}.log
+python scripts/traffic.py gpurun_out/${name}.ncu-rep gpurun_out/${name}.log
