@@ -74,6 +74,22 @@ int fbx_state_reset(fbx_state* d_state, unsigned long long* d_tile_status, size_
 int fbx_idset_clear(unsigned long long* d_ids, size_t n_words, unsigned long long* d_pairs,
                     size_t n_pair_words, const fbx_state* d_state, void* stream);
 
+/* The reference ArenaPool's PoolExhausted for the chunks a plan kernel flagged
+ * (state.pool_flagged != 0): one CTA per chunk ranks the chunk's joined rows by
+ * join-key image, sums each device token node's lane sizes per group of
+ * lanes_per_group rows and walks the grants against `capacity` with the head
+ * reset per layer (mempool.py:114-134, device.py:181-196, 328-338, 408-409);
+ * the first grant past capacity is raised as FBX_ERR_POOL at (chunk, layer,
+ * node) with detail (requested << 32) | remaining.  Scratch: n_tiles*tile_rows
+ * u32 + u64. */
+int fbx_pool_account(const unsigned char* d_tile_flag, const unsigned long long* d_tile_chunk,
+                     unsigned long long n_tiles, unsigned spc, unsigned tile_rows,
+                     const unsigned long long* d_keys, unsigned kw, const unsigned* d_sizes,
+                     unsigned ni, const unsigned char* d_joined, const fbx_pool_node* d_nodes,
+                     unsigned n_nodes, unsigned long long lanes_per_group,
+                     unsigned long long capacity, unsigned* d_rank_scratch,
+                     unsigned long long* d_sum_scratch, fbx_state* d_state, void* stream);
+
 /* Reset the per-launch part of the run state -- the bump-pool head (ArenaPool.reset,
  * mempool.py:136) and the persistent kernel's tile ticket -- between the launches of
  * one run, whose counters keep accumulating. */

@@ -37,13 +37,15 @@
 #define FBX_ERR_FLOAT_OVERFLOW 12 /* OverflowError: float32 pack of a too-large value */
 #define FBX_ERR_FLOAT_SLOWPATH 13 /* unsupported: inexact (>19 digit) decimal at a rounding tie */
 #define FBX_ERR_INTERNAL 14       /* a plan invariant failed (never expected) */
+#define FBX_ERR_POOL_KEY 15       /* unsupported: reference-arena order over Utf8 join keys */
 
 /* Device-resident run state: counters, the pool head, the error word.
  * One per engine, zeroed (error_key = ~0) before a launch. */
 typedef struct fbx_state {
   unsigned long long tile_ticket;   /* dynamic tile scheduler */
   unsigned long long pool_head;     /* bump pointer of the HBM arena */
-  unsigned long long pool_overflow; /* (requested << 32) | remaining on exhaustion */
+  unsigned long long pool_overflow; /* device arena too small: the head this launch needed
+                                       (the engine grows the arena and re-runs) */
   unsigned long long error_key;     /* min over failures (pipeline order) */
   unsigned long long error_detail;
   unsigned long long digest;        /* XOR of instance digests */
@@ -58,8 +60,19 @@ typedef struct fbx_state {
   unsigned long long emit_key;      /* min (batch | null-before-range | position) of
                                        the label errors met at emission */
   unsigned long long emit_detail;   /* the offending label of emit_key */
-  unsigned long long reserved;
+  unsigned long long pool_flagged;  /* tiles whose reference ArenaPool demand may exceed
+                                       pool_bytes: fbx_pool_account decides exactly */
 } fbx_state;
+
+/* One device-placed pool-consuming operator node (reference: token pre/post
+ * calls placed on the device, featureops.py:392-412, device.py:328-338), in the
+ * order the reference runs them: layer, then name within the layer. */
+typedef struct fbx_pool_node {
+  unsigned int layer; /* 1-based layer */
+  unsigned int rank;  /* node rank of the error key */
+  unsigned int input; /* plane of the per-row lane sizes */
+  unsigned int pad;
+} fbx_pool_node;
 
 /* Kernel parameter block: program-defined u64 slots (device pointers, sizes,
  * row ranges).  The planner that generated the program assigns the slots. */

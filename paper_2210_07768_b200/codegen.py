@@ -47,7 +47,8 @@ MASK64 = (1 << 64) - 1
 STAGE = {"prepare": 0, "read": 1, "clean": 2, "join": 3, "extract": 4, "merge": 5, "emit": 6}
 ERR = {"type": 1, "value": 2, "encode": 3, "pool": 4, "null_label": 5, "label_range": 6,
        "dup_id": 7, "multi_match": 8, "json_bigint": 9, "json_deep": 10,
-       "unicode_lower": 11, "float_overflow": 12, "float_slow": 13, "internal": 14}
+       "unicode_lower": 11, "float_overflow": 12, "float_slow": 13, "internal": 14,
+       "pool_key": 15}
 
 
 def library_source() -> str:
@@ -91,6 +92,7 @@ class NodeIR:
     inputs: tuple[str, ...] = ()    # body: operator inputs; pre: (column,)
     slot: int | None = None
     writes: tuple[str, ...] = ()
+    ref_pool: bool = False          # the reference runs it on the device from its arena pool
 
 
 @dataclass
@@ -111,6 +113,8 @@ class PlanIR:
     extract_outputs: list[tuple[str, str]] = field(default_factory=list)  # (col, domain)
     stage_strings: bool = True
     mode: str = "pipeline"          # "pipeline" | "extract" (row-aligned _extract_batch)
+    pool_bytes: int = 8 << 20       # the reference arena's capacity (config device.pool_bytes)
+    lanes_per_group: int = 256      # its group size (config device.lanes_per_group)
 
 
 @dataclass
@@ -125,6 +129,13 @@ class Program:
     int_keyed: tuple[int, ...] = ()   # tables with 16-B fbx::ISlot slots
     json_kind: bool = False           # Json-kind extraction: canonical JSON into the pool
     tiles_per_chunk: int = 1          # > 1: chunk cut into 512-row sub-tiles (merged after)
+    # the reference arena's accounting (fbx_pool_account): device token nodes as
+    # (layer, rank, input plane) in the reference's order, key words per row
+    # (~0: rows in table order), lane-size planes, rows per tile
+    ref_pool: tuple = ()
+    pool_kw: int = 0
+    pool_ni: int = 0
+    tile_rows: int = 512
 
 
 # ---------------------------------------------------------------------------
@@ -237,6 +248,18 @@ class PlanCodegen:
         self.pool_sites = 0
         self.json_kind = False
         self._ids_tail: list[str] = []
+        # the reference arena (mempool.py): device token nodes in the reference's
+        # order; nodes on the same input share one plane of per-row lane sizes
+        self.pool_nodes = [nd for nd in ir.nodes if nd.ref_pool]
+        planes: dict[tuple, int] = {}
+        self.pool_plane_of: dict[str, int] = {}
+        for nd in self.pool_nodes:
+            key = ("col", nd.inputs[0]) if nd.role == "pre" else ("post", nd.op)
+            self.pool_plane_of[nd.name] = planes.setdefault(key, len(planes))
+        self.pool_ni = len(planes)
+        self.pool_stored: set[int] = set()
+        self.pool_kw = 0
+        self.pool_kw_bad = False
         self.pf_slot: dict[int, int] = {}
         self.prefetched: dict[tuple, str] = {}
         self.defer_gathers = os.environ.get("FBX_DEFER_GATHERS", "1") != "0"
@@ -322,10 +345,91 @@ class PlanCodegen:
         g("bool exh = false;")
         g(f"{ptr} = fbx::pool_alloc<NT>(sm.scan, &sm.pool_base, ST, POOL, POOL_CAP, "
           f"(u32)({size_expr}), &exh);")
-        g(f"if (exh && ({size_expr}) != 0u && alive) {{ fbx::raise_err(ST, fbx::err_key(chunk, "
-          f"CUR_STAGE, CUR_LAYER, CUR_RANK, {ERR['pool']}u), 0ull); alive = false; }}")
+        g("(void)exh;  // device arena too small: state.pool_overflow, the engine grows it + re-runs")
         g("}")
         return ptr
+
+    # -- the reference arena's demand (fbx_pool_account) -----------------------------
+    def pool_decls(self):
+        """Shared state of the tile's reference-arena bound (pipeline kernel)."""
+        g = self.g
+        ni, kw = max(1, self.pool_ni), max(1, len(self.ir.join_keys) if self.ir.sides else 0)
+        g("// the reference ArenaPool's demand (mempool.py:114-134): per-input CTA sums of the")
+        g("// lane sizes, joined-row count, and per-row key words / sizes / joined flags for")
+        g("// fbx_pool_account when the tile's conservative bound exceeds pool_bytes")
+        g(f"__shared__ unsigned long long fbx_psum[{ni}]; __shared__ u32 fbx_pjoin;")
+        g(f"__shared__ u64 fbx_pkey[{kw}][NT]; __shared__ u32 fbx_psz[{ni}][NT]; __shared__ u8 fbx_pjf[NT];")
+        g(f"if (threadIdx.x < {ni}u) fbx_psum[threadIdx.x] = 0ull;")
+        g("if (threadIdx.x == 0) fbx_pjoin = 0u;")
+        g("__syncthreads();")
+
+    def pool_join_site(self, keys: list[V]):
+        """Key words of the joined table's order (viewpipe.py:451-534: key image,
+        then driver row) and the joined flag of this row."""
+        g = self.g
+        g("// ---- the reference arena's group order: join-key image, then row ----")
+        g("fbx_pjf[RT] = (u8)joined;")
+        self.pool_kw = len(keys)
+        for j, k in enumerate(keys):
+            if k.t in ("i64", "u64", "f32"):  # BE image order == unsigned order of the bits
+                g(f"fbx_pkey[{j}][RT] = (u64){k.c};")
+            else:
+                self.pool_kw_bad = True  # Utf8 keys: the exact accounting fails loudly
+        g("{ const u32 pb = __ballot_sync(0xFFFFFFFFu, joined != 0u);")
+        g("if ((threadIdx.x & 31u) == 0u && pb) atomicAdd(&fbx_pjoin, (u32)__popc(pb)); }")
+
+    def pool_lane(self, nd: NodeIR, a: V):
+        """A device token node's lane size, len(str(v).encode()) or 0 (device.py:
+        328-338, featureops.py:325-326), once per input plane."""
+        if not nd.ref_pool:
+            return
+        plane = self.pool_plane_of[nd.name]
+        if plane in self.pool_stored:
+            return
+        self.pool_stored.add(plane)
+        g = self.g
+        nul = f" && !{a.n}" if a.nullable else ""
+        if self.ir.mode == "extract":
+            g(f"if (inrange) {g.p('pool_sizes', 'u32*')}[{plane}ull * N + row] = "
+              f"(alive{nul}) ? {a.c}.n : 0u;")
+            return
+        g(f"{{ const u32 psz = (joined{nul}) ? {a.c}.n : 0u; fbx_psz[{plane}][RT] = psz;")
+        g("const u32 pws = __reduce_add_sync(0xFFFFFFFFu, psz);")
+        g(f"if ((threadIdx.x & 31u) == 0u && pws) atomicAdd(&fbx_psum[{plane}], "
+          "(unsigned long long)pws); }")
+
+    def pool_tile_check(self):
+        """Thread 0, after the tile's last barrier: the reference demand per layer is
+        at most sum(lane sizes) + 127 per group; a tile whose bound may exceed its
+        share of pool_bytes leaves its rows for fbx_pool_account."""
+        g, ir = self.g, self.ir
+        lpg, cap, spc, tr = ir.lanes_per_group, ir.pool_bytes, self.spc, self.tile_rows
+        g("{")
+        g(f"const u64 PG = ((u64)fbx_pjoin + {lpg - 1}ull) / {lpg}ull;")
+        g("bool pneed = false;")
+        layers: dict[int, list[int]] = {}
+        for nd in self.pool_nodes:
+            layers.setdefault(nd.layer, []).append(self.pool_plane_of[nd.name])
+        for layer, planes in sorted(layers.items()):
+            terms = " + ".join(f"(fbx_psum[{p}] ? fbx_psum[{p}] + 127ull * PG : 0ull)"
+                               for p in planes)
+            g(f"if (({terms}) * {spc}ull > {cap}ull) pneed = true;  // layer {layer}")
+        g(f"{g.p('pool_flag', 'u8*')}[tile] = (u8)pneed;")
+        g("if (pneed) {")
+        if self.pool_kw_bad:
+            g(f"fbx::raise_err(ST, fbx::err_key(chunk, 4u, 0u, 0u, {ERR['pool_key']}u), 0ull);  // Utf8 join keys")
+        g(f"{g.p('pool_chunk', 'u64*')}[tile] = chunk;")
+        g("atomicAdd((unsigned long long*)&ST->pool_flagged, 1ull);")
+        g(f"const u64 PL = {g.p('pool_plane')}, PB = (u64)tile * {tr}ull;")
+        g(f"for (u32 r = 0; r < {tr}u; ++r) {{")
+        g(f"{g.p('pool_joined', 'u8*')}[PB + r] = fbx_pjf[r];")
+        for j in range(self.pool_kw):
+            g(f"{g.p('pool_keys', 'u64*')}[{j}ull * PL + PB + r] = fbx_pkey[{j}][r];")
+        for p in range(self.pool_ni):
+            g(f"{g.p('pool_sizes', 'u32*')}[{p}ull * PL + PB + r] = fbx_psz[{p}][r];")
+        g("}")
+        g("}")
+        g("}")
 
     # -- column access --------------------------------------------------------------
     def load_driver_column(self, name: str, kind: Kind) -> V:
@@ -782,6 +886,7 @@ class PlanCodegen:
             (col, delim), fields = self.token_groups[nd.name]
             gk = f"{col}|{delim}"
             a = args[0]
+            self.pool_lane(nd, a)
             if gk not in self.token_done:
                 base = g.fresh("tg")
                 kk = len(fields)
@@ -803,6 +908,7 @@ class PlanCodegen:
             return out
         if op == "token":
             a = self.as_str(args[0], fn.spec)
+            self.pool_lane(nd, a)
             if a.lower and fn.delim.isascii() and fn.delim.isalpha():
                 a = self.materialize(a)  # a letter delimiter must see lowered bytes
             out = V("str", g.fresh("n"), a.nullable, a.lone, a.lower)
@@ -1106,6 +1212,8 @@ class PlanCodegen:
         g("u64 span_lo[16]; u32 span_len[16];")
         g("u64 red[NT / 32][4];")
         g("} sm;")
+        if self.pool_nodes:
+            self.pool_decls()
         if self.phase_timers:
             g("u64 ph_t = clock64();")
         g("// tiles in blockIdx order: the hardware dispatches CTAs in order, so every")
@@ -1288,6 +1396,8 @@ class PlanCodegen:
                     env[c] = ("side", k, c)
         g("u32 joined = alive ? 1u : 0u;")
         self.env = env
+        if self.pool_nodes:
+            self.pool_join_site([env[c] for c in ir.join_keys] if ir.sides else [])
         # ---- basic merge probe (side-effect free; the drop is applied later) -------
         idv = env[ir.instance_column]
         if ir.basic is not None:
@@ -1595,6 +1705,8 @@ class PlanCodegen:
         g("if (r1) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)r1);")
         g("if (r2) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)r2);")
         g("if (r3) atomicAdd((unsigned long long*)&ST->joined, (unsigned long long)r3);")
+        if self.pool_nodes:
+            self.pool_tile_check()
         g("}")
 
     def emit_lookback(self):
@@ -1721,6 +1833,9 @@ class PlanCodegen:
             return out
         return v
 
+    def pool_program(self) -> tuple:
+        return tuple((nd.layer, nd.rank, self.pool_plane_of[nd.name]) for nd in self.pool_nodes)
+
     # ------------------------------------------------------------------------------------
     def generate(self) -> Program:
         ir = self.ir
@@ -1765,7 +1880,8 @@ class PlanCodegen:
                     f"__device__ const __align__(16) u8 K_STR[] = {_c_bytes(consts + bytes(16))};",
                     *self.globals, ""]
             return Program("\n".join(head + self.g.lines), dict(self.g.slots), 256, 0,
-                           [kname], [], self.notes)
+                           [kname], [], self.notes, ref_pool=self.pool_program(),
+                           pool_kw=0xFFFFFFFF, pool_ni=self.pool_ni)
         side_names = []
         for k, sv in enumerate(ir.sides):
             side_names.append(self.side_prep_kernel(k, sv, False))
@@ -1786,7 +1902,8 @@ class PlanCodegen:
         nt_ = len(ir.sides) + (1 if ir.basic is not None else 0)
         return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes,
                        tuple(k for k in range(nt_) if self.int_keyed(k)),
-                       self.json_kind, self.spc)
+                       self.json_kind, self.spc, self.pool_program(), self.pool_kw,
+                       self.pool_ni, self.tile_rows)
 
 
 def _filter_columns(expr) -> set[str]:

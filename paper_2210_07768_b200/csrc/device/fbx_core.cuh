@@ -653,7 +653,11 @@ struct BlockScanU32 {
 // Block bump allocation from the HBM arena (Algorithm 1; reference
 // mempool.py:114-134): exclusive prefix of lane sizes, ONE atomicAdd per CTA,
 // 128-byte group alignment.  Returns the lane's pointer (nullptr when its size
-// is 0 or the pool is exhausted -- then *exhausted is set CTA-uniformly).
+// is 0 or the arena is exhausted -- then *exhausted is set, CTA-uniformly for
+// the CTA grant and warp-uniformly for the warp grant).  This is the engine's
+// own arena: running out of it is not the reference's PoolExhausted (that is
+// the config's pool_bytes, settled by fbx_pool_account) -- the run is repeated
+// with an arena of state.pool_overflow bytes.
 template <int NT>
 FBX_DI u8* pool_alloc(BlockScanU32<NT>& scan, u64* base_smem, fbx_state* st, u8* pool,
                       u64 pool_cap, u32 size, bool* exhausted) {
@@ -674,9 +678,8 @@ FBX_DI u8* pool_alloc(BlockScanU32<NT>& scan, u64* base_smem, fbx_state* st, u8*
   if (lane == 31u) {
     const u64 tot = ((u64)total + 15ull) & ~15ull;
     b = atomicAdd((unsigned long long*)&st->pool_head, (unsigned long long)tot);
-    if (b + tot > pool_cap) {
-      const u64 rem = b < pool_cap ? pool_cap - b : 0ull;
-      atomicMax((unsigned long long*)&st->pool_overflow, (unsigned long long)((tot << 32) | (rem & 0xFFFFFFFFull)));
+    if (b + tot > pool_cap) {  // the head this launch needs: the engine grows the arena
+      atomicMax((unsigned long long*)&st->pool_overflow, (unsigned long long)(b + tot));
       b = ~0ull;
     }
   }
@@ -694,10 +697,8 @@ FBX_DI u8* pool_alloc(BlockScanU32<NT>& scan, u64* base_smem, fbx_state* st, u8*
   if (threadIdx.x == 0) {
     u64 tot = ((u64)total + 127ull) & ~127ull;
     u64 b = tot ? atomicAdd((unsigned long long*)&st->pool_head, (unsigned long long)tot) : 0ull;
-    if (tot && b + tot > pool_cap) {
-      // exhausted: report (requested, remaining) like PoolExhausted
-      u64 rem = b < pool_cap ? pool_cap - b : 0ull;
-      atomicMax((unsigned long long*)&st->pool_overflow, (unsigned long long)((tot << 32) | (rem & 0xFFFFFFFFull)));
+    if (tot && b + tot > pool_cap) {  // the head this launch needs: the engine grows the arena
+      atomicMax((unsigned long long*)&st->pool_overflow, (unsigned long long)(b + tot));
       b = ~0ull;
     }
     *base_smem = b;

@@ -198,6 +198,98 @@ __global__ void k_gather_strings(const unsigned long long* ptrs, const unsigned 
   }
 }
 
+// ---- the reference ArenaPool's exact demand for flagged chunks ---------------
+// PoolExhausted semantics (mempool.py:114-134, device.py:181-196, 328-338,
+// 408-409): per chunk and layer the head starts at 0; every device-placed token
+// node, in the reference's order, takes one grant of round_up_128(sum of lane
+// sizes) per group of lanes_per_group consecutive rows of the JOINED table
+// (ordered by join-key image, then driver row: viewpipe.py:451-534); the first
+// grant past capacity raises PoolExhausted(requested, remaining) at that node.
+// The plan kernel flags a tile whose conservative bound may exceed capacity and
+// leaves its rows' key words / lane sizes / joined flags in scratch; one CTA
+// per chunk settles it here.  Quadratic ranking: a rare, failing-path check.
+struct PoolAcct {
+  const unsigned char* tile_flag;
+  const unsigned long long* tile_chunk;
+  const unsigned long long* keys;   // kw planes of n_tiles * tile_rows
+  const unsigned int* sizes;        // ni planes
+  const unsigned char* joined;
+  const fbx_pool_node* nodes;
+  unsigned int* rank;               // scratch: n_tiles * tile_rows
+  unsigned long long* gsum;         // scratch: n_tiles * tile_rows
+  unsigned long long n_tiles, lpg, cap;
+  unsigned int spc, tile_rows, kw, ni, n_nodes;
+};
+
+__device__ __forceinline__ bool pool_key_less(const PoolAcct& a, size_t plane, size_t i,
+                                              size_t j) {
+  for (unsigned k = 0; k < a.kw; ++k) {
+    const unsigned long long x = a.keys[k * plane + i], y = a.keys[k * plane + j];
+    if (x != y) return x < y;
+  }
+  return i < j;  // then driver row
+}
+
+__global__ void __launch_bounds__(512) k_pool_account(PoolAcct a, fbx_state* st) {
+  const unsigned long long t0 = (unsigned long long)blockIdx.x * a.spc;
+  if (t0 >= a.n_tiles) return;
+  const unsigned long long t1 = min(t0 + a.spc, a.n_tiles);
+  bool any = a.tile_flag == nullptr;  // no flags: every chunk
+  for (unsigned long long t = t0; t < t1 && !any; ++t) any = a.tile_flag[t] != 0;
+  if (!any) return;
+  const size_t plane = (size_t)a.n_tiles * a.tile_rows;
+  const size_t r0 = (size_t)t0 * a.tile_rows, n = (size_t)(t1 - t0) * a.tile_rows;
+  const unsigned long long chunk = a.tile_chunk ? a.tile_chunk[t0] : 0ull;
+  __shared__ unsigned long long s_head, s_stop;
+  __shared__ unsigned int s_nj;
+  if (threadIdx.x == 0) { s_nj = 0; s_stop = 0; }
+  __syncthreads();
+  // rank of every joined row in the joined table's order (kw == ~0: a table
+  // handed to _extract_batch as is -- every row, in row order)
+  const bool table_order = a.kw == 0xFFFFFFFFu;
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) {
+    if (table_order) { a.rank[r0 + i] = (unsigned)i; continue; }
+    if (!a.joined[r0 + i]) continue;
+    atomicAdd(&s_nj, 1u);
+    unsigned int r = 0;
+    for (size_t j = 0; j < n; ++j)
+      if (a.joined[r0 + j] && pool_key_less(a, plane, r0 + j, r0 + i)) ++r;
+    a.rank[r0 + i] = r;
+  }
+  if (table_order && threadIdx.x == 0) s_nj = (unsigned)n;
+  __syncthreads();
+  const unsigned long long groups = (s_nj + a.lpg - 1) / a.lpg;
+  unsigned int layer = 0;
+  if (threadIdx.x == 0) s_head = 0;
+  for (unsigned q = 0; q < a.n_nodes; ++q) {
+    const fbx_pool_node nd = a.nodes[q];
+    for (size_t g = threadIdx.x; g < groups; g += blockDim.x) a.gsum[r0 + g] = 0ull;
+    __syncthreads();
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x)
+      if (table_order || a.joined[r0 + i])
+        atomicAdd(&a.gsum[r0 + a.rank[r0 + i] / a.lpg],
+                  (unsigned long long)a.sizes[(size_t)nd.input * plane + r0 + i]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (nd.layer != layer) { layer = nd.layer; s_head = 0; }  // reset at the layer barrier
+      for (unsigned long long g = 0; g < groups; ++g) {
+        const unsigned long long tot = (a.gsum[r0 + g] + 127ull) & ~127ull;
+        if (!tot) continue;
+        if (s_head + tot > a.cap) {
+          fbx::raise_err(st, fbx::err_key(chunk, FBX_STAGE_EXTRACT, nd.layer, nd.rank,
+                                          FBX_ERR_POOL),
+                         (tot << 32) | ((a.cap - s_head) & 0xFFFFFFFFull));
+          s_stop = 1;
+          break;
+        }
+        s_head += tot;
+      }
+    }
+    __syncthreads();
+    if (s_stop) return;
+  }
+}
+
 __global__ void k_flush(unsigned int* buf, size_t n) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
@@ -455,6 +547,22 @@ int fbx_pool_reset(fbx_state* d_state, void* stream) {
   static_assert(offsetof(fbx_state, pool_head) == offsetof(fbx_state, tile_ticket) + 8, "layout");
   return cuda_check(cudaMemsetAsync(&d_state->tile_ticket, 0, 16, (cudaStream_t)stream),
                     "fbx_pool_reset");
+}
+
+int fbx_pool_account(const unsigned char* d_tile_flag, const unsigned long long* d_tile_chunk,
+                     unsigned long long n_tiles, unsigned spc, unsigned tile_rows,
+                     const unsigned long long* d_keys, unsigned kw, const unsigned* d_sizes,
+                     unsigned ni, const unsigned char* d_joined, const fbx_pool_node* d_nodes,
+                     unsigned n_nodes, unsigned long long lanes_per_group,
+                     unsigned long long capacity, unsigned* d_rank_scratch,
+                     unsigned long long* d_sum_scratch, fbx_state* d_state, void* stream) {
+  if (!spc || !tile_rows || !lanes_per_group) return fail(FBX_E_ARG, "fbx_pool_account: zero size");
+  if (!n_tiles || !n_nodes) return FBX_OK;
+  PoolAcct a{d_tile_flag, d_tile_chunk, d_keys, d_sizes, d_joined, d_nodes, d_rank_scratch,
+             d_sum_scratch, n_tiles, lanes_per_group, capacity, spc, tile_rows, kw, ni, n_nodes};
+  const unsigned long long chunks = (n_tiles + spc - 1) / spc;
+  k_pool_account<<<(unsigned)chunks, 512, 0, (cudaStream_t)stream>>>(a, d_state);
+  return cuda_check(cudaGetLastError(), "fbx_pool_account");
 }
 
 int fbx_state_snapshot(const fbx_state* d_state, void* h_mapped_dst, void* stream) {

@@ -38,8 +38,9 @@ from .config import (ConfigError, EmitError, BatchInvariantError, CleanConfigErr
                      StageError, UnsupportedOnDevice, bind_filter, cleaned_kinds,
                      validate_clean_policy)
 from .featureops import FeatureConfigError, output_domains, resolve_function
-from .opgraph import (OperatorDag, LayerPlan, PlacementBudget, expand_call_graph,
-                      layer_schedule, place_operators)
+from .opgraph import (DEVICE, OperatorDag, LayerPlan, PlacementBudget, expand_call_graph,
+                      layer_schedule, place_operators, reference_node_order,
+                      reference_placement)
 
 STAGE_NAMES = {v: k for k, v in codegen.STAGE.items()}
 ERR_NAMES = {v: k for k, v in codegen.ERR.items()}
@@ -178,7 +179,8 @@ def prepare(config: PipelineConfig, views: Mapping[str, ViewImage] | None = None
         return codegen.ViewIR(name, dict(raw[name]), dict(pol.fills), list(pol.extractions),
                               flt, keys)
 
-    order = plan.node_order()
+    refplace = reference_placement(dag, config.device_budget_bytes)
+    order = reference_node_order(plan, refplace)
     rank = {n: i for i, (_, n) in enumerate(order)}
     specs = {s.name: s for s in config.operators}
     pre_of: dict[str, dict[int, str]] = {}
@@ -192,8 +194,10 @@ def prepare(config: PipelineConfig, views: Mapping[str, ViewImage] | None = None
             inputs = specs[nd.op].inputs
         else:
             inputs = ()
+        ref_pool = (fns[name].op == "token" and nd.role != "body"
+                    and refplace[name] == DEVICE)
         nodes.append(codegen.NodeIR(name, nd.role, nd.op, fns[name], layer, rank[name],
-                                    tuple(inputs), nd.slot, nd.writes))
+                                    tuple(inputs), nd.slot, nd.writes, ref_pool))
     tables = {t: i for i, t in enumerate(sorted(config.tables))}
     ir = codegen.PlanIR(
         driver=view_ir(config.driver),
@@ -204,7 +208,8 @@ def prepare(config: PipelineConfig, views: Mapping[str, ViewImage] | None = None
         instance_column=config.instance_column, label_column=config.label_column,
         chunk=config.batch_size, tables=tables,
         table_defaults={t: config.tables[t].default for t in config.tables},
-        extract_outputs=[(c, d) for c, _, d in extract_outputs], stage_strings=stage_strings)
+        extract_outputs=[(c, d) for c, _, d in extract_outputs], stage_strings=stage_strings,
+        pool_bytes=config.pool_bytes, lanes_per_group=config.lanes_per_group)
     prog = codegen.generate(ir)
     cubin = runtime.compile_source(prog.source) if compile_program else b""
     return Prepared(config, dag, plan, ir, prog, cubin, tuple(extract_outputs),
@@ -558,9 +563,6 @@ class Engine:
                 if ek < key:
                     key, detail = ek, st["emit_detail"]
         if key == (1 << 64) - 1:
-            if st["pool_overflow"]:
-                req, rem = st["pool_overflow"] >> 32, st["pool_overflow"] & 0xFFFFFFFF
-                raise StageError("extract", None, PoolExhausted(req, rem))
             return
         chunk = key >> 32
         stage = STAGE_NAMES.get((key >> 28) & 0xF, "extract")
@@ -575,9 +577,33 @@ class Engine:
 
     def check_run(self, st: dict):
         """End of a run: note whether the id set saw a repeat (its pair array
-        then needs clearing) and raise the run's first failure."""
+        then needs clearing), repeat the run if the device arena ran out
+        (ArenaRetry), settle the reference arena's PoolExhausted for flagged
+        chunks (fbx_pool_account) and raise the run's first failure."""
         self._dup_dirty = bool(st["dup_seen"])
+        if st["pool_overflow"]:
+            raise ArenaRetry(st["pool_overflow"])
+        if st["pool_flagged"]:
+            self._pool_account()
+            st = dict(st, **{k: v for k, v in self._read_state().items()
+                             if k in ("error_key", "error_detail")})
         self._raise_if_error(st)
+
+    def _pool_account(self):
+        p = self.prog
+        runtime.pool_account(self.pool_flag.data_ptr(), self.pool_chunk.data_ptr(),
+                             self._run_tiles, p.tiles_per_chunk, p.tile_rows,
+                             self.pool_keys.data_ptr(), p.pool_kw, self.pool_sizes.data_ptr(),
+                             p.pool_ni, self.pool_joined.data_ptr(), self.pool_nodes.data_ptr(),
+                             len(p.ref_pool), self.config.lanes_per_group,
+                             self.config.pool_bytes, self.pool_rank.data_ptr(),
+                             self.pool_gsum.data_ptr(), self.state.data_ptr(), self._stream())
+
+    def grow_arena(self, need: int):
+        """Size the device arena for ``need`` bytes per launch (+25 %) and drop the
+        run buffers so the next ``reserve`` reallocates them."""
+        self._arena_min = max(getattr(self, "_arena_min", 0), int(need * 1.25) + (1 << 20))
+        self._arena_key = None
 
     def _dup_key(self) -> tuple[int, int]:
         """(error key, id) of check_unique_ids' failure: the merge of the chunk
@@ -729,7 +755,7 @@ class Engine:
         launch_rows = rows if launch_rows is None else max(1, min(launch_rows, rows))
         tiles = self.tiles_for(rows)
         k = max(1, len(self.ir.features))
-        need = (tiles, rows, k, launch_rows)
+        need = (tiles, rows, k, launch_rows, getattr(self, "_arena_min", 0))
         if getattr(self, "_arena_key", None) != need:
             dev = self.device
             self.status = torch.zeros(tiles + 1, dtype=torch.int64, device=dev)
@@ -742,8 +768,28 @@ class Engine:
             if codegen_pool_sites(self.prog):
                 lt = (launch_rows + self.ir.chunk - 1) // self.ir.chunk
                 pool_cap = self.pool_bytes_per_row * launch_rows + 128 * lt * 8 + (1 << 20)
+                pool_cap = max(pool_cap, getattr(self, "_arena_min", 0))
             self.pool = torch.empty(pool_cap + 256, dtype=torch.uint8, device=dev)
             self.pool_cap = pool_cap
+            if self.prog.ref_pool:  # rows of flagged tiles for fbx_pool_account
+                p = self.prog
+                plane = tiles * p.tile_rows
+                self.pool_flag = torch.zeros(tiles + 1, dtype=torch.uint8, device=dev)
+                self.pool_chunk = torch.zeros(tiles + 1, dtype=torch.int64, device=dev)
+                self.pool_keys = torch.zeros(max(1, p.pool_kw) * plane + 1, dtype=torch.int64,
+                                             device=dev)
+                self.pool_sizes = torch.zeros(p.pool_ni * plane + 1, dtype=torch.int32, device=dev)
+                self.pool_joined = torch.zeros(plane + 1, dtype=torch.uint8, device=dev)
+                self.pool_rank = torch.zeros(plane + 1, dtype=torch.int32, device=dev)
+                self.pool_gsum = torch.zeros(plane + 1, dtype=torch.int64, device=dev)
+                self.pool_nodes = torch.tensor([[l, r, i, 0] for l, r, i in p.ref_pool],
+                                               dtype=torch.int32, device=dev)
+                self._set("pool_flag", self.pool_flag.data_ptr())
+                self._set("pool_chunk", self.pool_chunk.data_ptr())
+                self._set("pool_keys", self.pool_keys.data_ptr())
+                self._set("pool_sizes", self.pool_sizes.data_ptr())
+                self._set("pool_joined", self.pool_joined.data_ptr())
+                self._set("pool_plane", plane)
             self._arena_key = need
         self._set("tile_status", self.status.data_ptr())
         self._set("out.ids", self.o_ids.data_ptr())
@@ -939,12 +985,17 @@ class StreamedRun:
                                       "chunks are merged on the device before their D2H)")
 
     def run(self) -> Counters:
-        if self.zero_copy:
-            return self._run_zero_copy()
-        self.start()
-        tot = self.finish()
-        self.wait()
-        return tot
+        while True:
+            try:
+                if self.zero_copy:
+                    return self._run_zero_copy()
+                self.start()
+                tot = self.finish()
+                self.wait()
+                return tot
+            except ArenaRetry as exc:  # the device arena was too small: grow, repeat
+                self.wait()
+                self.eng.grow_arena(exc.need)
 
     def start(self):
         """Enqueue every slice's H2D and fused kernel (no host synchronisation).
@@ -1122,6 +1173,16 @@ class StreamedRun:
                 "signs": o["signs"][:m].numpy().view(np.uint64)}
 
 
+class ArenaRetry(Exception):
+    """The engine's own device arena was too small for a run (``need`` bytes per
+    launch): not a reference failure -- the caller grows the arena and repeats
+    the run (``Engine.grow_arena``)."""
+
+    def __init__(self, need: int):
+        super().__init__(f"device arena needs {need} bytes")
+        self.need = need
+
+
 def codegen_pool_sites(prog: codegen.Program) -> bool:
     return "fbx::pool_alloc<NT>" in prog.source.split("// ===== generated plan =====", 1)[-1]
 
@@ -1131,9 +1192,10 @@ def _cause(code: str, detail: int, st: dict) -> BaseException:
         return TypeError("unsupported operand type for mix/fold")
     if code == "encode":
         return UnicodeEncodeError("utf-8", "", 0, 1, "surrogates not allowed")
-    if code == "pool":
-        req, rem = st["pool_overflow"] >> 32, st["pool_overflow"] & 0xFFFFFFFF
-        return PoolExhausted(req, rem)
+    if code == "pool":  # fbx_pool_account: (requested << 32) | remaining
+        return PoolExhausted(detail >> 32, detail & 0xFFFFFFFF)
+    if code == "pool_key":
+        return UnsupportedOnDevice("reference arena accounting over Utf8 join keys")
     if code == "null_label":
         return EmitError("null label at emission")
     if code == "label_range":
@@ -1244,16 +1306,21 @@ def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: Vie
     # one reserved run: the look-back, the CSR positions and the id set span
     # every launch, so emission order and error placement are run-global
     step = eng.max_rows
-    eng.reserve(n, min(step, max(n, 1)))
-    eng.begin_run(n)
     t2 = time.perf_counter()
-    tiles = 0
-    launches = 0
-    for lo in range(0, n, step):
-        hi = min(lo + step, n)
-        tiles += eng.launch(lo, hi, tile_base=tiles)
-        launches += 1
-    b = eng.finish()
+    while True:
+        eng.reserve(n, min(step, max(n, 1)))
+        eng.begin_run(n)
+        tiles = 0
+        launches = 0
+        for lo in range(0, n, step):
+            hi = min(lo + step, n)
+            tiles += eng.launch(lo, hi, tile_base=tiles)
+            launches += 1
+        try:
+            b = eng.finish()
+            break
+        except ArenaRetry as exc:  # the device arena was too small: grow, repeat the run
+            eng.grow_arena(exc.need)
     total = b.counters
     total.launches = launches
     stage["extract"] = time.perf_counter() - t2
@@ -1327,7 +1394,8 @@ def prepare_extract(config: PipelineConfig, table_kinds: Mapping[str, Kind]) -> 
                 raise ConfigError(f"output column {col!r} collides with a table column")
             extract_outputs.append((col, Kind.INT64 if domains[col] == "u64" else Kind.UTF8,
                                     domains[col]))
-    order = plan.node_order()
+    refplace = reference_placement(dag, config.device_budget_bytes)
+    order = reference_node_order(plan, refplace)
     rank = {n: i for i, (_, n) in enumerate(order)}
     specs = {s.name: s for s in config.operators}
     pre_of: dict[str, dict[int, str]] = {}
@@ -1341,8 +1409,10 @@ def prepare_extract(config: PipelineConfig, table_kinds: Mapping[str, Kind]) -> 
             inputs = specs[nd.op].inputs
         else:
             inputs = ()
+        ref_pool = (fns[name].op == "token" and nd.role != "body"
+                    and refplace[name] == DEVICE)
         nodes.append(codegen.NodeIR(name, nd.role, nd.op, fns[name], layer, rank[name],
-                                    tuple(inputs), nd.slot, nd.writes))
+                                    tuple(inputs), nd.slot, nd.writes, ref_pool))
     ir = codegen.PlanIR(
         driver=codegen.ViewIR("table", kinds, {}, [], None), sides=[], basic=None,
         join_keys=(), nodes=nodes, pre_of=pre_of, producer=dict(dag.col_producer),
@@ -1350,7 +1420,7 @@ def prepare_extract(config: PipelineConfig, table_kinds: Mapping[str, Kind]) -> 
         chunk=256, tables={t: i for i, t in enumerate(sorted(config.tables))},
         table_defaults={t: config.tables[t].default for t in config.tables},
         extract_outputs=[(c, d) for c, _, d in extract_outputs], stage_strings=False,
-        mode="extract")
+        mode="extract", pool_bytes=config.pool_bytes, lanes_per_group=config.lanes_per_group)
     prog = codegen.generate(ir)
     return Prepared(config, dag, plan, ir, prog, runtime.compile_source(prog.source),
                     tuple(extract_outputs), [n for _, n in order], {"table": kinds}, {})
@@ -1387,10 +1457,24 @@ class ExtractEngine(Engine):
             for part in ("nulls", "data", "offsets"):
                 self._set(f"drv.{c}.{part}", dv.ptr(c, part))
         self._set("rows", n)
+        while True:
+            try:
+                return self._extract_once(table, dv, n)
+            except ArenaRetry as exc:  # the device arena was too small: grow, repeat
+                self._arena_min = int(exc.need * 1.25) + (1 << 16)
+
+    def _extract_once(self, table: ViewImage, dv, n: int) -> ViewImage:
+        torch = self.torch
+        dev = self.device
         pool_cap = self.pool_bytes_per_row * n + 128 * ((n + 255) // 256) * 8 + (1 << 16)
+        pool_cap = max(pool_cap, getattr(self, "_arena_min", 0))
         pool = torch.empty(pool_cap + 256, dtype=torch.uint8, device=dev)
         self._set("pool", pool.data_ptr())
         self._set("pool_cap", pool_cap)
+        p = self.prog
+        if p.ref_pool:  # lane sizes of the device token nodes, per row
+            sizes = torch.zeros(p.pool_ni * max(n, 1) + 1, dtype=torch.int32, device=dev)
+            self._set("pool_sizes", sizes.data_ptr())
         outs = []
         words = (n + 31) // 32 + 1
         for j, (col, kind, domain) in enumerate(self.prepared.extract_outputs):
@@ -1411,9 +1495,20 @@ class ExtractEngine(Engine):
         runtime.state_reset(self.state.data_ptr(), status.data_ptr(), 1, stream)
         grid = max(1, min((n + 255) // 256, 148 * 8))
         self.module.launch("fbx_extract_rows", grid, 256, 0, stream, self.params)
+        if p.ref_pool and n:  # the reference arena over this table, in row order
+            rank = torch.empty(n + 1, dtype=torch.int32, device=dev)
+            gsum = torch.empty(n + 1, dtype=torch.int64, device=dev)
+            nodes = torch.tensor([[l, r, i, 0] for l, r, i in p.ref_pool], dtype=torch.int32,
+                                 device=dev)
+            runtime.pool_account(0, 0, 1, 1, n, 0, 0xFFFFFFFF, sizes.data_ptr(), p.pool_ni, 0,
+                                 nodes.data_ptr(), len(p.ref_pool), self.config.lanes_per_group,
+                                 self.config.pool_bytes, rank.data_ptr(), gsum.data_ptr(),
+                                 self.state.data_ptr(), stream)
         st = self._read_state()
+        if st["pool_overflow"]:
+            raise ArenaRetry(st["pool_overflow"])
         key = st["error_key"]
-        if key != (1 << 64) - 1 or st["pool_overflow"]:
+        if key != (1 << 64) - 1:
             try:
                 self._raise_if_error(st)
             except StageError as exc:

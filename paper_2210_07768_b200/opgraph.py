@@ -197,6 +197,23 @@ def place_operators(plan: LayerPlan, budget: PlacementBudget | None,
     return placed
 
 
+def reference_placement(dag: OperatorDag, budget_bytes: int | float) -> dict[str, str]:
+    """Where the REFERENCE would run each node: host iff its footprint exceeds the
+    device budget (opgraph.py:295-324).  The B200 runs every node on the device,
+    but two results depend on this: which token calls draw from the reference's
+    arena pool (device.py:328-338) and which failure a layer reports first --
+    its device nodes in name order, then its host nodes (device.py:362-406)."""
+    return {n: HOST if nd.footprint_bytes > budget_bytes else DEVICE
+            for n, nd in dag.nodes.items()}
+
+
+def reference_node_order(plan: LayerPlan, placement: Mapping[str, str]) -> list[tuple[int, str]]:
+    """(layer, name) in the reference's failure-precedence order: per layer the
+    device nodes by name, then the host nodes by name."""
+    return [(i + 1, n) for i, layer in enumerate(plan.layers)
+            for n in sorted(layer, key=lambda m: (placement[m] != DEVICE, m))]
+
+
 def validate_plan(plan: LayerPlan, dag: OperatorDag) -> None:
     layer_of = plan.layer_of
     if set(layer_of) != set(dag.nodes):

@@ -24,7 +24,7 @@ _lib = None
 FBX_MAX_PARAM_SLOTS = 384
 STATE_FIELDS = ("tile_ticket", "pool_head", "pool_overflow", "error_key", "error_detail",
                 "digest", "instances", "signs", "malformed", "filtered", "joined", "side_rows",
-                "dup_seen", "emit_key", "emit_detail", "reserved")
+                "dup_seen", "emit_key", "emit_detail", "pool_flagged")
 STATE_BYTES = 8 * len(STATE_FIELDS)
 
 EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_program_load",
@@ -32,7 +32,8 @@ EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_prog
            "fbx_kernel_set_max_dynamic_smem", "fbx_launch", "fbx_state_reset",
            "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
            "fbx_dup_resolve", "fbx_state_snapshot",
-           "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words", "fbx_idset_clear")
+           "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words", "fbx_idset_clear",
+           "fbx_pool_account")
 
 
 class FbxError(RuntimeError):
@@ -72,6 +73,9 @@ def lib() -> ctypes.CDLL:
             L.fbx_state_snapshot.argtypes = [vp, vp, vp]
             L.fbx_pool_reset.argtypes = [vp, vp]
             L.fbx_idset_clear.argtypes = [vp, sz, vp, sz, vp, vp]
+            u, ull = ctypes.c_uint, ctypes.c_ulonglong
+            L.fbx_pool_account.argtypes = [vp, vp, ull, u, u, vp, u, vp, u, vp, vp, u, ull, ull,
+                                           vp, vp, vp, vp]
             L.fbx_crc32.argtypes = [vp, ctypes.c_ulonglong, vp, vp, vp]
             L.fbx_crc32_scratch_words.argtypes = [ctypes.c_ulonglong]
             L.fbx_crc32_scratch_words.restype = ctypes.c_ulonglong
@@ -214,6 +218,17 @@ def dup_resolve(d_winner: int, d_later: int, n_slots: int, d_out: int, stream: i
     _check(lib().fbx_dup_resolve(ctypes.c_void_p(d_winner), ctypes.c_void_p(d_later),
                                  int(n_slots), ctypes.c_void_p(d_out), ctypes.c_void_p(stream)),
            "dup resolve")
+
+
+def pool_account(d_flag: int, d_chunk: int, n_tiles: int, spc: int, tile_rows: int,
+                 d_keys: int, kw: int, d_sizes: int, ni: int, d_joined: int, d_nodes: int,
+                 n_nodes: int, lanes_per_group: int, capacity: int, d_rank: int, d_sum: int,
+                 d_state: int, stream: int):
+    vp = ctypes.c_void_p
+    _check(lib().fbx_pool_account(vp(d_flag), vp(d_chunk), n_tiles, spc, tile_rows, vp(d_keys),
+                                  kw, vp(d_sizes), ni, vp(d_joined), vp(d_nodes), n_nodes,
+                                  lanes_per_group, capacity, vp(d_rank), vp(d_sum), vp(d_state),
+                                  vp(stream)), "pool account")
 
 
 def exclusive_scan_u32(d_in: int, d_out: int, n: int, stream: int):

@@ -553,3 +553,54 @@ def test_engine_reused_after_a_duplicate_id_run(tmp_path):
             ref = O.run_pipelined(raw, views, bas, tables, sizes)
             assert (got.digest, got.instances, got.signs) == (ref.digest, ref.instances,
                                                               ref.signs)
+
+
+POOL_OPS = [
+    {"name": "t0", "inputs": ["query"], "outputs": ["t0"], "pre": [{"fn": "token: :0"}],
+     "body": {"fn": "hash:3"}},
+    {"name": "t1", "inputs": ["query"], "outputs": ["t1"], "pre": [{"fn": "token: :1"}],
+     "body": {"fn": "hash:4"}},
+    {"name": "tx", "inputs": ["cx"], "outputs": ["tx"], "pre": [{"fn": "token:u:0"}],
+     "body": {"fn": "hash:5"}},
+    {"name": "th", "inputs": ["city"], "outputs": ["th"],   # host-placed: no arena
+     "pre": [{"fn": "token:a:1", "footprint_bytes": 1 << 30}], "body": {"fn": "hash:6"}},
+    {"name": "cc", "inputs": ["city", "query"], "outputs": ["cc"], "body": {"fn": "concat:+"}},
+    {"name": "tc", "inputs": ["cc"], "outputs": ["tc"], "pre": [{"fn": "token:+:1"}],
+     "body": {"fn": "hash:7"}},
+    {"name": "ta", "inputs": ["age"], "outputs": ["ta"], "pre": [{"fn": "token:1:0"}],
+     "body": {"fn": "hash:8"}},
+]
+POOL_FEATS = {"t0": 3, "t1": 4, "tx": 5, "th": 6, "tc": 7, "ta": 8}
+
+
+POOL_CASES = [(128, 256, 512, "all"), (1024, 7, 64, "all"), (4096, 256, 512, "all"),
+              (4096, 100, 1500, "all"), (3200, 7, 64, "all"), (8960, 1, 40, "all"),
+              (4096, 7, 64, "all"), (8 << 20, 256, 512, "all"), (8 << 20, 100, 1500, "all"),
+              (1024, 256, 512, "layer2"), (2048, 3, 100, "layer2")]
+
+
+@pytest.mark.parametrize("pool,lpg,batch_size,ops", POOL_CASES)
+def test_pool_bytes_matches_reference(pool, lpg, batch_size, ops, tmp_path):
+    """config device.pool_bytes / lanes_per_group: the reference ArenaPool's
+    PoolExhausted (mempool.py:114-134) -- same chunk, layer, node, requested and
+    remaining bytes -- or the same run when nothing exhausts."""
+    drv, prof, bas = _views(2000, 9)
+    _write_views(tmp_path, drv, prof, bas)
+    dag = POOL_OPS if ops == "all" else [o for o in POOL_OPS if o["name"] in ("cc", "tc")]
+    feats = {k: v for k, v in POOL_FEATS.items() if any(o["name"] == k for o in dag)}
+    raw = _config(batch_size, dag, feats, filt="age != -12345")
+    raw["device"] = {"budget_bytes": 65536, "pool_bytes": pool, "lanes_per_group": lpg}
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    if ref_err is None:
+        assert got_err is None, got_err
+        assert (got.report.digest, got.report.instances, got.report.signs) == \
+            (ref.digest, ref.instances, ref.signs)
+        return
+    assert got_err is not None, "engine did not fail"
+    assert (got_err.stage, got_err.batch_index) == (ref_err.stage, ref_err.chunk)
+    lay = got_err.__cause__
+    assert (lay.layer_index, lay.node) == (ref_err.layer, ref_err.node)
+    cause, want = lay.__cause__, ref_err.cause
+    assert type(cause).__name__ == type(want).__name__
+    if type(want).__name__ == "PoolExhausted":
+        assert (cause.requested, cause.remaining) == (want.requested, want.remaining)
