@@ -37,7 +37,6 @@ typedef struct fbx_program fbx_program; /* a loaded plan module (CUmodule) */
 typedef struct fbx_kernel fbx_kernel;   /* one kernel of a program */
 
 const char* fbx_version(void);
-const char* fbx_last_error(void);
 
 /* -- plan compilation (host-only; no GPU needed) ------------------------
  * Compile a generated plan source (NVRTC, -arch=sm_100a) to a cubin.
@@ -137,6 +136,145 @@ int fbx_crc32(const void* d_buf, unsigned long long n, unsigned* d_scratch, unsi
 unsigned long long fbx_crc32_scratch_words(unsigned long long n);
 
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream);
+
+/* =======================================================================
+ * The engine object: the drop-in for the reference's extraction boundary
+ * (SURVEY.md §8 b).
+ *
+ *   fbx_create      NodeEvaluator.__init__ + ExecContext     device.py:99-149, 263-293
+ *                   (plan bound once, tables built in HBM)   featureops.py:104-167
+ *   fbx_extract     pipeline._extract_batch(table, prep, ctx) pipeline.py:718-737
+ *                   = execute_plan over the layered DAG       device.py:434-444
+ *                   counters as ExecContext's                 device.py:110-113
+ *   fbx_output_*    the appended output columns (count pass, then copy)
+ *   fbx_emit_csr    emit_minibatch + MiniBatch.validate +     pipeline.py:357-433
+ *                   instance_digest / batch_digest
+ *   fbx_last_error  LayerExecutionError(layer, node, cause)   device.py:34-41
+ *   fbx_destroy
+ *
+ * Columns cross as FBXC images (fbxc_format.md:68-126): a null bitmap
+ * (LSB-first, set = null), int64[n] / float32[n] payloads or u32 offsets[n+1]
+ * + UTF-8 bytes.  Input and output pointers may be host (pageable or pinned)
+ * or device memory: the engine stages through its own HBM buffers.  One
+ * engine per GPU and per calling thread; calls do not touch the Python GIL.
+ * ======================================================================= */
+
+/* fbx_extract / fbx_emit_csr status: the reference exception they stand for */
+#define FBX_S_OK 0
+#define FBX_S_CONFIG 1         /* ConfigError / FeatureConfigError */
+#define FBX_S_POOL_EXHAUSTED 2 /* PoolExhausted(requested, remaining) */
+#define FBX_S_TYPE 3           /* TypeError (mix / fold of str or float) */
+#define FBX_S_VALUE 4          /* ValueError (wrap_u64 of a negative, bad delimiter, ...) */
+#define FBX_S_ENCODE 5         /* UnicodeEncodeError (lone surrogate) */
+#define FBX_S_CUDA 6           /* CUDA failure */
+#define FBX_S_OVERFLOW 7       /* OverflowError (float32 pack) */
+#define FBX_S_UNSUPPORTED 8    /* a row needs a path the device does not implement */
+#define FBX_S_EMIT 9           /* EmitError (null instance id / label at emission) */
+#define FBX_S_INVARIANT 10     /* BatchInvariantError (duplicate id, label not 0/1) */
+#define FBX_S_INTERNAL 11
+
+#define FBX_KIND_INT64 0
+#define FBX_KIND_FLOAT32 1
+#define FBX_KIND_UTF8 2
+#define FBX_KIND_JSON 3
+
+typedef struct fbx_engine fbx_engine;
+
+typedef struct fbx_column {
+  unsigned int kind;              /* FBX_KIND_* */
+  const unsigned char* nulls;     /* (n+7)/8 bytes */
+  const void* data;               /* int64[n] | float32[n] | data_bytes UTF-8 bytes */
+  const unsigned int* offsets;    /* var-length kinds: n+1 */
+  unsigned long long data_bytes;  /* var-length kinds: offsets[n] */
+} fbx_column;
+
+/* A plan as the host planner emits it: the compiled row-aligned extraction
+ * kernel (fbx_compile of the generated source) and its parameter-slot map.
+ * Slot -1 = unused. */
+typedef struct fbx_plan {
+  const void* cubin;
+  size_t cubin_bytes;
+  const char* kernel;                  /* "fbx_extract_rows" */
+  int slot_state, slot_rows, slot_pool, slot_pool_cap, slot_pool_sizes;
+  unsigned int n_inputs;               /* table columns, in fbx_extract's order */
+  const unsigned int* input_kinds;     /* [n_inputs] */
+  const int* input_slots;              /* [n_inputs][3]: nulls, data, offsets */
+  unsigned int n_outputs;              /* appended columns, in output order */
+  const unsigned int* output_kinds;    /* [n_outputs]: FBX_KIND_INT64 | FBX_KIND_UTF8 */
+  const int* output_slots;             /* [n_outputs][4]: nulls, data, ptr, len */
+  unsigned int n_tables;
+  const int* table_slots;              /* [n_tables][3]: slots, mask, keys */
+  unsigned int n_pool_nodes;           /* device token nodes, reference order */
+  const fbx_pool_node* pool_nodes;
+  unsigned int pool_planes;
+  unsigned long long pool_bytes;       /* config device.pool_bytes */
+  unsigned long long lanes_per_group;  /* config device.lanes_per_group */
+  unsigned int n_nodes;                /* every DAG node, error-rank order */
+  const char* const* node_names;
+  unsigned long long arena_bytes_per_row; /* initial device arena (grown on demand) */
+} fbx_plan;
+
+/* One dictionary (featureops.DictTable): keys as a byte blob + u32 offsets[n+1],
+ * u64 values; host or device memory. */
+typedef struct fbx_table {
+  const unsigned char* keys;
+  const unsigned int* key_offsets;
+  const unsigned long long* values;
+  unsigned long long n;
+} fbx_table;
+
+typedef struct fbx_counters {      /* ExecContext counters (device.py:110-113) */
+  unsigned long long launches;     /* kernels launched by the call */
+  unsigned long long rows;
+  unsigned long long bytes_h2d;    /* input bytes staged from host memory */
+  double device_ms;                /* CUDA-event time of the extraction kernels */
+} fbx_counters;
+
+typedef struct fbx_csr {           /* caller buffers (host or device) */
+  unsigned long long* ids;         /* n   (u64 image of the instance id) */
+  unsigned char* labels;           /* n */
+  unsigned long long* offsets;     /* n+1 */
+  unsigned short* slots;           /* capacity */
+  unsigned long long* signs;       /* capacity */
+  unsigned long long capacity;     /* sign slots available; 0 = count pass only */
+  unsigned long long n_signs;      /* out: signs of the batch */
+  unsigned long long digest;       /* out: batch_digest (XOR of instance digests) */
+} fbx_csr;
+
+int fbx_create(const fbx_plan* plan, const fbx_table* tables, int device, fbx_engine** out);
+int fbx_destroy(fbx_engine* e);
+
+/* Run the plan over n_rows rows of the table (columns in plan input order).
+ * Returns FBX_S_* (the reference's failure, located by fbx_last_error) or a
+ * negative FBX_E_* for a misuse.  Outputs stay in the engine until the next
+ * call. */
+int fbx_extract(fbx_engine* e, const fbx_column* cols, unsigned int n_cols,
+                unsigned long long n_rows, fbx_counters* counters, void* stream);
+/* Output j of the last fbx_extract: its kind and payload byte count (count pass). */
+int fbx_output_info(const fbx_engine* e, unsigned int j, unsigned int* kind,
+                    unsigned long long* n_rows, unsigned long long* data_bytes);
+/* Copy output j into caller buffers: nulls (n+7)/8 bytes, data (int64[n] or
+ * data_bytes), offsets u32[n+1] (var-length only). */
+int fbx_output_copy(fbx_engine* e, unsigned int j, unsigned char* nulls, void* data,
+                    unsigned int* offsets, void* stream);
+
+/* emit_minibatch over n rows: per row the non-null features as (slot, sign)
+ * pairs, deduplicated and sorted; ids / labels; the batch digest.  Fails like
+ * the reference: FBX_S_EMIT for the first null id or label, FBX_S_INVARIANT for
+ * a duplicate id or a label outside {0, 1} (MiniBatch.validate).  Call with
+ * capacity 0 to size the sign buffers (n_signs). */
+int fbx_emit_csr(fbx_engine* e, const fbx_column* ids, const fbx_column* labels,
+                 const fbx_column* features, const unsigned int* slots, unsigned int k,
+                 unsigned long long n_rows, fbx_csr* out, void* stream);
+
+/* The last call's failure: returns its FBX_S_* status and sets *layer (0 when
+ * not an operator failure), *node (node name or NULL) and, when non-NULL,
+ * *detail (PoolExhausted: requested << 32 | remaining; emit: the row). */
+int fbx_last_error(const fbx_engine* e, int* layer, const char** node,
+                   unsigned long long* detail);
+/* Human-readable message of the last failure of e, or (e == NULL) of the
+ * calling thread's last API error. */
+const char* fbx_error_message(const fbx_engine* e);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB = PKG / "libfbx.so"
-SOURCES = [PKG / "csrc" / "fbx_runtime.cu"]
+SOURCES = [PKG / "csrc" / "fbx_runtime.cu", PKG / "csrc" / "fbx_engine.cu"]
 HEADERS = [ROOT / "include" / "fbx.h", ROOT / "include" / "fbx_abi.h"]
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 

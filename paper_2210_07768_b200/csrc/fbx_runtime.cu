@@ -420,7 +420,9 @@ struct fbx_kernel {
 extern "C" {
 
 const char* fbx_version(void) { return "fbx 0.1 (sm_100a, abi " "1" ")"; }
-const char* fbx_last_error(void) { return g_err.c_str(); }
+/* internal (fbx_engine.cu): the calling thread's API error */
+const char* fbx_internal_api_error(void) { return g_err.c_str(); }
+int fbx_internal_fail(int code, const char* msg) { return fail(code, msg ? msg : ""); }
 void fbx_free(void* p) { free(p); }
 
 int fbx_compile(const char* source, const char* name, const char* const* options, int n_options,

@@ -1426,111 +1426,22 @@ def prepare_extract(config: PipelineConfig, table_kinds: Mapping[str, Kind]) -> 
                     tuple(extract_outputs), [n for _, n in order], {"table": kinds}, {})
 
 
-class ExtractEngine(Engine):
-    """Device state for the row-aligned ``_extract_batch`` kernel."""
+class ExtractEngine:
+    """``_extract_batch`` on the device through the C-ABI engine object
+    (``fbx_create`` / ``fbx_extract`` / ``fbx_output_*``, include/fbx.h): staging,
+    launch, the reference arena, error decoding and string compaction all happen
+    in libfbx.so; see capi.CEngine."""
 
-    def __init__(self, prepared: Prepared, device: str = "cuda", pool_bytes_per_row: int = 64):
+    def __init__(self, prepared: Prepared, device: str = "cuda"):
         torch = _torch()
-        self.torch = torch
+        dev = torch.device(device)
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        from .capi import CEngine
+        self.c = CEngine(prepared, idx)
         self.prepared = prepared
-        self.device = torch.device(device)
-        self.config = prepared.config
-        self.ir = prepared.ir
-        self.prog = prepared.program
-        self.slots = self.prog.slots
-        self.params = np.zeros(runtime.FBX_MAX_PARAM_SLOTS, dtype=np.uint64)
-        self.pool_bytes_per_row = pool_bytes_per_row
-        self._keep: list = []
-        with torch.cuda.device(self.device):
-            self.module = runtime.Program(prepared.cubin)
-            self.state = torch.zeros(runtime.STATE_BYTES // 8, dtype=torch.int64,
-                                     device=self.device)
-            self._set("state", self.state.data_ptr())
-            self._upload_tables()
 
     def extract(self, table: ViewImage) -> ViewImage:
-        """``_extract_batch``: the table's columns plus the output columns."""
-        torch, dev = self.torch, self.device
-        n = table.row_count
-        dv = DeviceView(table, device=dev)
-        for c in dv.tensors:
-            for part in ("nulls", "data", "offsets"):
-                self._set(f"drv.{c}.{part}", dv.ptr(c, part))
-        self._set("rows", n)
-        while True:
-            try:
-                return self._extract_once(table, dv, n)
-            except ArenaRetry as exc:  # the device arena was too small: grow, repeat
-                self._arena_min = int(exc.need * 1.25) + (1 << 16)
-
-    def _extract_once(self, table: ViewImage, dv, n: int) -> ViewImage:
-        torch = self.torch
-        dev = self.device
-        pool_cap = self.pool_bytes_per_row * n + 128 * ((n + 255) // 256) * 8 + (1 << 16)
-        pool_cap = max(pool_cap, getattr(self, "_arena_min", 0))
-        pool = torch.empty(pool_cap + 256, dtype=torch.uint8, device=dev)
-        self._set("pool", pool.data_ptr())
-        self._set("pool_cap", pool_cap)
-        p = self.prog
-        if p.ref_pool:  # lane sizes of the device token nodes, per row
-            sizes = torch.zeros(p.pool_ni * max(n, 1) + 1, dtype=torch.int32, device=dev)
-            self._set("pool_sizes", sizes.data_ptr())
-        outs = []
-        words = (n + 31) // 32 + 1
-        for j, (col, kind, domain) in enumerate(self.prepared.extract_outputs):
-            nulls = torch.zeros(words, dtype=torch.int32, device=dev)
-            self._set(f"out{j}.nulls", nulls.data_ptr())
-            if domain == "u64":
-                data = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-                self._set(f"out{j}.data", data.data_ptr())
-                outs.append((col, kind, nulls, data, None))
-            else:
-                ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-                ln = torch.zeros(n + 1, dtype=torch.int32, device=dev)
-                self._set(f"out{j}.ptr", ptr.data_ptr())
-                self._set(f"out{j}.len", ln.data_ptr())
-                outs.append((col, kind, nulls, ptr, ln))
-        stream = self._stream()
-        status = torch.zeros(1, dtype=torch.int64, device=dev)
-        runtime.state_reset(self.state.data_ptr(), status.data_ptr(), 1, stream)
-        grid = max(1, min((n + 255) // 256, 148 * 8))
-        self.module.launch("fbx_extract_rows", grid, 256, 0, stream, self.params)
-        if p.ref_pool and n:  # the reference arena over this table, in row order
-            rank = torch.empty(n + 1, dtype=torch.int32, device=dev)
-            gsum = torch.empty(n + 1, dtype=torch.int64, device=dev)
-            nodes = torch.tensor([[l, r, i, 0] for l, r, i in p.ref_pool], dtype=torch.int32,
-                                 device=dev)
-            runtime.pool_account(0, 0, 1, 1, n, 0, 0xFFFFFFFF, sizes.data_ptr(), p.pool_ni, 0,
-                                 nodes.data_ptr(), len(p.ref_pool), self.config.lanes_per_group,
-                                 self.config.pool_bytes, rank.data_ptr(), gsum.data_ptr(),
-                                 self.state.data_ptr(), stream)
-        st = self._read_state()
-        if st["pool_overflow"]:
-            raise ArenaRetry(st["pool_overflow"])
-        key = st["error_key"]
-        if key != (1 << 64) - 1:
-            try:
-                self._raise_if_error(st)
-            except StageError as exc:
-                raise exc.__cause__ from None
-        cols = {c: table.columns[c] for c in table.order}
-        for col, kind, nulls, a, b in outs:
-            nb = nulls.cpu().numpy().view(np.uint8)[: (n + 7) // 8].copy()
-            if b is None:
-                cols[col] = ColumnImage(Kind.INT64, n, nb, a[:n].cpu().numpy().copy())
-            else:
-                offs = torch.empty(n + 1, dtype=torch.int64, device=dev)
-                runtime.exclusive_scan_u32(b.data_ptr(), offs.data_ptr(), n, stream)
-                total = int(offs[n].item()) if n else 0
-                data = torch.empty(total + 16, dtype=torch.uint8, device=dev)
-                runtime.gather_strings(a.data_ptr(), b.data_ptr(), offs.data_ptr(), n,
-                                       data.data_ptr(), stream)
-                if total > 0xFFFFFFFF:
-                    raise ValueError("var-length payload exceeds u32 offset range")
-                cols[col] = ColumnImage(Kind.UTF8, n, nb, data[:total].cpu().numpy().copy(),
-                                        offs.cpu().numpy().astype(np.uint32))
-        return ViewImage(cols, table.key_columns, tuple(table.order) + tuple(
-            c for c, *_ in outs))
+        return self.c.extract(table)
 
 
 def extract_batch(table: ViewImage, config: PipelineConfig, device: str = "cuda") -> ViewImage:

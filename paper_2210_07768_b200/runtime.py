@@ -27,7 +27,7 @@ STATE_FIELDS = ("tile_ticket", "pool_head", "pool_overflow", "error_key", "error
                 "dup_seen", "emit_key", "emit_detail", "pool_flagged")
 STATE_BYTES = 8 * len(STATE_FIELDS)
 
-EXPORTS = ("fbx_version", "fbx_last_error", "fbx_compile", "fbx_free", "fbx_program_load",
+EXPORTS = ("fbx_version", "fbx_error_message", "fbx_compile", "fbx_free", "fbx_program_load",
            "fbx_program_unload", "fbx_program_kernel", "fbx_kernel_attributes",
            "fbx_kernel_set_max_dynamic_smem", "fbx_launch", "fbx_state_reset",
            "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
@@ -50,7 +50,8 @@ def lib() -> ctypes.CDLL:
             L = ctypes.CDLL(str(LIB))
             vp, sz, c = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
             L.fbx_version.restype = ctypes.c_char_p
-            L.fbx_last_error.restype = ctypes.c_char_p
+            L.fbx_error_message.restype = ctypes.c_char_p
+            L.fbx_error_message.argtypes = [ctypes.c_void_p]
             L.fbx_compile.argtypes = [ctypes.c_char_p, ctypes.c_char_p,
                                       ctypes.POINTER(ctypes.c_char_p), c,
                                       ctypes.POINTER(vp), ctypes.POINTER(sz),
@@ -82,7 +83,8 @@ def lib() -> ctypes.CDLL:
             for name in EXPORTS:
                 getattr(L, name).restype = getattr(L, name).restype or c
             L.fbx_version.restype = ctypes.c_char_p
-            L.fbx_last_error.restype = ctypes.c_char_p
+            L.fbx_error_message.restype = ctypes.c_char_p
+            L.fbx_error_message.argtypes = [ctypes.c_void_p]
             L.fbx_free.restype = None
             _lib = L
     return _lib
@@ -90,7 +92,7 @@ def lib() -> ctypes.CDLL:
 
 def _check(rc: int, what: str):
     if rc != 0:
-        msg = lib().fbx_last_error().decode(errors="replace")
+        msg = lib().fbx_error_message(None).decode(errors="replace")
         raise FbxError(f"{what} failed ({rc}): {msg}")
 
 
@@ -123,7 +125,7 @@ def compile_source(source: str, name: str = "plan.cu", options: tuple[str, ...] 
     rc = L.fbx_compile(source.encode(), name.encode(), arr, len(opts), ctypes.byref(img),
                        ctypes.byref(n), log, len(log))
     if rc != 0:
-        raise FbxError(f"plan compilation failed: {L.fbx_last_error().decode(errors='replace')}")
+        raise FbxError(f"plan compilation failed: {L.fbx_error_message(None).decode(errors='replace')}")
     data = ctypes.string_at(img, n.value)
     L.fbx_free(img)
     _CUBIN_CACHE[key] = data

@@ -54,3 +54,15 @@ def corpus(rows, users, seed, views=2):
 
 def reference_available() -> bool:
     return (REFERENCE / "featurebox" / "__init__.py").exists()
+
+
+# The unmodified reference as installed for the reference arm (pip --target
+# baseline/_ref, git-ignored, travels to the GPU box); /root/reference here.
+INSTALLED_REFERENCE = ROOT / "baseline" / "_ref"
+
+
+def reference_package_path() -> Path | None:
+    for p in (INSTALLED_REFERENCE, REFERENCE):
+        if (p / "featurebox" / "__init__.py").exists():
+            return p
+    return None

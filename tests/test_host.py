@@ -155,7 +155,7 @@ def test_library_exports_every_declared_symbol():
     for name in sorted(declared):
         assert hasattr(L, name), name
     assert L.fbx_version().decode().startswith("fbx")
-    assert isinstance(L.fbx_last_error(), bytes)
+    assert isinstance(L.fbx_error_message(None), bytes)
     assert ctypes.sizeof(ctypes.c_uint64) * 384 == 3072  # fbx_params
 
 
@@ -209,3 +209,30 @@ def test_json_canon_model_matches_json_dumps():
     """jsoncanon.json_canon (model of fbx::json_canon) == json.dumps(sort_keys, (",", ":"))."""
     from paper_2210_07768_b200.jsoncanon import check_json_canon
     assert check_json_canon(4000) == 4000
+
+
+@pytest.mark.parametrize("seed", [12, 1000, 1099])
+def test_fast_generator_matches_reference_shard_files(seed, tmp_path):
+    """The 1M-row shards the bench regenerates with the C generator are the exact
+    files the unmodified reference generated for tests/golden/shard_goldens.json
+    (sha256 of every file), so the per-shard reference digests apply to them."""
+    import json
+    from paper_2210_07768_b200.corpus import make_corpus_fast, write_corpus
+    doc = json.loads((ROOT / "tests" / "golden" / "shard_goldens.json").read_text())
+    want = next(r for r in doc["shards"] if r["seed"] == seed)["corpus_sha256"]
+    files = write_corpus(make_corpus_fast(1_000_000, 5000, seed, 2), tmp_path)
+    got = {k: hashlib.sha256(Path(v).read_bytes()).hexdigest() for k, v in files.items()}
+    assert got == want
+
+
+def test_shard_goldens_compose_to_c5():
+    """C5's run digest is the XOR of its 100 independently generated shards."""
+    import json
+    doc = json.loads((ROOT / "tests" / "golden" / "shard_goldens.json").read_text())
+    c5 = [r for r in doc["shards"] if r["dag"] == "default" and 1000 <= r["seed"] < 1100]
+    assert len(c5) == 100 and sorted(r["seed"] for r in c5) == list(range(1000, 1100))
+    x = 0
+    for r in c5:
+        x ^= int(r["digest"], 16)
+    assert f"0x{x:016x}" == doc["c5"]["xor_digest"]
+    assert sum(r["rows"] for r in c5) == 100_000_000
