@@ -80,6 +80,8 @@ def parse_args():
     ap.add_argument("--users", type=int, default=5000)
     ap.add_argument("--seed", type=int, default=11)
     ap.add_argument("--cpu-sample-rows", type=int, default=24576)
+    ap.add_argument("--ref-sample-rows", type=int, default=4096,
+                    help="driver rows per host process per step of the reference arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--shards", type=int, default=0,
@@ -302,9 +304,17 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     launches = [0]
 
-    def run_shard(eng, n, ev=None):
-        """One pass over a shard: clear the run's id set, then launches of at
-        most --launch-rows rows with the look-back continuing across them."""
+    def run_shard(eng, n, ev=None, iev=None):
+        """One run over a shard, as the reference runs it (pipeline.py:952-1094):
+        the per-run prepare phase -- the side-view and basic-view indices rebuilt
+        on the device from their resident images (:970-980) -- then the run's id
+        set cleared and launches of at most --launch-rows rows, the look-back
+        continuing across them."""
+        if iev is not None:
+            iev[0].record(stream)
+        launches[0] += eng.rebuild_indices(stream.cuda_stream)
+        if iev is not None:
+            iev[1].record(stream)
         launches[0] += eng.begin_run(n)  # k_idset_clear + k_state_reset
         if ev is not None:
             ev[0].record(stream)
@@ -342,6 +352,8 @@ def main():
     K = args.steps
     evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in shards] for _ in range(K)]
+    ievs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in shards] for _ in range(K)]
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(K)]
     clocks = Clocks(local)
@@ -353,8 +365,8 @@ def main():
     for k in range(K):
         runtime.l2_flush(flush.data_ptr(), flush.numel(), stream.cuda_stream)  # L2 flush
         step_ev[k][0].record(stream)
-        for (corp, e, _, _), ev in zip(shards, evs[k]):
-            run_shard(e, corp.driver.row_count, ev)
+        for (corp, e, _, _), ev, iev in zip(shards, evs[k], ievs[k]):
+            run_shard(e, corp.driver.row_count, ev, iev)
         step_ev[k][1].record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
@@ -362,6 +374,7 @@ def main():
         dist.barrier()
     total_ms = sum(a.elapsed_time(b) for a, b in step_ev)
     kern_total = sum(a.elapsed_time(b) for row in evs for a, b in row)
+    index_total = sum(a.elapsed_time(b) for row in ievs for a, b in row)
     results = [e.finish().counters for _, e, _, _ in shards]
     tot = torch.tensor([total_ms, kern_total], dtype=torch.float64, device=dev)
     if dist:
@@ -407,6 +420,7 @@ def main():
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "bytes_per_launch": ab, "kernel_ms": round(kern_avg_s * 1e3, 4),
+                "index_build_ms": round(index_total / K, 4),
                 "ceilings_ms": {"hbm": round(hbm_floor * 1e3, 4),
                                 "int_pipe_fnv": round(int_floor * 1e3, 4)},
                 "limiter": "instruction issue (see profiles/: inst_executed, issue_active)",
@@ -434,7 +448,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(corpus, raw, tmp, args.cpu_sample_rows)
+            if reference_installed():  # the unmodified reference on this very log's files
+                (tmp / "cfg.json").write_text(json.dumps(raw))
+                cpu = reference_cpu(tmp, args.ref_sample_rows, rows=args.rows)
+            else:
+                cpu = cpu_baseline(corpus, raw, tmp, args.cpu_sample_rows)
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "error": str(exc)[:200]}
     out = {
@@ -558,25 +576,141 @@ def measure_e2e(torch, E, eng, corpus, dev, stream, K, world, dist, slice_rows=1
                     f"({len(sr.bounds)} tapered slices of <= {sr.slice_rows} rows)"}
 
 
+# ---------------------------------------------------------------------------
+# the UNMODIFIED reference on the host cores (baseline/_ref: pip-installed from
+# /root/reference/pkg; travels to the GPU box).  Falls back to the oracle port
+# (oracle/featurebox_oracle.py) only when the installed reference is absent.
+# ---------------------------------------------------------------------------
+
+REF_PKG = ROOT / "baseline" / "_ref"
+
+
+def reference_installed() -> bool:
+    return (REF_PKG / "featurebox" / "__init__.py").exists()
+
+
+def _ref_modules():
+    if str(REF_PKG) not in sys.path:
+        sys.path.insert(0, str(REF_PKG))
+    import featurebox.columnstore as RCS
+    import featurebox.corpus as RC
+    import featurebox.pipeline as RP
+    return RC, RCS, RP
+
+
+def reference_log(dag: str, rows: int, users: int, seed: int, batch_size: int) -> Path:
+    """The benchmark log written by the reference's own (pure-Python) gen_corpus,
+    with the Appendix-B DAG's config beside it."""
+    from paper_2210_07768_b200.workloads import workload_config, write_lookup_tables
+    RC, _, _ = _ref_modules()
+    dest = Path(tempfile.mkdtemp(prefix="fbxreflog"))
+    RC.gen_corpus(dest, rows=rows, users=users, seed=seed, views=2)
+    if dag == "lookup_heavy":
+        write_lookup_tables(dest, users)
+    (dest / "cfg.json").write_text(json.dumps(workload_config(dag, batch_size=batch_size)))
+    return dest
+
+
+def _ref_sample(args):
+    """One process: rows [lo, hi) of the log (driver + the matching basic rows,
+    the whole profile view) through the unmodified reference -- its
+    run_pipelined end to end, and its _extract_batch alone over the same
+    sample's cleaned + joined chunks.  Returns (rows, e2e s, extract s, joined)."""
+    log, lo, hi = args
+    import shutil
+    RC, RCS, RP = _ref_modules()
+    sample = Path(tempfile.mkdtemp(prefix="fbxrefsample"))
+    for name in ("user_profile.fbxc", "cfg.json", "city_dict.tsv", "token_dict.tsv",
+                 "user_dict.tsv", "query_dict.tsv"):
+        if (log / name).exists():
+            shutil.copy(log / name, sample / name)
+    for name in ("user_events.fbxc", "basic.fbxc"):  # gen_corpus: basic row i <-> driver row i
+        batch, _ = RCS.read_columns(log / name, rows=(lo, hi))
+        RCS.write_view(batch, sample / name)
+    cfg = RP.load_config(sample / "cfg.json")
+    t0 = time.perf_counter()
+    RP.run_pipelined(cfg)
+    t_e2e = time.perf_counter() - t0
+    # extract-only: the same chunks, cleaned and joined outside the timed part
+    prep = RP.prepare(cfg)
+    ctx = RP._make_ctx(prep)
+    drv = next(v for v in cfg.views if v.name == cfg.driver)
+    sides = [v for v in cfg.views if v.name != cfg.driver]
+    from featurebox.viewpipe import JoinIndex, JoinSpec, clean_views, join_with_index
+    idx = [JoinIndex(clean_views(RCS.read_columns(v.path, v.columns)[0], v.policy),
+                     JoinSpec(cfg.join_keys)) for v in sides]
+    n = hi - lo
+    t_ex, joined = 0.0, 0
+    for c0 in range(0, n, cfg.batch_size):
+        batch, _ = RCS.read_columns(drv.path, drv.columns, rows=(c0, min(c0 + cfg.batch_size, n)))
+        t = clean_views(batch, drv.policy)
+        for ix in idx:
+            t = join_with_index(t, ix)
+        joined += t.schema.row_count
+        t1 = time.perf_counter()
+        RP._extract_batch(t, prep, ctx)
+        t_ex += time.perf_counter() - t1
+    shutil.rmtree(sample, ignore_errors=True)
+    return n, t_e2e, t_ex, joined
+
+
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def reference_cpu(log: Path, sample_rows: int, procs: int | None = None,
+                  offset: int = 0, rows: int = 1_000_000) -> dict:
+    """All host cores, one process each, on disjoint samples cut from the exact
+    log.  Rates = sample rows / slowest process (they run concurrently)."""
+    import multiprocessing as mp
+    import platform
+    procs = procs or os.cpu_count() or 1
+    jobs = []
+    for k in range(procs):
+        lo = (offset + k * sample_rows) % max(1, rows - sample_rows)
+        jobs.append((log, lo, lo + sample_rows))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_ref_sample, jobs)
+    wall = time.perf_counter() - t0
+    n = sum(r[0] for r in res)
+    e2e = n / max(r[1] for r in res)
+    ext = sum(r[3] for r in res) / max(r[2] for r in res)
+    return {"value": e2e, "unit": "records/s", "cores": procs, "kind": "reference",
+            "extract_only_joined_rows_per_s": round(ext, 1),
+            "hot_path_records_per_s": round(e2e, 1),
+            "sample": f"{procs} processes x {sample_rows} driver rows (+ their basic rows, the whole "
+                      f"profile view) cut from the benchmark log, each through the UNMODIFIED "
+                      f"reference (baseline/_ref): run_pipelined end to end, and _extract_batch "
+                      f"alone over the same cleaned + joined chunks; rate = rows / slowest "
+                      f"process (wall {wall:.1f}s)",
+            "cpu_model": _cpu_model(), "python": platform.python_version()}
+
+
 def reference_arm(args, rank, world):
-    """The reference's CPU path (oracle port) on the host cores, rank 0 only."""
+    """The reference's own CPU implementation of the path on the host cores,
+    rank 0 only: the unmodified reference package (baseline/_ref) over bounded
+    samples of the same log the B200 arm extracts."""
     if rank != 0:
         return
-    from paper_2210_07768_b200.corpus import make_corpus_fast as make_corpus, write_corpus
-    from paper_2210_07768_b200.workloads import workload_config, write_lookup_tables
-    sample = args.cpu_sample_rows
+    if not reference_installed():
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref missing: pip install "
+                          "--no-index --target baseline/_ref /root/reference/pkg"}), flush=True)
+        return
+    seed = args.seed
+    log = reference_log(args.dag, args.rows, args.users, seed, args.batch_size)
+    sample = args.ref_sample_rows
     procs = os.cpu_count() or 1
-    rows = max(sample * procs, 1)
-    corpus = make_corpus(min(rows, args.rows), args.users, args.seed)
-    tmp = Path(tempfile.mkdtemp(prefix="fbxref"))
-    write_corpus(corpus, tmp)
-    raw = workload_config(args.dag, batch_size=args.batch_size)
-    if args.dag == "lookup_heavy":
-        write_lookup_tables(tmp, args.users)
-    rates = []
-    last = None
+    rates, last = [], None
     for k in range(args.warmup + args.steps):
-        last = cpu_baseline(corpus, raw, tmp, sample, procs)
+        last = reference_cpu(log, sample, procs, offset=k * procs * sample, rows=args.rows)
         if k >= args.warmup:
             rates.append(last["value"])
     value = statistics.mean(rates) if rates else 0.0
@@ -584,10 +718,11 @@ def reference_arm(args, rank, world):
            "value": round(value, 1), "unit": "records/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(sample * procs / value * 1e3, 3) if value
            else None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "u64", "data": "synthetic",
-           "config": {"workload": f"{args.dag} DAG, sample of the {args.rows}-record log "
-                                  f"(users {args.users}, seed {args.seed})",
-                      "batch_size": 512, "parallelism": f"{procs} host processes"},
+           "dtype": "u64", "data": "synthetic (the reference's own gen_corpus)",
+           "config": {"workload": f"{args.dag} DAG (SURVEY Appendix B), samples of the "
+                                  f"{args.rows}-record log (users {args.users}, seed {seed}), "
+                                  "full emit incl. basic merge",
+                      "batch_size": args.batch_size, "parallelism": f"{procs} host processes"},
            "cpu_baseline": {**(last or {}), "value": round(value, 1)},
            "e2e": {"value": round(value, 1), "unit": "records/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}

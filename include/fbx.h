@@ -89,6 +89,9 @@ int fbx_pool_account(const unsigned char* d_tile_flag, const unsigned long long*
                      unsigned long long capacity, unsigned* d_rank_scratch,
                      unsigned long long* d_sum_scratch, fbx_state* d_state, void* stream);
 
+/* cudaMemsetAsync on `stream` (zeroing the hash tables before an index rebuild). */
+int fbx_memset_async(void* d_ptr, int value, size_t bytes, void* stream);
+
 /* Reset the per-launch part of the run state -- the bump-pool head (ArenaPool.reset,
  * mempool.py:136) and the persistent kernel's tile ticket -- between the launches of
  * one run, whose counters keep accumulating. */

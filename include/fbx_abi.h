@@ -38,6 +38,7 @@
 #define FBX_ERR_FLOAT_SLOWPATH 13 /* unsupported: inexact (>19 digit) decimal at a rounding tie */
 #define FBX_ERR_INTERNAL 14       /* a plan invariant failed (never expected) */
 #define FBX_ERR_POOL_KEY 15       /* unsupported: reference-arena order over Utf8 join keys */
+#define FBX_ERR_BASIC_DUP 16      /* MergeUniquenessError: basic features repeat an instance id */
 
 /* Device-resident run state: counters, the pool head, the error word.
  * One per engine, zeroed (error_key = ~0) before a launch. */

@@ -48,7 +48,7 @@ STAGE = {"prepare": 0, "read": 1, "clean": 2, "join": 3, "extract": 4, "merge": 
 ERR = {"type": 1, "value": 2, "encode": 3, "pool": 4, "null_label": 5, "label_range": 6,
        "dup_id": 7, "multi_match": 8, "json_bigint": 9, "json_deep": 10,
        "unicode_lower": 11, "float_overflow": 12, "float_slow": 13, "internal": 14,
-       "pool_key": 15}
+       "pool_key": 15, "basic_dup": 16}
 
 
 def library_source() -> str:
@@ -855,7 +855,13 @@ class PlanCodegen:
         g(f"if (alive && !({null_any})) {{")
         self.key_hash(keys, kk, "tag")
         if self.int_keyed(k):
-            g(f"fbx::islot_insert((fbx::ISlot*)TBL, MASK, tag, (u64){keys[0].c}, (u32)row); ++nidx;")
+            if is_basic:  # check_unique_ids over the basic view (pipeline.py:975-980)
+                g(f"if (fbx::islot_insert((fbx::ISlot*)TBL, MASK, tag, (u64){keys[0].c}, (u32)row))")
+                g(f"fbx::raise_err(ST, fbx::err_key(0ull, {STAGE['prepare']}u, 0u, 0u, "
+                  f"{ERR['basic_dup']}u), (u64){keys[0].c});")
+                g("++nidx;")
+            else:
+                g(f"fbx::islot_insert((fbx::ISlot*)TBL, MASK, tag, (u64){keys[0].c}, (u32)row); ++nidx;")
             g("}")
             g("}")
             g("if (nmal) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)nmal);")

@@ -1119,21 +1119,31 @@ FBX_DI u32 ld_acquire_u32(const u32* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// build-side insert (count duplicates); returns after the key is counted
-FBX_DI void islot_insert(ISlot* T, u64 mask, u64 h, u64 key, u32 row) {
+// build-side insert (count duplicates): the whole slot {key, ref, count = 1} is
+// claimed by ONE 128-bit compare-and-swap (atom.cas.b128, sm_90+), so no other
+// thread can see a claimed slot without its key -- no fence, no publish step.
+// An equal key already present bumps the count (its key is immutable by then).
+FBX_DI void cas128(void* addr, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u64* old_lo,
+                   u64* old_hi) {
+  asm volatile(
+      "{\n\t.reg .b128 c, n, d;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 n, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, n;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(*old_lo), "=l"(*old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
+      : "memory");
+}
+// Returns true when the key was already present (a repeated key).
+FBX_DI bool islot_insert(ISlot* T, u64 mask, u64 h, u64 key, u32 row) {
   u64 i = h & mask;
+  const u64 hi = (1ull << 32) | (u64)row;  // {ref = row, aux = count 1}
   while (true) {
-    unsigned long long* ra = (unsigned long long*)&T[i].ref;  // {ref, aux}
-    const unsigned long long old = atomicCAS(ra, 0ull, (0xFFFFFFFFull << 32) | (unsigned long long)row);
-    if (old == 0ull) {
-      *((volatile u64*)&T[i].key) = key;
-      __threadfence();
-      atomicExch(&T[i].aux, 1u);
-      return;
-    }
-    u32 c;
-    do { c = ld_acquire_u32(&T[i].aux); } while (c == 0xFFFFFFFFu);  // claimed, key not yet visible
-    if (*((volatile u64*)&T[i].key) == key) { atomicAdd(&T[i].aux, 1u); return; }
+    u64 ok, oh;
+    cas128(&T[i], 0ull, 0ull, key, hi, &ok, &oh);
+    if (ok == 0ull && oh == 0ull) return false;  // claimed an empty slot
+    if (ok == key) { atomicAdd(&T[i].aux, 1u); return true; }
     i = (i + 1) & mask;
   }
 }

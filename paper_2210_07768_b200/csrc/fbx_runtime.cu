@@ -544,6 +544,10 @@ int fbx_idset_clear(unsigned long long* d_ids, size_t n_words, unsigned long lon
   return cuda_check(cudaGetLastError(), "fbx_idset_clear");
 }
 
+int fbx_memset_async(void* d_ptr, int value, size_t bytes, void* stream) {
+  return cuda_check(cudaMemsetAsync(d_ptr, value, bytes, (cudaStream_t)stream), "fbx_memset_async");
+}
+
 int fbx_pool_reset(fbx_state* d_state, void* stream) {
   // tile ticket + pool head (adjacent): the per-launch part of the run state
   static_assert(offsetof(fbx_state, pool_head) == offsetof(fbx_state, tile_ticket) + 8, "layout");

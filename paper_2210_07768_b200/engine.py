@@ -491,16 +491,32 @@ class Engine:
         stream = self._stream()
         status = torch.zeros(1, dtype=torch.int64, device=self.device)
         runtime.state_reset(self.state.data_ptr(), status.data_ptr(), 1, stream)
-        for k, v, n in prepared_views:
-            grid = max(1, min((n + 255) // 256, 1184))
-            self.module.launch(f"fbx_side_prep_{k}", grid, 256, 0, stream, self.params)
+        self._side_views = prepared_views
+        self._launch_side_prep(stream)
         st = self._read_state()
         self.prepare_counters.malformed = st["malformed"]
         self.prepare_counters.filtered = st["filtered"]
         self._raise_if_error(st, prepare=True)
-        # basic uniqueness (pipeline.py:975): any basic key indexed twice
-        if ir.basic is not None:
+        # basic uniqueness (pipeline.py:975): int-keyed basic indices raise it in the
+        # prep kernel itself (basic_dup); other key shapes count repeats in the slots
+        if ir.basic is not None and len(ir.sides) not in self.prog.int_keyed:
             self._check_basic_unique(len(ir.sides))
+
+    def _launch_side_prep(self, stream: int) -> int:
+        for k, v, n in self._side_views:
+            grid = max(1, min((n + 255) // 256, 1184))
+            self.module.launch(f"fbx_side_prep_{k}", grid, 256, 0, stream, self.params)
+        return len(self._side_views)
+
+    def rebuild_indices(self, stream: int | None = None) -> int:
+        """Rebuild the side-view and basic-view hash indices from their resident
+        images (the per-run prepare phase of pipeline.py:970-980, on the device):
+        zero the tables, re-run the prep kernels.  Returns the launch count.
+        Prepare-time failures were checked when the engine was built."""
+        stream = self._stream() if stream is None else stream
+        for t in self.side_tables.values():
+            runtime.memset_async(t.data_ptr(), 0, t.numel(), stream)
+        return self._launch_side_prep(stream)
 
     def _check_basic_unique(self, k: int):
         torch = self.torch
@@ -1200,6 +1216,8 @@ def _cause(code: str, detail: int, st: dict) -> BaseException:
         return EmitError("null label at emission")
     if code == "label_range":
         return BatchInvariantError(f"label {detail - (1 << 64) if detail >> 63 else detail!r} not 0/1")
+    if code == "basic_dup":
+        return MergeUniquenessError("basic features: duplicate instance id")
     if code == "dup_id":
         return MergeUniquenessError(f"extracted features: duplicate instance id {detail}")
     if code == "multi_match":

@@ -33,7 +33,7 @@ EXPORTS = ("fbx_version", "fbx_error_message", "fbx_compile", "fbx_free", "fbx_p
            "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
            "fbx_dup_resolve", "fbx_state_snapshot",
            "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words", "fbx_idset_clear",
-           "fbx_pool_account")
+           "fbx_pool_account", "fbx_memset_async")
 
 
 class FbxError(RuntimeError):
@@ -74,6 +74,7 @@ def lib() -> ctypes.CDLL:
             L.fbx_state_snapshot.argtypes = [vp, vp, vp]
             L.fbx_pool_reset.argtypes = [vp, vp]
             L.fbx_idset_clear.argtypes = [vp, sz, vp, sz, vp, vp]
+            L.fbx_memset_async.argtypes = [vp, c, sz, vp]
             u, ull = ctypes.c_uint, ctypes.c_ulonglong
             L.fbx_pool_account.argtypes = [vp, vp, ull, u, u, vp, u, vp, u, vp, vp, u, ull, ull,
                                            vp, vp, vp, vp]
@@ -220,6 +221,11 @@ def dup_resolve(d_winner: int, d_later: int, n_slots: int, d_out: int, stream: i
     _check(lib().fbx_dup_resolve(ctypes.c_void_p(d_winner), ctypes.c_void_p(d_later),
                                  int(n_slots), ctypes.c_void_p(d_out), ctypes.c_void_p(stream)),
            "dup resolve")
+
+
+def memset_async(d_ptr: int, value: int, nbytes: int, stream: int):
+    _check(lib().fbx_memset_async(ctypes.c_void_p(d_ptr), value, int(nbytes),
+                                  ctypes.c_void_p(stream)), "memset")
 
 
 def pool_account(d_flag: int, d_chunk: int, n_tiles: int, spc: int, tile_rows: int,

@@ -604,3 +604,26 @@ def test_pool_bytes_matches_reference(pool, lpg, batch_size, ops, tmp_path):
     assert type(cause).__name__ == type(want).__name__
     if type(want).__name__ == "PoolExhausted":
         assert (cause.requested, cause.remaining) == (want.requested, want.remaining)
+
+
+def _basic_dup(dst, src):
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+
+    def mut(drv, prof, bas):
+        ids = bas.columns["instance_id"].to_pylist()
+        ids[dst] = ids[src]
+        bas.columns["instance_id"] = ColumnImage.from_values(Kind.INT64, ids)
+        return drv, prof, bas
+    return mut
+
+
+@pytest.mark.parametrize("dst,src", [(-1, 0), (5, 6)])
+def test_basic_view_duplicate_id_fails_prepare(dst, src, tmp_path):
+    """check_unique_ids over the basic view (pipeline.py:975-980): raised by the
+    device index build itself -- stage prepare, no batch index."""
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    raw = _config(512, ops, {"c": 3}, filt="age != -12345")
+    ref_err, got_err = _err(raw, tmp_path, _basic_dup(dst, src))
+    assert (got_err.stage, got_err.batch_index) == ("prepare", None) == (ref_err.stage,
+                                                                         ref_err.chunk)
+    assert "basic features" in str(got_err.__cause__)

@@ -181,6 +181,7 @@ EDGE_TESTS = [  # (test function name, parameter sets)
     ("test_json_float32_leaves_match_oracle", [{}]),
     ("test_json_float32_overflow_is_stage_error", "bad"),
     ("test_float32_str_repr_matches_oracle", [{}]),
+    ("test_basic_view_duplicate_id_fails_prepare", [{"dst": -1, "src": 0}, {"dst": 5, "src": 6}]),
     ("test_pool_bytes_matches_reference", [dict(zip(("pool", "lpg", "batch_size", "ops"), c))
                                            for c in __import__("test_gpu_edge").POOL_CASES]),
 ]
