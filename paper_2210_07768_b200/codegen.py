@@ -25,6 +25,7 @@ Constructs without a bit-exact device implementation raise
 
 from __future__ import annotations
 
+import os
 import struct
 from dataclasses import dataclass, field
 from fractions import Fraction
@@ -864,9 +865,7 @@ class PlanCodegen:
                 g(f"fbx::islot_insert((fbx::ISlot*)TBL, MASK, tag, (u64){keys[0].c}, (u32)row); ++nidx;")
             g("}")
             g("}")
-            g("if (nmal) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)nmal);")
-            g("if (nfilt) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)nfilt);")
-            g("if (nidx) atomicAdd((unsigned long long*)&ST->side_rows, (unsigned long long)nidx);")
+            g("fbx::block_side_counts(ST, nmal, nfilt, nidx);")
             g("}")
             return name
         g("u64 i = tag & MASK;")
@@ -885,9 +884,7 @@ class PlanCodegen:
         g("}")
         g("}")
         g("}")
-        g("if (nmal) atomicAdd((unsigned long long*)&ST->malformed, (unsigned long long)nmal);")
-        g("if (nfilt) atomicAdd((unsigned long long*)&ST->filtered, (unsigned long long)nfilt);")
-        g("if (nidx) atomicAdd((unsigned long long*)&ST->side_rows, (unsigned long long)nidx);")
+        g("fbx::block_side_counts(ST, nmal, nfilt, nidx);")
         g("}")
         return name
 

@@ -601,6 +601,30 @@ FBX_DI void dup_note(fbx_state* st, u64* pair, u32 chunk) {
   atomicExch((unsigned long long*)&st->dup_seen, 1ull);
 }
 
+// Index-build tail: the CTA's malformed / filtered / indexed counts reach the
+// run state by ONE atomic each per CTA (per-thread atomics on three shared
+// words serialise in L2: 1M rows cost ~240 us that way).  Every thread of the
+// CTA must call it (block-uniform control flow).
+FBX_DI void block_side_counts(fbx_state* st, u32 nmal, u32 nfilt, u32 nidx) {
+  __shared__ u32 acc[3];
+  if (threadIdx.x < 3u) acc[threadIdx.x] = 0u;
+  __syncthreads();
+  const u32 a = __reduce_add_sync(0xFFFFFFFFu, nmal);
+  const u32 b = __reduce_add_sync(0xFFFFFFFFu, nfilt);
+  const u32 c = __reduce_add_sync(0xFFFFFFFFu, nidx);
+  if ((threadIdx.x & 31u) == 0u) {
+    if (a) atomicAdd(&acc[0], a);
+    if (b) atomicAdd(&acc[1], b);
+    if (c) atomicAdd(&acc[2], c);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (acc[0]) atomicAdd((unsigned long long*)&st->malformed, (unsigned long long)acc[0]);
+    if (acc[1]) atomicAdd((unsigned long long*)&st->filtered, (unsigned long long)acc[1]);
+    if (acc[2]) atomicAdd((unsigned long long*)&st->side_rows, (unsigned long long)acc[2]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Block-level primitives (blockDim.x == NT, a multiple of 32, <= 1024)
 // ---------------------------------------------------------------------------
