@@ -1601,6 +1601,150 @@ FBX_DI bool j_lit(const JReader& r, u32 i, const char* w, u32 wl) {
   return true;
 }
 
+// Mask-mode walker (documents jmask_build accepted: <= 60 bytes, no backslash,
+// no byte < 0x20).  The same grammar and path semantics as the byte scanner in
+// json_extract below, walked one MEMBER per iteration (key, ':', value, then the
+// closers and the comma that follow it) instead of one token per iteration: the
+// documents of a warp mostly share their shape, so lanes stay on the same
+// instruction stream (a token loop diverges on the token kind every step).
+// Whitespace is a clz over the non-space mask, a string's end a clz over the
+// quote mask (no escapes); the masks' sentinels bound every scan.
+template <int NP, class KM>
+FBX_DI u32 json_extract_m(const u8* p, const u32 n, const u64 q, const u64 nsp,
+                          const JPathSet ps, JLeaf (&leaf)[NP]) {
+#define FBX_JSKIP(x) ((x) + (u32)__clzll((long long)(nsp << (x))))
+  u64 kind = 0;   // bit d: the container at depth d+1 is an object
+  u32 depth = 0;
+  u64 live = 0;   // byte d (d < 8): paths live in the object at depth d+1
+  u32 i = (u32)__clzll((long long)nsp);
+  while (true) {
+    // ---- one member (object) or element (array) at i, or the top-level value
+    u32 leafm = 0u, descm = 0u;
+    const bool obj = depth && ((kind >> (depth - 1u)) & 1ull);
+    if (obj) {
+      if (i >= n || p[i] != '"') return JS_MALFORMED;
+      const u32 kb = i + 1u;
+      const u32 ke = kb + (u32)__clzll((long long)(q << kb));
+      if (ke >= n) return JS_MALFORMED;
+      if (depth <= 8u) {
+        const u32 lv = (u32)((live >> ((depth - 1u) * 8u)) & 0xFFull);
+        if (lv) {
+          const u32 sidx = depth - 1u, klen = ke - kb;
+          const u64 kpre = load_prefix8(p + kb, klen);
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) {
+            if (!(lv & (1u << pp))) continue;
+            const u32 ns = KM::nseg(pp);
+            if (sidx >= ns) continue;
+            bool eq = KM::eq(pp, sidx, kpre, klen);
+            if (eq && klen > 8u) {
+              const u32 off = ps.seg_off[pp * 8 + sidx];
+              FBX_ROLLED
+              for (u32 k = 8; k < klen && eq; ++k) eq = p[kb + k] == ps.seg[off + k];
+            }
+            if (!eq) continue;
+            leaf[pp] = JLeaf{0, 0, J_MISSING, 0};  // a later duplicate key replaces the value
+            if (sidx + 1u == ns) leafm |= (1u << pp); else descm |= (1u << pp);
+          }
+        }
+      }
+      i = FBX_JSKIP(ke + 1u);
+      if (i >= n || p[i] != ':') return JS_MALFORMED;
+      i = FBX_JSKIP(i + 1u);
+    }
+    // ---- the value at i
+    if (i >= n) return JS_MALFORMED;
+    const u32 c = p[i];
+    if (c == '{' || c == '[') {
+      const bool o = c == '{';
+      if (o) kind |= (1ull << depth); else kind &= ~(1ull << depth);
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+        if (leafm & (1u << pp)) leaf[pp] = JLeaf{i, i, J_CONTAINER, 0};
+      const u32 childlive = o ? (depth == 0u ? ((1u << NP) - 1u) : descm) : 0u;
+      ++depth;
+      if (depth <= 8u) {
+        live &= ~(0xFFull << ((depth - 1u) * 8u));
+        live |= (u64)(childlive & 0xFFu) << ((depth - 1u) * 8u);
+      }
+      i = FBX_JSKIP(i + 1u);
+      if (i >= n) return JS_MALFORMED;
+      if (p[i] != (o ? '}' : ']')) continue;  // first member / element
+      --depth;  // empty container: a complete value
+      i = FBX_JSKIP(i + 1u);
+    } else {
+      u32 vb = i, ve, vt;
+      if (c == '"') {
+        vb = i + 1u;
+        ve = vb + (u32)__clzll((long long)(q << vb));
+        if (ve >= n) return JS_MALFORMED;
+        vt = J_STRING;
+        i = ve + 1u;
+      } else {
+        // a number or literal (4300-digit limit unreachable in 60 bytes)
+        u32 e;
+        const u32 neg = c == '-' ? 1u : 0u;
+        const u32 d = i + neg < n ? p[i + neg] : 0u;
+        if (d - '0' < 10u) {
+          e = i + neg + 1u;
+          if (d != '0') {
+            FBX_ROLLED
+            while (e < n && p[e] - '0' < 10u) ++e;
+          }
+          vt = J_INT;
+          if (e + 1u < n && p[e] == '.' && p[e + 1u] - '0' < 10u) {
+            e += 2u;
+            FBX_ROLLED
+            while (e < n && p[e] - '0' < 10u) ++e;
+            vt = J_FLOAT;
+          }
+          if (e < n && (p[e] | 0x20u) == 'e') {
+            u32 k = e + 1u;
+            if (k < n && (p[k] == '+' || p[k] == '-')) ++k;
+            if (k < n && p[k] - '0' < 10u) {
+              FBX_ROLLED
+              while (k < n && p[k] - '0' < 10u) ++k;
+              e = k;
+              vt = J_FLOAT;
+            }
+          }
+        } else {
+          const u64 w = load_prefix8(p + i, n - i);
+          if ((w & 0xFFFFFFFFull) == 0x65757274ull) { vt = J_TRUE; e = i + 4u; }               // true
+          else if ((w & 0xFFFFFFFFFFull) == 0x65736C6166ull) { vt = J_FALSE; e = i + 5u; }     // false
+          else if ((w & 0xFFFFFFFFull) == 0x6C6C756Eull) { vt = J_NULL; e = i + 4u; }          // null
+          else if ((w & 0xFFFFFFull) == 0x4E614Eull) { vt = J_NAN; e = i + 3u; }               // NaN
+          else if (w == 0x7974696E69666E49ull) { vt = J_POSINF; e = i + 8u; }                  // Infinity
+          else if (neg && w == 0x74696E69666E492Dull && i + 8u < n && p[i + 8u] == 'y') {   // -Infinity
+            vt = J_NEGINF; e = i + 9u;
+          } else {
+            return JS_MALFORMED;
+          }
+        }
+        ve = e;
+        i = e;
+      }
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+        if (leafm & (1u << pp)) leaf[pp] = JLeaf{vb, ve, vt, 0};
+      i = FBX_JSKIP(i);
+    }
+    // ---- after a complete value: closers, then one comma (or the end)
+    while (true) {
+      if (depth == 0u) return i >= n ? JS_OK : JS_MALFORMED;
+      if (i >= n) return JS_MALFORMED;
+      const u32 ch = p[i];
+      const bool ob = (kind >> (depth - 1u)) & 1ull;
+      if (ch == ',') break;
+      if (ch != (ob ? '}' : ']')) return JS_MALFORMED;
+      --depth;
+      i = FBX_JSKIP(i + 1u);
+    }
+    i = FBX_JSKIP(i + 1u);
+  }
+#undef FBX_JSKIP
+}
+
 // Validate the whole document (CPython json.loads, strict) and extract the NP
 // dot paths.  Inlined so the leaves live in registers.  Returns JS_*.
 // KM: plan-generated key matcher -- KM::nseg(p) and KM::eq(p, sidx, prefix8, len)
@@ -1609,12 +1753,17 @@ template <int NP, class KM>
 FBX_DI u32 json_extract(Str doc, const JPathSet ps, JLeaf (&leaf)[NP]) {
 #pragma unroll
   for (int p = 0; p < NP; ++p) leaf[p] = JLeaf{0, 0, J_MISSING, 0};
+  {
+    u64 q = 0ull, nsp = 0ull;
+    if (jmask_build(doc.p, doc.n, &q, &nsp)) return json_extract_m<NP, KM>(doc.p, doc.n, q, nsp, ps, leaf);
+  }
+  // every other document: the byte scanner (escapes, control bytes, long documents)
   JReader r;
   r.p = doc.p;
   r.n = doc.n;
   r.q = 0ull;
   r.nsp = 0ull;
-  r.fast = jmask_build(doc.p, doc.n, &r.q, &r.nsp);
+  r.fast = false;
   const u32 n = doc.n;
   u64 kind_stack = 0;  // bit d: container at depth d+1 is an object
   u32 depth = 0;
