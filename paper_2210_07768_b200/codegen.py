@@ -1257,7 +1257,8 @@ class PlanCodegen:
         g("// tiles in blockIdx order: the hardware dispatches CTAs in order, so every")
         g("// predecessor a look-back waits on is resident or done (as CUB relies on)")
         bid = "blockIdx.x"
-        g(f"const u32 tile = (u32){g.p('tile_base')} + {bid};  // run-global tile id")
+        g(f"const u32 TILE0 = (u32){g.p('tile_base')};  // this launch's first tile")
+        g(f"const u32 tile = TILE0 + {bid};  // run-global tile id")
         if self.spc == 1:
             g(f"const u64 chunk = CHUNK0 + {bid};")
             g(f"const u64 row0 = ROW_LO + (u64){bid} * {ir.chunk}ull;")
@@ -1579,8 +1580,19 @@ class PlanCodegen:
         g(f"u64* O_IDS = {g.p('out.ids', 'u64*')}; u8* O_LAB = {g.p('out.labels', 'u8*')};")
         g(f"u64* O_OFF = {g.p('out.offsets', 'u64*')}; u16* O_SLOT = {g.p('out.slots', 'u16*')};")
         g(f"u64* O_SIGN = {g.p('out.signs', 'u64*')};")
-        g("const u64 ei = sm.ex_inst, es = sm.ex_signs;")
-        g(f"if (emit_bad) fbx::raise_emit(ST, ei + myrank, {ir.chunk}u, emit_bad == 2u, {lab.c});")
+        g("// the look-back is launch-local (28-bit counts per launch); the run totals")
+        g("// before this launch come from the previous launch's last tile (LB), so a")
+        g("// run has no row limit.  Ring mode: the CSR of a launch lands at the start")
+        g("// of its own output slot (offsets launch-local), for bounded-memory streams.")
+        g(f"const u64* LB = {g.p('launch_base', 'const u64*')};")
+        g("const u64 lb_i = LB[0], lb_s = LB[1];")
+        g(f"const bool RING = {g.p('csr_ring')} != 0ull;")
+        g("const u64 ei = (RING ? 0ull : lb_i) + sm.ex_inst, es = (RING ? 0ull : lb_s) + sm.ex_signs;")
+        g("if (blockIdx.x == gridDim.x - 1u && threadIdx.x == 0u) {  // this launch's run totals")
+        g(f"u64* LN = {g.p('launch_next', 'u64*')};")
+        g("LN[0] = lb_i + sm.ex_inst + n_inst; LN[1] = lb_s + sm.ex_signs + tile_signs;")
+        g("}")
+        g(f"if (emit_bad) fbx::raise_emit(ST, lb_i + sm.ex_inst + myrank, {ir.chunk}u, emit_bad == 2u, {lab.c});")
         # sub-tiled chunks: the merge re-places label failures from the final order,
         # so a bad label is marked in the emitted label byte (0xFE null, 0xFF range;
         # such a run fails, its CSR is never handed out)
@@ -1756,7 +1768,7 @@ class PlanCodegen:
         g = self.g
         g("if (threadIdx.x < 32u) {")
         g("u64 ei = 0, es = 0;")
-        g("fbx::lookback(STATUS, tile, n_inst, tile_signs, &ei, &es);")
+        g("fbx::lookback(STATUS, tile, TILE0, n_inst, tile_signs, &ei, &es);")
         g("if (threadIdx.x == 0) { sm.ex_inst = ei; sm.ex_signs = es; }")
         g("}")
         if self.phase_timers:
@@ -1785,7 +1797,7 @@ class PlanCodegen:
             g(f"const u32 n_inst = sm.scan.sum({live} ? 1u : 0u);")
             g(f"const u32 tile_signs = sm.scan.sum({mm});")
         g("// publish the aggregate now: successors' look-back overlaps our sort")
-        g("if (threadIdx.x == 0) fbx::publish_aggregate(STATUS, tile, n_inst, tile_signs);")
+        g("if (threadIdx.x == 0) fbx::publish_aggregate(STATUS, tile, TILE0, n_inst, tile_signs);")
         g("// Emitted ids are unique (else the run fails): a row's rank is the number")
         g("// of live ids below its own.  Adaptive radix buckets carrying the sign counts")
         g("// (rank and sign offset in one pass); bitonic sort + offset scan fallback.")

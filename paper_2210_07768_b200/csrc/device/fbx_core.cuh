@@ -1216,9 +1216,11 @@ FBX_DI void mbar_wait(u64* bar, u32 phase) {
 }
 
 // ---------------------------------------------------------------------------
-// Decoupled look-back over tiles (chunks) for the global CSR offsets.
+// Decoupled look-back over tiles (chunks) for the CSR offsets, within one
+// launch (a launch covers at most 2^24 rows, so 28-bit counts never wrap; the
+// run totals before a launch are carried in device memory, see codegen).
 // status word: flag(2) | instances(28) | signs(34); flag 1 = aggregate,
-// 2 = inclusive prefix.
+// 2 = launch-inclusive prefix.
 // ---------------------------------------------------------------------------
 #ifndef FBX_LB_SLEEP
 #define FBX_LB_SLEEP 64  // ns between polls of an unpublished predecessor
@@ -1235,17 +1237,19 @@ FBX_DI u64 pack_status(u64 flag, u64 inst, u64 signs) {
   return (flag << 62) | ((inst & 0xFFFFFFFull) << 34) | (signs & 0x3FFFFFFFFull);
 }
 
-// Thread 0, as soon as the tile's totals are known: tile 0 publishes its
-// inclusive prefix, every other tile its aggregate (decoupled look-back).
-FBX_DI void publish_aggregate(u64* status, u32 tile, u64 inst, u64 signs) {
-  st_release(status + tile, pack_status(tile == 0 ? 2 : 1, inst, signs));
+// Thread 0, as soon as the tile's totals are known: the launch's first tile
+// publishes its inclusive prefix, every other tile its aggregate (decoupled
+// look-back).  Counts are launch-local: a launch never looks back past `first`.
+FBX_DI void publish_aggregate(u64* status, u32 tile, u32 first, u64 inst, u64 signs) {
+  st_release(status + tile, pack_status(tile == first ? 2 : 1, inst, signs));
 }
 
 // Warp 0, later: sum predecessors back to the first inclusive prefix, then
 // publish this tile's inclusive prefix.  Returns the exclusive prefix.
-FBX_DI void lookback(u64* status, u32 tile, u64 inst, u64 signs, u64* ex_inst, u64* ex_signs) {
+FBX_DI void lookback(u64* status, u32 tile, u32 first, u64 inst, u64 signs, u64* ex_inst,
+                     u64* ex_signs) {
   const u32 lane = threadIdx.x & 31u;
-  if (tile == 0) {
+  if (tile == first) {
     *ex_inst = 0;
     *ex_signs = 0;
     return;
@@ -1255,7 +1259,7 @@ FBX_DI void lookback(u64* status, u32 tile, u64 inst, u64 signs, u64* ex_inst, u
   while (true) {
     i64 idx = base - (i64)lane;
     u64 w = 0;
-    if (idx >= 0) {
+    if (idx >= (i64)first) {
       w = ld_acquire(status + idx);
       while ((w >> 62) == 0) {  // predecessor not published yet: yield the issue slot
 #if FBX_LB_SLEEP > 0

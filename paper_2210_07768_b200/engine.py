@@ -388,6 +388,8 @@ def _next_pow2(n: int) -> int:
 class Engine:
     """Device state of one prepared plan on one GPU."""
 
+    LAUNCH_ROWS_MAX = 1 << 24  # look-back counts are launch-local, 28 bits
+
     def __init__(self, prepared: Prepared, views: Mapping[str, ViewImage] | None = None,
                  basic: ViewImage | None = None, device: str = "cuda",
                  max_rows_per_launch: int = 1 << 22, pool_bytes_per_row: int = 96):
@@ -401,7 +403,8 @@ class Engine:
         self.slots = self.prog.slots
         self.params = np.zeros(runtime.FBX_MAX_PARAM_SLOTS, dtype=np.uint64)
         # launches cover whole chunks; round UP so a run of <= max rows is one launch
-        self.max_rows = -(-max_rows_per_launch // ir.chunk) * ir.chunk
+        self.max_rows = min(-(-max_rows_per_launch // ir.chunk) * ir.chunk,
+                            max(ir.chunk, self.LAUNCH_ROWS_MAX // ir.chunk * ir.chunk))
         self.pool_bytes_per_row = pool_bytes_per_row
         if prepared.program.json_kind:  # canonical JSON can outgrow its source (escapes)
             self.pool_bytes_per_row += 512
@@ -637,12 +640,24 @@ class Engine:
         key = (chunk << 32) | (codegen.STAGE["merge"] << 28) | codegen.ERR["dup_id"]
         return key, ident
 
+    def _global_incl(self, t0: int, t1: int) -> np.ndarray:
+        """Run-global inclusive instance counts of tiles [t0, t1): the look-back
+        status words are launch-local, plus the run total before each launch
+        (written by the previous launch's last tile)."""
+        words = self.status[t0:t1].cpu().numpy().view(np.uint64)
+        incl = ((words >> np.uint64(34)) & np.uint64(0xFFFFFFF)).astype(np.int64)
+        lb = self.lbuf.cpu().numpy().view(np.uint64)
+        for a, b, k in self._launch_tiles:
+            lo, hi = max(a, t0), min(b, t1)
+            if lo < hi:
+                incl[lo - t0:hi - t0] += np.int64(lb[2 * k])
+        return incl
+
     def _chunk_ends(self, t0: int, t1: int) -> np.ndarray:
         """Run-global inclusive instance counts at the end of every chunk whose
         sub-tiles are [t0, t1) (look-back status words)."""
         spc = self.prog.tiles_per_chunk
-        words = self.status[t0:t1].cpu().numpy().view(np.uint64)
-        incl = ((words >> np.uint64(34)) & np.uint64(0xFFFFFFF)).astype(np.int64)
+        incl = self._global_incl(t0, t1)
         nch = -(-(t1 - t0) // spc)
         return np.array([incl[min((c + 1) * spc, t1 - t0) - 1] for c in range(nch)],
                         dtype=np.int64)
@@ -719,9 +734,8 @@ class Engine:
         batch, rng, pos = ek >> 13, (ek >> 12) & 1, ek & 0xFFF
         code = codegen.ERR["label_range" if rng else "null_label"]
         sub = (((1 + rng) & 0xFF) << 20) | ((pos & 0xFFF) << 8) | code  # after the dup check
-        words = self.status[: self._run_tiles].cpu().numpy().view(np.uint64)
-        incl = (words >> np.uint64(34)) & np.uint64(0xFFFFFFF)
-        hit = np.nonzero(incl >= np.uint64((batch + 1) * bs))[0]
+        incl = self._global_incl(0, self._run_tiles)
+        hit = np.nonzero(incl >= (batch + 1) * bs)[0]
         if hit.size == 0:
             return (0xFFFFFFFF << 32) | (codegen.STAGE["emit"] << 28) | sub
         chunk = int(hit[0]) + self._chunk_minus_tile
@@ -751,9 +765,12 @@ class Engine:
                                 self.state.data_ptr(), self._stream())
             nk += 1
         if getattr(self, "status", None) is not None:
-            runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(),
-                                self.status.numel(), self._stream())
+            # the launch run-total words and every tile's look-back status
+            runtime.state_reset(self.state.data_ptr(), self.status_all.data_ptr(),
+                                self.status_all.numel(), self._stream())
             nk += 1
+        self._launch_k = 0
+        self._launch_tiles = []
         self._dup_dirty = False
         self._set("idset", self.idset.data_ptr())
         self._set("idset_mask", self._idset_cap - 1)
@@ -774,7 +791,11 @@ class Engine:
         need = (tiles, rows, k, launch_rows, getattr(self, "_arena_min", 0))
         if getattr(self, "_arena_key", None) != need:
             dev = self.device
-            self.status = torch.zeros(tiles + 1, dtype=torch.int64, device=dev)
+            # [run totals before launch k: 2 words per launch (<= one launch per
+            #  tile) | look-back status per tile], cleared together by state_reset
+            self.status_all = torch.zeros(3 * (tiles + 1), dtype=torch.int64, device=dev)
+            self.lbuf = self.status_all[: 2 * (tiles + 1)]
+            self.status = self.status_all[2 * (tiles + 1):]
             self.o_ids = torch.empty(rows + 1, dtype=torch.int64, device=dev)
             self.o_lab = torch.empty(rows + 16, dtype=torch.uint8, device=dev)
             self.o_off = torch.empty(rows + 2, dtype=torch.int64, device=dev)
@@ -849,10 +870,16 @@ class Engine:
             raise ValueError("row_lo must start a driver chunk")
         rows = row_hi - row_lo
         stream = self._stream() if stream is None else stream
+        if rows > self.LAUNCH_ROWS_MAX:
+            raise ValueError(f"a launch covers at most {self.LAUNCH_ROWS_MAX} rows "
+                             "(28-bit look-back counts)")
         if tile_base is None:
             tiles = self._arena(rows)
-            runtime.state_reset(self.state.data_ptr(), self.status.data_ptr(), tiles + 1, stream)
+            runtime.state_reset(self.state.data_ptr(), self.status_all.data_ptr(),
+                                2 * (self.status.numel()) + tiles + 1, stream)
             tile_base = 0
+            self._launch_k = 0
+            self._launch_tiles = []
         else:
             # continuation of a reserved run: counters / digest / error word keep
             # accumulating across launches; only the bump pool is reset
@@ -863,6 +890,13 @@ class Engine:
         self._set("row_hi", row_hi)
         self._set("chunk0", row_lo // self.ir.chunk)
         self._set("tile_base", tile_base)
+        k = self._launch_k
+        lb = self.lbuf.data_ptr()
+        self._set("launch_base", lb + 16 * k)
+        self._set("launch_next", lb + 16 * (k + 1))
+        self._set("csr_ring", 0)
+        self._launch_tiles.append((tile_base, tile_base + tiles, k))
+        self._launch_k = k + 1
         self._chunk_minus_tile = row_lo // self.ir.chunk - tile_base
         self._run_chunk0 = row_lo // self.ir.chunk - tile_base // self.prog.tiles_per_chunk
         self._run_tiles = tile_base + tiles
