@@ -32,6 +32,7 @@ extern "C" {
 #define FBX_E_CUDA (-3)
 #define FBX_E_NOT_FOUND (-4)
 #define FBX_E_DUPLICATE (-5)
+#define FBX_E_IO (-6)
 
 typedef struct fbx_program fbx_program; /* a loaded plan module (CUmodule) */
 typedef struct fbx_kernel fbx_kernel;   /* one kernel of a program */
@@ -139,6 +140,17 @@ int fbx_crc32(const void* d_buf, unsigned long long n, unsigned* d_scratch, unsi
 unsigned long long fbx_crc32_scratch_words(unsigned long long n);
 
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream);
+
+/* Host ingest of a driver slice (read_columns with a row range,
+ * columnstore.py:499-608; pipeline.py:986-1006 reads the driver chunk by chunk):
+ * n_spans byte spans of one FBXC file, span i = file bytes
+ * [file_off[i], file_off[i] + len[i]) -> dst + dst_off[i].  pread(2) from a pool
+ * of n_threads host threads (1 MiB pieces) straight into the (pinned) staging
+ * buffer that the H2D copy reads next.  FBX_E_IO on an open / read failure or a
+ * span past the end of the file (the reference's TruncatedError). */
+int fbx_read_spans(const char* path, void* dst, const unsigned long long* file_off,
+                   const unsigned long long* len, const unsigned long long* dst_off,
+                   unsigned n_spans, unsigned n_threads);
 
 /* =======================================================================
  * The engine object: the drop-in for the reference's extraction boundary

@@ -449,13 +449,14 @@ class PlanCodegen:
             terms = " + ".join(f"(fbx_psum[{p}] ? fbx_psum[{p}] + 127ull * PG : 0ull)"
                                for p in planes)
             g(f"if (({terms}) * {spc}ull > {cap}ull) pneed = true;  // layer {layer}")
-        g(f"{g.p('pool_flag', 'u8*')}[tile] = (u8)pneed;")
+        g(f"const u32 ptile = tile - (u32){g.p('pool_tile0')};  // plane index (ring: launch-local)")
+        g(f"{g.p('pool_flag', 'u8*')}[ptile] = (u8)pneed;")
         g("if (pneed) {")
         if self.pool_kw_bad:
             g(f"fbx::raise_err(ST, fbx::err_key(chunk, 4u, 0u, 0u, {ERR['pool_key']}u), 0ull);  // Utf8 join keys")
-        g(f"{g.p('pool_chunk', 'u64*')}[tile] = chunk;")
+        g(f"{g.p('pool_chunk', 'u64*')}[ptile] = chunk;")
         g("atomicAdd((unsigned long long*)&ST->pool_flagged, 1ull);")
-        g(f"const u64 PL = {g.p('pool_plane')}, PB = (u64)tile * {tr}ull;")
+        g(f"const u64 PL = {g.p('pool_plane')}, PB = (u64)ptile * {tr}ull;")
         g(f"for (u32 r = 0; r < {tr}u; ++r) {{")
         g(f"{g.p('pool_joined', 'u8*')}[PB + r] = fbx_pjf[r];")
         for j in range(self.pool_kw):

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import enum
 import mmap
+import os
 import struct
 import zlib
 from dataclasses import dataclass, field
@@ -307,54 +308,74 @@ class ViewFile:
 
 
 def open_view(path: str | Path) -> ViewFile:
-    """Parse an FBXC header + directory (``columnstore.py:401-478``)."""
+    """Parse an FBXC header + directory (``columnstore.py:401-478``).
+
+    Only the header, the directory and the 4-byte CRC trailer are read (the
+    body is read later, span by span); the file length is checked against the
+    directory."""
     path = Path(path)
     with open(path, "rb") as fh:
-        blob = fh.read()
-    if len(blob) < 6 or blob[:4] != MAGIC:
-        raise FormatError(f"{path}: not an FBXC file")
-    if _U16.unpack_from(blob, 4)[0] != VERSION:
-        raise FormatError(f"{path}: unsupported version")
-    try:
-        pos = 6
-        (rows,) = _U64.unpack_from(blob, pos)
-        (ncols,) = _U16.unpack_from(blob, pos + 8)
-        (nkeys,) = _U16.unpack_from(blob, pos + 10)
-        pos += 12
-        schema = []
-        for _ in range(ncols):
-            kind = Kind(blob[pos])
-            (ln,) = _U16.unpack_from(blob, pos + 1)
-            schema.append((blob[pos + 3 : pos + 3 + ln].decode("utf-8"), kind))
-            pos += 3 + ln
-        keys = []
-        for _ in range(nkeys):
-            keys.append(schema[_U16.unpack_from(blob, pos)[0]][0])
-            pos += 2
-        (nseg,) = _U32.unpack_from(blob, pos)
-        pos += 4
-        spans = [_SEG.unpack_from(blob, pos + i * _SEG.size) for i in range(nseg)]
-        pos += nseg * _SEG.size
-    except (struct.error, IndexError, ValueError) as exc:
-        raise TruncatedError(f"{path}: malformed header ({exc})") from None
-    parts = [
-        (n, p)
-        for n, k in schema
-        for p in (("nulls", "offsets", "data") if k.var_length else ("nulls", "data"))
-    ]
-    if len(parts) != nseg:
-        raise FormatError(f"{path}: directory/schema mismatch")
-    cursor = pos
-    segs = {}
-    for key, (off, ln) in zip(parts, spans):
-        if off != cursor:
-            raise FormatError(f"{path}: segment {key} not contiguous")
-        segs[key] = (off, ln)
-        cursor += ln
-    if cursor + 4 != len(blob):
-        raise TruncatedError(f"{path}: length mismatch")
-    return ViewFile(path, tuple(schema), tuple(keys), rows, segs, pos, cursor - pos,
-                    _U32.unpack_from(blob, cursor)[0])
+        size = os.fstat(fh.fileno()).st_size
+        blob = fh.read(min(size, 1 << 16))
+
+        def more(upto: int):
+            nonlocal blob
+            if upto > len(blob):
+                blob += fh.read(upto - len(blob))
+            if upto > len(blob):
+                raise struct.error("header past the end of the file")
+
+        if len(blob) < 6 or blob[:4] != MAGIC:
+            raise FormatError(f"{path}: not an FBXC file")
+        if _U16.unpack_from(blob, 4)[0] != VERSION:
+            raise FormatError(f"{path}: unsupported version")
+        try:
+            pos = 6
+            more(pos + 12)
+            (rows,) = _U64.unpack_from(blob, pos)
+            (ncols,) = _U16.unpack_from(blob, pos + 8)
+            (nkeys,) = _U16.unpack_from(blob, pos + 10)
+            pos += 12
+            schema = []
+            for _ in range(ncols):
+                more(pos + 3)
+                kind = Kind(blob[pos])
+                (ln,) = _U16.unpack_from(blob, pos + 1)
+                more(pos + 3 + ln)
+                schema.append((blob[pos + 3 : pos + 3 + ln].decode("utf-8"), kind))
+                pos += 3 + ln
+            keys = []
+            for _ in range(nkeys):
+                more(pos + 2)
+                keys.append(schema[_U16.unpack_from(blob, pos)[0]][0])
+                pos += 2
+            more(pos + 4)
+            (nseg,) = _U32.unpack_from(blob, pos)
+            pos += 4
+            more(pos + nseg * _SEG.size)
+            spans = [_SEG.unpack_from(blob, pos + i * _SEG.size) for i in range(nseg)]
+            pos += nseg * _SEG.size
+        except (struct.error, IndexError, ValueError) as exc:
+            raise TruncatedError(f"{path}: malformed header ({exc})") from None
+        parts = [
+            (n, p)
+            for n, k in schema
+            for p in (("nulls", "offsets", "data") if k.var_length else ("nulls", "data"))
+        ]
+        if len(parts) != nseg:
+            raise FormatError(f"{path}: directory/schema mismatch")
+        cursor = pos
+        segs = {}
+        for key, (off, ln) in zip(parts, spans):
+            if off != cursor:
+                raise FormatError(f"{path}: segment {key} not contiguous")
+            segs[key] = (off, ln)
+            cursor += ln
+        if cursor + 4 != size:
+            raise TruncatedError(f"{path}: length mismatch")
+        fh.seek(cursor)
+        (crc,) = _U32.unpack(fh.read(4))
+    return ViewFile(path, tuple(schema), tuple(keys), rows, segs, pos, cursor - pos, crc)
 
 
 def read_view(

@@ -11,14 +11,20 @@
 // Declarations and the reference interfaces they replace: include/fbx.h.
 
 #include <dlfcn.h>
+#include <errno.h>
+#include <fcntl.h>
 #include <nvrtc.h>
+#include <unistd.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
+#include <condition_variable>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fbx.h"
@@ -663,6 +669,155 @@ unsigned long long fbx_crc32_scratch_words(unsigned long long n) {
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream) {
   k_flush<<<1184, 512, 0, (cudaStream_t)stream>>>((unsigned int*)d_buf, bytes / 4);
   return cuda_check(cudaGetLastError(), "fbx_l2_flush");
+}
+
+}  // extern "C"
+
+// ---- host ingest: parallel positional reads of FBXC spans ------------------
+// The reference reads a driver chunk with seek + read per segment span
+// (columnstore.py:499-608).  Here one call copies every span of a slice of
+// row-range spans into one (pinned) staging buffer with pread(2) from a pool
+// of host threads: the page cache copies straight into the destination, there
+// are no page faults on a file mapping, and large spans are cut into 1 MiB
+// pieces so the copy runs at the host's memory bandwidth, not one core's.
+namespace {
+
+struct ReadJob {
+  int fd;
+  unsigned char* dst;
+  unsigned long long off, len;
+};
+
+class ReadPool {
+ public:
+  explicit ReadPool(unsigned n) {
+    for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~ReadPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  unsigned size() const { return (unsigned)workers_.size(); }
+  // runs every job (the caller takes part); returns the first errno, 0 = ok, -1 = short read
+  int run(std::vector<ReadJob>& jobs) {
+    std::unique_lock<std::mutex> lk(run_mu_);  // one batch at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      jobs_ = &jobs;
+      next_ = 0;
+      left_ = jobs.size();
+      err_ = 0;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [this] { return left_ == 0; });
+    jobs_ = nullptr;
+    return err_;
+  }
+
+ private:
+  void loop() {
+    while (true) {
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [this] { return stop_ || (jobs_ && next_ < jobs_->size()); });
+        if (stop_) return;
+      }
+      work();
+    }
+  }
+  void work() {
+    while (true) {
+      size_t k;
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (!jobs_ || next_ >= jobs_->size()) return;
+        k = next_++;
+      }
+      const ReadJob& j = (*jobs_)[k];
+      int e = 0;
+      unsigned long long done = 0;
+      while (done < j.len) {
+        const ssize_t r = pread(j.fd, j.dst + done, (size_t)(j.len - done), (off_t)(j.off + done));
+        if (r < 0) {
+          if (errno == EINTR) continue;
+          e = errno;
+          break;
+        }
+        if (r == 0) {
+          e = -1;
+          break;
+        }
+        done += (unsigned long long)r;
+      }
+      std::lock_guard<std::mutex> g(mu_);
+      if (e && !err_) err_ = e;
+      if (--left_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<ReadJob>* jobs_ = nullptr;
+  size_t next_ = 0, left_ = 0;
+  int err_ = 0;
+  bool stop_ = false;
+};
+
+std::mutex g_pool_mu;
+ReadPool* g_pool = nullptr;
+
+}  // namespace
+
+extern "C" {
+
+int fbx_read_spans(const char* path, void* dst, const unsigned long long* file_off,
+                   const unsigned long long* len, const unsigned long long* dst_off,
+                   unsigned n_spans, unsigned n_threads) {
+  if (!path || (!dst && n_spans)) return fail(FBX_E_ARG, "fbx_read_spans: null argument");
+  const int fd = open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return fail(FBX_E_IO, std::string("fbx_read_spans: open ") + path + ": " +
+                                        strerror(errno));
+  constexpr unsigned long long PIECE = 1ull << 20;
+  std::vector<ReadJob> jobs;
+  for (unsigned i = 0; i < n_spans; ++i)
+    for (unsigned long long o = 0; o < len[i]; o += PIECE)
+      jobs.push_back(ReadJob{fd, (unsigned char*)dst + dst_off[i] + o, file_off[i] + o,
+                             len[i] - o < PIECE ? len[i] - o : PIECE});
+  int rc = 0;
+  if (n_threads <= 1 || jobs.size() <= 1) {
+    for (auto& j : jobs) {
+      unsigned long long done = 0;
+      while (done < j.len && !rc) {
+        const ssize_t r = pread(fd, j.dst + done, (size_t)(j.len - done), (off_t)(j.off + done));
+        if (r < 0 && errno == EINTR) continue;
+        if (r <= 0) rc = r < 0 ? errno : -1;
+        else done += (unsigned long long)r;
+      }
+      if (rc) break;
+    }
+  } else {
+    ReadPool* pool;
+    {
+      std::lock_guard<std::mutex> g(g_pool_mu);
+      if (!g_pool || g_pool->size() + 1 < n_threads) {
+        delete g_pool;
+        g_pool = new ReadPool(n_threads - 1);  // the caller is the last reader
+      }
+      pool = g_pool;
+    }
+    rc = pool->run(jobs);
+  }
+  close(fd);
+  if (rc == -1) return fail(FBX_E_IO, std::string("fbx_read_spans: ") + path +
+                                          ": segment extends past end of file");
+  if (rc) return fail(FBX_E_IO, std::string("fbx_read_spans: ") + path + ": " + strerror(rc));
+  return FBX_OK;
 }
 
 }  // extern "C"

@@ -307,6 +307,64 @@ class DeviceView:
         return self
 
 
+    @classmethod
+    def from_file(cls, path, columns=None, device="cuda", verify: bool = True) -> "DeviceView":
+        """FBXC ingest through the host reader (fbx_read_spans): the wanted
+        segments are read by parallel pread into pinned memory and reach HBM in
+        one H2D copy, with no decode, no page faults on a mapping and no pageable
+        staging.  A full read (every column) moves the whole body and checks its
+        CRC-32 on the device first (columnstore.py:554-562), then lays the
+        segments out 16-B aligned by device copies."""
+        from .columns import ChecksumError, UnknownColumnError
+        torch = _torch()
+        vf = open_view(path)
+        names = [n for n, _ in vf.schema]
+        if columns is not None:
+            unknown = set(columns) - set(names)
+            if unknown:
+                raise UnknownColumnError(sorted(unknown)[0])
+        full = columns is None or set(columns) >= set(names)
+        dev = torch.device(device)
+        want = [(name, part) for name, _ in vf.schema
+                if columns is None or name in columns
+                for part in ("nulls", "data", "offsets") if (name, part) in vf.segments]
+        place, cur = {}, 0
+        for key in want:
+            place[key] = cur
+            cur += (vf.segments[key][1] + 31) // 16 * 16
+        self = cls.__new__(cls)
+        self.n = vf.row_count
+        self.kinds = {n: k for n, k in vf.schema if columns is None or n in columns}
+        self.tensors, self.bytes, self.torch = {}, 0, torch
+        arena = torch.zeros(cur + 16, dtype=torch.uint8, device=dev)
+        if full and verify:
+            host = torch.empty(vf.body_bytes + 16, dtype=torch.uint8, pin_memory=True)
+            runtime.read_spans(vf.path, host.data_ptr(), [vf.body_offset], [vf.body_bytes], [0])
+            body = torch.empty(vf.body_bytes + 64, dtype=torch.uint8, device=dev)
+            body[:vf.body_bytes].copy_(host[:vf.body_bytes], non_blocking=True)
+            crc = crc32_device(body[:vf.body_bytes])
+            if crc != vf.checksum:
+                raise ChecksumError(f"{vf.path}: body CRC {crc:#010x} != {vf.checksum:#010x}")
+            for (name, part), dst in place.items():
+                o, ln = vf.segments[(name, part)]
+                if ln:
+                    a = o - vf.body_offset
+                    arena[dst:dst + ln].copy_(body[a:a + ln])
+        else:
+            host = torch.empty(cur + 16, dtype=torch.uint8, pin_memory=True)
+            keys = list(place)
+            runtime.read_spans(vf.path, host.data_ptr(), [vf.segments[k][0] for k in keys],
+                               [vf.segments[k][1] for k in keys], [place[k] for k in keys])
+            arena.copy_(host, non_blocking=True)
+        for (name, part), dst in place.items():
+            ln = vf.segments[(name, part)][1]
+            self.tensors.setdefault(name, {})[part] = arena[dst:dst + ln]
+            self.bytes += ln
+        self._arena = arena
+        self.h2d_bytes = (vf.body_bytes if full and verify else cur)
+        return self
+
+
 def crc32_device(t) -> int:
     """zlib CRC-32 of a contiguous device tensor's bytes (fbx_crc32)."""
     torch = _torch()
@@ -392,7 +450,8 @@ class Engine:
 
     def __init__(self, prepared: Prepared, views: Mapping[str, ViewImage] | None = None,
                  basic: ViewImage | None = None, device: str = "cuda",
-                 max_rows_per_launch: int = 1 << 22, pool_bytes_per_row: int = 96):
+                 max_rows_per_launch: int = 1 << 22, pool_bytes_per_row: int = 96,
+                 device_views: Mapping[str, "DeviceView"] | None = None):
         torch = _torch()
         self.torch = torch
         self.prepared = prepared
@@ -415,7 +474,7 @@ class Engine:
             self._set("state", self.state.data_ptr())
             self.prepare_counters = Counters()
             self._keep: list = []
-            self._upload_sides(views or {}, basic)
+            self._upload_sides(views or {}, basic, device_views or {})
             self._upload_tables()
             self._idset_cap = 0
             self.idset = None
@@ -443,7 +502,10 @@ class Engine:
             return given.project(columns)
         return read_view(path, columns)
 
-    def _upload_sides(self, views: Mapping[str, ViewImage], basic: ViewImage | None):
+    def _upload_sides(self, views: Mapping[str, ViewImage], basic: ViewImage | None,
+                      device_views: Mapping[str, "DeviceView"]):
+        """Side views and the basic view into HBM (``device_views``: already there,
+        keyed by view name / "basic"), their hash indexes built by the prep kernels."""
         torch, cfg, ir = self.torch, self.config, self.ir
         sides = [(k, v) for k, v in enumerate(ir.sides)]
         if ir.basic is not None:
@@ -452,14 +514,17 @@ class Engine:
         prepared_views = []
         self.side_tables = {}
         for k, v in sides:
-            if v is ir.basic:
-                img = self._load_view("basic", cfg.basic_path, cfg.basic_columns, basic)
-            else:
-                src = cfg.view(v.name)
-                img = self._load_view(v.name, src.path, src.columns, views.get(v.name))
-            dv = DeviceView(img, device=self.device)
+            key = "basic" if v is ir.basic else v.name
+            dv = device_views.get(key)
+            if dv is None:
+                if v is ir.basic:
+                    img = self._load_view("basic", cfg.basic_path, cfg.basic_columns, basic)
+                else:
+                    src = cfg.view(v.name)
+                    img = self._load_view(v.name, src.path, src.columns, views.get(v.name))
+                dv = DeviceView(img, device=self.device)
             self._keep.append(dv)
-            n = img.row_count
+            n = dv.n
             cap = _next_pow2(2 * n)
             table = torch.zeros(cap * 32, dtype=torch.uint8, device=self.device)
             self._keep.append(table)
@@ -467,7 +532,7 @@ class Engine:
             self._set(f"side{k}.rows", n)
             self._set(f"side{k}.table", table.data_ptr())
             self._set(f"side{k}.mask", cap - 1)
-            for c in img.order:
+            for c in dv.tensors:
                 for part in ("nulls", "data", "offsets"):
                     self._set(f"side{k}.{c}.{part}", dv.ptr(c, part))
             for e in v.extractions:
@@ -483,9 +548,9 @@ class Engine:
                     self._keep += [val, nul]
                     self._set(f"side{k}.ext.{e.output}.val", val.data_ptr())
                     self._set(f"side{k}.ext.{e.output}.null", nul.data_ptr())
-                src_col = img.columns[e.source]
+                src_bytes = int(dv.tensors[e.source]["data"].numel())
                 grow = 6 if e.kind is Kind.JSON else 1  # ensure_ascii: 1 byte -> "\\uXXXX"
-                side_pool_cap += grow * int(src_col.data.nbytes) + 128 * (n // 256 + 1)
+                side_pool_cap += grow * src_bytes + 128 * (n // 256 + 1)
             prepared_views.append((k, v, n))
         pool = torch.zeros(side_pool_cap + 256, dtype=torch.uint8, device=self.device)
         self._keep.append(pool)
@@ -602,21 +667,32 @@ class Engine:
         self._dup_dirty = bool(st["dup_seen"])
         if st["pool_overflow"]:
             raise ArenaRetry(st["pool_overflow"])
-        if st["pool_flagged"]:
+        if st["pool_flagged"] and not getattr(self, "ring", False):  # ring: per launch
             self._pool_account()
             st = dict(st, **{k: v for k, v in self._read_state().items()
                              if k in ("error_key", "error_detail")})
         self._raise_if_error(st)
 
-    def _pool_account(self):
+    def ring_after_launch(self, stream: int) -> int:
+        """Ring runs: the reference arena's demand of the launch just enqueued is
+        settled now (fbx_pool_account, stream-ordered), before the next launch
+        reuses the planes.  Returns the number of launches enqueued."""
+        if not (self.ring and self.prog.ref_pool):
+            return 0
+        self._pool_account(self._last_launch_tiles, stream)
+        return 1
+
+    def _pool_account(self, n_tiles: int | None = None, stream: int | None = None):
         p = self.prog
         runtime.pool_account(self.pool_flag.data_ptr(), self.pool_chunk.data_ptr(),
-                             self._run_tiles, p.tiles_per_chunk, p.tile_rows,
+                             self._run_tiles if n_tiles is None else n_tiles,
+                             p.tiles_per_chunk, p.tile_rows,
                              self.pool_keys.data_ptr(), p.pool_kw, self.pool_sizes.data_ptr(),
                              p.pool_ni, self.pool_joined.data_ptr(), self.pool_nodes.data_ptr(),
                              len(p.ref_pool), self.config.lanes_per_group,
                              self.config.pool_bytes, self.pool_rank.data_ptr(),
-                             self.pool_gsum.data_ptr(), self.state.data_ptr(), self._stream())
+                             self.pool_gsum.data_ptr(), self.state.data_ptr(),
+                             self._stream() if stream is None else stream)
 
     def grow_arena(self, need: int):
         """Size the device arena for ``need`` bytes per launch (+25 %) and drop the
@@ -779,16 +855,21 @@ class Engine:
         self._run_tiles = 0
         return nk
 
-    def reserve(self, rows: int, launch_rows: int | None = None):
+    def reserve(self, rows: int, launch_rows: int | None = None, ring: bool = False):
         """Run-wide buffers: look-back status for every tile of the run (the
         look-back continues across launches), the CSR for every row, and a
-        bump pool sized for the largest launch."""
+        bump pool sized for the largest launch.  ``ring``: the CSR and the
+        reference-arena planes hold ONE launch (each launch writes its CSR at
+        the start, offsets launch-local) -- bounded memory for file streams."""
         torch = self.torch
         # no launch of this run covers more than its rows: size the pool for that
         launch_rows = rows if launch_rows is None else max(1, min(launch_rows, rows))
         tiles = self.tiles_for(rows)
         k = max(1, len(self.ir.features))
-        need = (tiles, rows, k, launch_rows, getattr(self, "_arena_min", 0))
+        self.ring = ring
+        crows = launch_rows if ring else rows
+        ptiles = self.tiles_for(launch_rows) if ring else tiles
+        need = (tiles, rows, k, launch_rows, getattr(self, "_arena_min", 0), ring)
         if getattr(self, "_arena_key", None) != need:
             dev = self.device
             # [run totals before launch k: 2 words per launch (<= one launch per
@@ -796,11 +877,11 @@ class Engine:
             self.status_all = torch.zeros(3 * (tiles + 1), dtype=torch.int64, device=dev)
             self.lbuf = self.status_all[: 2 * (tiles + 1)]
             self.status = self.status_all[2 * (tiles + 1):]
-            self.o_ids = torch.empty(rows + 1, dtype=torch.int64, device=dev)
-            self.o_lab = torch.empty(rows + 16, dtype=torch.uint8, device=dev)
-            self.o_off = torch.empty(rows + 2, dtype=torch.int64, device=dev)
-            self.o_slot = torch.empty(rows * k + 8, dtype=torch.int16, device=dev)
-            self.o_sign = torch.empty(rows * k + 1, dtype=torch.int64, device=dev)
+            self.o_ids = torch.empty(crows + 1, dtype=torch.int64, device=dev)
+            self.o_lab = torch.empty(crows + 16, dtype=torch.uint8, device=dev)
+            self.o_off = torch.empty(crows + 2, dtype=torch.int64, device=dev)
+            self.o_slot = torch.empty(crows * k + 8, dtype=torch.int16, device=dev)
+            self.o_sign = torch.empty(crows * k + 1, dtype=torch.int64, device=dev)
             pool_cap = 0
             if codegen_pool_sites(self.prog):
                 lt = (launch_rows + self.ir.chunk - 1) // self.ir.chunk
@@ -810,9 +891,9 @@ class Engine:
             self.pool_cap = pool_cap
             if self.prog.ref_pool:  # rows of flagged tiles for fbx_pool_account
                 p = self.prog
-                plane = tiles * p.tile_rows
-                self.pool_flag = torch.zeros(tiles + 1, dtype=torch.uint8, device=dev)
-                self.pool_chunk = torch.zeros(tiles + 1, dtype=torch.int64, device=dev)
+                plane = ptiles * p.tile_rows
+                self.pool_flag = torch.zeros(ptiles + 1, dtype=torch.uint8, device=dev)
+                self.pool_chunk = torch.zeros(ptiles + 1, dtype=torch.int64, device=dev)
                 self.pool_keys = torch.zeros(max(1, p.pool_kw) * plane + 1, dtype=torch.int64,
                                              device=dev)
                 self.pool_sizes = torch.zeros(p.pool_ni * plane + 1, dtype=torch.int32, device=dev)
@@ -894,8 +975,10 @@ class Engine:
         lb = self.lbuf.data_ptr()
         self._set("launch_base", lb + 16 * k)
         self._set("launch_next", lb + 16 * (k + 1))
-        self._set("csr_ring", 0)
+        self._set("csr_ring", 1 if self.ring else 0)
+        self._set("pool_tile0", tile_base if self.ring else 0)
         self._launch_tiles.append((tile_base, tile_base + tiles, k))
+        self._last_launch_tiles = tiles
         self._launch_k = k + 1
         self._chunk_minus_tile = row_lo // self.ir.chunk - tile_base
         self._run_chunk0 = row_lo // self.ir.chunk - tile_base // self.prog.tiles_per_chunk
@@ -1389,19 +1472,137 @@ def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: Vie
     return RunResult(rep, csr)
 
 
-def run_pipelined(config: PipelineConfig, collect: bool = False) -> RunReport:
-    """Reference-compatible ``run_pipelined`` (pipeline.py:952) on the B200."""
-    views = {}
+_PREPARED: dict[str, Prepared] = {}
+
+
+def _prepared(config: PipelineConfig) -> Prepared:
+    """prepare() once per (config, input schemas): the plan cache.  The schemas
+    come from the files' headers, so an edited file re-plans."""
+    import hashlib
+    import pickle
+    key_parts = [repr(config)]
     for v in config.views:
+        key_parts.append(repr(open_view(v.path).schema))
+    key_parts.append(repr(open_view(config.basic_path).schema))
+    key = hashlib.sha256(pickle.dumps(key_parts)).hexdigest()
+    prep = _PREPARED.get(key)
+    if prep is None:
+        prep = prepare(config)
+        _PREPARED.clear()  # one plan at a time (the engines hold its module)
+        _PREPARED[key] = prep
+    return prep
+
+
+def run_pipelined(config: PipelineConfig, collect: bool = False,
+                  slice_rows: int = 1 << 18) -> RunReport:
+    """Reference-compatible ``run_pipelined`` (pipeline.py:952-1114) on the B200.
+
+    prepare (plan cached per config + schemas) -> side views and basic features
+    read by the host reader into HBM, CRC-checked on the device, indexed by
+    the prep kernels (pipeline.py:970-980) -> the driver streamed from its file
+    in slices of whole chunks (stream.FileRun: parallel pread into a pinned
+    ring, H2D on a copy stream, the fused kernel on a compute stream, CSR in a
+    one-slice ring; bounded host and device memory) -> the run's counters and
+    digest, failures raised in the reference's pipeline order.  ``collect``:
+    the device-resident run over in-memory views (the whole CSR returned in
+    ``run_views``' result; tests)."""
+    if collect:
+        views = {}
+        for v in config.views:
+            try:
+                views[v.name] = read_view(v.path, v.columns)
+            except Exception as exc:  # noqa: BLE001
+                raise StageError("prepare", None, exc) from exc
         try:
-            views[v.name] = read_view(v.path, v.columns)
+            basic = read_view(config.basic_path, config.basic_columns)
         except Exception as exc:  # noqa: BLE001
             raise StageError("prepare", None, exc) from exc
+        return run_views(config, views, basic, collect=collect).report
+    from .stream import FileRun, _ReadFailure
+    t0 = time.perf_counter()
+    stage: dict[str, float] = {}
+    prep = _prepared(config)
+    drv_cfg = config.view(config.driver)
+    torch = _torch()
     try:
-        basic = read_view(config.basic_path, config.basic_columns)
+        dvs = {v.name: DeviceView.from_file(v.path, v.columns) for v in config.views
+               if v.name != config.driver}
+        dvs["basic"] = DeviceView.from_file(config.basic_path, config.basic_columns)
+        dfile = open_view(drv_cfg.path)
     except Exception as exc:  # noqa: BLE001
         raise StageError("prepare", None, exc) from exc
-    return run_views(config, views, basic, collect=collect).report
+    bytes_h2d = sum(d.h2d_bytes for d in dvs.values())
+    eng = Engine(prep, device_views=dvs)
+    torch.cuda.synchronize(eng.device)
+    launches = 1 + len(eng._side_views)  # the prepare-time state reset + index builds
+    stage["prepare"] = time.perf_counter() - t0
+    n = dfile.row_count
+    bs = config.batch_size
+    names = [c for c, _ in dfile.schema]
+    full_read = drv_cfg.columns is None or set(drv_cfg.columns) >= set(names)
+    t1 = time.perf_counter()
+    launch_s = 0.0
+    if eng.prog.tiles_per_chunk > 1 or (full_read and n <= bs):
+        # one chunk reads the whole body (the reference then checks its CRC), or
+        # chunks larger than a CTA (merged on the device): device-resident run
+        try:
+            dv = DeviceView.from_file(drv_cfg.path, drv_cfg.columns)
+        except Exception as exc:  # noqa: BLE001
+            raise StageError("read", 0, exc) from exc
+        bytes_h2d += dv.h2d_bytes
+        stage["read"] = time.perf_counter() - t1
+        eng.bind_driver(dv)
+        t2 = time.perf_counter()
+        step = eng.max_rows
+        while True:
+            eng.reserve(n, min(step, max(n, 1)))
+            launches += eng.begin_run(n)
+            tiles = 0
+            for lo in range(0, n, step):
+                tiles += eng.launch(lo, min(lo + step, n), tile_base=tiles)
+                launches += 1
+            try:
+                b = eng.finish()
+                break
+            except ArenaRetry as exc:
+                eng.grow_arena(exc.need)
+        launch_s = time.perf_counter() - t2
+        stage["extract"] = time.perf_counter() - t2
+        transfer_s = stage["read"]
+        c = b.counters
+    else:
+        while True:
+            fr = FileRun(eng, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows)
+            eng.reserve(n, fr.slice_rows, ring=True)
+            launches += eng.begin_run(n)
+            try:
+                t = fr.run()
+            except _ReadFailure as exc:
+                raise StageError("read", (exc.index * fr.slice_rows) // bs, exc.cause) from exc
+            launches += t["launches"]
+            launch_s += t["launch_s"]
+            st = eng._read_state()
+            try:
+                eng.check_run(st)
+                break
+            except ArenaRetry as exc:
+                eng.grow_arena(exc.need)
+        stage["read"] = t["read_s"]
+        stage["transfer"] = t["h2d_s"]
+        stage["extract"] = t["kernel_s"]
+        transfer_s = t["h2d_s"]
+        bytes_h2d += t["h2d_bytes"]
+        c = Counters(st["digest"], st["instances"], st["signs"], st["malformed"],
+                     st["filtered"], st["joined"], t["slices"])
+    stage["stream"] = time.perf_counter() - t1
+    return RunReport(
+        mode="pipelined", digest=c.digest, batches=math.ceil(c.instances / bs),
+        instances=c.instances, signs=c.signs, launches=launches,
+        overhead_us=1e6 * launch_s / max(1, launches), bytes_h2d=bytes_h2d,
+        transfer_seconds=transfer_s, intermediate_bytes_written=0, intermediate_files=(),
+        rows_dropped=c.malformed + eng.prepare_counters.malformed,
+        rows_filtered=c.filtered + eng.prepare_counters.filtered,
+        batch_size=bs, workers=1, wall_seconds=time.perf_counter() - t0, stage_seconds=stage)
 
 
 def run_pipeline(config: PipelineConfig, mode: str | None = None) -> RunReport:

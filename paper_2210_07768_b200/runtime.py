@@ -33,7 +33,7 @@ EXPORTS = ("fbx_version", "fbx_error_message", "fbx_compile", "fbx_free", "fbx_p
            "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
            "fbx_dup_resolve", "fbx_state_snapshot",
            "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words", "fbx_idset_clear",
-           "fbx_pool_account", "fbx_memset_async")
+           "fbx_pool_account", "fbx_memset_async", "fbx_read_spans")
 
 
 class FbxError(RuntimeError):
@@ -79,6 +79,8 @@ def lib() -> ctypes.CDLL:
             L.fbx_pool_account.argtypes = [vp, vp, ull, u, u, vp, u, vp, u, vp, vp, u, ull, ull,
                                            vp, vp, vp, vp]
             L.fbx_crc32.argtypes = [vp, ctypes.c_ulonglong, vp, vp, vp]
+            L.fbx_read_spans.argtypes = [ctypes.c_char_p, vp, vp, vp, vp, ctypes.c_uint,
+                                         ctypes.c_uint]
             L.fbx_crc32_scratch_words.argtypes = [ctypes.c_ulonglong]
             L.fbx_crc32_scratch_words.restype = ctypes.c_ulonglong
             for name in EXPORTS:
@@ -248,3 +250,24 @@ def gather_strings(d_ptrs: int, d_lens: int, d_offsets: int, n: int, d_out: int,
     _check(lib().fbx_gather_strings(ctypes.c_void_p(d_ptrs), ctypes.c_void_p(d_lens),
                                     ctypes.c_void_p(d_offsets), n, ctypes.c_void_p(d_out),
                                     ctypes.c_void_p(stream)), "gather strings")
+
+
+def host_threads() -> int:
+    """Reader threads for the host ingest (fbx_read_spans)."""
+    return max(1, min(16, os.cpu_count() or 1))
+
+
+def read_spans(path, dst: int, file_off, length, dst_off, threads: int | None = None):
+    """Parallel pread of FBXC spans into host memory at ``dst`` (fbx_read_spans);
+    raises FbxError (FBX_E_IO) on open / read failures and truncated files."""
+    fo = np.ascontiguousarray(file_off, dtype=np.uint64)
+    ln = np.ascontiguousarray(length, dtype=np.uint64)
+    do = np.ascontiguousarray(dst_off, dtype=np.uint64)
+    n = int(fo.size)
+    if not (ln.size == do.size == n):
+        raise ValueError("read_spans: span arrays differ in length")
+    vp = ctypes.c_void_p
+    _check(lib().fbx_read_spans(str(path).encode(), vp(dst), fo.ctypes.data_as(vp),
+                                ln.ctypes.data_as(vp), do.ctypes.data_as(vp), n,
+                                host_threads() if threads is None else int(threads)),
+           "read spans")

@@ -1,0 +1,191 @@
+"""The drop-in ``run_pipelined``'s driver stream: FBXC file -> HBM in bounded memory.
+
+The reference reads the driver view ``batch_size`` rows at a time through a
+bounded queue of chunks (``read_driver`` + ``_pump``, pipeline.py:986-1006) and
+never holds the whole log.  Here a slice of whole chunks is the unit:
+
+  host reader thread   parallel pread of the slice's column spans (libfbx
+                       ``fbx_read_spans``) into one of ``nbuf`` pinned buffers
+  copy stream          one H2D of the packed slice into one of ``nbuf`` device
+                       buffers
+  compute stream       the fused kernel over the slice (the look-back and the
+                       counters continue across slices); its CSR lands in a
+                       one-slice ring (launch-local offsets), which a trainer
+                       reads per slice and the digest sink never needs
+
+Host and device memory are O(slice), whatever the log size (the run-wide
+instance-id set of ``check_unique_ids`` and one status word per chunk aside).
+"""
+
+from __future__ import annotations
+
+import os
+import threading
+import time
+
+from . import runtime
+from .columns import open_view
+
+
+class FileRun:
+    """One driver file streamed through an ``Engine`` (bounded memory)."""
+
+    PARTS = ("nulls", "offsets", "data")
+
+    def __init__(self, eng, path, columns=None, slice_rows: int = 1 << 18, nbuf: int = 3,
+                 threads: int | None = None):
+        self.eng = eng
+        self.torch = torch = eng.torch
+        self.vf = vf = open_view(path)
+        self.n = n = vf.row_count
+        chunk = eng.ir.chunk
+        if eng.prog.tiles_per_chunk > 1:
+            raise ValueError("FileRun: batch_size > 1024 runs device-resident (chunk merge)")
+        S = max(chunk, slice_rows // chunk * chunk)
+        S = min(S, eng.LAUNCH_ROWS_MAX // chunk * chunk)
+        self.slice_rows = S
+        self.bounds = [(lo, min(lo + S, n)) for lo in range(0, n, S)]
+        kinds = dict(vf.schema)
+        self.cols = [c for c, _ in vf.schema
+                     if (columns is None or c in columns)
+                     and any(f"drv.{c}.{p}" in eng.slots for p in self.PARTS)]
+        self.threads = runtime.host_threads() if threads is None else threads
+        # boundary offsets of every var-length column at every slice edge: the data
+        # span of a slice is [off[lo], off[hi]) (one 4-byte pread per edge)
+        edges = [lo for lo, _ in self.bounds] + [n]
+        self.edge_off: dict[str, list[int]] = {}
+        with open(vf.path, "rb") as fh:
+            fd = fh.fileno()
+            for c in self.cols:
+                if kinds[c].var_length:
+                    o0 = vf.segments[(c, "offsets")][0]
+                    self.edge_off[c] = [int.from_bytes(os.pread(fd, 4, o0 + 4 * r), "little")
+                                        for r in edges]
+        self.kinds = kinds
+        self.layout = [self._pieces(k) for k in range(len(self.bounds))]
+        self.cap = max([sum((b - a + 15) // 16 * 16 for _, _, a, b, _ in pcs)
+                        for pcs in self.layout] or [16]) + 16
+        dev = eng.device
+        self.host = [torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
+                     for _ in range(min(nbuf, max(1, len(self.bounds))))]
+        self.dev = [torch.empty(self.cap + 32, dtype=torch.uint8, device=dev)
+                    for _ in range(len(self.host))]
+        self.s_h2d = torch.cuda.Stream(dev)
+        self.s_comp = torch.cuda.Stream(dev)
+        self.h2d_bytes = sum(sum(b - a for _, _, a, b, _ in pcs) for pcs in self.layout)
+
+    def _pieces(self, k: int):
+        """(column, part, start, end, dst) byte spans of slice k within each
+        segment, dst 16-B aligned in the packed slice."""
+        lo, hi = self.bounds[k]
+        vf = self.vf
+        out, off = [], 0
+        for c in self.cols:
+            kind = self.kinds[c]
+            sp = {"nulls": (lo // 8, (hi + 7) // 8)}
+            if kind.var_length:
+                e = self.edge_off[c]
+                seg_len = vf.segments[(c, "data")][1]
+                sp["offsets"] = (lo * 4, (hi + 1) * 4)
+                sp["data"] = (e[k] & ~15, min((e[k + 1] + 15) & ~15, seg_len))
+            else:
+                w = kind.fixed_width
+                sp["data"] = (lo * w, hi * w)
+            for p, (a, b) in sp.items():
+                out.append((c, p, a, b, off))
+                off += (b - a + 15) // 16 * 16
+        return out
+
+    def run(self) -> dict:
+        """Stream every slice through the engine; returns the timing / byte
+        counters of the run (the engine's state holds the results)."""
+        torch, eng = self.torch, self.eng
+        nb = len(self.host)
+        K = len(self.bounds)
+        ready = [threading.Event() for _ in range(K)]
+        recorded = [threading.Event() for _ in range(K)]
+        h2d_done = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        h2d_start = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        comp_done = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        comp_start = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        failure: list = [None, None]
+        read_s = [0.0]
+        vf = self.vf
+
+        cancel = threading.Event()
+
+        def reader():
+            k = 0
+            try:
+                for k in range(K):
+                    if cancel.is_set():
+                        return
+                    if k >= nb:
+                        recorded[k - nb].wait()
+                        h2d_done[k - nb].synchronize()  # the pinned buffer is free again
+                    t = time.perf_counter()
+                    pcs = self.layout[k]
+                    runtime.read_spans(vf.path, self.host[k % nb].data_ptr(),
+                                       [vf.segments[(c, p)][0] + a for c, p, a, _, _ in pcs],
+                                       [b - a for _, _, a, b, _ in pcs],
+                                       [o for *_, o in pcs], self.threads)
+                    read_s[0] += time.perf_counter() - t
+                    ready[k].set()
+            except BaseException as exc:  # noqa: BLE001 -- re-raised by the host loop
+                failure[0], failure[1] = k, exc
+                for e in ready[k:]:
+                    e.set()
+
+        th = threading.Thread(target=reader, name="fbx-read", daemon=True)
+        th.start()
+        cur = torch.cuda.current_stream(eng.device)
+        self.s_comp.wait_stream(cur)
+        self.s_h2d.wait_stream(cur)
+        launch_s = 0.0
+        launches = 0
+        tiles_before = 0
+        try:
+            for k, (lo, hi) in enumerate(self.bounds):
+                ready[k].wait()
+                if failure[1] is not None and failure[0] <= k:
+                    raise _ReadFailure(failure[0], failure[1])
+                buf = k % nb
+                pcs = self.layout[k]
+                nbytes = pcs[-1][4] + (pcs[-1][3] - pcs[-1][2]) if pcs else 0
+                with torch.cuda.stream(self.s_h2d):
+                    if k >= nb:
+                        self.s_h2d.wait_event(comp_done[k - nb])  # device buffer reuse
+                    h2d_start[k].record(self.s_h2d)
+                    self.dev[buf][:nbytes].copy_(self.host[buf][:nbytes], non_blocking=True)
+                    h2d_done[k].record(self.s_h2d)
+                recorded[k].set()
+                base = self.dev[buf].data_ptr()
+                for c, p, a, _, o in pcs:
+                    eng._set(f"drv.{c}.{p}", base + o - a)
+                with torch.cuda.stream(self.s_comp):
+                    self.s_comp.wait_event(h2d_done[k])
+                    comp_start[k].record(self.s_comp)
+                    t = time.perf_counter()
+                    tiles = eng.launch(lo, hi, self.s_comp.cuda_stream, tile_base=tiles_before)
+                    launches += 1 + eng.ring_after_launch(self.s_comp.cuda_stream)
+                    launch_s += time.perf_counter() - t
+                    comp_done[k].record(self.s_comp)
+                tiles_before += tiles
+        finally:
+            cancel.set()
+            for e in recorded:
+                e.set()
+            th.join()
+        self.s_comp.synchronize()
+        self.s_h2d.synchronize()
+        cur.wait_stream(self.s_comp)
+        return {"launches": launches, "launch_s": launch_s, "read_s": read_s[0],
+                "h2d_s": sum(a.elapsed_time(b) for a, b in zip(h2d_start, h2d_done)) / 1e3,
+                "kernel_s": sum(a.elapsed_time(b) for a, b in zip(comp_start, comp_done)) / 1e3,
+                "h2d_bytes": self.h2d_bytes, "slices": K}
+
+
+class _ReadFailure(Exception):
+    def __init__(self, index: int, cause: BaseException):
+        super().__init__(str(cause))
+        self.index, self.cause = index, cause
