@@ -308,14 +308,16 @@ class DeviceView:
 
 
     @classmethod
-    def from_file(cls, path, columns=None, device="cuda", verify: bool = True) -> "DeviceView":
+    def from_file(cls, path, columns=None, device="cuda", verify: bool = True,
+                  defer_crc: bool = False) -> "DeviceView":
         """FBXC ingest through the host reader (fbx_read_spans): the wanted
         segments are read by parallel pread into pinned memory and reach HBM in
         one H2D copy, with no decode, no page faults on a mapping and no pageable
         staging.  A full read (every column) moves the whole body and checks its
         CRC-32 on the device first (columnstore.py:554-562), then lays the
-        segments out 16-B aligned by device copies."""
-        from .columns import ChecksumError, UnknownColumnError
+        segments out 16-B aligned by device copies.  ``defer_crc``: the CRC stays
+        on the device until ``verify_crc()`` (no host synchronisation here)."""
+        from .columns import UnknownColumnError
         torch = _torch()
         vf = open_view(path)
         names = [n for n, _ in vf.schema]
@@ -333,6 +335,7 @@ class DeviceView:
             place[key] = cur
             cur += (vf.segments[key][1] + 31) // 16 * 16
         self = cls.__new__(cls)
+        self._crc = None
         self.n = vf.row_count
         self.kinds = {n: k for n, k in vf.schema if columns is None or n in columns}
         self.tensors, self.bytes, self.torch = {}, 0, torch
@@ -342,9 +345,9 @@ class DeviceView:
             runtime.read_spans(vf.path, host.data_ptr(), [vf.body_offset], [vf.body_bytes], [0])
             body = torch.empty(vf.body_bytes + 64, dtype=torch.uint8, device=dev)
             body[:vf.body_bytes].copy_(host[:vf.body_bytes], non_blocking=True)
-            crc = crc32_device(body[:vf.body_bytes])
-            if crc != vf.checksum:
-                raise ChecksumError(f"{vf.path}: body CRC {crc:#010x} != {vf.checksum:#010x}")
+            self._crc = (crc32_device_async(body[:vf.body_bytes]), vf.checksum, vf.path)
+            if not defer_crc:
+                self.verify_crc()
             for (name, part), dst in place.items():
                 o, ln = vf.segments[(name, part)]
                 if ln:
@@ -364,9 +367,22 @@ class DeviceView:
         self.h2d_bytes = (vf.body_bytes if full and verify else cur)
         return self
 
+    def verify_crc(self):
+        """Raise ChecksumError if the body CRC computed on the device (a full
+        read) differs from the file's trailer."""
+        from .columns import ChecksumError
+        if getattr(self, "_crc", None) is None:
+            return
+        out, want, path = self._crc
+        crc = int(out.cpu().numpy().view(np.uint32)[0])
+        self._crc = None
+        if crc != want:
+            raise ChecksumError(f"{path}: body CRC {crc:#010x} != {want:#010x}")
 
-def crc32_device(t) -> int:
-    """zlib CRC-32 of a contiguous device tensor's bytes (fbx_crc32)."""
+
+def crc32_device_async(t):
+    """zlib CRC-32 of a contiguous device tensor's bytes (fbx_crc32), left in a
+    one-word device tensor (no host synchronisation)."""
     torch = _torch()
     t = t.contiguous().view(torch.uint8)
     n = t.numel()
@@ -375,7 +391,12 @@ def crc32_device(t) -> int:
     stream = torch.cuda.current_stream(t.device).cuda_stream
     runtime.crc32(t.data_ptr() if n else out.data_ptr(), n, scratch.data_ptr(), out.data_ptr(),
                   stream)
-    return int(out.cpu().numpy().view(np.uint32)[0])
+    return out
+
+
+def crc32_device(t) -> int:
+    """zlib CRC-32 of a contiguous device tensor's bytes (fbx_crc32)."""
+    return int(crc32_device_async(t).cpu().numpy().view(np.uint32)[0])
 
 
 # ---------------------------------------------------------------------------
@@ -451,7 +472,8 @@ class Engine:
     def __init__(self, prepared: Prepared, views: Mapping[str, ViewImage] | None = None,
                  basic: ViewImage | None = None, device: str = "cuda",
                  max_rows_per_launch: int = 1 << 22, pool_bytes_per_row: int = 96,
-                 device_views: Mapping[str, "DeviceView"] | None = None):
+                 device_views: Mapping[str, "DeviceView"] | None = None,
+                 defer_prepare_check: bool = False):
         torch = _torch()
         self.torch = torch
         self.prepared = prepared
@@ -468,12 +490,17 @@ class Engine:
         if prepared.program.json_kind:  # canonical JSON can outgrow its source (escapes)
             self.pool_bytes_per_row += 512
         with torch.cuda.device(self.device):
-            self.module = runtime.Program(prepared.cubin)
+            # one loaded module per plan and device (engines of a plan share it)
+            mods = prepared.__dict__.setdefault("_modules", {})
+            if self.device not in mods:
+                mods[self.device] = runtime.Program(prepared.cubin)
+            self.module = mods[self.device]
             self.state = torch.zeros(runtime.STATE_BYTES // 8, dtype=torch.int64,
                                      device=self.device)
             self._set("state", self.state.data_ptr())
             self.prepare_counters = Counters()
             self._keep: list = []
+            self._defer_prepare = defer_prepare_check
             self._upload_sides(views or {}, basic, device_views or {})
             self._upload_tables()
             self._idset_cap = 0
@@ -561,14 +588,30 @@ class Engine:
         runtime.state_reset(self.state.data_ptr(), status.data_ptr(), 1, stream)
         self._side_views = prepared_views
         self._launch_side_prep(stream)
-        st = self._read_state()
-        self.prepare_counters.malformed = st["malformed"]
-        self.prepare_counters.filtered = st["filtered"]
-        self._raise_if_error(st, prepare=True)
+        if self._defer_prepare:
+            # the prepare-time state is kept on the device (stream-ordered copy)
+            # and checked by finish_prepare() after the run: no host sync here
+            self._prep_state = self.state.clone()
+        else:
+            self._settle_prepare(self._read_state())
         # basic uniqueness (pipeline.py:975): int-keyed basic indices raise it in the
         # prep kernel itself (basic_dup); other key shapes count repeats in the slots
         if ir.basic is not None and len(ir.sides) not in self.prog.int_keyed:
             self._check_basic_unique(len(ir.sides))
+
+    def _settle_prepare(self, st: dict):
+        self.prepare_counters.malformed = st["malformed"]
+        self.prepare_counters.filtered = st["filtered"]
+        self._raise_if_error(st, prepare=True)
+
+    def finish_prepare(self):
+        """A deferred prepare check (``defer_prepare_check``): the side views'
+        clean counters and the first prepare-time failure."""
+        ps = getattr(self, "_prep_state", None)
+        if ps is not None:
+            self._prep_state = None
+            raw = ps.cpu().numpy().view(np.uint64)
+            self._settle_prepare({f: int(raw[i]) for i, f in enumerate(runtime.STATE_FIELDS)})
 
     def _launch_side_prep(self, stream: int) -> int:
         for k, v, n in self._side_views:
@@ -1525,24 +1568,50 @@ def run_pipelined(config: PipelineConfig, collect: bool = False,
     drv_cfg = config.view(config.driver)
     torch = _torch()
     try:
-        dvs = {v.name: DeviceView.from_file(v.path, v.columns) for v in config.views
-               if v.name != config.driver}
-        dvs["basic"] = DeviceView.from_file(config.basic_path, config.basic_columns)
         dfile = open_view(drv_cfg.path)
     except Exception as exc:  # noqa: BLE001
         raise StageError("prepare", None, exc) from exc
-    bytes_h2d = sum(d.h2d_bytes for d in dvs.values())
-    eng = Engine(prep, device_views=dvs)
-    torch.cuda.synchronize(eng.device)
-    launches = 1 + len(eng._side_views)  # the prepare-time state reset + index builds
-    stage["prepare"] = time.perf_counter() - t0
     n = dfile.row_count
     bs = config.batch_size
     names = [c for c, _ in dfile.schema]
     full_read = drv_cfg.columns is None or set(drv_cfg.columns) >= set(names)
+    streamed = not (prep.program.tiles_per_chunk > 1 or (full_read and n <= bs))
+    fr = None
+    if streamed:
+        # the driver's first slices are read while the side views are prepared
+        fr = FileRun(prep, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows)
+        fr.start()
+    try:
+        dvs = {v.name: DeviceView.from_file(v.path, v.columns, defer_crc=streamed)
+               for v in config.views if v.name != config.driver}
+        dvs["basic"] = DeviceView.from_file(config.basic_path, config.basic_columns,
+                                            defer_crc=streamed)
+    except Exception as exc:  # noqa: BLE001
+        if fr is not None:
+            fr.stop()
+        raise StageError("prepare", None, exc) from exc
+
+    def settle_prepare():
+        """Deferred prepare checks, in the reference's order: each side view's
+        and the basic view's body CRC, then the index builds' failures."""
+        try:
+            for dv in dvs.values():
+                dv.verify_crc()
+        except Exception as exc:  # noqa: BLE001
+            raise StageError("prepare", None, exc) from exc
+        eng.finish_prepare()
+    bytes_h2d = sum(d.h2d_bytes for d in dvs.values())
+    try:
+        eng = Engine(prep, device_views=dvs, defer_prepare_check=streamed)
+    except BaseException:
+        if fr is not None:
+            fr.stop()
+        raise
+    launches = 1 + len(eng._side_views)  # the prepare-time state reset + index builds
+    stage["prepare"] = time.perf_counter() - t0
     t1 = time.perf_counter()
     launch_s = 0.0
-    if eng.prog.tiles_per_chunk > 1 or (full_read and n <= bs):
+    if not streamed:
         # one chunk reads the whole body (the reference then checks its CRC), or
         # chunks larger than a CTA (merged on the device): device-resident run
         try:
@@ -1572,21 +1641,25 @@ def run_pipelined(config: PipelineConfig, collect: bool = False,
         c = b.counters
     else:
         while True:
-            fr = FileRun(eng, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows)
+            if fr is None:  # a repeat after the device arena grew
+                fr = FileRun(prep, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows)
             eng.reserve(n, fr.slice_rows, ring=True)
             launches += eng.begin_run(n)
             try:
-                t = fr.run()
+                t = fr.run(eng)
             except _ReadFailure as exc:
+                settle_prepare()
                 raise StageError("read", (exc.index * fr.slice_rows) // bs, exc.cause) from exc
             launches += t["launches"]
             launch_s += t["launch_s"]
+            settle_prepare()
             st = eng._read_state()
             try:
                 eng.check_run(st)
                 break
             except ArenaRetry as exc:
                 eng.grow_arena(exc.need)
+                fr = None
         stage["read"] = t["read_s"]
         stage["transfer"] = t["h2d_s"]
         stage["extract"] = t["kernel_s"]

@@ -28,27 +28,31 @@ from .columns import open_view
 
 
 class FileRun:
-    """One driver file streamed through an ``Engine`` (bounded memory)."""
+    """One driver file streamed through an ``Engine`` (bounded memory).
+
+    Built from the prepared plan alone, so ``start()`` can begin reading the
+    first slices while the side views, the basic features and their indexes
+    are still being prepared; ``run(engine)`` then consumes the slices."""
 
     PARTS = ("nulls", "offsets", "data")
 
-    def __init__(self, eng, path, columns=None, slice_rows: int = 1 << 18, nbuf: int = 3,
-                 threads: int | None = None):
-        self.eng = eng
-        self.torch = torch = eng.torch
+    def __init__(self, prepared, path, columns=None, device="cuda", slice_rows: int = 1 << 18,
+                 nbuf: int = 3, threads: int | None = None):
+        import torch
+        self.torch = torch
         self.vf = vf = open_view(path)
         self.n = n = vf.row_count
-        chunk = eng.ir.chunk
-        if eng.prog.tiles_per_chunk > 1:
+        chunk = prepared.ir.chunk
+        if prepared.program.tiles_per_chunk > 1:
             raise ValueError("FileRun: batch_size > 1024 runs device-resident (chunk merge)")
-        S = max(chunk, slice_rows // chunk * chunk)
-        S = min(S, eng.LAUNCH_ROWS_MAX // chunk * chunk)
-        self.slice_rows = S
+        limit = (1 << 24) // chunk * chunk  # Engine.LAUNCH_ROWS_MAX
+        self.slice_rows = S = min(max(chunk, slice_rows // chunk * chunk), max(chunk, limit))
         self.bounds = [(lo, min(lo + S, n)) for lo in range(0, n, S)]
+        slots = prepared.program.slots
         kinds = dict(vf.schema)
         self.cols = [c for c, _ in vf.schema
                      if (columns is None or c in columns)
-                     and any(f"drv.{c}.{p}" in eng.slots for p in self.PARTS)]
+                     and any(f"drv.{c}.{p}" in slots for p in self.PARTS)]
         self.threads = runtime.host_threads() if threads is None else threads
         # boundary offsets of every var-length column at every slice edge: the data
         # span of a slice is [off[lo], off[hi]) (one 4-byte pread per edge)
@@ -65,14 +69,24 @@ class FileRun:
         self.layout = [self._pieces(k) for k in range(len(self.bounds))]
         self.cap = max([sum((b - a + 15) // 16 * 16 for _, _, a, b, _ in pcs)
                         for pcs in self.layout] or [16]) + 16
-        dev = eng.device
-        self.host = [torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
-                     for _ in range(min(nbuf, max(1, len(self.bounds))))]
-        self.dev = [torch.empty(self.cap + 32, dtype=torch.uint8, device=dev)
-                    for _ in range(len(self.host))]
+        dev = torch.device(device)
+        nb = min(nbuf, max(1, len(self.bounds)))
+        self.host = [torch.empty(self.cap, dtype=torch.uint8, pin_memory=True) for _ in range(nb)]
+        self.dev = [torch.empty(self.cap + 32, dtype=torch.uint8, device=dev) for _ in range(nb)]
         self.s_h2d = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev)
         self.h2d_bytes = sum(sum(b - a for _, _, a, b, _ in pcs) for pcs in self.layout)
+        K = len(self.bounds)
+        self.ready = [threading.Event() for _ in range(K)]
+        self.recorded = [threading.Event() for _ in range(K)]
+        self.h2d_done = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        self.h2d_start = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        self.comp_done = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        self.comp_start = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        self.failure: list = [None, None]
+        self.read_s = 0.0
+        self.cancel = threading.Event()
+        self.thread = None
 
     def _pieces(self, k: int):
         """(column, part, start, end, dst) byte spans of slice k within each
@@ -96,93 +110,103 @@ class FileRun:
                 off += (b - a + 15) // 16 * 16
         return out
 
-    def run(self) -> dict:
-        """Stream every slice through the engine; returns the timing / byte
-        counters of the run (the engine's state holds the results)."""
-        torch, eng = self.torch, self.eng
-        nb = len(self.host)
-        K = len(self.bounds)
-        ready = [threading.Event() for _ in range(K)]
-        recorded = [threading.Event() for _ in range(K)]
-        h2d_done = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-        h2d_start = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-        comp_done = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-        comp_start = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-        failure: list = [None, None]
-        read_s = [0.0]
-        vf = self.vf
-
-        cancel = threading.Event()
-
-        def reader():
-            k = 0
-            try:
-                for k in range(K):
-                    if cancel.is_set():
+    def _reader(self):
+        """Host thread: read slice k into pinned buffer k % nb, then enqueue its
+        H2D on the copy stream -- so the first slices are in HBM before the
+        engine exists.  Reuse waits: the pinned buffer for slice k - nb's H2D,
+        the device buffer (on the device) for slice k - nb's kernel."""
+        torch, nb, vf = self.torch, len(self.host), self.vf
+        k = 0
+        try:
+            for k in range(len(self.bounds)):
+                if self.cancel.is_set():
+                    return
+                if k >= nb:
+                    self.h2d_done[k - nb].synchronize()  # the pinned buffer is free again
+                t = time.perf_counter()
+                pcs = self.layout[k]
+                runtime.read_spans(vf.path, self.host[k % nb].data_ptr(),
+                                   [vf.segments[(c, p)][0] + a for c, p, a, _, _ in pcs],
+                                   [b - a for _, _, a, b, _ in pcs],
+                                   [o for *_, o in pcs], self.threads)
+                self.read_s += time.perf_counter() - t
+                if k >= nb:
+                    self.recorded[k - nb].wait()  # slice k - nb's kernel is enqueued
+                    if self.cancel.is_set():
                         return
+                buf = k % nb
+                nbytes = pcs[-1][4] + (pcs[-1][3] - pcs[-1][2]) if pcs else 0
+                with torch.cuda.stream(self.s_h2d):
                     if k >= nb:
-                        recorded[k - nb].wait()
-                        h2d_done[k - nb].synchronize()  # the pinned buffer is free again
-                    t = time.perf_counter()
-                    pcs = self.layout[k]
-                    runtime.read_spans(vf.path, self.host[k % nb].data_ptr(),
-                                       [vf.segments[(c, p)][0] + a for c, p, a, _, _ in pcs],
-                                       [b - a for _, _, a, b, _ in pcs],
-                                       [o for *_, o in pcs], self.threads)
-                    read_s[0] += time.perf_counter() - t
-                    ready[k].set()
-            except BaseException as exc:  # noqa: BLE001 -- re-raised by the host loop
-                failure[0], failure[1] = k, exc
-                for e in ready[k:]:
-                    e.set()
+                        self.s_h2d.wait_event(self.comp_done[k - nb])  # device buffer reuse
+                    self.h2d_start[k].record(self.s_h2d)
+                    self.dev[buf][:nbytes].copy_(self.host[buf][:nbytes], non_blocking=True)
+                    self.h2d_done[k].record(self.s_h2d)
+                self.ready[k].set()
+        except BaseException as exc:  # noqa: BLE001 -- re-raised by the host loop
+            self.failure[0], self.failure[1] = k, exc
+            for e in self.ready[k:]:
+                e.set()
 
-        th = threading.Thread(target=reader, name="fbx-read", daemon=True)
-        th.start()
+    def start(self):
+        """Begin reading slices into the pinned ring and copying them to HBM
+        (a host thread)."""
+        if self.thread is None:
+            cur = self.torch.cuda.current_stream(self.dev[0].device)
+            self.s_h2d.wait_stream(cur)  # the staging buffers' allocation
+            self.thread = threading.Thread(target=self._reader, name="fbx-read", daemon=True)
+            self.thread.start()
+
+    def stop(self):
+        self.cancel.set()
+        for e in self.recorded:
+            e.set()
+        if self.thread is not None:
+            self.thread.join()
+
+    def run(self, eng) -> dict:
+        """Stream every slice through ``eng`` (reserved with ``ring=True`` and a
+        begun run); returns the timing / byte counters of the stream (the
+        engine's state holds the results)."""
+        torch = self.torch
+        nb = len(self.host)
+        self.start()
         cur = torch.cuda.current_stream(eng.device)
-        self.s_comp.wait_stream(cur)
-        self.s_h2d.wait_stream(cur)
+        self.s_comp.wait_stream(cur)  # the engine's prepare work (index builds, run reset)
         launch_s = 0.0
         launches = 0
         tiles_before = 0
         try:
             for k, (lo, hi) in enumerate(self.bounds):
-                ready[k].wait()
-                if failure[1] is not None and failure[0] <= k:
-                    raise _ReadFailure(failure[0], failure[1])
+                self.ready[k].wait()
+                if self.failure[1] is not None and self.failure[0] <= k:
+                    raise _ReadFailure(self.failure[0], self.failure[1])
                 buf = k % nb
                 pcs = self.layout[k]
-                nbytes = pcs[-1][4] + (pcs[-1][3] - pcs[-1][2]) if pcs else 0
-                with torch.cuda.stream(self.s_h2d):
-                    if k >= nb:
-                        self.s_h2d.wait_event(comp_done[k - nb])  # device buffer reuse
-                    h2d_start[k].record(self.s_h2d)
-                    self.dev[buf][:nbytes].copy_(self.host[buf][:nbytes], non_blocking=True)
-                    h2d_done[k].record(self.s_h2d)
-                recorded[k].set()
                 base = self.dev[buf].data_ptr()
                 for c, p, a, _, o in pcs:
                     eng._set(f"drv.{c}.{p}", base + o - a)
                 with torch.cuda.stream(self.s_comp):
-                    self.s_comp.wait_event(h2d_done[k])
-                    comp_start[k].record(self.s_comp)
+                    self.s_comp.wait_event(self.h2d_done[k])
+                    self.comp_start[k].record(self.s_comp)
                     t = time.perf_counter()
                     tiles = eng.launch(lo, hi, self.s_comp.cuda_stream, tile_base=tiles_before)
                     launches += 1 + eng.ring_after_launch(self.s_comp.cuda_stream)
                     launch_s += time.perf_counter() - t
-                    comp_done[k].record(self.s_comp)
+                    self.comp_done[k].record(self.s_comp)
+                self.recorded[k].set()
                 tiles_before += tiles
         finally:
-            cancel.set()
-            for e in recorded:
-                e.set()
-            th.join()
+            self.stop()
         self.s_comp.synchronize()
         self.s_h2d.synchronize()
         cur.wait_stream(self.s_comp)
-        return {"launches": launches, "launch_s": launch_s, "read_s": read_s[0],
-                "h2d_s": sum(a.elapsed_time(b) for a, b in zip(h2d_start, h2d_done)) / 1e3,
-                "kernel_s": sum(a.elapsed_time(b) for a, b in zip(comp_start, comp_done)) / 1e3,
-                "h2d_bytes": self.h2d_bytes, "slices": K}
+        ev = zip(self.h2d_start, self.h2d_done)
+        return {"launches": launches, "launch_s": launch_s, "read_s": self.read_s,
+                "h2d_s": sum(a.elapsed_time(b) for a, b in ev) / 1e3,
+                "kernel_s": sum(a.elapsed_time(b)
+                                for a, b in zip(self.comp_start, self.comp_done)) / 1e3,
+                "h2d_bytes": self.h2d_bytes, "slices": len(self.bounds)}
 
 
 class _ReadFailure(Exception):

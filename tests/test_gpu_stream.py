@@ -48,11 +48,11 @@ def test_file_run_memory_is_one_slice(goldens):
                                                 cfg.view("user_profile").columns),
            "basic": DeviceView.from_file(cfg.basic_path, cfg.basic_columns)}
     eng = Engine(prep, device_views=dvs)
-    fr = FileRun(eng, cfg.view("user_events").path, cfg.view("user_events").columns,
+    fr = FileRun(prep, cfg.view("user_events").path, cfg.view("user_events").columns,
                  slice_rows=2048)
     eng.reserve(fr.n, fr.slice_rows, ring=True)
     eng.begin_run(fr.n)
-    t = fr.run()
+    t = fr.run(eng)
     st = eng._read_state()
     eng.check_run(st)
     g = golden_run(goldens, 20000, 7, "sign_heavy")
@@ -134,3 +134,21 @@ def test_streamed_adversarial_records(batch_size, seed, tmp_path):
     assert got_err is None, got_err
     assert (got.digest, got.instances, got.signs) == (ref.digest, ref.instances, ref.signs)
     assert (got.rows_dropped, got.rows_filtered) == (ref.malformed, ref.filtered)
+
+
+@pytest.mark.parametrize("which", ["basic.fbxc", "pr.fbxc"])
+def test_streamed_checksum_error_is_prepare_failure(which, tmp_path):
+    """A corrupted side / basic body (full read) fails prepare with the
+    reference's ChecksumError -- checked on the device, raised after the stream."""
+    from paper_2210_07768_b200.columns import ChecksumError
+    from paper_2210_07768_b200.config import StageError
+    drv, prof, bas = _views(2000, 5)
+    _write_views(tmp_path, drv, prof, bas)
+    f = tmp_path / which
+    raw = bytearray(f.read_bytes())
+    raw[-9] ^= 0x40  # a body byte (the last 4 bytes are the CRC trailer)
+    f.write_bytes(bytes(raw))
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    _, err = _streamed(_config(512, ops, {"c": 3}, filt="age != -12345"), tmp_path, 512)
+    assert isinstance(err, StageError) and err.stage == "prepare"
+    assert isinstance(err.__cause__, ChecksumError)
