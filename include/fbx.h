@@ -122,14 +122,15 @@ int fbx_gather_strings(const unsigned long long* d_ptrs, const unsigned int* d_l
                        const unsigned long long* d_offsets, unsigned long long n,
                        unsigned char* d_out, void* stream);
 
-/* check_unique_ids' failing chunk (viewpipe.py:562-576 as called at
- * pipeline.py:1071): the chunk of an instance id's SECOND occurrence in chunk
- * order, minimised over ids.  d_winner_chunk[i] is the chunk of the row that
- * claimed id-set slot i, d_later_chunks[i] the two smallest chunks (+1, packed
- * hi|lo, 0 = none) of the rows that found the id already present.  Writes
- * (chunk << 32 | slot) of the answer to *d_out, ~0 when no id repeats. */
-int fbx_dup_resolve(const unsigned int* d_winner_chunk, const unsigned long long* d_later_chunks,
-                    unsigned long long n_slots, unsigned long long* d_out, void* stream);
+/* check_unique_ids' failing row (viewpipe.py:562-576 as called at
+ * pipeline.py:1071): the row of an instance id's SECOND occurrence in row
+ * order, minimised over ids (its chunk is row / batch_size).  d_winner_row[i] is
+ * the row that claimed id-set slot i, d_later_rows[2i], [2i+1] the two smallest
+ * rows (+1, 0 = none) that found the id already present.  Writes the answer row
+ * to d_out[0] and its slot to d_out[1] (~0 when no id repeats). */
+int fbx_dup_resolve(const unsigned long long* d_winner_row,
+                    const unsigned long long* d_later_rows, unsigned long long n_slots,
+                    unsigned long long* d_out, void* stream);
 
 /* Write `bytes` of a scratch buffer (an L2 flush between timed steps). */
 /* zlib CRC-32 of n device bytes into *d_out (columnstore.py:554-562: the FBXC body

@@ -137,6 +137,9 @@ class Program:
     pool_kw: int = 0
     pool_ni: int = 0
     tile_rows: int = 512
+    # bump-pool rounding per tile, summed over the plan's pool sites: a CTA grant
+    # rounds to 128 B, a warp grant to 16 B per warp (the engine's arena slack)
+    pool_slack_per_tile: int = 0
 
 
 # ---------------------------------------------------------------------------
@@ -1497,8 +1500,8 @@ class PlanCodegen:
         g(f"CUR_STAGE = {STAGE['merge']}u;")
         lab = self.col(ir.label_column, node_out)
         g("// ---- check_unique_ids over the run (pipeline.py:1071, viewpipe.py:562) ----")
-        g("// the winner of an id's slot stores its chunk; a later occurrence notes its")
-        g("// chunk for fbx_dup_resolve and stays live (its rank keeps the emission")
+        g("// the winner of an id's slot stores its row; a later occurrence notes its")
+        g("// row for fbx_dup_resolve and stays live (its rank keeps the emission")
         g("// positions of the chunks before the reported one exact)")
         g("// the first atomic is issued here; its result is only consumed at the very")
         g("// end of the kernel (collision probing + dup note), off the critical path")
@@ -1524,8 +1527,8 @@ class PlanCodegen:
             "}",
             "dup = ids_old != 0ull;",
             "}",
-            f"if (dup) fbx::dup_note(ST, {g.p('idset_d', 'u64*')} + ids_slot, (u32)chunk);",
-            f"else {g.p('idset_w', 'u32*')}[ids_slot] = (u32)chunk;",
+            f"if (dup) fbx::dup_note(ST, {g.p('idset_d', 'u64*')} + 2 * ids_slot, row);",
+            f"else {g.p('idset_w', 'u64*')}[ids_slot] = row;",
             "}",
         ]
         if ir.basic is not None:
@@ -1959,7 +1962,8 @@ class PlanCodegen:
         return Program(src, dict(self.g.slots), self.nt, smem, [kname], side_names, self.notes,
                        tuple(k for k in range(nt_) if self.int_keyed(k)),
                        self.json_kind, self.spc, self.pool_program(), self.pool_kw,
-                       self.pool_ni, self.tile_rows)
+                       self.pool_ni, self.tile_rows,
+                       self.pool_sites * ((self.nt // 32) * 16 if self.pool_warp else 128))
 
 
 def _filter_columns(expr) -> set[str]:

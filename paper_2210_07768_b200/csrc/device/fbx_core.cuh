@@ -579,24 +579,40 @@ FBX_DI void raise_emit(fbx_state* st, u64 pos, u32 batch_size, bool range, u64 d
   if (key < old) atomicExch((unsigned long long*)&st->emit_detail, (unsigned long long)detail);
 }
 
-// check_unique_ids (viewpipe.py:562-576) raises at the chunk of an id's SECOND
-// occurrence in chunk order.  The id-set winner records its chunk with a plain
-// store; a thread that finds its id already present (rare) folds its chunk into
-// the slot's two smallest "later" chunks (+1, 0 = none) and flags the run;
-// fbx_dup_resolve takes min over slots of the 2nd smallest after the run.
-FBX_DI void dup_note(fbx_state* st, u64* pair, u32 chunk) {
-  const u64 c = (u64)chunk + 1u;
-  u64 cur = *(volatile u64*)pair;
+// one 128-bit compare-and-swap (atom.cas.b128, sm_90+)
+FBX_DI void cas128(void* addr, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u64* old_lo,
+                   u64* old_hi) {
+  asm volatile(
+      "{\n\t.reg .b128 c, n, d;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 n, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, n;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(*old_lo), "=l"(*old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
+      : "memory");
+}
+
+// check_unique_ids (viewpipe.py:562-576) raises at the FIRST row, in row order,
+// whose id occurred before: the row of some id's SECOND occurrence, minimised
+// over ids.  The id-set winner records its row with a plain store; a thread that
+// finds its id already present (rare) folds its row into the slot's two smallest
+// "later" rows (+1, 0 = none; a 128-bit CAS keeps the pair consistent) and flags
+// the run; fbx_dup_resolve takes the second smallest of {winner, later rows} per
+// slot and the minimum over slots after the run.
+FBX_DI void dup_note(fbx_state* st, u64* pair, u64 row) {
+  const u64 r = row + 1u;
+  u64 lo = ((volatile u64*)pair)[0], hi = ((volatile u64*)pair)[1];
   while (true) {
-    const u64 a = cur >> 32, b = cur & 0xFFFFFFFFull;
-    u64 nw;
-    if (a == 0u || c < a) nw = (c << 32) | a;
-    else if (b == 0u || c < b) nw = (a << 32) | c;
+    u64 nlo, nhi;
+    if (lo == 0u || r < lo) { nlo = r; nhi = lo; }
+    else if (hi == 0u || r < hi) { nlo = lo; nhi = r; }
     else break;
-    const u64 old = atomicCAS((unsigned long long*)pair, (unsigned long long)cur,
-                              (unsigned long long)nw);
-    if (old == cur) break;
-    cur = old;
+    u64 olo, ohi;
+    cas128(pair, lo, hi, nlo, nhi, &olo, &ohi);
+    if (olo == lo && ohi == hi) break;
+    lo = olo;
+    hi = ohi;
   }
   atomicExch((unsigned long long*)&st->dup_seen, 1ull);
 }
@@ -1147,18 +1163,6 @@ FBX_DI u32 ld_acquire_u32(const u32* p) {
 // claimed by ONE 128-bit compare-and-swap (atom.cas.b128, sm_90+), so no other
 // thread can see a claimed slot without its key -- no fence, no publish step.
 // An equal key already present bumps the count (its key is immutable by then).
-FBX_DI void cas128(void* addr, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u64* old_lo,
-                   u64* old_hi) {
-  asm volatile(
-      "{\n\t.reg .b128 c, n, d;\n\t"
-      "mov.b128 c, {%2, %3};\n\t"
-      "mov.b128 n, {%4, %5};\n\t"
-      "atom.global.cas.b128 d, [%6], c, n;\n\t"
-      "mov.b128 {%0, %1}, d;\n\t}"
-      : "=l"(*old_lo), "=l"(*old_hi)
-      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
-      : "memory");
-}
 // Returns true when the key was already present (a repeated key).
 FBX_DI bool islot_insert(ISlot* T, u64 mask, u64 h, u64 key, u32 row) {
   u64 i = h & mask;

@@ -126,19 +126,31 @@ __global__ void k_state_snapshot(const unsigned long long* st, volatile unsigned
   if (threadIdx.x < n) dst[threadIdx.x] = st[threadIdx.x];
 }
 
-// second-smallest chunk over {winner, later occurrences} of every repeated id
-__global__ void k_dup_resolve(const unsigned int* w, const unsigned long long* later,
+// second-smallest row over {winner, later occurrences} of every repeated id;
+// pass 1: the minimum over slots, pass 2: the smallest slot holding it
+__device__ __forceinline__ unsigned long long dup_second(const unsigned long long* w,
+                                                         const unsigned long long* later,
+                                                         unsigned long long i) {
+  const unsigned long long x = later[2 * i], y = later[2 * i + 1];
+  if (x == 0ull) return ~0ull;
+  const unsigned long long a = w[i], b = x - 1ull, c = y ? y - 1ull : ~0ull;
+  return max(min(a, b), min(max(a, b), c));
+}
+__global__ void k_dup_resolve(const unsigned long long* w, const unsigned long long* later,
                               unsigned long long n, unsigned long long* out) {
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long p = later[i];
-    if (p == 0ull) continue;
-    const unsigned int x = (unsigned int)(p >> 32) - 1u;
-    const unsigned int y = (unsigned int)p ? (unsigned int)p - 1u : 0xFFFFFFFFu;
-    const unsigned int c = w[i];
-    const unsigned int second = max(min(c, x), min(max(c, x), y));
-    atomicMin(out, ((unsigned long long)second << 32) | (i & 0xFFFFFFFFull));
+    const unsigned long long r = dup_second(w, later, i);
+    if (r != ~0ull) atomicMin(out, r);
   }
+}
+__global__ void k_dup_slot(const unsigned long long* w, const unsigned long long* later,
+                           unsigned long long n, unsigned long long* out) {
+  const unsigned long long best = out[0];
+  if (best == ~0ull) return;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    if (dup_second(w, later, i) == best) atomicMin(out + 1, i);
 }
 
 using fbx::Slot;
@@ -640,14 +652,16 @@ int fbx_gather_strings(const unsigned long long* d_ptrs, const unsigned int* d_l
   return cuda_check(cudaGetLastError(), "fbx_gather_strings");
 }
 
-int fbx_dup_resolve(const unsigned int* d_winner_chunk, const unsigned long long* d_later_chunks,
-                    unsigned long long n_slots, unsigned long long* d_out, void* stream) {
+int fbx_dup_resolve(const unsigned long long* d_winner_row,
+                    const unsigned long long* d_later_rows, unsigned long long n_slots,
+                    unsigned long long* d_out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = cuda_check(cudaMemsetAsync(d_out, 0xFF, sizeof(unsigned long long), s), "dup out");
+  int rc = cuda_check(cudaMemsetAsync(d_out, 0xFF, 2 * sizeof(unsigned long long), s), "dup out");
   if (rc) return rc;
   const unsigned long long blocks = (n_slots + 255) / 256;
-  k_dup_resolve<<<(unsigned)(blocks < 4096 ? (blocks ? blocks : 1) : 4096), 256, 0, s>>>(
-      d_winner_chunk, d_later_chunks, n_slots, d_out);
+  const unsigned g = (unsigned)(blocks < 4096 ? (blocks ? blocks : 1) : 4096);
+  k_dup_resolve<<<g, 256, 0, s>>>(d_winner_row, d_later_rows, n_slots, d_out);
+  k_dup_slot<<<g, 256, 0, s>>>(d_winner_row, d_later_rows, n_slots, d_out);
   return cuda_check(cudaGetLastError(), "fbx_dup_resolve");
 }
 

@@ -745,17 +745,19 @@ class Engine:
 
     def _dup_key(self) -> tuple[int, int]:
         """(error key, id) of check_unique_ids' failure: the merge of the chunk
-        holding some id's second occurrence, minimised over ids."""
-        out = self.torch.empty(1, dtype=self.torch.int64, device=self.device)
+        holding the first row, in row order, whose id occurred before (some id's
+        second occurrence, minimised over ids); the id as the column's signed
+        Int64 value, as the reference's message prints it."""
+        out = self.torch.empty(2, dtype=self.torch.int64, device=self.device)
         runtime.dup_resolve(self.idset_w.data_ptr(), self.idset_d.data_ptr(),
                             self._idset_cap + 2, out.data_ptr(), self._stream())
-        v = int(out.cpu().numpy().view(np.uint64)[0])
-        if v == (1 << 64) - 1:
+        row, slot = (int(x) for x in out.cpu().numpy().view(np.uint64))
+        if row == (1 << 64) - 1:
             return (1 << 64) - 1, 0
-        chunk, slot = v >> 32, v & 0xFFFFFFFF
-        ident = int(self.idset[slot].item()) & ((1 << 64) - 1) if slot <= self._idset_cap else 0
+        ident = int(self.idset[slot].item()) if slot <= self._idset_cap else 0
         if slot == self._idset_cap + 1:
-            ident = 0
+            ident = 0  # id 0 has its own slot (the set stores it as 1)
+        chunk = row // self.ir.chunk
         key = (chunk << 32) | (codegen.STAGE["merge"] << 28) | codegen.ERR["dup_id"]
         return key, ident
 
@@ -873,8 +875,8 @@ class Engine:
             self.idset = torch.zeros(cap + 2 + 1024, dtype=torch.int64, device=self.device)
             # winner chunk per slot (no reset: read only for claimed slots) and the
             # later-occurrence chunk pairs (only written when an id repeats)
-            self.idset_w = torch.empty(cap + 2, dtype=torch.int32, device=self.device)
-            self.idset_d = torch.zeros(cap + 2, dtype=torch.int64, device=self.device)
+            self.idset_w = torch.empty(cap + 2, dtype=torch.int64, device=self.device)
+            self.idset_d = torch.zeros(2 * (cap + 2), dtype=torch.int64, device=self.device)
             self._idset_cap = cap
         else:
             # one launch: the id set, and the pairs only if the previous run's state
@@ -927,8 +929,9 @@ class Engine:
             self.o_sign = torch.empty(crows * k + 1, dtype=torch.int64, device=dev)
             pool_cap = 0
             if codegen_pool_sites(self.prog):
-                lt = (launch_rows + self.ir.chunk - 1) // self.ir.chunk
-                pool_cap = self.pool_bytes_per_row * launch_rows + 128 * lt * 8 + (1 << 20)
+                lt = self.tiles_for(launch_rows)  # grants round up per tile and site
+                pool_cap = (self.pool_bytes_per_row * launch_rows
+                            + lt * self.prog.pool_slack_per_tile + (1 << 20))
                 pool_cap = max(pool_cap, getattr(self, "_arena_min", 0))
             self.pool = torch.empty(pool_cap + 256, dtype=torch.uint8, device=dev)
             self.pool_cap = pool_cap
@@ -1376,8 +1379,9 @@ def _cause(code: str, detail: int, st: dict) -> BaseException:
         return EmitError("null label at emission")
     if code == "label_range":
         return BatchInvariantError(f"label {detail - (1 << 64) if detail >> 63 else detail!r} not 0/1")
-    if code == "basic_dup":
-        return MergeUniquenessError("basic features: duplicate instance id")
+    if code == "basic_dup":  # detail: the repeated Int64 id (two's complement)
+        sid = detail - (1 << 64) if detail >> 63 else detail
+        return MergeUniquenessError(f"basic features: duplicate instance id {sid}")
     if code == "dup_id":
         return MergeUniquenessError(f"extracted features: duplicate instance id {detail}")
     if code == "multi_match":

@@ -322,6 +322,21 @@ def test_duplicate_instance_ids(tmp_path):
     ref_err, got_err = _err(raw, tmp_path, mut)
     assert got_err.stage == "merge"
     assert got_err.batch_index == ref_err.chunk
+    assert str(got_err.__cause__) == str(ref_err.cause)  # the first repeat, signed id
+
+
+@pytest.mark.parametrize("pairs", [[(1500, 1400), (702, 1400)], [(1993, 12), (1200, 1102)],
+                                   [(1300, 1030), (1200, 1210)], [(1400, 1399), (1390, 1380)],
+                                   [(14, 7)]])
+def test_duplicate_id_message_is_first_repeat(pairs, tmp_path):
+    """check_unique_ids reports the first row, in row order, whose id occurred
+    before -- also when several ids repeat in the failing chunk (negative ids
+    print signed)."""
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    raw = _config(512, ops, {"c": 3}, filt="age != -12345")
+    ref_err, got_err = _err(raw, tmp_path, _set_ids(pairs))
+    assert (got_err.stage, got_err.batch_index) == (ref_err.stage, ref_err.chunk)
+    assert str(got_err.__cause__) == str(ref_err.cause)
 
 
 @pytest.mark.parametrize("label", [None, 2, -1])
@@ -627,3 +642,30 @@ def test_basic_view_duplicate_id_fails_prepare(dst, src, tmp_path):
     assert (got_err.stage, got_err.batch_index) == ("prepare", None) == (ref_err.stage,
                                                                          ref_err.chunk)
     assert "basic features" in str(got_err.__cause__)
+
+
+def test_long_strings_grow_the_device_arena(tmp_path):
+    """Strings far above the arena's 96 B/row estimate (concat of ~300-byte
+    queries, materialised non-ASCII lower, escaped JSON strings): the launch
+    overflows the engine's own bump pool, the engine grows it and repeats the
+    run -- same result as the oracle, no failure (no fixed per-row cap)."""
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+    rng = random.Random(77)
+    drv, prof, bas = _views(20000, 8)
+    words = ["Ärger", "straße", "ΣΟΦΙΑ", "Mechanical", "keyboard", "İstanbul", "x" * 40]
+    qs = [" ".join(rng.choice(words) for _ in range(rng.randrange(20, 40))) for _ in range(20000)]
+    drv.columns["query"] = ColumnImage.from_values(Kind.UTF8, qs)
+    metas = [json.dumps({"u": {"city": "\u00c9" * rng.randrange(30, 60) + "Q" * 50}})
+             for _ in range(20000)]
+    drv.columns["meta"] = ColumnImage.from_values(Kind.JSON, metas)
+    _write_views(tmp_path, drv, prof, bas)
+    ops = [{"name": "cc", "inputs": ["query", "cx"], "outputs": ["cc"], "body": {"fn": "concat:|"}},
+           {"name": "cl", "inputs": ["cc"], "outputs": ["cl"], "pre": [{"fn": "lower"}],
+            "body": {"fn": "hash:3"}},
+           {"name": "t7", "inputs": ["query"], "outputs": ["t7"], "pre": [{"fn": "token: :7"}],
+            "body": {"fn": "hash:4"}}]
+    raw = _config(512, ops, {"cl": 3, "t7": 4}, filt="age != -12345")
+    ref, ref_err, got, got_err = _run_both(raw, drv, prof, bas, tmp_path)
+    assert ref_err is None and got_err is None, (ref_err, got_err)
+    assert (got.report.digest, got.report.instances, got.report.signs) == \
+        (ref.digest, ref.instances, ref.signs)
