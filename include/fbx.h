@@ -142,6 +142,24 @@ unsigned long long fbx_crc32_scratch_words(unsigned long long n);
 
 int fbx_l2_flush(void* d_buf, size_t bytes, void* stream);
 
+/* batch_size > 1024 (a chunk cut into 512-row sub-tiles): the n
+ * instances of a range, emitted as spc sorted runs per chunk, re-ordered into
+ * each chunk's ascending-id order (emit order, viewpipe.py:521) with their
+ * (slot, sign) segments -- the CSR of d_ids/d_lab/d_off[n+1]/d_slot/d_sign
+ * (offsets absolute, the range's signs start at s0) written to the _o arrays.
+ * d_tile_start[n_tiles+1]: first instance of every sub-tile relative to the
+ * range.  d_scratch: 3n+1 words.  *d_bad set (nothing written) when a length
+ * is outside [0, max_len] -- only a failing run's CSR (repeated id). */
+int fbx_merge_subtiles(const unsigned long long* d_tile_start, unsigned spc,
+                       unsigned long long n_tiles, unsigned long long n, unsigned long long s0,
+                       unsigned max_len, const unsigned long long* d_ids,
+                       const unsigned char* d_lab, const unsigned long long* d_off,
+                       const unsigned short* d_slot, const unsigned long long* d_sign,
+                       unsigned long long* d_ids_o, unsigned char* d_lab_o,
+                       unsigned long long* d_off_o, unsigned short* d_slot_o,
+                       unsigned long long* d_sign_o, unsigned long long* d_scratch,
+                       unsigned* d_bad, void* stream);
+
 /* Host ingest of a driver slice (read_columns with a row range,
  * columnstore.py:499-608; pipeline.py:986-1006 reads the driver chunk by chunk):
  * n_spans byte spans of one FBXC file, span i = file bytes

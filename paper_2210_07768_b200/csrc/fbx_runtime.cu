@@ -687,6 +687,118 @@ int fbx_l2_flush(void* d_buf, size_t bytes, void* stream) {
 
 }  // extern "C"
 
+// ---- batch_size > 1024: chunks emitted as sorted sub-tiles, merged in place --
+// Every chunk of the range [i0, i1) was emitted as spc sorted runs (one per
+// 512-row sub-tile, tile_start[] = first instance of every sub-tile, relative
+// to i0, tile_start[n_tiles] = i1 - i0).  An instance's place in its chunk's
+// ascending-id order is its index in its own run plus, for every other run of
+// the chunk, the number of ids below it (ties -- only in a failing run with a
+// repeated id -- broken by run order, so every place is distinct).
+namespace {
+__device__ __forceinline__ unsigned long long count_below(const unsigned long long* ids,
+                                                          unsigned long long lo,
+                                                          unsigned long long hi,
+                                                          unsigned long long key, bool or_equal) {
+  unsigned long long a = lo, b = hi;  // first index in [lo, hi) with ids[] > key (>= key)
+  while (a < b) {
+    const unsigned long long m = (a + b) >> 1;
+    if (or_equal ? ids[m] <= key : ids[m] < key) a = m + 1; else b = m;
+  }
+  return a - lo;
+}
+
+__global__ void k_merge_rank(const unsigned long long* tile_start, unsigned spc,
+                             unsigned long long n_tiles, unsigned long long n,
+                             const unsigned long long* ids, const unsigned long long* off,
+                             unsigned long long* pos, unsigned long long* newlen,
+                             unsigned max_len, unsigned* bad) {
+  for (unsigned long long j = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (unsigned long long)gridDim.x * blockDim.x) {
+    // the run holding j: the last t with tile_start[t] <= j
+    unsigned long long a = 0, b = n_tiles;
+    while (b - a > 1) {
+      const unsigned long long m = (a + b) >> 1;
+      if (tile_start[m] <= j) a = m; else b = m;
+    }
+    const unsigned long long t = a, c0 = t - t % spc;
+    const unsigned long long c1 = (c0 + spc < n_tiles) ? c0 + spc : n_tiles;
+    const unsigned long long key = ids[j];
+    unsigned long long r = j - tile_start[c0];  // own run: (j - own start) + earlier runs' sizes
+    r -= (tile_start[t] - tile_start[c0]);
+    for (unsigned long long u = c0; u < c1; ++u)
+      if (u != t) r += count_below(ids, tile_start[u], tile_start[u + 1], key, u < t);
+    const unsigned long long p = tile_start[c0] + r;
+    pos[j] = p;
+    const long long len = (long long)(off[j + 1] - off[j]);
+    if (len < 0 || len > (long long)max_len || p >= n) {
+      atomicOr(bad, 1u);
+      continue;
+    }
+    newlen[p] = (unsigned long long)len;
+  }
+}
+
+__global__ void k_merge_scatter(unsigned long long n, const unsigned long long* pos,
+                                const unsigned long long* newoff, unsigned long long s0,
+                                const unsigned long long* ids, const unsigned char* lab,
+                                const unsigned long long* off, const unsigned short* slot,
+                                const unsigned long long* sign, unsigned long long* ids_o,
+                                unsigned char* lab_o, unsigned long long* off_o,
+                                unsigned short* slot_o, unsigned long long* sign_o,
+                                const unsigned* bad) {
+  if (*bad) return;
+  for (unsigned long long j = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long p = pos[j];
+    ids_o[p] = ids[j];
+    lab_o[p] = lab[j];
+    const unsigned long long src = off[j] - s0, dst = newoff[p], m = off[j + 1] - off[j];
+    off_o[p] = s0 + dst;
+    for (unsigned long long q = 0; q < m; ++q) {
+      slot_o[dst + q] = slot[src + q];
+      sign_o[dst + q] = sign[src + q];
+    }
+    if (p + 1 == n) off_o[n] = s0 + dst + m;
+  }
+}
+}  // namespace
+
+extern "C" int fbx_merge_subtiles(const unsigned long long* d_tile_start, unsigned spc,
+                                  unsigned long long n_tiles, unsigned long long n,
+                                  unsigned long long s0, unsigned max_len,
+                                  const unsigned long long* d_ids, const unsigned char* d_lab,
+                                  const unsigned long long* d_off, const unsigned short* d_slot,
+                                  const unsigned long long* d_sign, unsigned long long* d_ids_o,
+                                  unsigned char* d_lab_o, unsigned long long* d_off_o,
+                                  unsigned short* d_slot_o, unsigned long long* d_sign_o,
+                                  unsigned long long* d_scratch, unsigned* d_bad, void* stream) {
+  if (!spc || !n_tiles) return fail(FBX_E_ARG, "fbx_merge_subtiles: empty tiling");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = cuda_check(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), s), "merge flag");
+  if (rc || n == 0) return rc;
+  unsigned long long* pos = d_scratch;           // [n]
+  unsigned long long* newlen = d_scratch + n;    // [n]
+  unsigned long long* newoff = d_scratch + 2 * n;  // [n + 1]
+  rc = cuda_check(cudaMemsetAsync(newlen, 0, n * sizeof(unsigned long long), s), "merge lens");
+  if (rc) return rc;
+  const unsigned g = (unsigned)((n + 255) / 256 < 4736 ? (n + 255) / 256 : 4736);
+  k_merge_rank<<<g, 256, 0, s>>>(d_tile_start, spc, n_tiles, n, d_ids, d_off, pos, newlen,
+                                 max_len, d_bad);
+  size_t tmp = 0;
+  rc = cuda_check(cudaMemsetAsync(newoff, 0, sizeof(unsigned long long), s), "merge off0");
+  if (rc) return rc;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp, newlen, newoff + 1, (int)n, s);
+  void* d_tmp = nullptr;
+  rc = cuda_check(cudaMallocAsync(&d_tmp, tmp, s), "merge scan temp");
+  if (rc) return rc;
+  cub::DeviceScan::InclusiveSum(d_tmp, tmp, newlen, newoff + 1, (int)n, s);
+  cudaFreeAsync(d_tmp, s);
+  k_merge_scatter<<<g, 256, 0, s>>>(n, pos, newoff, s0, d_ids, d_lab, d_off,
+                                    d_slot, d_sign, d_ids_o, d_lab_o, d_off_o, d_slot_o,
+                                    d_sign_o, d_bad);
+  return cuda_check(cudaGetLastError(), "fbx_merge_subtiles");
+}
+
 // ---- host ingest: parallel positional reads of FBXC spans ------------------
 // The reference reads a driver chunk with seek + read per segment span
 // (columnstore.py:499-608).  Here one call copies every span of a slice of

@@ -460,6 +460,24 @@ class DeviceMiniBatch:
     signs: object    # torch int64 (u64 bits)
 
 
+def _nvtx_push(msg: str):
+    """NVTX range around a launch / slice (visible to nsys / ncu --nvtx; a no-op
+    without a tool attached)."""
+    try:
+        import torch
+        torch.cuda.nvtx.range_push(msg)
+    except Exception:  # noqa: BLE001 -- tracing must never fail a run
+        pass
+
+
+def _nvtx_pop():
+    try:
+        import torch
+        torch.cuda.nvtx.range_pop()
+    except Exception:  # noqa: BLE001
+        pass
+
+
 def _next_pow2(n: int) -> int:
     return 1 << max(4, (max(n, 1) - 1).bit_length())
 
@@ -787,38 +805,52 @@ class Engine:
                      st: dict, stream=None):
         """batch_size > 1024: the chunks of tiles [t0, t1) hold instances [i0, i1)
         and signs [s0, s1), each chunk emitted as sorted 512-row sub-tiles; re-order
-        every chunk's instances by ascending u64 id (a stable two-key sort on the
-        device) and rebuild its offsets / slots / signs in place."""
+        every chunk's instances by ascending u64 id and rebuild its offsets / slots
+        / signs (fbx_merge_subtiles: per-instance rank by binary search in the
+        chunk's other sub-tiles, a scan of the new lengths, one scatter)."""
         torch = self.torch
         n, m = i1 - i0, s1 - s0
         if n <= 0:
             return
-        ends = self._chunk_ends(t0, t1)
-        counts = np.diff(np.concatenate([[i0], ends]))
+        incl = self._global_incl(t0, t1)
+        starts = np.concatenate([[i0], incl]).astype(np.int64) - i0
         dev = self.device
-        ids = self.o_ids[i0:i1]
-        chunk_of = torch.repeat_interleave(torch.arange(len(ends), device=dev),
-                                           torch.from_numpy(counts).to(dev))
-        key = ids ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=dev)  # u64 order
-        p1 = torch.sort(key, stable=True).indices
-        perm = p1[torch.sort(chunk_of[p1], stable=True).indices]
-        off = self.o_off[i0:i1 + 1] - s0
-        lens = off[1:] - off[:-1]
-        self.o_ids[i0:i1] = ids[perm]
-        self.o_lab[i0:i1] = self.o_lab[i0:i1][perm]
-        # a repeated id (the run fails) ties two rows' ranks and leaves an instance
-        # slot unwritten: only a consistent CSR is re-ordered
-        if bool(((lens >= 0).all() & (lens.sum() == m)).item()):
-            new_lens = lens[perm]
-            new_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-            new_off[1:] = torch.cumsum(new_lens, 0)
-            seg = torch.repeat_interleave(torch.arange(n, device=dev), new_lens)
-            src = off[:-1][perm][seg] + (torch.arange(m, device=dev) - new_off[:-1][seg])
-            self.o_slot[s0:s1] = self.o_slot[s0:s1][src]
-            self.o_sign[s0:s1] = self.o_sign[s0:s1][src]
-            self.o_off[i0:i1 + 1] = new_off + s0
-        elif not (st["dup_seen"] or st["error_key"] != (1 << 64) - 1):
-            raise RuntimeError("inconsistent CSR after a run without failures")
+        d_starts = torch.from_numpy(starts).to(dev, non_blocking=False)
+        ids_o = torch.empty(n, dtype=torch.int64, device=dev)
+        lab_o = torch.empty(n, dtype=torch.uint8, device=dev)
+        off_o = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        slot_o = torch.empty(max(m, 1), dtype=torch.int16, device=dev)
+        sign_o = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+        scratch = torch.empty(3 * n + 1, dtype=torch.int64, device=dev)
+        bad = torch.empty(1, dtype=torch.int32, device=dev)
+        s = self._stream() if stream is None else stream
+        ins = (self.o_ids[i0:].data_ptr(), self.o_lab[i0:].data_ptr(), self.o_off[i0:].data_ptr(),
+               self.o_slot[s0:].data_ptr(), self.o_sign[s0:].data_ptr())
+        outs = (ids_o.data_ptr(), lab_o.data_ptr(), off_o.data_ptr(), slot_o.data_ptr(),
+                sign_o.data_ptr())
+        runtime.merge_subtiles(d_starts.data_ptr(), self.prog.tiles_per_chunk, t1 - t0, n, s0,
+                               max(1, len(self.ir.features)), ins, outs, scratch.data_ptr(),
+                               bad.data_ptr(), s)
+        # a repeated id (the run then fails) can leave the CSR inconsistent: the
+        # kernel flags it and writes nothing -- such a CSR is never handed out
+        # (the run raises), and _check_merges raises if the run did not fail
+        self.o_ids[i0:i1].copy_(ids_o)
+        self.o_lab[i0:i1].copy_(lab_o)
+        self.o_off[i0:i1 + 1].copy_(off_o)
+        if m:
+            self.o_slot[s0:s1].copy_(slot_o[:m])
+            self.o_sign[s0:s1].copy_(sign_o[:m])
+        if not hasattr(self, "_merge_bad"):
+            self._merge_bad = []
+        self._merge_bad.append((bad, st))
+
+    def _check_merges(self):
+        """After a run with chunk merges: an inconsistent CSR is only legal in a
+        run that fails (a repeated id)."""
+        for bad, st in getattr(self, "_merge_bad", []):
+            if int(bad.item()) and not (st["dup_seen"] or st["error_key"] != (1 << 64) - 1):
+                raise RuntimeError("inconsistent CSR after a run without failures")
+        self._merge_bad = []
 
     def _resolve_big_label_error(self, st: dict):
         """Place a label failure from the final (merged) order: the kernel marked
@@ -845,6 +877,7 @@ class Engine:
     def _merge_big_chunks(self, st: dict):
         self._merge_range(0, int(st["instances"]), 0, int(st["signs"]), 0, self._run_tiles, st)
         self._resolve_big_label_error(st)
+        self._check_merges()
 
     def _emit_error_key(self, ek: int) -> int:
         """Map a label error at emission position (batch b) to the chunk whose
@@ -1029,8 +1062,12 @@ class Engine:
         self._chunk_minus_tile = row_lo // self.ir.chunk - tile_base
         self._run_chunk0 = row_lo // self.ir.chunk - tile_base // self.prog.tiles_per_chunk
         self._run_tiles = tile_base + tiles
-        self.module.launch("fbx_pipeline", tiles, self.prog.threads, self.prog.smem_bytes,
-                           stream, self.params)
+        _nvtx_push(f"fbx_pipeline rows {row_lo}-{row_hi} tiles {tile_base}+{tiles}")
+        try:
+            self.module.launch("fbx_pipeline", tiles, self.prog.threads, self.prog.smem_bytes,
+                               stream, self.params)
+        finally:
+            _nvtx_pop()
         return tiles
 
     def finish(self) -> CsrBatch:
@@ -1287,6 +1324,7 @@ class StreamedRun:
         if eng.prog.tiles_per_chunk > 1:
             self.s_comp.synchronize()
             eng._resolve_big_label_error(last)
+            eng._check_merges()
         eng.check_run(last)
         self.d2h_bytes = (tot.instances * 17 + 8 + tot.signs * 10 if self.sink == "host"
                           else runtime.STATE_BYTES * len(self.bounds))

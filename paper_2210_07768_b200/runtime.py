@@ -33,7 +33,8 @@ EXPORTS = ("fbx_version", "fbx_error_message", "fbx_compile", "fbx_free", "fbx_p
            "fbx_dict_build", "fbx_l2_flush", "fbx_exclusive_scan_u32", "fbx_gather_strings",
            "fbx_dup_resolve", "fbx_state_snapshot",
            "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words", "fbx_idset_clear",
-           "fbx_pool_account", "fbx_memset_async", "fbx_read_spans")
+           "fbx_pool_account", "fbx_memset_async", "fbx_read_spans",
+           "fbx_merge_subtiles")
 
 
 class FbxError(RuntimeError):
@@ -81,6 +82,9 @@ def lib() -> ctypes.CDLL:
             L.fbx_crc32.argtypes = [vp, ctypes.c_ulonglong, vp, vp, vp]
             L.fbx_read_spans.argtypes = [ctypes.c_char_p, vp, vp, vp, vp, ctypes.c_uint,
                                          ctypes.c_uint]
+            L.fbx_merge_subtiles.argtypes = [vp, ctypes.c_uint, ctypes.c_ulonglong,
+                                             ctypes.c_ulonglong, ctypes.c_ulonglong,
+                                             ctypes.c_uint] + [vp] * 12 + [vp]
             L.fbx_crc32_scratch_words.argtypes = [ctypes.c_ulonglong]
             L.fbx_crc32_scratch_words.restype = ctypes.c_ulonglong
             for name in EXPORTS:
@@ -271,3 +275,12 @@ def read_spans(path, dst: int, file_off, length, dst_off, threads: int | None = 
                                 ln.ctypes.data_as(vp), do.ctypes.data_as(vp), n,
                                 host_threads() if threads is None else int(threads)),
            "read spans")
+
+
+def merge_subtiles(d_tile_start: int, spc: int, n_tiles: int, n: int, s0: int, max_len: int,
+                   ins: tuple, outs: tuple, d_scratch: int, d_bad: int, stream: int):
+    """fbx_merge_subtiles: ins / outs = (ids, labels, offsets, slots, signs) pointers."""
+    vp = ctypes.c_void_p
+    _check(lib().fbx_merge_subtiles(vp(d_tile_start), spc, n_tiles, n, s0, max_len,
+                                    *[vp(x) for x in ins], *[vp(x) for x in outs], vp(d_scratch),
+                                    vp(d_bad), vp(stream)), "merge sub-tiles")

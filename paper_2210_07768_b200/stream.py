@@ -125,10 +125,12 @@ class FileRun:
                     self.h2d_done[k - nb].synchronize()  # the pinned buffer is free again
                 t = time.perf_counter()
                 pcs = self.layout[k]
+                torch.cuda.nvtx.range_push(f"fbx read slice {k}")
                 runtime.read_spans(vf.path, self.host[k % nb].data_ptr(),
                                    [vf.segments[(c, p)][0] + a for c, p, a, _, _ in pcs],
                                    [b - a for _, _, a, b, _ in pcs],
                                    [o for *_, o in pcs], self.threads)
+                torch.cuda.nvtx.range_pop()
                 self.read_s += time.perf_counter() - t
                 if k >= nb:
                     self.recorded[k - nb].wait()  # slice k - nb's kernel is enqueued
