@@ -160,6 +160,47 @@ int fbx_merge_subtiles(const unsigned long long* d_tile_start, unsigned spc,
                        unsigned long long* d_sign_o, unsigned long long* d_scratch,
                        unsigned* d_bad, void* stream);
 
+/* Whole-table operations of the staged mode (pipeline.run_staged,
+ * pipeline.py:783-895; csrc/fbx_table.cu).  Keys: the u64 whose unsigned order
+ * is the reference key image's order (join_key_bytes, viewpipe.py:451-459):
+ * Int64 two's-complement bits, Float32 IEEE bits. */
+/* clean_views' survivors: indices of the rows with keep[i] != 0, in order. */
+int fbx_select_rows(const unsigned char* d_keep, unsigned long long n, unsigned* d_rows,
+                    unsigned long long* d_count, void* stream);
+/* dst[i] = src[rows[i]] for elements of 1, 2, 4 or 8 bytes. */
+int fbx_take(const void* d_src, unsigned elem_bytes, const unsigned* d_rows,
+             unsigned long long n, void* d_dst, void* stream);
+/* FBXC null bitmap (LSB-first, set = null) of rows[i] (or i when rows is NULL). */
+int fbx_pack_nulls(const unsigned char* d_isnull, const unsigned* d_rows, unsigned long long n,
+                   unsigned char* d_bitmap, void* stream);
+/* Per-row null bytes of an FBXC bitmap; (pointer, length) of every string of a
+ * Utf8 / Json image (offsets[n+1] into data). */
+int fbx_unpack_nulls(const unsigned char* d_bitmap, unsigned long long n,
+                     unsigned char* d_isnull, void* stream);
+int fbx_spans(const unsigned* d_offsets, const unsigned char* d_data, unsigned long long n,
+              unsigned long long* d_ptr, unsigned* d_len, void* stream);
+/* JoinIndex (viewpipe.py:498-511): the non-null keys and their rows, sorted by key
+ * (stable); *d_count = how many.  Scratch: n rows, n keys, n flag bytes. */
+int fbx_sort_keys(const unsigned long long* d_key, const unsigned char* d_isnull,
+                  unsigned long long n, unsigned long long* d_skey, unsigned* d_srow,
+                  unsigned long long* d_count, unsigned* d_rows_scratch,
+                  unsigned long long* d_key_scratch, unsigned char* d_flag_scratch, void* stream);
+/* join_with_index (viewpipe.py:537-547): matches per left row (first sorted index,
+ * count); the host scans the counts into offsets, then fbx_join_fill writes the
+ * m matches' (left row, right row) in _materialize_join's (key, left, right) order. */
+int fbx_join_count(const unsigned long long* d_lkey, const unsigned char* d_lnull,
+                   unsigned long long nl, const unsigned long long* d_skey,
+                   unsigned long long nr_valid, unsigned long long* d_first, unsigned* d_cnt,
+                   void* stream);
+int fbx_join_fill(const unsigned long long* d_lkey, unsigned long long nl,
+                  const unsigned long long* d_first, const unsigned* d_cnt,
+                  const unsigned long long* d_off, const unsigned* d_srow, unsigned long long m,
+                  unsigned* d_left, unsigned* d_right, void* stream);
+/* check_unique_ids (viewpipe.py:562-576) over sorted keys: the first row, in row
+ * order, whose key occurred before (~0 when none). */
+int fbx_first_repeat(const unsigned long long* d_skey, const unsigned* d_srow,
+                     unsigned long long n_valid, unsigned long long* d_best, void* stream);
+
 /* Host ingest of a driver slice (read_columns with a row range,
  * columnstore.py:499-608; pipeline.py:986-1006 reads the driver chunk by chunk):
  * n_spans byte spans of one FBXC file, span i = file bytes

@@ -14,7 +14,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB = PKG / "libfbx.so"
-SOURCES = [PKG / "csrc" / "fbx_runtime.cu", PKG / "csrc" / "fbx_engine.cu"]
+SOURCES = [PKG / "csrc" / "fbx_runtime.cu", PKG / "csrc" / "fbx_engine.cu",
+           PKG / "csrc" / "fbx_table.cu"]
 HEADERS = [ROOT / "include" / "fbx.h", ROOT / "include" / "fbx_abi.h"]
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 

@@ -114,6 +114,7 @@ class PlanIR:
     extract_outputs: list[tuple[str, str]] = field(default_factory=list)  # (col, domain)
     stage_strings: bool = True
     mode: str = "pipeline"          # "pipeline" | "extract" (row-aligned _extract_batch)
+    #                                 | "clean" (clean_views of `driver`, row-aligned: staged mode)
     pool_bytes: int = 8 << 20       # the reference arena's capacity (config device.pool_bytes)
     lanes_per_group: int = 256      # its group size (config device.lanes_per_group)
 
@@ -889,6 +890,59 @@ class PlanCodegen:
         g("}")
         g("}")
         g("fbx::block_side_counts(ST, nmal, nfilt, nidx);")
+        g("}")
+        return name
+
+    def clean_rows_kernel(self, view: ViewIR) -> str:
+        """``clean_views`` of a whole view (viewpipe.py:334-431), row-aligned, for
+        the staged mode: per row the keep flag (not malformed, passes the filter)
+        and every cleaned column -- fills applied, JSON extraction outputs coerced
+        -- as value (Int64 / Float32) or pointer + length (Utf8 / Json), and a
+        null byte (null slots hold 0 / the empty string).  The host compacts the kept rows into the
+        cleaned view's FBXC image (fbx_select_rows / fbx_take / fbx_pack_nulls).
+        A cleaned string holding a lone surrogate cannot be written as UTF-8:
+        the staged clean stage fails with UnicodeEncodeError, as the reference's
+        writer does."""
+        g = self.g
+        k = 0
+        name = "fbx_clean_rows"
+        g(f'extern "C" __global__ void __launch_bounds__(256) {name}(const fbx_params P) {{')
+        g("fbx_state* ST = (fbx_state*)P.v[0];")
+        g(f"const u64 n = {g.p('side0.rows')};")
+        g(f"u8* POOL = {g.p('side_pool', 'u8*')}; const u64 POOL_CAP = {g.p('side_pool_cap')};")
+        g(f"u8* KEEP = {g.p('clean.keep', 'u8*')};")
+        g("u32 nmal = 0, nfilt = 0;")
+        g("const u64 chunk = 0;")
+        g("for (u64 base = (u64)blockIdx.x * 256u; base < n; base += (u64)gridDim.x * 256u) {")
+        g("const u64 srow = base + threadIdx.x;")
+        g("bool alive = srow < n;")
+        g("const u64 row = alive ? srow : 0ull;")
+        g("__shared__ struct { fbx::BlockScanU32<256> scan; u64 pool_base; } sm;")
+        g("constexpr int NT = 256;")
+        g(f"u32 CUR_STAGE = {STAGE['clean']}u, CUR_LAYER = 0u, CUR_RANK = 0u;")
+        g("u32 malformed = 0, filtered = 0;")
+        ckinds = view.cleaned_kinds()
+        loader = self.side_loader(k, "row")
+        vals = self.clean_view(view, "cl_", loader, "clean", set(ckinds), "")
+        g("nmal += malformed; nfilt += filtered;")
+        g("if (srow < n) {")
+        g("KEEP[row] = alive ? 1u : 0u;")
+        for c, kind in ckinds.items():
+            v = vals[c]
+            if v.t == "str":
+                if v.lone:
+                    g(f"if (alive && !{v.n} && {v.l}) {{")
+                    self.row_error("clean", "encode")
+                    g("}")
+                g(f"{g.p(f'clean.{c}.ptr', 'u64*')}[row] = (u64){v.c}.p;")
+                g(f"{g.p(f'clean.{c}.len', 'u32*')}[row] = {v.n} ? 0u : {v.c}.n;")
+            else:  # a null slot holds 0, as the reference's Column.build writes it
+                w = "u32" if kind is Kind.FLOAT32 else "u64"
+                g(f"(({w}*){g.p(f'clean.{c}.val', 'u64*')})[row] = {v.n} ? ({w})0 : ({w}){v.c};")
+            g(f"{g.p(f'clean.{c}.null', 'u8*')}[row] = {v.n} ? 1u : 0u;")
+        g("}")
+        g("}")
+        g("fbx::block_side_counts(ST, nmal, nfilt, 0u);")
         g("}")
         return name
 
@@ -1932,6 +1986,14 @@ class PlanCodegen:
                                 for j, (name, c, t) in enumerate(dpf)}
                 self.dyn_smem = max(self.dyn_smem, d_need) // 16 * 16
         self.g.slot("state")  # slot 0
+        if ir.mode == "clean":
+            kname = self.clean_rows_kernel(ir.driver)
+            consts = b"".join(self.g.consts)
+            head = [library_source(), "", "// ===== generated plan =====",
+                    f"__device__ const __align__(16) u8 K_STR[] = {_c_bytes(consts + bytes(16))};",
+                    *self.globals, ""]
+            return Program("\n".join(head + self.g.lines), dict(self.g.slots), 256, 0,
+                           [kname], [], self.notes)
         if ir.mode == "extract":
             kname = self.extract_rows_kernel()
             consts = b"".join(self.g.consts)

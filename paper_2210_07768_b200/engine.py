@@ -1721,11 +1721,14 @@ def run_pipelined(config: PipelineConfig, collect: bool = False,
 
 
 def run_pipeline(config: PipelineConfig, mode: str | None = None) -> RunReport:
+    """Dispatch to the configured (or overridden) mode (pipeline.py:1117-1124)."""
     effective = mode or config.mode
-    if effective != "pipelined":
-        raise UnsupportedOnDevice(f"mode {effective!r}: only the pipelined path is on device "
-                                  "(staged mode writes intermediate files; out of scope)")
-    return run_pipelined(config)
+    if effective == "staged":
+        from .staged import run_staged
+        return run_staged(config)
+    if effective == "pipelined":
+        return run_pipelined(config)
+    raise ConfigError(f"unknown mode {effective!r}")
 
 
 # ---------------------------------------------------------------------------
@@ -1810,6 +1813,25 @@ class ExtractEngine:
 
     def extract(self, table: ViewImage) -> ViewImage:
         return self.c.extract(table)
+
+
+def prepare_clean_ir(config: PipelineConfig, view_cfg, kinds: Mapping[str, Kind]) -> codegen.PlanIR:
+    """The plan of one view's ``clean_views`` kernel (staged mode, codegen mode
+    "clean"): the view's fills, JSON extractions and bound filter."""
+    pol = view_cfg.policy
+    try:
+        validate_clean_policy(dict(kinds), pol)
+    except (CleanConfigError, KeyError) as exc:
+        raise ConfigError(f"view {view_cfg.name!r}: {exc}") from exc
+    cleaned = cleaned_kinds(dict(kinds), pol)
+    flt = bind_filter(pol.filter, cleaned) if pol.filter is not None else None
+    drv = codegen.ViewIR(view_cfg.name, dict(kinds), dict(pol.fills), list(pol.extractions), flt,
+                         ())
+    return codegen.PlanIR(
+        driver=drv, sides=[], basic=None, join_keys=(), nodes=[], pre_of={}, producer={},
+        features={}, instance_column=config.instance_column, label_column=config.label_column,
+        chunk=256, tables={}, table_defaults={}, extract_outputs=[], stage_strings=False,
+        mode="clean", pool_bytes=config.pool_bytes, lanes_per_group=config.lanes_per_group)
 
 
 def extract_batch(table: ViewImage, config: PipelineConfig, device: str = "cuda") -> ViewImage:

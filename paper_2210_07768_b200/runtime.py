@@ -34,7 +34,9 @@ EXPORTS = ("fbx_version", "fbx_error_message", "fbx_compile", "fbx_free", "fbx_p
            "fbx_dup_resolve", "fbx_state_snapshot",
            "fbx_pool_reset", "fbx_crc32", "fbx_crc32_scratch_words", "fbx_idset_clear",
            "fbx_pool_account", "fbx_memset_async", "fbx_read_spans",
-           "fbx_merge_subtiles")
+           "fbx_merge_subtiles", "fbx_select_rows", "fbx_take", "fbx_pack_nulls",
+           "fbx_sort_keys", "fbx_join_count", "fbx_join_fill", "fbx_first_repeat",
+           "fbx_unpack_nulls", "fbx_spans")
 
 
 class FbxError(RuntimeError):
@@ -85,6 +87,16 @@ def lib() -> ctypes.CDLL:
             L.fbx_merge_subtiles.argtypes = [vp, ctypes.c_uint, ctypes.c_ulonglong,
                                              ctypes.c_ulonglong, ctypes.c_ulonglong,
                                              ctypes.c_uint] + [vp] * 12 + [vp]
+            ull = ctypes.c_ulonglong
+            L.fbx_select_rows.argtypes = [vp, ull, vp, vp, vp]
+            L.fbx_take.argtypes = [vp, ctypes.c_uint, vp, ull, vp, vp]
+            L.fbx_pack_nulls.argtypes = [vp, vp, ull, vp, vp]
+            L.fbx_sort_keys.argtypes = [vp, vp, ull, vp, vp, vp, vp, vp, vp, vp]
+            L.fbx_join_count.argtypes = [vp, vp, ull, vp, ull, vp, vp, vp]
+            L.fbx_join_fill.argtypes = [vp, ull, vp, vp, vp, vp, ull, vp, vp, vp]
+            L.fbx_first_repeat.argtypes = [vp, vp, ull, vp, vp]
+            L.fbx_unpack_nulls.argtypes = [vp, ull, vp, vp]
+            L.fbx_spans.argtypes = [vp, vp, ull, vp, vp, vp]
             L.fbx_crc32_scratch_words.argtypes = [ctypes.c_ulonglong]
             L.fbx_crc32_scratch_words.restype = ctypes.c_ulonglong
             for name in EXPORTS:
@@ -284,3 +296,8 @@ def merge_subtiles(d_tile_start: int, spc: int, n_tiles: int, n: int, s0: int, m
     _check(lib().fbx_merge_subtiles(vp(d_tile_start), spc, n_tiles, n, s0, max_len,
                                     *[vp(x) for x in ins], *[vp(x) for x in outs], vp(d_scratch),
                                     vp(d_bad), vp(stream)), "merge sub-tiles")
+
+
+def call(name: str, *args):
+    """A libfbx table operation (include/fbx.h); pointers and sizes as ints."""
+    _check(getattr(lib(), name)(*args), name)
