@@ -663,19 +663,26 @@ class Engine:
             if f"dict{ti}.slots" not in self.slots:
                 continue
             t = self.config.tables[name]
-            blob, offs, vals = t.arrays()
-            cap = _next_pow2(2 * len(vals))
-            slots = torch.empty(cap * 32, dtype=torch.uint8, device=self.device)
-            dblob = torch.from_numpy(_pad16(blob)).to(self.device)
-            doffs = torch.from_numpy(_pad16(offs)).to(self.device)
-            dvals = torch.from_numpy(_pad16(vals)).to(self.device)
-            dup = torch.zeros(1, dtype=torch.int64, device=self.device)
+            # the HBM table is immutable: built once per loaded DictTable and device,
+            # shared by every engine of that config (the reference parses the TSV
+            # once per load_config too)
+            built = t.__dict__.setdefault("_device_tables", {})
+            if self.device not in built:
+                blob, offs, vals = t.arrays()
+                cap = _next_pow2(2 * len(vals))
+                slots = torch.empty(cap * 32, dtype=torch.uint8, device=self.device)
+                dblob = torch.from_numpy(_pad16(blob)).to(self.device)
+                doffs = torch.from_numpy(_pad16(offs)).to(self.device)
+                dvals = torch.from_numpy(_pad16(vals)).to(self.device)
+                dup = torch.zeros(1, dtype=torch.int64, device=self.device)
+                try:
+                    runtime.dict_build(slots.data_ptr(), cap, dblob.data_ptr(), doffs.data_ptr(),
+                                       dvals.data_ptr(), len(vals), dup.data_ptr(), stream)
+                except runtime.FbxError as exc:
+                    raise ConfigError(f"table {name!r}: {exc}") from exc
+                built[self.device] = (slots, dblob, doffs, dvals, dup, cap)
+            slots, dblob, doffs, dvals, dup, cap = built[self.device]
             self._keep += [slots, dblob, doffs, dvals, dup]
-            try:
-                runtime.dict_build(slots.data_ptr(), cap, dblob.data_ptr(), doffs.data_ptr(),
-                                   dvals.data_ptr(), len(vals), dup.data_ptr(), stream)
-            except runtime.FbxError as exc:
-                raise ConfigError(f"table {name!r}: {exc}") from exc
             self._set(f"dict{ti}.slots", slots.data_ptr())
             self._set(f"dict{ti}.mask", cap - 1)
             self._set(f"dict{ti}.keys", dblob.data_ptr())
@@ -1560,21 +1567,40 @@ def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: Vie
 _PREPARED: dict[str, Prepared] = {}
 
 
-def _prepared(config: PipelineConfig) -> Prepared:
-    """prepare() once per (config, input schemas): the plan cache.  The schemas
-    come from the files' headers, so an edited file re-plans."""
+def _config_key(config: PipelineConfig) -> str:
+    """What the generated plan depends on: every config field, with each
+    dictionary table reduced to (default, size, entry count) -- its contents
+    only reach the device tables, which the engine builds from the config of
+    the call -- and the input files' schemas (an edited file re-plans)."""
+    import dataclasses
     import hashlib
-    import pickle
-    key_parts = [repr(config)]
+    parts = []
+    for f in dataclasses.fields(config):
+        v = getattr(config, f.name)
+        if f.name == "tables":
+            v = sorted((n, t.default, t.size_bytes, len(t.entries)) for n, t in v.items())
+        parts.append((f.name, repr(v)))
     for v in config.views:
-        key_parts.append(repr(open_view(v.path).schema))
-    key_parts.append(repr(open_view(config.basic_path).schema))
-    key = hashlib.sha256(pickle.dumps(key_parts)).hexdigest()
+        parts.append(repr(open_view(v.path).schema))
+    parts.append(repr(open_view(config.basic_path).schema))
+    return hashlib.sha256(repr(parts).encode()).hexdigest()
+
+
+def _prepared(config: PipelineConfig) -> Prepared:
+    """prepare() once per plan key (_config_key): the plan cache.  The returned
+    Prepared carries the CALL's config (its dictionary tables)."""
+    import dataclasses
+    key = _config_key(config)
     prep = _PREPARED.get(key)
     if prep is None:
         prep = prepare(config)
         _PREPARED.clear()  # one plan at a time (the engines hold its module)
         _PREPARED[key] = prep
+    if prep.config is not config:
+        mods = prep.__dict__.get("_modules")
+        prep = dataclasses.replace(prep, config=config)
+        if mods is not None:
+            prep.__dict__["_modules"] = mods
     return prep
 
 
