@@ -820,7 +820,11 @@ class PlanCodegen:
         """Index one side view (or the basic view) into its HBM join table."""
         g = self.g
         name = f"fbx_side_prep_{k}"
-        g(f'extern "C" __global__ void __launch_bounds__(256) {name}(const fbx_params P) {{')
+        # a device function: every view's index build runs in ONE launch
+        # (fbx_side_prep_all dispatches CTA ranges), so the small side views
+        # build concurrently with the basic view instead of one after another
+        g(f"static __device__ __forceinline__ void {name}(const fbx_params& P, const u32 BID, "
+          "const u32 NBLK) {")
         g("fbx_state* ST = (fbx_state*)P.v[0];")
         g(f"const u64 n = {g.p(f'side{k}.rows')};")
         g(f"fbx::Slot* TBL = {g.p(f'side{k}.table', 'fbx::Slot*')};")
@@ -828,7 +832,7 @@ class PlanCodegen:
         g(f"u8* POOL = {g.p('side_pool', 'u8*')}; const u64 POOL_CAP = {g.p('side_pool_cap')};")
         g("u32 nmal = 0, nfilt = 0, nidx = 0;")
         g("const u64 chunk = 0;")
-        g("for (u64 base = (u64)blockIdx.x * 256u; base < n; base += (u64)gridDim.x * 256u) {")
+        g("for (u64 base = (u64)BID * 256u; base < n; base += (u64)NBLK * 256u) {")
         g("const u64 srow = base + threadIdx.x;")
         g("bool alive = srow < n;")
         g("const u64 row = alive ? srow : 0ull;")
@@ -945,6 +949,18 @@ class PlanCodegen:
         g("fbx::block_side_counts(ST, nmal, nfilt, 0u);")
         g("}")
         return name
+
+    def side_prep_dispatch(self, nviews: int):
+        """fbx_side_prep_all: CTA b runs the index build of the view whose range
+        [start_k, start_k + grid_k) holds b (side{k}.grid, set by the engine)."""
+        g = self.g
+        g('extern "C" __global__ void __launch_bounds__(256) fbx_side_prep_all(const fbx_params P) {')
+        g("u32 b = blockIdx.x;")
+        for k in range(nviews):
+            g(f"{{ const u32 gk = (u32){g.p(f'side{k}.grid')};")
+            g(f"if (b < gk) {{ fbx_side_prep_{k}(P, b, gk); return; }}")
+            g("b -= gk; }")
+        g("}")
 
     # -- operator library --------------------------------------------------------------
     def node_code(self, nd: NodeIR, args: list[V]) -> V:
@@ -2009,6 +2025,9 @@ class PlanCodegen:
             self.g("")
         if ir.basic is not None:
             side_names.append(self.side_prep_kernel(len(ir.sides), ir.basic, True))
+            self.g("")
+        if side_names:
+            self.side_prep_dispatch(len(side_names))
             self.g("")
         body_start = len(self.g.lines)
         kname = self.pipeline_kernel()

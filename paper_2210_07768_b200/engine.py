@@ -632,10 +632,17 @@ class Engine:
             self._settle_prepare({f: int(raw[i]) for i, f in enumerate(runtime.STATE_FIELDS)})
 
     def _launch_side_prep(self, stream: int) -> int:
+        """Every side view's and the basic view's index build in one launch
+        (fbx_side_prep_all: a CTA range per view)."""
+        if not self._side_views:
+            return 0
+        total = 0
         for k, v, n in self._side_views:
             grid = max(1, min((n + 255) // 256, 1184))
-            self.module.launch(f"fbx_side_prep_{k}", grid, 256, 0, stream, self.params)
-        return len(self._side_views)
+            self._set(f"side{k}.grid", grid)
+            total += grid
+        self.module.launch("fbx_side_prep_all", total, 256, 0, stream, self.params)
+        return 1
 
     def rebuild_indices(self, stream: int | None = None) -> int:
         """Rebuild the side-view and basic-view hash indices from their resident
