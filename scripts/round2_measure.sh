@@ -15,3 +15,10 @@ for d in ${PROF_DAGS:-sign_heavy}; do
     --no-e2e --no-cpu-baseline > gpurun_out/r2_full_$d.log 2>&1
   python scripts/traffic.py gpurun_out/r2_full_$d.ncu-rep gpurun_out/r2_full_$d.log
 done
+# C5: 100 independent shards (default DAG), shards over 3 streams, run_pipelined per shard
+timeout 1200 python bench.py --dag default --shards 100 --steps 3 --warmup 3 --no-cpu-baseline \
+  2>gpurun_out/r2_bench_c5.err | tail -1 > gpurun_out/r2_bench_c5.json
+python -c "import json;d=json.load(open('gpurun_out/r2_bench_c5.json'));print('C5', d['value'], d['ms_per_step'], d['e2e']['value'], d['parity']['shards_checked'])"
+# the default bench line with its cpu baseline (the driver's own run)
+timeout 900 python bench.py > gpurun_out/r2_bench_default_full.json 2>gpurun_out/r2_bench_default_full.err
+python scripts/pcie_probe.py > gpurun_out/r2_pcie.txt 2>&1
