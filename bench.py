@@ -272,7 +272,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    if world > 1 or "WORLD_SIZE" in os.environ:  # under torchrun: the NCCL path, any N
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     # what this rank extracts per step: one log (seed 11 + rank, weak scaling)
