@@ -93,7 +93,7 @@ def parse_args():
     ap.add_argument("--launch-rows", type=int, default=1 << 24)
     ap.add_argument("--e2e-slice-rows", type=int, default=1 << 18)
     ap.add_argument("--e2e-stream-slice-rows", type=int, default=1 << 20)
-    ap.add_argument("--api-slice-rows", type=int, default=1 << 18,
+    ap.add_argument("--api-slice-rows", type=int, default=1 << 19,
                     help="driver slice of the drop-in run_pipelined file stream")
     ap.add_argument("--lookup-fillers", type=int, default=10_000_000,
                     help="lookup_heavy: never-matching query_dict fillers (SURVEY 8d: >= 1e7 so "

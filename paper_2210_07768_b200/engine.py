@@ -1612,7 +1612,7 @@ def _prepared(config: PipelineConfig) -> Prepared:
 
 
 def run_pipelined(config: PipelineConfig, collect: bool = False,
-                  slice_rows: int = 1 << 18) -> RunReport:
+                  slice_rows: int = 1 << 19) -> RunReport:
     """Reference-compatible ``run_pipelined`` (pipeline.py:952-1114) on the B200.
 
     prepare (plan cached per config + schemas) -> side views and basic features

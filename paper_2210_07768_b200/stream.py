@@ -36,7 +36,7 @@ class FileRun:
 
     PARTS = ("nulls", "offsets", "data")
 
-    def __init__(self, prepared, path, columns=None, device="cuda", slice_rows: int = 1 << 18,
+    def __init__(self, prepared, path, columns=None, device="cuda", slice_rows: int = 1 << 19,
                  nbuf: int = 3, threads: int | None = None):
         import torch
         self.torch = torch
