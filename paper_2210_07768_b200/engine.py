@@ -1586,6 +1586,10 @@ def _config_key(config: PipelineConfig) -> str:
         v = getattr(config, f.name)
         if f.name == "tables":
             v = sorted((n, t.default, t.size_bytes, len(t.entries)) for n, t in v.items())
+        elif f.name == "views":  # file paths do not shape the plan; schemas do (below)
+            v = [(x.name, x.columns, x.policy) for x in v]
+        elif f.name in ("basic_path", "staging_dir"):
+            continue
         parts.append((f.name, repr(v)))
     for v in config.views:
         parts.append(repr(open_view(v.path).schema))
