@@ -152,3 +152,23 @@ def test_streamed_checksum_error_is_prepare_failure(which, tmp_path):
     _, err = _streamed(_config(512, ops, {"c": 3}, filt="age != -12345"), tmp_path, 512)
     assert isinstance(err, StageError) and err.stage == "prepare"
     assert isinstance(err.__cause__, ChecksumError)
+
+
+@pytest.mark.parametrize("rows", [0, 1, 511, 513])
+def test_streamed_tiny_and_empty_logs(rows, tmp_path):
+    """Empty and tiny driver files through the file stream (one partial chunk,
+    a chunk boundary, no rows at all) equal the oracle."""
+    drv, prof, bas = _views(max(rows, 1), 3)
+    if rows == 0:
+        drv = drv.slice(0, 0)
+    _write_views(tmp_path, drv, prof, bas)
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    raw = _config(512, ops, {"c": 3}, filt="age != -12345")
+    ref, ref_err = _oracle(raw, drv, prof, bas, tmp_path)
+    got, got_err = _streamed(raw, tmp_path, 512)
+    if ref_err is not None:
+        assert got_err is not None and got_err.stage == ref_err.stage
+        return
+    assert got_err is None, got_err
+    assert (got.digest, got.instances, got.signs, got.batches) == \
+        (ref.digest, ref.instances, ref.signs, -(-ref.instances // 512))
