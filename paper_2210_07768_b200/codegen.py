@@ -1118,7 +1118,7 @@ class PlanCodegen:
                 elif a.t == "f32":
                     g(f"h.word_be({a.c});")
                 else:
-                    g(f"h.u64_be({a.c});")
+                    g(f"h.u64_be_int({a.c});")
             g(f"{out.c} = h.value();")
             g("}")
             if nullable:

@@ -68,6 +68,37 @@ struct Fnv {
     lo = (u32)w;
   }
   FBX_DI void byte(u32 b) { mul(lo ^ b); }
+  // h = (x | hi << 32) * K for a 64-bit constant K: three multiply-adds.  k zero
+  // bytes in a row are one multiply by P^k ((h ^ 0) * P = h * P), so a run of
+  // known-zero bytes costs one FNV step instead of k.
+  template <u32 KLO, u32 KHI>
+  FBX_DI void mulk(u32 x) {
+    const u64 w = (u64)x * KLO;
+    u32 t, h2;
+    asm("mad.lo.u32 %0, %1, %3, %2;" : "=r"(t) : "r"(hi), "r"((u32)(w >> 32)), "n"(KLO));
+    asm("mad.lo.u32 %0, %1, %3, %2;" : "=r"(h2) : "r"(x), "r"(t), "n"(KHI));
+    hi = h2;
+    lo = (u32)w;
+  }
+  FBX_DI void zeros4() { mulk<0x5635BC91u, 0x9FFAAC08u>(lo); }   // P^4
+  FBX_DI void zeros6() { mulk<0xEDF1C639u, 0xDC966432u>(lo); }   // P^6
+  FBX_DI void zeros7() { mulk<0x51D3D2DBu, 0xC5527B8Au>(lo); }   // P^7
+  // an Int64 value's 8 big-endian bytes (value_bytes, featureops.py:73-87): the
+  // leading zero bytes of a small non-negative value fold into one multiply
+  FBX_DI void u64_be_int(u64 v) {
+    const u32 vh = (u32)(v >> 32), vl = (u32)v;
+    if (vh == 0u && vl < 0x100u) {
+      zeros7();
+      mul(lo ^ vl);
+    } else if (vh == 0u && vl < 0x10000u) {
+      zeros6();
+      mul(lo ^ (vl >> 8));
+      mul(lo ^ (vl & 0xFFu));
+    } else {
+      if (vh == 0u) zeros4(); else word_be(vh);
+      word_be(vl);
+    }
+  }
   // four bytes of a little-endian word, low byte first
   FBX_DI void word_le(u32 w) {
     mul(lo ^ (w & 0xFFu));
@@ -83,7 +114,14 @@ struct Fnv {
   }
   FBX_DI void u64_be(u64 v) { word_be((u32)(v >> 32)); word_be((u32)v); }
   FBX_DI void u64_le(u64 v) { word_le((u32)v); word_le((u32)(v >> 32)); }
-  FBX_DI void u16_le(u32 v) { mul(lo ^ (v & 0xFFu)); mul(lo ^ ((v >> 8) & 0xFFu)); }
+  FBX_DI void u16_le(u32 v) {
+    if (v < 0x100u) {  // a slot below 256 (all of them in practice): (h ^ v) * P^2
+      mulk<0x0002E329u, 0x00036600u>(lo ^ v);
+    } else {
+      mul(lo ^ (v & 0xFFu));
+      mul(lo ^ ((v >> 8) & 0xFFu));
+    }
+  }
   // arbitrary byte span.  Reads whole aligned 32-bit words and funnel-shifts
   // them into place.  The word after the last byte may be read: every span the
   // kernels hash (staged shared-memory spans, padded HBM segments, the pool,
