@@ -993,8 +993,13 @@ class Engine:
                 self.pool_joined = torch.zeros(plane + 1, dtype=torch.uint8, device=dev)
                 self.pool_rank = torch.zeros(plane + 1, dtype=torch.int32, device=dev)
                 self.pool_gsum = torch.zeros(plane + 1, dtype=torch.int64, device=dev)
-                self.pool_nodes = torch.tensor([[l, r, i, 0] for l, r, i in p.ref_pool],
-                                               dtype=torch.int32, device=dev)
+                # the node table is per plan: built once (a pageable H2D would
+                # synchronise the host with every queued upload and index build)
+                nodes = self.prepared.__dict__.setdefault("_pool_nodes", {})
+                if dev not in nodes:
+                    nodes[dev] = torch.tensor([[l, r, i, 0] for l, r, i in p.ref_pool],
+                                              dtype=torch.int32, device=dev)
+                self.pool_nodes = nodes[dev]
                 self._set("pool_flag", self.pool_flag.data_ptr())
                 self._set("pool_chunk", self.pool_chunk.data_ptr())
                 self._set("pool_keys", self.pool_keys.data_ptr())
@@ -1658,6 +1663,7 @@ def run_pipelined(config: PipelineConfig, collect: bool = False,
     fr = None
     if streamed:
         # the driver's first slices are read while the side views are prepared
+        # (measured: faster than reading the side / basic files first)
         fr = FileRun(prep, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows)
         fr.start()
     try:
