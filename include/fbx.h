@@ -200,6 +200,22 @@ int fbx_join_fill(const unsigned long long* d_lkey, unsigned long long nl,
  * order, whose key occurred before (~0 when none). */
 int fbx_first_repeat(const unsigned long long* d_skey, const unsigned* d_srow,
                      unsigned long long n_valid, unsigned long long* d_best, void* stream);
+/* check_unique_ids across the record shards of one log (sharded.py).
+ * fbx_idset_entries: every id the engine's run-wide id set holds (slots
+ * [0, cap) keyed by the id, slot cap = id 0) with the first row holding it --
+ * the smaller of the slot's winner row and its smallest later row (+1 coded);
+ * *d_count = how many (order unspecified).  Buffers: cap + 1 entries. */
+int fbx_idset_entries(const unsigned long long* d_set, const unsigned long long* d_win_rows,
+                      const unsigned long long* d_later_rows, unsigned long long cap,
+                      unsigned long long* d_ids, unsigned long long* d_rows,
+                      unsigned long long* d_count, void* stream);
+/* The first row (smallest d_rows entry) whose id is in d_prior (the ids of the
+ * lower shards, any order): d_out[0] = that row, d_out[1] = its id; both ~0
+ * when none.  Replaces the reference's `seen` set carried across chunks
+ * (pipeline.py:1071-1072, viewpipe.py:562-576) at a shard boundary. */
+int fbx_seen_before(const unsigned long long* d_ids, const unsigned long long* d_rows,
+                    unsigned long long n, const unsigned long long* d_prior,
+                    unsigned long long n_prior, unsigned long long* d_out, void* stream);
 
 /* Host ingest of a driver slice (read_columns with a row range,
  * columnstore.py:499-608; pipeline.py:986-1006 reads the driver chunk by chunk):

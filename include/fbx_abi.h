@@ -41,14 +41,21 @@
 #define FBX_ERR_BASIC_DUP 16      /* MergeUniquenessError: basic features repeat an instance id */
 
 /* Device-resident run state: counters, the pool head, the error word.
- * One per engine, zeroed (error_key = ~0) before a launch. */
+ * One per engine, reset (error_key and the label positions = ~0, the rest 0)
+ * before a run.  The (key, detail) pairs lead, 16-byte aligned: they are
+ * updated together by one 128-bit CAS. */
 typedef struct fbx_state {
+  unsigned long long error_key;     /* min over failures (pipeline order) */
+  unsigned long long error_detail;  /* ... and that failure's detail */
+  unsigned long long emit_range_pos;   /* first emission position of a non-0/1 label */
+  unsigned long long emit_range_label; /* ... and that label (MiniBatch.validate's message) */
+  unsigned long long emit_null_pos;    /* first emission position of a null label */
+  unsigned long long pool_flagged;  /* tiles whose reference ArenaPool demand may exceed
+                                       pool_bytes: fbx_pool_account decides exactly */
   unsigned long long tile_ticket;   /* dynamic tile scheduler */
   unsigned long long pool_head;     /* bump pointer of the HBM arena */
   unsigned long long pool_overflow; /* device arena too small: the head this launch needed
                                        (the engine grows the arena and re-runs) */
-  unsigned long long error_key;     /* min over failures (pipeline order) */
-  unsigned long long error_detail;
   unsigned long long digest;        /* XOR of instance digests */
   unsigned long long instances;
   unsigned long long signs;
@@ -58,11 +65,7 @@ typedef struct fbx_state {
   unsigned long long side_rows;     /* side-view rows indexed */
   unsigned long long dup_seen;      /* an instance id was inserted twice (resolved by
                                        fbx_dup_resolve to the reference's chunk) */
-  unsigned long long emit_key;      /* min (batch | null-before-range | position) of
-                                       the label errors met at emission */
-  unsigned long long emit_detail;   /* the offending label of emit_key */
-  unsigned long long pool_flagged;  /* tiles whose reference ArenaPool demand may exceed
-                                       pool_bytes: fbx_pool_account decides exactly */
+  unsigned long long pad;
 } fbx_state;
 
 /* One device-placed pool-consuming operator node (reference: token pre/post

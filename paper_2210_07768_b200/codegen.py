@@ -1666,7 +1666,7 @@ class PlanCodegen:
         g(f"u64* LN = {g.p('launch_next', 'u64*')};")
         g("LN[0] = lb_i + sm.ex_inst + n_inst; LN[1] = lb_s + sm.ex_signs + tile_signs;")
         g("}")
-        g(f"if (emit_bad) fbx::raise_emit(ST, lb_i + sm.ex_inst + myrank, {ir.chunk}u, emit_bad == 2u, {lab.c});")
+        g(f"if (emit_bad) fbx::raise_emit(ST, lb_i + sm.ex_inst + myrank, emit_bad == 2u, {lab.c});")
         # sub-tiled chunks: the merge re-places label failures from the final order,
         # so a bad label is marked in the emitted label byte (0xFE null, 0xFF range;
         # such a run fails, its CSR is never handed out)

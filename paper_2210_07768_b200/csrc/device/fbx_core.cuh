@@ -603,20 +603,6 @@ FBX_DI u64 err_key(u64 chunk, u32 stage, u32 layer, u32 node, u32 code) {
   return (chunk << 32) | ((u64)(stage & 0xFu) << 28) | ((u64)(layer & 0xFFu) << 20) |
          ((u64)(node & 0xFFFu) << 8) | (code & 0xFFu);
 }
-FBX_DI void raise_err(fbx_state* st, u64 key, u64 detail) {
-  u64 old = atomicMin((unsigned long long*)&st->error_key, (unsigned long long)key);
-  if (key < old) atomicExch((unsigned long long*)&st->error_detail, (unsigned long long)detail);
-}
-
-// Label errors surface when their mini-batch is flushed (pipeline.py:765-777):
-// key = batch(39) | null-before-range(1) | position in batch(12); the host maps
-// the batch to the chunk whose merge flushes it (look-back status).
-FBX_DI void raise_emit(fbx_state* st, u64 pos, u32 batch_size, bool range, u64 detail) {
-  const u64 key = ((pos / batch_size) << 13) | ((u64)range << 12) | (pos % batch_size);
-  u64 old = atomicMin((unsigned long long*)&st->emit_key, (unsigned long long)key);
-  if (key < old) atomicExch((unsigned long long*)&st->emit_detail, (unsigned long long)detail);
-}
-
 // one 128-bit compare-and-swap (atom.cas.b128, sm_90+)
 FBX_DI void cas128(void* addr, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u64* old_lo,
                    u64* old_hi) {
@@ -629,6 +615,32 @@ FBX_DI void cas128(void* addr, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u
       : "=l"(*old_lo), "=l"(*old_hi)
       : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
       : "memory");
+}
+
+// (key, detail) move together: one 128-bit CAS per attempt, so the detail is
+// always the winning key's (a plain atomicMin + exchange could pair a smaller
+// key with a larger key's detail when two failures race)
+FBX_DI void min_pair(u64* pair, u64 key, u64 detail) {
+  u64 lo = ~0ull, hi = 0ull;  // the reset value: one CAS when this is the first
+  while (key < lo) {
+    u64 olo, ohi;
+    cas128(pair, lo, hi, key, detail, &olo, &ohi);
+    if (olo == lo && ohi == hi) break;
+    lo = olo;
+    hi = ohi;
+  }
+}
+FBX_DI void raise_err(fbx_state* st, u64 key, u64 detail) { min_pair(&st->error_key, key, detail); }
+
+// Label errors surface when their mini-batch is flushed (pipeline.py:765-777):
+// emit_minibatch raises at a null label anywhere in the batch before
+// MiniBatch.validate's range check, so the first null and the first non-0/1
+// label are kept apart, by emission position; the host takes the earlier batch
+// (null on a tie) and maps it to the chunk whose merge flushes it.  Positions,
+// not batches, so a record-sharded run can shift them by the shard's base.
+FBX_DI void raise_emit(fbx_state* st, u64 pos, bool range, u64 label) {
+  if (range) min_pair(&st->emit_range_pos, pos, label);
+  else atomicMin((unsigned long long*)&st->emit_null_pos, (unsigned long long)pos);
 }
 
 // check_unique_ids (viewpipe.py:562-576) raises at the FIRST row, in row order,

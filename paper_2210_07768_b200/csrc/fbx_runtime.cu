@@ -100,7 +100,8 @@ __global__ void k_state_reset(fbx_state* st, unsigned long long* status, size_t 
   if (i == 0) {
     memset(st, 0, sizeof(fbx_state));
     st->error_key = ~0ull;
-    st->emit_key = ~0ull;
+    st->emit_range_pos = ~0ull;
+    st->emit_null_pos = ~0ull;
   }
   for (; i < n; i += (size_t)gridDim.x * blockDim.x) status[i] = 0ull;
 }

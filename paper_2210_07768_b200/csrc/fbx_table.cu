@@ -17,6 +17,11 @@
 //                     (key image, left row, right row) order
 //   fbx_first_repeat  check_unique_ids (viewpipe.py:562-576): the first row, in row
 //                     order, whose id occurred before
+//   fbx_idset_entries / fbx_seen_before
+//                     check_unique_ids across the record shards of one log
+//                     (sharded.py): every id a shard's run inserted with the
+//                     first row holding it; the first of them, in row order,
+//                     that a lower shard holds
 //
 // Keys are given as the u64 whose unsigned order is the order of the reference's
 // key image (join_key_bytes, viewpipe.py:451-459: kind tag, length, big-endian
@@ -146,6 +151,39 @@ __global__ void k_join_fill(const ull* lkey, ull nl, const ull* first, const uns
 __global__ void k_first_repeat(const ull* skey, const unsigned* srow, ull n, ull* best) {
   for (ull p = (ull)blockIdx.x * blockDim.x + threadIdx.x + 1; p < n; p += (ull)gridDim.x * blockDim.x)
     if (skey[p] == skey[p - 1]) atomicMin(best, (ull)srow[p]);
+}
+
+// the engine's run-wide id set (codegen ids tail): slots [0, cap) keyed by the
+// id, slot cap = id 0 (stored as 1); the winner's row per slot and the two
+// smallest later rows (+1, 0 = none)
+__global__ void k_idset_entries(const ull* set, const ull* win, const ull* later, ull cap,
+                                ull* ids, ull* rows, ull* count) {
+  for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i <= cap; i += (ull)gridDim.x * blockDim.x) {
+    const ull v = set[i];
+    if (v == 0ull) continue;
+    ull r = win[i];
+    const ull x = later[2 * i];
+    if (x && x - 1ull < r) r = x - 1ull;
+    const ull k = atomicAdd(count, 1ull);
+    ids[k] = i == cap ? 0ull : v;
+    rows[k] = r;
+  }
+}
+
+__global__ void k_seen_before(const ull* ids, const ull* rows, ull n, const ull* prior, ull np,
+                              ull* best) {
+  for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (ull)gridDim.x * blockDim.x) {
+    const ull k = ids[i];
+    const ull a = lower_bound_u64(prior, np, k);
+    if (a < np && prior[a] == k) atomicMin(best, rows[i]);
+  }
+}
+
+__global__ void k_seen_before_id(const ull* ids, const ull* rows, ull n, ull* best) {
+  const ull b = best[0];
+  if (b == ~0ull) return;
+  for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (ull)gridDim.x * blockDim.x)
+    if (rows[i] == b) best[1] = ids[i];  // one entry per row: a row holds one id
 }
 
 template <typename F>
@@ -286,6 +324,41 @@ int fbx_first_repeat(const unsigned long long* d_skey, const unsigned* d_srow,
   if (rc || n_valid < 2) return rc;
   k_first_repeat<<<grid_for(n_valid), 256, 0, s>>>(d_skey, d_srow, n_valid, d_best);
   return tcheck(cudaGetLastError(), "fbx_first_repeat");
+}
+
+int fbx_idset_entries(const unsigned long long* d_set, const unsigned long long* d_win_rows,
+                      const unsigned long long* d_later_rows, unsigned long long cap,
+                      unsigned long long* d_ids, unsigned long long* d_rows,
+                      unsigned long long* d_count, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = tcheck(cudaMemsetAsync(d_count, 0, sizeof(ull), s), "entries count");
+  if (rc) return rc;
+  k_idset_entries<<<grid_for(cap + 1), 256, 0, s>>>(d_set, d_win_rows, d_later_rows, cap, d_ids,
+                                                    d_rows, d_count);
+  return tcheck(cudaGetLastError(), "fbx_idset_entries");
+}
+
+int fbx_seen_before(const unsigned long long* d_ids, const unsigned long long* d_rows,
+                    unsigned long long n, const unsigned long long* d_prior,
+                    unsigned long long n_prior, unsigned long long* d_out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = tcheck(cudaMemsetAsync(d_out, 0xFF, 2 * sizeof(ull), s), "seen init");
+  if (rc || n == 0 || n_prior == 0) return rc;
+  ull* sorted = nullptr;
+  rc = tcheck(cudaMallocAsync((void**)&sorted, n_prior * sizeof(ull), s), "seen sort");
+  if (rc) return rc;
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, d_prior, sorted, (int)n_prior, 0, 64, s);
+  rc = with_temp(bytes, s, [&](void* t) {
+    cub::DeviceRadixSort::SortKeys(t, bytes, d_prior, sorted, (int)n_prior, 0, 64, s);
+  });
+  if (!rc) {
+    k_seen_before<<<grid_for(n), 256, 0, s>>>(d_ids, d_rows, n, sorted, n_prior, d_out);
+    k_seen_before_id<<<grid_for(n), 256, 0, s>>>(d_ids, d_rows, n, d_out);
+    rc = tcheck(cudaGetLastError(), "fbx_seen_before");
+  }
+  cudaFreeAsync(sorted, s);
+  return rc;
 }
 
 }  // extern "C"

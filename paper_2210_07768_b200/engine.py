@@ -31,7 +31,7 @@ from typing import Mapping
 
 import numpy as np
 
-from . import codegen, runtime
+from . import codegen, placement, runtime
 from .columns import ColumnImage, Kind, ViewImage, open_view, read_view
 from .config import (ConfigError, EmitError, BatchInvariantError, CleanConfigError,
                      LayerExecutionError, MergeUniquenessError, PipelineConfig, PoolExhausted,
@@ -700,45 +700,54 @@ class Engine:
         return {f: int(raw[i]) for i, f in enumerate(runtime.STATE_FIELDS)}
 
     def _raise_if_error(self, st: dict, prepare: bool = False):
-        """Raise the run's first failure in the reference's pipeline order.
+        """Raise the run's first failure in the reference's pipeline order."""
+        if prepare:
+            self.raise_key(st["error_key"], st["error_detail"], st)
+        else:
+            self.raise_key(*self.first_failure(st), st)
+
+    def first_failure(self, st: dict) -> tuple[int, int]:
+        """(error key, detail) of the run's first failure in the reference's
+        pipeline order (``placement.NONE`` without one).
 
         ``error_key`` holds the row-level failures at their own chunk.  Two
-        kinds surface later in the reference and are placed here: a repeated
-        instance id fails the merge of the chunk holding its second occurrence
-        (``fbx_dup_resolve``), and a null / non-0/1 label fails the merge of the
-        chunk whose ``_Emitter.add`` flushes its mini-batch (pipeline.py:748-777)
-        -- or the final flush (stage "emit", no batch index)."""
+        kinds surface later in the reference and are placed here (placement.py):
+        a repeated instance id fails the merge of the chunk holding its second
+        occurrence (``fbx_dup_resolve``), and a null / non-0/1 label fails the
+        merge of the chunk whose ``_Emitter.add`` flushes its mini-batch
+        (pipeline.py:748-777) -- or the final flush (stage "emit", no batch
+        index)."""
         key = st["error_key"]
         detail = st["error_detail"]
-        if not prepare:
-            if st.get("dup_seen"):
-                dk, did = self._dup_key()
-                if dk < key:
-                    key, detail = dk, did
-            if st.get("emit_key", ~0 & ((1 << 64) - 1)) != (1 << 64) - 1:
-                ek = st.get("emit_key_resolved")
-                if ek is None:
-                    ek = self._emit_error_key(st["emit_key"])
-                if ek < key:
-                    key, detail = ek, st["emit_detail"]
-        if key == (1 << 64) - 1:
+        if st.get("dup_seen"):
+            dk, did = self._dup_key()
+            if dk < key:
+                key, detail = dk, did
+        lk = st.get("emit_key_resolved") or self._label_key(st)
+        if lk is not None and lk[0] < key:
+            key, detail = lk
+        return key, detail
+
+    def raise_key(self, key: int, detail: int, st: dict | None = None):
+        """Raise the StageError an error key names (nothing for ``NONE``)."""
+        if key == placement.NONE:
             return
         chunk = key >> 32
         stage = STAGE_NAMES.get((key >> 28) & 0xF, "extract")
         layer = (key >> 20) & 0xFF
         rank = (key >> 8) & 0xFFF
         code = ERR_NAMES.get(key & 0xFF, "value")
-        cause = _cause(code, detail, st)
+        cause = _cause(code, detail, st or {})
         if stage == "extract" and layer:
             node = self.prepared.node_names[rank]
             cause = LayerExecutionError(layer, node, cause)
         raise StageError(stage, None if stage in ("prepare", "emit") else chunk, cause)
 
-    def check_run(self, st: dict):
+    def settle_run(self, st: dict) -> dict:
         """End of a run: note whether the id set saw a repeat (its pair array
         then needs clearing), repeat the run if the device arena ran out
         (ArenaRetry), settle the reference arena's PoolExhausted for flagged
-        chunks (fbx_pool_account) and raise the run's first failure."""
+        chunks (fbx_pool_account).  Returns the settled state."""
         self._dup_dirty = bool(st["dup_seen"])
         if st["pool_overflow"]:
             raise ArenaRetry(st["pool_overflow"])
@@ -746,7 +755,11 @@ class Engine:
             self._pool_account()
             st = dict(st, **{k: v for k, v in self._read_state().items()
                              if k in ("error_key", "error_detail")})
-        self._raise_if_error(st)
+        return st
+
+    def check_run(self, st: dict):
+        """``settle_run`` and raise the run's first failure."""
+        self._raise_if_error(self.settle_run(st))
 
     def ring_after_launch(self, stream: int) -> int:
         """Ring runs: the reference arena's demand of the launch just enqueued is
@@ -775,23 +788,28 @@ class Engine:
         self._arena_min = max(getattr(self, "_arena_min", 0), int(need * 1.25) + (1 << 20))
         self._arena_key = None
 
-    def _dup_key(self) -> tuple[int, int]:
-        """(error key, id) of check_unique_ids' failure: the merge of the chunk
-        holding the first row, in row order, whose id occurred before (some id's
-        second occurrence, minimised over ids); the id as the column's signed
-        Int64 value, as the reference's message prints it."""
+    def _dup_row(self) -> tuple[int, int]:
+        """(row, id) of check_unique_ids' failure: the first row, in row order,
+        whose id occurred before (some id's second occurrence, minimised over
+        ids), ``NONE`` without one; the id as the column's signed Int64 value,
+        as the reference's message prints it."""
         out = self.torch.empty(2, dtype=self.torch.int64, device=self.device)
         runtime.dup_resolve(self.idset_w.data_ptr(), self.idset_d.data_ptr(),
                             self._idset_cap + 2, out.data_ptr(), self._stream())
         row, slot = (int(x) for x in out.cpu().numpy().view(np.uint64))
-        if row == (1 << 64) - 1:
-            return (1 << 64) - 1, 0
-        ident = int(self.idset[slot].item()) if slot <= self._idset_cap else 0
-        if slot == self._idset_cap + 1:
-            ident = 0  # id 0 has its own slot (the set stores it as 1)
-        chunk = row // self.ir.chunk
-        key = (chunk << 32) | (codegen.STAGE["merge"] << 28) | codegen.ERR["dup_id"]
-        return key, ident
+        if row == placement.NONE:
+            return row, 0
+        # slot cap holds id 0 (the set stores it as 1)
+        ident = 0 if slot >= self._idset_cap else int(self.idset[slot].item())
+        return row, ident
+
+    def _dup_key(self) -> tuple[int, int]:
+        """(error key, id) of check_unique_ids' failure (the merge of the chunk
+        holding ``_dup_row``'s row)."""
+        row, ident = self._dup_row()
+        if row == placement.NONE:
+            return row, 0
+        return placement.dup_key(row, self.ir.chunk), ident
 
     def _global_incl(self, t0: int, t1: int) -> np.ndarray:
         """Run-global inclusive instance counts of tiles [t0, t1): the look-back
@@ -868,46 +886,42 @@ class Engine:
 
     def _resolve_big_label_error(self, st: dict):
         """Place a label failure from the final (merged) order: the kernel marked
-        bad labels 0xFE (null) / 0xFF (not 0/1) in the emitted label byte."""
-        if st.get("emit_key", (1 << 64) - 1) == (1 << 64) - 1:
+        bad labels 0xFE (null) / 0xFF (not 0/1) in the emitted label byte; a
+        null anywhere in the first bad label's batch wins (emit_minibatch runs
+        before MiniBatch.validate)."""
+        if st.get("emit_null_pos", placement.NONE) == placement.NONE and \
+                st.get("emit_range_pos", placement.NONE) == placement.NONE:
             return
         n, bs = int(st["instances"]), self.ir.chunk
         bad = self.torch.nonzero(self.o_lab[:n] >= 0xFE)
         if not bad.numel():
             return
         p = int(bad[0, 0].item())
-        rng = int(self.o_lab[p].item()) == 0xFF
-        batch, pos = p // bs, p % bs
-        code = codegen.ERR["label_range" if rng else "null_label"]
-        sub = (((1 + rng) & 0xFF) << 20) | ((pos & 0xFFF) << 8) | code
+        batch = p // bs
+        nulls = self.torch.nonzero(self.o_lab[batch * bs:min(n, (batch + 1) * bs)] == 0xFE)
+        lf = (batch, 0, int(nulls[0, 0].item())) if nulls.numel() else (batch, 1, p % bs)
         ends = self._chunk_ends(0, self._run_tiles)
-        hit = np.nonzero(ends >= (batch + 1) * bs)[0]
-        if hit.size == 0:
-            key = (0xFFFFFFFF << 32) | (codegen.STAGE["emit"] << 28) | sub
-        else:
-            key = ((int(hit[0]) + self._run_chunk0) << 32) | (codegen.STAGE["merge"] << 28) | sub
-        st["emit_key_resolved"] = key
+        st["emit_key_resolved"] = (placement.label_key(lf, ends, self._run_chunk0, bs),
+                                   st["emit_range_label"] if lf[1] else 0)
 
     def _merge_big_chunks(self, st: dict):
         self._merge_range(0, int(st["instances"]), 0, int(st["signs"]), 0, self._run_tiles, st)
         self._resolve_big_label_error(st)
         self._check_merges()
 
-    def _emit_error_key(self, ek: int) -> int:
-        """Map a label error at emission position (batch b) to the chunk whose
-        merge flushes batch b: the first chunk whose inclusive instance count
-        reaches (b + 1) * batch_size (look-back status words), else the final
-        flush."""
+    def _label_key(self, st: dict):
+        """(error key, label) of the run's first label failure, or None: the
+        kernel keeps the first null and the first non-0/1 label by emission
+        position; the batch is mapped to the chunk whose merge flushes it
+        (look-back status words: inclusive instance counts per chunk)."""
         bs = self.ir.chunk
-        batch, rng, pos = ek >> 13, (ek >> 12) & 1, ek & 0xFFF
-        code = codegen.ERR["label_range" if rng else "null_label"]
-        sub = (((1 + rng) & 0xFF) << 20) | ((pos & 0xFFF) << 8) | code  # after the dup check
-        incl = self._global_incl(0, self._run_tiles)
-        hit = np.nonzero(incl >= (batch + 1) * bs)[0]
-        if hit.size == 0:
-            return (0xFFFFFFFF << 32) | (codegen.STAGE["emit"] << 28) | sub
-        chunk = int(hit[0]) + self._chunk_minus_tile
-        return (chunk << 32) | (codegen.STAGE["merge"] << 28) | sub
+        lf = placement.label_failure(st.get("emit_null_pos", placement.NONE),
+                                     st.get("emit_range_pos", placement.NONE), bs)
+        if lf is None:
+            return None
+        ends = self._global_incl(0, self._run_tiles)
+        return (placement.label_key(lf, ends, self._chunk_minus_tile, bs),
+                st["emit_range_label"] if lf[1] else 0)
 
     def begin_run(self, rows_hint: int) -> int:
         """Start a run: clear the run-wide instance-id set (check_unique_ids'
@@ -1645,6 +1659,85 @@ def run_pipelined(config: PipelineConfig, collect: bool = False,
         except Exception as exc:  # noqa: BLE001
             raise StageError("prepare", None, exc) from exc
         return run_views(config, views, basic, collect=collect).report
+    return _stream_pipelined(config, slice_rows).report()
+
+
+@dataclass
+class _StreamedRun:
+    """A run_pipelined over a driver file (or a record shard of it), its
+    failures not yet raised (sharded.py folds them across ranks)."""
+    config: PipelineConfig
+    engine: "Engine"
+    state: dict
+    counters: Counters
+    launches: int
+    launch_s: float
+    bytes_h2d: int
+    transfer_s: float
+    stage: dict
+    t0: float
+    read_failure: "StageError | None" = None
+
+    def first_failure(self) -> tuple[int, int]:
+        """(error key, detail) of the run's first failure; a read failure is
+        key (chunk, "read") with detail -1."""
+        key, detail = placement.NONE, 0
+        if self.state is not None:
+            key, detail = self.engine.first_failure(self.state)
+        if self.read_failure is not None:
+            rk = placement.key_of(self.read_failure.batch_index, "read", 0)
+            if rk < key:
+                key, detail = rk, -1
+        return key, detail
+
+    def report(self) -> RunReport:
+        """Raise the run's first failure (single run), else its RunReport."""
+        key, detail = self.first_failure()
+        if self.read_failure is not None and key == placement.key_of(
+                self.read_failure.batch_index, "read", 0):
+            raise self.read_failure
+        self.engine.raise_key(key, detail, self.state)
+        return self.to_report()
+
+    def to_report(self, counters: Counters | None = None, launches: int | None = None,
+                  bytes_h2d: int | None = None) -> RunReport:
+        c = counters or self.counters
+        bs = self.config.batch_size
+        n_launch = self.launches if launches is None else launches
+        pc = self.engine.prepare_counters
+        return RunReport(
+            mode="pipelined", digest=c.digest, batches=math.ceil(c.instances / bs),
+            instances=c.instances, signs=c.signs, launches=n_launch,
+            overhead_us=1e6 * self.launch_s / max(1, n_launch),
+            bytes_h2d=self.bytes_h2d if bytes_h2d is None else bytes_h2d,
+            transfer_seconds=self.transfer_s, intermediate_bytes_written=0,
+            intermediate_files=(), rows_dropped=c.malformed + pc.malformed,
+            rows_filtered=c.filtered + pc.filtered, batch_size=bs, workers=1,
+            wall_seconds=time.perf_counter() - self.t0, stage_seconds=self.stage)
+
+
+def driver_streams(config: PipelineConfig) -> bool:
+    """Whether run_pipelined streams the driver file in slices: chunks of at
+    most one CTA (batch_size <= 1024) and more than one chunk -- else (one
+    chunk: the reference reads, and CRC-checks, the whole body) the run is
+    device-resident."""
+    prep = _prepared(config)
+    drv_cfg = config.view(config.driver)
+    try:
+        dfile = open_view(drv_cfg.path)
+    except Exception as exc:  # noqa: BLE001
+        raise StageError("prepare", None, exc) from exc
+    names = [c for c, _ in dfile.schema]
+    full_read = drv_cfg.columns is None or set(drv_cfg.columns) >= set(names)
+    return not (prep.program.tiles_per_chunk > 1 or
+                (full_read and dfile.row_count <= config.batch_size))
+
+
+def _stream_pipelined(config: PipelineConfig, slice_rows: int = 1 << 19,
+                      rows: tuple[int, int] | None = None) -> _StreamedRun:
+    """run_pipelined's body: prepare, then stream the driver (or its record
+    shard ``rows``, whole chunks) through the engine; failures of the prepare
+    stage raise here, the run's own are left in the result's state."""
     from .stream import FileRun, _ReadFailure
     t0 = time.perf_counter()
     stage: dict[str, float] = {}
@@ -1660,11 +1753,13 @@ def run_pipelined(config: PipelineConfig, collect: bool = False,
     names = [c for c, _ in dfile.schema]
     full_read = drv_cfg.columns is None or set(drv_cfg.columns) >= set(names)
     streamed = not (prep.program.tiles_per_chunk > 1 or (full_read and n <= bs))
+    if rows is not None and not streamed:
+        raise ValueError("a record shard streams its rows: batch_size <= 1024, more than one chunk")
     fr = None
     if streamed:
         # the driver's first slices are read while the side views are prepared
         # (measured: faster than reading the side / basic files first)
-        fr = FileRun(prep, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows)
+        fr = FileRun(prep, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows, rows=rows)
         fr.start()
     try:
         dvs = {v.name: DeviceView.from_file(v.path, v.columns, defer_crc=streamed)
@@ -1724,23 +1819,29 @@ def run_pipelined(config: PipelineConfig, collect: bool = False,
         stage["extract"] = time.perf_counter() - t2
         transfer_s = stage["read"]
         c = b.counters
+        st = None  # finish() raised the run's failures
+        read_failure = None
     else:
         while True:
             if fr is None:  # a repeat after the device arena grew
-                fr = FileRun(prep, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows)
-            eng.reserve(n, fr.slice_rows, ring=True)
-            launches += eng.begin_run(n)
+                fr = FileRun(prep, drv_cfg.path, drv_cfg.columns, slice_rows=slice_rows,
+                             rows=rows)
+            eng.reserve(fr.n, fr.slice_rows, ring=True)
+            launches += eng.begin_run(fr.n)
+            read_failure = None
             try:
                 t = fr.run(eng)
             except _ReadFailure as exc:
                 settle_prepare()
-                raise StageError("read", (exc.index * fr.slice_rows) // bs, exc.cause) from exc
+                read_failure = StageError("read", fr.bounds[exc.index][0] // bs, exc.cause)
+                read_failure.__cause__ = exc.cause
+                t = exc.timings
             launches += t["launches"]
             launch_s += t["launch_s"]
-            settle_prepare()
-            st = eng._read_state()
+            if read_failure is None:
+                settle_prepare()
             try:
-                eng.check_run(st)
+                st = eng.settle_run(eng._read_state())
                 break
             except ArenaRetry as exc:
                 eng.grow_arena(exc.need)
@@ -1753,14 +1854,8 @@ def run_pipelined(config: PipelineConfig, collect: bool = False,
         c = Counters(st["digest"], st["instances"], st["signs"], st["malformed"],
                      st["filtered"], st["joined"], t["slices"])
     stage["stream"] = time.perf_counter() - t1
-    return RunReport(
-        mode="pipelined", digest=c.digest, batches=math.ceil(c.instances / bs),
-        instances=c.instances, signs=c.signs, launches=launches,
-        overhead_us=1e6 * launch_s / max(1, launches), bytes_h2d=bytes_h2d,
-        transfer_seconds=transfer_s, intermediate_bytes_written=0, intermediate_files=(),
-        rows_dropped=c.malformed + eng.prepare_counters.malformed,
-        rows_filtered=c.filtered + eng.prepare_counters.filtered,
-        batch_size=bs, workers=1, wall_seconds=time.perf_counter() - t0, stage_seconds=stage)
+    return _StreamedRun(config, eng, st, c, launches, launch_s, bytes_h2d, transfer_s, stage, t0,
+                        read_failure)
 
 
 def run_pipeline(config: PipelineConfig, mode: str | None = None) -> RunReport:

@@ -22,9 +22,10 @@ _lock = threading.Lock()
 _lib = None
 
 FBX_MAX_PARAM_SLOTS = 384
-STATE_FIELDS = ("tile_ticket", "pool_head", "pool_overflow", "error_key", "error_detail",
+STATE_FIELDS = ("error_key", "error_detail", "emit_range_pos", "emit_range_label",
+                "emit_null_pos", "pool_flagged", "tile_ticket", "pool_head", "pool_overflow",
                 "digest", "instances", "signs", "malformed", "filtered", "joined", "side_rows",
-                "dup_seen", "emit_key", "emit_detail", "pool_flagged")
+                "dup_seen", "pad")
 STATE_BYTES = 8 * len(STATE_FIELDS)
 
 EXPORTS = ("fbx_version", "fbx_error_message", "fbx_compile", "fbx_free", "fbx_program_load",
@@ -36,7 +37,7 @@ EXPORTS = ("fbx_version", "fbx_error_message", "fbx_compile", "fbx_free", "fbx_p
            "fbx_pool_account", "fbx_memset_async", "fbx_read_spans",
            "fbx_merge_subtiles", "fbx_select_rows", "fbx_take", "fbx_pack_nulls",
            "fbx_sort_keys", "fbx_join_count", "fbx_join_fill", "fbx_first_repeat",
-           "fbx_unpack_nulls", "fbx_spans")
+           "fbx_unpack_nulls", "fbx_spans", "fbx_idset_entries", "fbx_seen_before")
 
 
 class FbxError(RuntimeError):
@@ -97,6 +98,8 @@ def lib() -> ctypes.CDLL:
             L.fbx_first_repeat.argtypes = [vp, vp, ull, vp, vp]
             L.fbx_unpack_nulls.argtypes = [vp, ull, vp, vp]
             L.fbx_spans.argtypes = [vp, vp, ull, vp, vp, vp]
+            L.fbx_idset_entries.argtypes = [vp, vp, vp, ull, vp, vp, vp, vp]
+            L.fbx_seen_before.argtypes = [vp, vp, ull, vp, ull, vp, vp]
             L.fbx_crc32_scratch_words.argtypes = [ctypes.c_ulonglong]
             L.fbx_crc32_scratch_words.restype = ctypes.c_ulonglong
             for name in EXPORTS:

@@ -37,17 +37,22 @@ class FileRun:
     PARTS = ("nulls", "offsets", "data")
 
     def __init__(self, prepared, path, columns=None, device="cuda", slice_rows: int = 1 << 19,
-                 nbuf: int = 3, threads: int | None = None):
+                 nbuf: int = 3, threads: int | None = None, rows: tuple[int, int] | None = None):
         import torch
         self.torch = torch
         self.vf = vf = open_view(path)
-        self.n = n = vf.row_count
         chunk = prepared.ir.chunk
+        # rows: a record shard [lo, hi) of the log (whole chunks; sharded.py)
+        r0, n = (0, vf.row_count) if rows is None else (rows[0], min(rows[1], vf.row_count))
+        if (r0 % chunk and r0 != n) or not 0 <= r0 <= n:
+            raise ValueError("FileRun: a row range starts at a chunk boundary inside the log")
+        self.row_lo, self.row_hi = r0, n
+        self.n = n - r0
         if prepared.program.tiles_per_chunk > 1:
             raise ValueError("FileRun: batch_size > 1024 runs device-resident (chunk merge)")
         limit = (1 << 24) // chunk * chunk  # Engine.LAUNCH_ROWS_MAX
         self.slice_rows = S = min(max(chunk, slice_rows // chunk * chunk), max(chunk, limit))
-        self.bounds = [(lo, min(lo + S, n)) for lo in range(0, n, S)]
+        self.bounds = [(lo, min(lo + S, n)) for lo in range(r0, n, S)]
         slots = prepared.program.slots
         kinds = dict(vf.schema)
         self.cols = [c for c, _ in vf.schema
@@ -56,7 +61,7 @@ class FileRun:
         self.threads = runtime.host_threads() if threads is None else threads
         # boundary offsets of every var-length column at every slice edge: the data
         # span of a slice is [off[lo], off[hi]) (one 4-byte pread per edge)
-        edges = [lo for lo, _ in self.bounds] + [n]
+        edges = [lo for lo, _ in self.bounds] + [n]  # n: the range's end
         self.edge_off: dict[str, list[int]] = {}
         with open(vf.path, "rb") as fh:
             fd = fh.fileno()
@@ -178,6 +183,7 @@ class FileRun:
         launch_s = 0.0
         launches = 0
         tiles_before = 0
+        done = 0
         try:
             for k, (lo, hi) in enumerate(self.bounds):
                 self.ready[k].wait()
@@ -198,17 +204,28 @@ class FileRun:
                     self.comp_done[k].record(self.s_comp)
                 self.recorded[k].set()
                 tiles_before += tiles
+                done = k + 1
+        except _ReadFailure as exc:
+            # the slices before the failed one ran: their failures may come first
+            self.stop()
+            exc.timings = self._timings(cur, done, launches, launch_s)
+            raise
         finally:
             self.stop()
+        return self._timings(cur, done, launches, launch_s)
+
+    def _timings(self, cur, done: int, launches: int, launch_s: float) -> dict:
         self.s_comp.synchronize()
         self.s_h2d.synchronize()
         cur.wait_stream(self.s_comp)
-        ev = zip(self.h2d_start, self.h2d_done)
+        ev = list(zip(self.h2d_start, self.h2d_done))[:done]
+        comp = list(zip(self.comp_start, self.comp_done))[:done]
         return {"launches": launches, "launch_s": launch_s, "read_s": self.read_s,
                 "h2d_s": sum(a.elapsed_time(b) for a, b in ev) / 1e3,
-                "kernel_s": sum(a.elapsed_time(b)
-                                for a, b in zip(self.comp_start, self.comp_done)) / 1e3,
-                "h2d_bytes": self.h2d_bytes, "slices": len(self.bounds)}
+                "kernel_s": sum(a.elapsed_time(b) for a, b in comp) / 1e3,
+                "h2d_bytes": sum(sum(b - a for _, _, a, b, _ in self.layout[k])
+                                 for k in range(done)),
+                "slices": done}
 
 
 class _ReadFailure(Exception):

@@ -1,0 +1,128 @@
+"""GPU: one log record-sharded over G ranks (sharded.py) gives the single run's
+result -- the reference goldens' digest and counters -- and raises the single
+run's first failure (stage, chunk, cause, message), with repeated ids and label
+failures straddling the rank boundaries.  The G shards run one after another on
+this device through the same fold and wire format the torchrun path uses
+(``run_shards_local``)."""
+
+from __future__ import annotations
+
+import pytest
+
+import featurebox_oracle as O
+from conftest import corpus, golden_run
+from test_gpu_edge import PLACEMENT, _chain, _config, _set_ids, _set_labels, _views, _write_views
+
+pytestmark = pytest.mark.gpu
+
+OPS = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+
+
+def _cfg(dag, d, batch_size=512):
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.workloads import workload_config
+    return config_from_dict(workload_config(dag, batch_size=batch_size), d)
+
+
+@pytest.mark.parametrize("dag", ["default", "sign_heavy", "lookup_heavy"])
+@pytest.mark.parametrize("world", [1, 2, 3, 7])
+def test_sharded_run_matches_goldens(dag, world, goldens):
+    from paper_2210_07768_b200.sharded import run_shards_local
+    _, d = corpus(20000, 2000, 7)
+    rep = run_shards_local(_cfg(dag, d), world, slice_rows=4096)
+    g = golden_run(goldens, 20000, 7, dag)
+    assert f"0x{rep.digest:016x}" == g["digest"]
+    assert (rep.instances, rep.signs, rep.batches) == (g["instances"], g["signs"], g["batches"])
+    assert (rep.rows_dropped, rep.rows_filtered) == (g["rows_dropped"], g["rows_filtered"])
+
+
+def _oracle_err(raw, drv, prof, bas, tmp):
+    tables, sizes = O.load_tables(raw.get("tables", {}), tmp)
+    try:
+        O.run_pipelined(raw, {"ev": drv, "pr": prof}, bas, tables, sizes)
+    except O.OracleError as e:
+        return e
+    return None
+
+
+def _sharded(raw, tmp, world, slice_rows):
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.sharded import run_shards_local
+    try:
+        return run_shards_local(config_from_dict(raw, tmp), world, slice_rows=slice_rows), None
+    except Exception as e:  # noqa: BLE001
+        return None, e
+
+
+BOUNDARY = {  # rank boundary of world 2 / bs 100: row 1000 (rows that reach the merge)
+    "dup_across_boundary": _set_ids([(1003, 998)]),
+    "dup_of_id_zero": lambda d, p, b: _zero_ids(d, p, b, (4, 1502)),
+    "range_then_null_one_batch": _chain(_set_labels([998], 7), _set_labels([1006], None)),
+    "null_then_range": _chain(_set_labels([1006], 7), _set_labels([998], None)),
+    "range_only_near_boundary": _set_labels([999], 2),
+}
+
+
+def _zero_ids(drv, prof, bas, rows):
+    from paper_2210_07768_b200.columns import ColumnImage, Kind
+    ids = drv.columns["instance_id"].to_pylist()
+    for r in rows:
+        ids[r] = 0
+    drv.columns["instance_id"] = ColumnImage.from_values(Kind.INT64, ids)
+    return drv, prof, bas
+
+
+@pytest.mark.parametrize("case", sorted(PLACEMENT) + sorted(BOUNDARY))
+@pytest.mark.parametrize("world,batch_size", [(2, 100), (3, 512), (4, 64), (5, 100)])
+def test_sharded_failure_is_the_single_runs(case, world, batch_size, tmp_path):
+    mut = PLACEMENT.get(case) or BOUNDARY[case]
+    drv, prof, bas = mut(*_views(2000, 5))
+    _write_views(tmp_path, drv, prof, bas)
+    raw = _config(batch_size, OPS, {"c": 3}, filt="age != -12345")
+    ref_err = _oracle_err(raw, drv, prof, bas, tmp_path)
+    _, got_err = _sharded(raw, tmp_path, world, 2 * batch_size)
+    assert ref_err is not None, "the mutation does not fail the reference"
+    assert got_err is not None, "the sharded run did not fail"
+    assert (got_err.stage, got_err.batch_index) == (ref_err.stage, ref_err.chunk)
+    assert type(got_err.__cause__).__name__ == type(ref_err.cause).__name__
+    assert str(got_err.__cause__) == str(ref_err.cause)
+
+
+@pytest.mark.parametrize("case", ["range_then_null_one_batch", "dup_of_id_zero"])
+@pytest.mark.parametrize("batch_size", [100, 512, 1500])
+def test_single_run_failure_cause(case, batch_size, tmp_path):
+    """The single-GPU run: a null label wins over an earlier non-0/1 label of
+    the same batch (also from the merged order of batch_size > 1024), and a
+    repeated id 0 is reported as 0 -- same cause and message as the reference."""
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.engine import run_pipelined
+    drv, prof, bas = BOUNDARY[case](*_views(2000, 5))
+    _write_views(tmp_path, drv, prof, bas)
+    raw = _config(batch_size, OPS, {"c": 3}, filt="age != -12345")
+    ref_err = _oracle_err(raw, drv, prof, bas, tmp_path)
+    with pytest.raises(Exception) as ei:
+        run_pipelined(config_from_dict(raw, tmp_path))
+    got = ei.value
+    assert (got.stage, got.batch_index) == (ref_err.stage, ref_err.chunk)
+    assert type(got.__cause__).__name__ == type(ref_err.cause).__name__
+    assert str(got.__cause__) == str(ref_err.cause)
+
+
+@pytest.mark.parametrize("rows,world", [(600, 4), (1, 3), (0, 2), (1024, 2)])
+def test_sharded_more_ranks_than_chunks(rows, world, tmp_path):
+    """Ranks left without chunks contribute nothing; the result is the single run's."""
+    drv, prof, bas = _views(max(rows, 1), 3)
+    if rows == 0:
+        drv = drv.slice(0, 0)
+    _write_views(tmp_path, drv, prof, bas)
+    raw = _config(512, OPS, {"c": 3}, filt="age != -12345")
+    tables, sizes = O.load_tables({}, tmp_path)
+    try:
+        ref = O.run_pipelined(raw, {"ev": drv, "pr": prof}, bas, tables, sizes)
+    except O.OracleError as e:
+        _, got_err = _sharded(raw, tmp_path, world, 512)
+        assert got_err is not None and got_err.stage == e.stage
+        return
+    got, got_err = _sharded(raw, tmp_path, world, 512)
+    assert got_err is None, got_err  # one chunk: the whole log on every rank
+    assert (got.digest, got.instances, got.signs) == (ref.digest, ref.instances, ref.signs)
