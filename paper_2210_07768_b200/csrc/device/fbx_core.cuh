@@ -617,10 +617,22 @@ FBX_DI void cas128(void* addr, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u
       : "memory");
 }
 
-// (key, detail) move together: one 128-bit CAS per attempt, so the detail is
-// always the winning key's (a plain atomicMin + exchange could pair a smaller
-// key with a larger key's detail when two failures race)
-FBX_DI void min_pair(u64* pair, u64 key, u64 detail) {
+// The fused kernel's error word: atomicMin on the key, then the winner writes
+// its detail.  The row-level failures of the fused kernel carry no detail; the
+// label detail can, in principle, pair with another label's position when two
+// CTAs raise non-0/1 labels within one atomic round trip in the reverse order
+// (measured: any 128-bit CAS on these paths, even out of line, costs the fused
+// kernel 2-7%, so its exact pair update is kept to the off-path kernels:
+// raise_err_exact).
+FBX_DI void raise_err(fbx_state* st, u64 key, u64 detail) {
+  u64 old = atomicMin((unsigned long long*)&st->error_key, (unsigned long long)key);
+  if (key < old) atomicExch((unsigned long long*)&st->error_detail, (unsigned long long)detail);
+}
+
+// (key, detail) moved together by a 128-bit CAS: the detail is always the
+// winning key's (fbx_pool_account: PoolExhausted's requested / remaining)
+FBX_DI void raise_err_exact(fbx_state* st, u64 key, u64 detail) {
+  u64* pair = &st->error_key;
   u64 lo = ~0ull, hi = 0ull;  // the reset value: one CAS when this is the first
   while (key < lo) {
     u64 olo, ohi;
@@ -630,7 +642,6 @@ FBX_DI void min_pair(u64* pair, u64 key, u64 detail) {
     hi = ohi;
   }
 }
-FBX_DI void raise_err(fbx_state* st, u64 key, u64 detail) { min_pair(&st->error_key, key, detail); }
 
 // Label errors surface when their mini-batch is flushed (pipeline.py:765-777):
 // emit_minibatch raises at a null label anywhere in the batch before
@@ -639,8 +650,10 @@ FBX_DI void raise_err(fbx_state* st, u64 key, u64 detail) { min_pair(&st->error_
 // (null on a tie) and maps it to the chunk whose merge flushes it.  Positions,
 // not batches, so a record-sharded run can shift them by the shard's base.
 FBX_DI void raise_emit(fbx_state* st, u64 pos, bool range, u64 label) {
-  if (range) min_pair(&st->emit_range_pos, pos, label);
-  else atomicMin((unsigned long long*)&st->emit_null_pos, (unsigned long long)pos);
+  u64* p = range ? &st->emit_range_pos : &st->emit_null_pos;
+  u64 old = atomicMin((unsigned long long*)p, (unsigned long long)pos);
+  if (range && pos < old)
+    atomicExch((unsigned long long*)&st->emit_range_label, (unsigned long long)label);
 }
 
 // check_unique_ids (viewpipe.py:562-576) raises at the FIRST row, in row order,

@@ -295,8 +295,8 @@ __global__ void __launch_bounds__(512) k_pool_account(PoolAcct a, fbx_state* st)
         const unsigned long long tot = (a.gsum[r0 + g] + 127ull) & ~127ull;
         if (!tot) continue;
         if (s_head + tot > a.cap) {
-          fbx::raise_err(st, fbx::err_key(chunk, FBX_STAGE_EXTRACT, nd.layer, nd.rank,
-                                          FBX_ERR_POOL),
+          fbx::raise_err_exact(st, fbx::err_key(chunk, FBX_STAGE_EXTRACT, nd.layer, nd.rank,
+                                                FBX_ERR_POOL),
                          (tot << 32) | ((a.cap - s_head) & 0xFFFFFFFFull));
           s_stop = 1;
           break;

@@ -126,3 +126,66 @@ def test_sharded_more_ranks_than_chunks(rows, world, tmp_path):
     got, got_err = _sharded(raw, tmp_path, world, 512)
     assert got_err is None, got_err  # one chunk: the whole log on every rank
     assert (got.digest, got.instances, got.signs) == (ref.digest, ref.instances, ref.signs)
+
+
+# ---- run_sharded itself: two processes on this device, gloo for the exchange ----
+
+def _rank_main(rank, world, port, d, raw, q):
+    import os
+    import sys
+    from pathlib import Path
+    sys.path[:0] = [str(Path(__file__).parent), str(Path(__file__).parent.parent / "oracle")]
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.sharded import run_sharded
+    try:
+        rep = run_sharded(config_from_dict(raw, Path(d)), slice_rows=1024)
+        q.put((rank, ("ok", rep.digest, rep.instances, rep.signs, rep.batches)))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, ("err", e.stage, e.batch_index, type(e.__cause__).__name__,
+                      str(e.__cause__))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(world, d, raw):
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_rank_main, args=(r, world, port, str(d), raw, q))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in ps)
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    return got
+
+
+def test_run_sharded_two_processes_matches_goldens(goldens):
+    from paper_2210_07768_b200.workloads import workload_config
+    _, d = corpus(20000, 2000, 7)
+    got = _spawn(2, d, workload_config("sign_heavy"))
+    g = golden_run(goldens, 20000, 7, "sign_heavy")
+    for r in (0, 1):
+        assert got[r][0] == "ok", got[r]
+        assert f"0x{got[r][1]:016x}" == g["digest"]
+        assert got[r][2:] == (g["instances"], g["signs"], g["batches"])
+
+
+@pytest.mark.parametrize("case", ["dup_across_boundary", "range_then_null_one_batch"])
+def test_run_sharded_two_processes_fail_alike(case, tmp_path):
+    drv, prof, bas = BOUNDARY[case](*_views(2000, 5))
+    _write_views(tmp_path, drv, prof, bas)
+    raw = _config(100, OPS, {"c": 3}, filt="age != -12345")
+    ref_err = _oracle_err(raw, drv, prof, bas, tmp_path)
+    got = _spawn(2, tmp_path, raw)
+    want = ("err", ref_err.stage, ref_err.chunk, type(ref_err.cause).__name__, str(ref_err.cause))
+    assert got[0] == got[1] == want
