@@ -126,7 +126,7 @@ int fbx_gather_strings(const unsigned long long* d_ptrs, const unsigned int* d_l
  * pipeline.py:1071): the row of an instance id's SECOND occurrence in row
  * order, minimised over ids (its chunk is row / batch_size).  d_winner_row[i] is
  * the row that claimed id-set slot i, d_later_rows[2i], [2i+1] the two smallest
- * rows (+1, 0 = none) that found the id already present.  Writes the answer row
+ * rows (stored as ~row, 0 = none) that found the id already present.  Writes the answer row
  * to d_out[0] and its slot to d_out[1] (~0 when no id repeats). */
 int fbx_dup_resolve(const unsigned long long* d_winner_row,
                     const unsigned long long* d_later_rows, unsigned long long n_slots,
@@ -203,7 +203,7 @@ int fbx_first_repeat(const unsigned long long* d_skey, const unsigned* d_srow,
 /* check_unique_ids across the record shards of one log (sharded.py).
  * fbx_idset_entries: every id the engine's run-wide id set holds (slots
  * [0, cap) keyed by the id, slot cap = id 0) with the first row holding it --
- * the smaller of the slot's winner row and its smallest later row (+1 coded);
+ * the smaller of the slot's winner row and its smallest later row (~row coded);
  * *d_count = how many (order unspecified).  Buffers: cap + 1 entries. */
 int fbx_idset_entries(const unsigned long long* d_set, const unsigned long long* d_win_rows,
                       const unsigned long long* d_later_rows, unsigned long long cap,

@@ -660,23 +660,17 @@ FBX_DI void raise_emit(fbx_state* st, u64 pos, bool range, u64 label) {
 // whose id occurred before: the row of some id's SECOND occurrence, minimised
 // over ids.  The id-set winner records its row with a plain store; a thread that
 // finds its id already present (rare) folds its row into the slot's two smallest
-// "later" rows (+1, 0 = none; a 128-bit CAS keeps the pair consistent) and flags
-// the run; fbx_dup_resolve takes the second smallest of {winner, later rows} per
-// slot and the minimum over slots after the run.
+// "later" rows and flags the run; fbx_dup_resolve takes the second smallest of
+// {winner, later rows} per slot and the minimum over slots after the run.
+// The pair holds ~row (0 = none), so the two smallest rows are the two largest
+// words: one atomicMax keeps the smallest, and whatever it displaces or rejects
+// -- every row but the smallest, at some point -- goes through a second
+// atomicMax into the runner-up (64-bit atomics only: a 128-bit CAS loop here
+// measured slower for the whole fused kernel).
 FBX_DI void dup_note(fbx_state* st, u64* pair, u64 row) {
-  const u64 r = row + 1u;
-  u64 lo = ((volatile u64*)pair)[0], hi = ((volatile u64*)pair)[1];
-  while (true) {
-    u64 nlo, nhi;
-    if (lo == 0u || r < lo) { nlo = r; nhi = lo; }
-    else if (hi == 0u || r < hi) { nlo = lo; nhi = r; }
-    else break;
-    u64 olo, ohi;
-    cas128(pair, lo, hi, nlo, nhi, &olo, &ohi);
-    if (olo == lo && ohi == hi) break;
-    lo = olo;
-    hi = ohi;
-  }
+  const u64 x = ~row;
+  const u64 old = atomicMax((unsigned long long*)&pair[0], (unsigned long long)x);
+  if (old != 0ull) atomicMax((unsigned long long*)&pair[1], (unsigned long long)(old < x ? old : x));
   atomicExch((unsigned long long*)&st->dup_seen, 1ull);
 }
 

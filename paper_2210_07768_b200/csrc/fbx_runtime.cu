@@ -132,9 +132,9 @@ __global__ void k_state_snapshot(const unsigned long long* st, volatile unsigned
 __device__ __forceinline__ unsigned long long dup_second(const unsigned long long* w,
                                                          const unsigned long long* later,
                                                          unsigned long long i) {
-  const unsigned long long x = later[2 * i], y = later[2 * i + 1];
+  const unsigned long long x = later[2 * i], y = later[2 * i + 1];  // ~row, 0 = none
   if (x == 0ull) return ~0ull;
-  const unsigned long long a = w[i], b = x - 1ull, c = y ? y - 1ull : ~0ull;
+  const unsigned long long a = w[i], b = ~x, c = y ? ~y : ~0ull;
   return max(min(a, b), min(max(a, b), c));
 }
 __global__ void k_dup_resolve(const unsigned long long* w, const unsigned long long* later,

@@ -155,15 +155,15 @@ __global__ void k_first_repeat(const ull* skey, const unsigned* srow, ull n, ull
 
 // the engine's run-wide id set (codegen ids tail): slots [0, cap) keyed by the
 // id, slot cap = id 0 (stored as 1); the winner's row per slot and the two
-// smallest later rows (+1, 0 = none)
+// smallest later rows (as ~row, 0 = none)
 __global__ void k_idset_entries(const ull* set, const ull* win, const ull* later, ull cap,
                                 ull* ids, ull* rows, ull* count) {
   for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i <= cap; i += (ull)gridDim.x * blockDim.x) {
     const ull v = set[i];
     if (v == 0ull) continue;
     ull r = win[i];
-    const ull x = later[2 * i];
-    if (x && x - 1ull < r) r = x - 1ull;
+    const ull x = later[2 * i];  // ~(smallest later row), 0 = none
+    if (x && ~x < r) r = ~x;
     const ull k = atomicAdd(count, 1ull);
     ids[k] = i == cap ? 0ull : v;
     rows[k] = r;
