@@ -13,11 +13,10 @@ reduction, so it is folded after the gather).
 Two ways to split a workload (``bench.py`` uses both):
 
 * one log cut into contiguous chunk ranges (``shard_rows``): the ranks' CSRs
-  concatenate to the single-GPU emission order.  Limitation: the reference's
-  instance-id uniqueness check (pipeline.py:1071-1072) is applied per rank --
-  a duplicate id whose two occurrences land on different ranks is not
-  detected, and a bad-label failure is placed against the rank's own batch
-  boundaries.  Use it for logs whose ids are unique by construction;
+  concatenate to the single-GPU emission order.  ``sharded.run_sharded`` runs it
+  with the single run's result AND failures: the instance-id uniqueness check
+  (pipeline.py:1071-1072) across ranks and the mini-batch boundaries are
+  exchanged after the shards finish (sharded.py);
 * independent logs (SURVEY.md §8 d: C5's 1M-record shards, each its own
   reference pipeline with ids restarting at 0): shard k goes to rank k mod G
   (``assign_shards``), every shard is checked against the reference's digest
