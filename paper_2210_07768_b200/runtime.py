@@ -125,6 +125,11 @@ def compile_source(source: str, name: str = "plan.cu", options: tuple[str, ...] 
     """NVRTC -> sm_100a cubin (host-only).  Cached per process and on disk."""
     opts = ("-arch=sm_100a", "-std=c++17", "-lineinfo", "-diag-suppress=177,550", *options,
             *os.environ.get("FBX_NVRTC_OPTS", "").split())  # A/B experiments only
+    patch = os.environ.get("FBX_SOURCE_PATCH")
+    if patch:  # A/B experiments only: a script's patch(source) -> source
+        ns: dict = {}
+        exec(compile(Path(patch).read_text(), patch, "exec"), ns)
+        source = ns["patch"](source)
     dump = os.environ.get("FBX_DUMP_SOURCE")
     if dump:  # profiling aid: keep the generated plan so ncu can import it by name
         Path(dump).write_text(source)
