@@ -130,14 +130,16 @@ def test_sharded_more_ranks_than_chunks(rows, world, tmp_path):
 
 # ---- run_sharded itself: two processes on this device, gloo for the exchange ----
 
-def _rank_main(rank, world, port, d, raw, q):
+def _rank_main(rank, world, port, d, raw, q, backend="gloo"):
     import os
     import sys
     from pathlib import Path
     sys.path[:0] = [str(Path(__file__).parent), str(Path(__file__).parent.parent / "oracle")]
+    import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
     from paper_2210_07768_b200.config import config_from_dict
     from paper_2210_07768_b200.sharded import run_sharded
     try:
@@ -150,7 +152,7 @@ def _rank_main(rank, world, port, d, raw, q):
         dist.destroy_process_group()
 
 
-def _spawn(world, d, raw):
+def _spawn(world, d, raw, backend="gloo"):
     import multiprocessing as mp
     import socket
     with socket.socket() as s:
@@ -158,7 +160,7 @@ def _spawn(world, d, raw):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_rank_main, args=(r, world, port, str(d), raw, q))
+    ps = [ctx.Process(target=_rank_main, args=(r, world, port, str(d), raw, q, backend))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -189,3 +191,14 @@ def test_run_sharded_two_processes_fail_alike(case, tmp_path):
     got = _spawn(2, tmp_path, raw)
     want = ("err", ref_err.stage, ref_err.chunk, type(ref_err.cause).__name__, str(ref_err.cause))
     assert got[0] == got[1] == want
+
+
+def test_run_sharded_nccl_one_rank(goldens):
+    """The NCCL exchange path (device tensors) with the one GPU of this box."""
+    from paper_2210_07768_b200.workloads import workload_config
+    _, d = corpus(20000, 2000, 7)
+    got = _spawn(1, d, workload_config("lookup_heavy"), backend="nccl")
+    g = golden_run(goldens, 20000, 7, "lookup_heavy")
+    assert got[0][0] == "ok", got[0]
+    assert f"0x{got[0][1]:016x}" == g["digest"]
+    assert got[0][2:] == (g["instances"], g["signs"], g["batches"])
