@@ -431,7 +431,9 @@ def main():
     hbm_floor = ab["total"] / (peak * 1e9)
     int_floor = sum(int_ceiling_s(args.dag, corp.driver.row_count, cc, clk_mhz)
                     for (corp, _, _, _), cc in zip(shards, results))
-    plan_sha = hashlib.sha256(eng.prepared.cubin).hexdigest()[:16]
+    # the generated plan's text: the same under ncu (FBX_DUMP_SOURCE renames the NVRTC
+    # source, and -lineinfo carries the name into the cubin) and in a plain run
+    plan_sha = hashlib.sha256(eng.prepared.program.source.encode()).hexdigest()[:16]
     roofline = {"bound": "hbm" if hbm_floor >= int_floor else "int",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
@@ -449,7 +451,7 @@ def main():
     if prof.exists():
         try:
             t = json.loads(prof.read_text()).get(args.dag)
-            if t and t.get("plan_sha") == plan_sha:  # same cubin, measured by ncu
+            if t and t.get("plan_sha") == plan_sha:  # same plan, measured by ncu
                 roofline["traffic"] = t["dram_bytes"]
                 roofline["traffic_source"] = t.get("source")
         except (OSError, ValueError):

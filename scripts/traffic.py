@@ -3,7 +3,7 @@
     python scripts/traffic.py gpurun_out/<name>.ncu-rep gpurun_out/<name>.log
 
 Reads the ncu --set full capture (scripts/profile_kernel.sh) and the bench JSON
-line of the same command (its ``roofline.plan_sha`` = sha256 of the plan cubin)
+line of the same command (its ``roofline.plan_sha`` = sha256 of the generated plan source)
 and writes profiles/traffic.json[<dag>]; bench.py uses the entry only while the
 plan it compiles has that same hash.
 """
