@@ -53,6 +53,15 @@ class FileRun:
         limit = (1 << 24) // chunk * chunk  # Engine.LAUNCH_ROWS_MAX
         self.slice_rows = S = min(max(chunk, slice_rows // chunk * chunk), max(chunk, limit))
         self.bounds = [(lo, min(lo + S, n)) for lo in range(r0, n, S)]
+        # a short last slice: once the reads are done (the call is bound by the page
+        # cache -> pinned copy), only its H2D + kernel remain (measured: 5.16 -> 4.89
+        # ms per 1M-record run_pipelined; FBX_TAPER=0 turns it off)
+        tail = max(chunk, (S // 4) // chunk * chunk)
+        if os.environ.get("FBX_TAPER", "1") != "0" and len(self.bounds) >= 2:
+            lo, hi = self.bounds[-1]
+            cut = (hi - tail) // chunk * chunk
+            if cut - lo >= tail:
+                self.bounds[-1:] = [(lo, cut), (cut, hi)]
         slots = prepared.program.slots
         kinds = dict(vf.schema)
         self.cols = [c for c, _ in vf.schema
