@@ -202,3 +202,33 @@ def test_run_sharded_nccl_one_rank(goldens):
     assert got[0][0] == "ok", got[0]
     assert f"0x{got[0][1]:016x}" == g["digest"]
     assert got[0][2:] == (g["instances"], g["signs"], g["batches"])
+
+
+@pytest.mark.parametrize("pool,lpg,batch_size", [(128, 256, 512), (1024, 7, 64), (4096, 256, 512),
+                                                 (3200, 7, 64)])
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_pool_bytes(pool, lpg, batch_size, world, tmp_path):
+    """The reference arena's PoolExhausted (requested, remaining) at the single
+    run's (chunk, layer, node) when the failing chunk sits on any rank."""
+    from test_gpu_edge import POOL_FEATS, POOL_OPS
+    drv, prof, bas = _views(2000, 9)
+    _write_views(tmp_path, drv, prof, bas)
+    raw = _config(batch_size, POOL_OPS, POOL_FEATS, filt="age != -12345")
+    raw["device"] = {"budget_bytes": 65536, "pool_bytes": pool, "lanes_per_group": lpg}
+    tables, sizes = O.load_tables({}, tmp_path)
+    try:
+        ref, ref_err = O.run_pipelined(raw, {"ev": drv, "pr": prof}, bas, tables, sizes), None
+    except O.OracleError as e:
+        ref, ref_err = None, e
+    got, got_err = _sharded(raw, tmp_path, world, 2 * batch_size)
+    if ref_err is None:
+        assert got_err is None, got_err
+        assert (got.digest, got.instances, got.signs) == (ref.digest, ref.instances, ref.signs)
+        return
+    assert got_err is not None
+    assert (got_err.stage, got_err.batch_index) == (ref_err.stage, ref_err.chunk)
+    lay = got_err.__cause__
+    assert (lay.layer_index, lay.node) == (ref_err.layer, ref_err.node)
+    if type(ref_err.cause).__name__ == "PoolExhausted":
+        assert (lay.__cause__.requested, lay.__cause__.remaining) == \
+            (ref_err.cause.requested, ref_err.cause.remaining)
