@@ -1,6 +1,7 @@
 """Command-line front end, the reference's (cli.py:1-290) on the B200 engine.
 
     python -m paper_2210_07768_b200.cli run --config pipeline.json [--mode staged --staging dir]
+    torchrun --nproc-per-node G -m paper_2210_07768_b200.cli run --config pipeline.json --sharded
     python -m paper_2210_07768_b200.cli plan --config pipeline.json
     python -m paper_2210_07768_b200.cli gen-corpus --out dir [--instances N ...]
     python -m paper_2210_07768_b200.cli bench-launch [--counts 1,10,100]
@@ -51,13 +52,42 @@ def cmd_run(args) -> int:
             overrides["staging_dir"] = Path(args.staging)
         if overrides:
             config = replace(config, **overrides)
-        report = run_pipeline(config)
+        if args.sharded:
+            report = _run_sharded(config)
+            if report is None:  # ranks other than 0 print nothing
+                return 0
+        else:
+            report = run_pipeline(config)
     except ConfigError as exc:
         return _fail(str(exc), 2)
     except Exception as exc:  # noqa: BLE001 -- data or stage failure: runtime, not usage
         return _fail(str(exc), 1)
     _write_report(args, report.to_text())
     return 0
+
+
+def _run_sharded(config):
+    """One log over the torchrun ranks (sharded.run_sharded, NCCL): every rank
+    gets the single run's report or failure; rank 0's is printed."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+    from .config import ConfigError
+    from .sharded import run_sharded
+    if config.mode != "pipelined":
+        raise ConfigError("--sharded runs the pipelined mode")
+    if not dist.is_initialized():
+        if "RANK" not in os.environ:
+            raise ConfigError("--sharded: launch under torchrun (RANK / WORLD_SIZE unset)")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    try:
+        report = run_sharded(config)
+    finally:
+        rank = dist.get_rank()
+        dist.destroy_process_group()
+    return report if rank == 0 else None
 
 
 def cmd_plan(args) -> int:
@@ -147,6 +177,8 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--batch-size", type=int, dest="batch_size")
     p.add_argument("--staging", help="directory for staged mode files")
     p.add_argument("--report", help="also write the report to this file")
+    p.add_argument("--sharded", action="store_true",
+                   help="one log over the torchrun ranks (one GPU each), the single run's report")
     p.set_defaults(func=cmd_run)
 
     p = sub.add_parser("plan", help="print the layer plan and the generated kernel")

@@ -46,3 +46,31 @@ def test_run_both_modes(mode, capsys):
     kv = parse_report_block(capsys.readouterr().out)
     assert kv["digest"] == "0x483d13d62f945805" and kv["instances"] == "1764"
     assert kv["mode"] == mode
+
+
+def test_sharded_needs_torchrun(tmp_path, capsys, monkeypatch):
+    d = tmp_path / "c"
+    assert cli.main(["gen-corpus", "--out", str(d), "--instances", "400", "--users", "40"]) == 0
+    monkeypatch.delenv("RANK", raising=False)
+    assert cli.main(["run", "--config", str(d / "pipeline.json"), "--sharded"]) == 2
+    assert "torchrun" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_run_sharded_under_torchrun(tmp_path):
+    """`torchrun -m ...cli run --sharded` with the box's one GPU: rank 0 prints the
+    single run's report (the published 2k corpus digest)."""
+    import subprocess
+    import sys
+    d = tmp_path / "c"
+    assert cli.main(["gen-corpus", "--out", str(d), "--instances", "2000", "--users", "300",
+                     "--seed", "7"]) == 0
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "1", "--master-addr", "127.0.0.1",
+                        "--master-port", "29531", "-m", "paper_2210_07768_b200.cli", "run",
+                        "--config", str(d / "pipeline.json"), "--sharded"],
+                       capture_output=True, text=True, cwd=root, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    kv = parse_report_block(r.stdout)
+    assert kv["digest"] == "0x483d13d62f945805" and kv["instances"] == "1764"
