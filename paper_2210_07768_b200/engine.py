@@ -569,6 +569,8 @@ class Engine:
                     img = self._load_view(v.name, src.path, src.columns, views.get(v.name))
                 dv = DeviceView(img, device=self.device)
             self._keep.append(dv)
+            if v is ir.basic:
+                self._basic_dv = dv
             n = dv.n
             cap = _next_pow2(2 * n)
             table = torch.zeros(cap * 32, dtype=torch.uint8, device=self.device)
@@ -620,7 +622,51 @@ class Engine:
     def _settle_prepare(self, st: dict):
         self.prepare_counters.malformed = st["malformed"]
         self.prepare_counters.filtered = st["filtered"]
+        if st["error_key"] != placement.NONE and \
+                (st["error_key"] & 0xFF) == codegen.ERR["basic_dup"]:
+            self._raise_basic_dup()
         self._raise_if_error(st, prepare=True)
+
+    def _raise_basic_dup(self):
+        """The basic view repeats an instance id (the index build saw it): name the
+        id check_unique_ids names -- the first row, in row order, whose id occurred
+        before (viewpipe.py:562-576, pipeline.py:975-980) -- by sorting the id
+        column on the device (fbx_sort_keys + fbx_first_repeat, the staged mode's
+        check)."""
+        torch = self.torch
+        dv = self._basic_dv
+        col = self.ir.instance_column
+        kind = dv.kinds[col]
+        n = dv.n
+        stream = self._stream()
+        raw = dv.tensors[col]["data"]
+        if kind is Kind.FLOAT32:
+            bits = raw[:4 * n].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        else:
+            bits = raw[:8 * n].view(torch.int64)
+        m = max(n, 1)
+        isnull = torch.zeros(m + 16, dtype=torch.uint8, device=self.device)
+        runtime.call("fbx_unpack_nulls", dv.ptr(col, "nulls"), n, isnull.data_ptr(), stream)
+        skey = torch.empty(m, dtype=torch.int64, device=self.device)
+        srow = torch.empty(m, dtype=torch.int32, device=self.device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+        rs = torch.empty(m, dtype=torch.int32, device=self.device)
+        ks = torch.empty(m, dtype=torch.int64, device=self.device)
+        fs = torch.empty(m, dtype=torch.uint8, device=self.device)
+        runtime.call("fbx_sort_keys", bits.data_ptr(), isnull.data_ptr(), n, skey.data_ptr(),
+                     srow.data_ptr(), cnt.data_ptr(), rs.data_ptr(), ks.data_ptr(), fs.data_ptr(),
+                     stream)
+        best = torch.empty(1, dtype=torch.int64, device=self.device)
+        runtime.call("fbx_first_repeat", skey.data_ptr(), srow.data_ptr(), int(cnt.item()),
+                     best.data_ptr(), stream)
+        row = int(best.cpu().numpy().view(np.uint64)[0])
+        if row == placement.NONE:
+            return  # not a repeat after all: the error word decides
+        v = int(bits[row].item())
+        if kind is Kind.FLOAT32:
+            v = float(np.int32(np.uint32(v)).view(np.float32))
+        raise StageError("prepare", None,
+                         MergeUniquenessError(f"basic features: duplicate instance id {v}"))
 
     def finish_prepare(self):
         """A deferred prepare check (``defer_prepare_check``): the side views'
@@ -660,6 +706,7 @@ class Engine:
         aux = self.side_tables[k].view(torch.int32).view(-1, words)[:, 3]
         mx = int(aux.max().item()) if aux.numel() else 0
         if mx > 1:
+            self._raise_basic_dup()
             raise StageError("prepare", None,
                              MergeUniquenessError("basic features: duplicate instance id"))
 

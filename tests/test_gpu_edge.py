@@ -642,6 +642,35 @@ def test_basic_view_duplicate_id_fails_prepare(dst, src, tmp_path):
     assert (got_err.stage, got_err.batch_index) == ("prepare", None) == (ref_err.stage,
                                                                          ref_err.chunk)
     assert "basic features" in str(got_err.__cause__)
+    assert str(got_err.__cause__) == str(ref_err.cause)
+
+
+@pytest.mark.parametrize("pairs", [[(1500, 3), (700, 600)], [(700, 600), (1500, 3)],
+                                   [(9, 8), (10, 8), (4, 1800)]])
+@pytest.mark.parametrize("streamed", [False, True])
+def test_basic_view_names_the_first_repeat(pairs, streamed, tmp_path):
+    """Several ids repeat in the basic view: the message names the id of the first
+    row, in row order, whose id occurred before (viewpipe.py:562-576) -- found by a
+    device sort of the id column, whatever order the index build saw them in."""
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.engine import run_pipelined
+    ops = [{"name": "c", "inputs": ["query"], "outputs": ["c"], "body": {"fn": "hash:3"}}]
+    raw = _config(512, ops, {"c": 3}, filt="age != -12345")
+    drv, prof, bas = _views(2000, 5)
+    for dst, src in pairs:
+        drv, prof, bas = _basic_dup(dst, src)(drv, prof, bas)
+    _write_views(tmp_path, drv, prof, bas)
+    tables, sizes = O.load_tables({}, tmp_path)
+    with pytest.raises(O.OracleError) as ref:
+        O.run_pipelined(raw, {"ev": drv, "pr": prof}, bas, tables, sizes)
+    cfg = config_from_dict(raw, tmp_path)
+    with pytest.raises(Exception) as got:
+        if streamed:
+            run_pipelined(cfg)
+        else:
+            run_pipelined(cfg, collect=True)
+    assert (got.value.stage, got.value.batch_index) == ("prepare", None)
+    assert str(got.value.__cause__) == str(ref.value.cause)
 
 
 def test_long_strings_grow_the_device_arena(tmp_path):
