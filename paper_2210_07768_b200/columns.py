@@ -44,6 +44,14 @@ class ChecksumError(FormatError):
     """Body CRC32 does not match the footer (``columnstore.py:51``)."""
 
 
+class BadMagicError(FormatError):
+    pass
+
+
+class UnsupportedVersionError(FormatError):
+    pass
+
+
 class TruncatedError(FormatError):
     pass
 
@@ -319,16 +327,20 @@ def open_view(path: str | Path) -> ViewFile:
         blob = fh.read(min(size, 1 << 16))
 
         def more(upto: int):
+            # read on as the header needs; past the end of the file the parse below
+            # fails exactly as the reference's does on its whole-file blob
             nonlocal blob
             if upto > len(blob):
                 blob += fh.read(upto - len(blob))
-            if upto > len(blob):
-                raise struct.error("header past the end of the file")
 
-        if len(blob) < 6 or blob[:4] != MAGIC:
-            raise FormatError(f"{path}: not an FBXC file")
-        if _U16.unpack_from(blob, 4)[0] != VERSION:
-            raise FormatError(f"{path}: unsupported version")
+        # the reference's checks and messages (columnstore.py:401-478)
+        if len(blob) < 6:
+            raise TruncatedError(f"{path}: too short for a header")
+        if blob[:4] != MAGIC:
+            raise BadMagicError(f"{path}: magic {bytes(blob[:4])!r}, expected {MAGIC!r}")
+        (version,) = _U16.unpack_from(blob, 4)
+        if version != VERSION:
+            raise UnsupportedVersionError(f"{path}: version {version}, expected {VERSION}")
         try:
             pos = 6
             more(pos + 12)
@@ -342,7 +354,10 @@ def open_view(path: str | Path) -> ViewFile:
                 kind = Kind(blob[pos])
                 (ln,) = _U16.unpack_from(blob, pos + 1)
                 more(pos + 3 + ln)
-                schema.append((blob[pos + 3 : pos + 3 + ln].decode("utf-8"), kind))
+                name = blob[pos + 3 : pos + 3 + ln].decode("utf-8")
+                if len(name.encode("utf-8")) != ln:
+                    raise TruncatedError(f"{path}: truncated column name")
+                schema.append((name, kind))
                 pos += 3 + ln
             keys = []
             for _ in range(nkeys):
@@ -356,6 +371,8 @@ def open_view(path: str | Path) -> ViewFile:
             spans = [_SEG.unpack_from(blob, pos + i * _SEG.size) for i in range(nseg)]
             pos += nseg * _SEG.size
         except (struct.error, IndexError, ValueError) as exc:
+            if isinstance(exc, FormatError):
+                raise
             raise TruncatedError(f"{path}: malformed header ({exc})") from None
         parts = [
             (n, p)
@@ -363,16 +380,17 @@ def open_view(path: str | Path) -> ViewFile:
             for p in (("nulls", "offsets", "data") if k.var_length else ("nulls", "data"))
         ]
         if len(parts) != nseg:
-            raise FormatError(f"{path}: directory/schema mismatch")
+            raise FormatError(f"{path}: directory has {nseg} segments, schema implies "
+                              f"{len(parts)}")
         cursor = pos
         segs = {}
         for key, (off, ln) in zip(parts, spans):
             if off != cursor:
-                raise FormatError(f"{path}: segment {key} not contiguous")
+                raise FormatError(f"{path}: segment {key[0]}/{key[1]} not contiguous")
             segs[key] = (off, ln)
             cursor += ln
         if cursor + 4 != size:
-            raise TruncatedError(f"{path}: length mismatch")
+            raise TruncatedError(f"{path}: file is {size} bytes, layout implies {cursor + 4}")
         fh.seek(cursor)
         (crc,) = _U32.unpack(fh.read(4))
     return ViewFile(path, tuple(schema), tuple(keys), rows, segs, pos, cursor - pos, crc)

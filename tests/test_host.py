@@ -236,3 +236,49 @@ def test_shard_goldens_compose_to_c5():
         x ^= int(r["digest"], 16)
     assert f"0x{x:016x}" == doc["c5"]["xor_digest"]
     assert sum(r["rows"] for r in c5) == 100_000_000
+
+
+# ---- FBXC header validation: the reference's error types and messages --------------
+
+def _fbxc_cases(tmp_path):
+    """(name, bytes) of damaged FBXC files, as the reference's own tests make them
+    (test_columnstore.py: bad magic, version 2, truncated, tiny) plus a cut
+    column name, a cut directory and a body one byte long."""
+    import struct as st
+    from paper_2210_07768_b200.columns import ColumnImage, Kind, ViewImage, write_view
+    v = ViewImage.from_pydict([("id", Kind.INT64), ("name", Kind.UTF8)],
+                              {"id": [1, 2, None], "name": ["a", None, "ccc"]}, ("id",))
+    path = tmp_path / "ok.fbxc"
+    write_view(v, path)
+    blob = path.read_bytes()
+    bad_magic = b"XXXX" + blob[4:]
+    v2 = blob[:4] + st.pack("<H", 2) + blob[6:]
+    return {"bad_magic": bad_magic, "version": v2, "truncated": blob[:-5], "tiny": b"FB",
+            "cut_name": blob[:22], "cut_directory": blob[:40], "long": blob + b"\0",
+            "empty": b""}
+
+
+def test_fbxc_header_errors_match_reference(tmp_path):
+    import sys
+    from conftest import reference_package_path
+    from paper_2210_07768_b200 import columns as C
+    ref = reference_package_path()
+    for name, data in _fbxc_cases(tmp_path).items():
+        f = tmp_path / f"{name}.fbxc"
+        f.write_bytes(data)
+        with pytest.raises(C.FormatError) as got:
+            C.open_view(f)
+        want = {"bad_magic": C.BadMagicError, "version": C.UnsupportedVersionError,
+                "tiny": C.TruncatedError, "truncated": C.TruncatedError,
+                "empty": C.TruncatedError}.get(name)
+        if want is not None:
+            assert type(got.value) is want, (name, got.value)
+        if ref is None:
+            continue
+        if str(ref) not in sys.path:
+            sys.path.insert(0, str(ref))
+        import featurebox.columnstore as RC
+        with pytest.raises(RC.FormatError) as exp:
+            RC.open_view(f)
+        assert type(got.value).__name__ == type(exp.value).__name__, name
+        assert str(got.value) == str(exp.value), name
