@@ -419,7 +419,7 @@ def read_view(
     if verify and wanted_set == set(names):
         crc = zlib.crc32(buf[vf.body_offset : vf.body_offset + vf.body_bytes]) & 0xFFFFFFFF
         if crc != vf.checksum:
-            raise ChecksumError(f"{vf.path}: body CRC {crc:#010x} != {vf.checksum:#010x}")
+            raise ChecksumError(f"{vf.path}: body CRC {crc:#010x} != footer {vf.checksum:#010x}")
     n = vf.row_count
     cols = {}
     for name, kind in vf.schema:

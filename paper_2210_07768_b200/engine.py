@@ -280,7 +280,7 @@ class DeviceView:
         if verify and (columns is None or set(columns) >= set(names)):
             crc = crc32_device(body[:vf.body_bytes])
             if crc != vf.checksum:
-                raise ChecksumError(f"{vf.path}: body CRC {crc:#010x} != {vf.checksum:#010x}")
+                raise ChecksumError(f"{vf.path}: body CRC {crc:#010x} != footer {vf.checksum:#010x}")
         self = cls.__new__(cls)
         self.n = vf.row_count
         self.kinds = {n: k for n, k in vf.schema}
@@ -377,7 +377,7 @@ class DeviceView:
         crc = int(out.cpu().numpy().view(np.uint32)[0])
         self._crc = None
         if crc != want:
-            raise ChecksumError(f"{path}: body CRC {crc:#010x} != {want:#010x}")
+            raise ChecksumError(f"{path}: body CRC {crc:#010x} != footer {want:#010x}")
 
 
 def crc32_device_async(t):

@@ -282,3 +282,27 @@ def test_fbxc_header_errors_match_reference(tmp_path):
             RC.open_view(f)
         assert type(got.value).__name__ == type(exp.value).__name__, name
         assert str(got.value) == str(exp.value), name
+
+
+def test_fbxc_checksum_error_matches_reference(tmp_path):
+    import sys
+    from conftest import reference_package_path
+    from paper_2210_07768_b200 import columns as C
+    from paper_2210_07768_b200.columns import Kind, ViewImage, write_view
+    v = ViewImage.from_pydict([("id", Kind.INT64)], {"id": [1, 2, 3]}, ("id",))
+    f = tmp_path / "crc.fbxc"
+    write_view(v, f)
+    raw = bytearray(f.read_bytes())
+    raw[-9] ^= 0x40
+    f.write_bytes(bytes(raw))
+    with pytest.raises(C.ChecksumError) as got:
+        C.read_view(f)
+    ref = reference_package_path()
+    if ref is None:
+        return
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import featurebox.columnstore as RC
+    with pytest.raises(RC.ChecksumError) as exp:
+        RC.read_columns(RC.open_view(f), None)
+    assert str(got.value) == str(exp.value)
