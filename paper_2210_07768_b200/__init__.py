@@ -6,8 +6,9 @@ it): same config schema, operator specs, errors and report, executed as a
 runtime-compiled fused CUDA kernel per plan on sm_100a.
 """
 
-from .columns import (ChecksumError, ColumnImage, FormatError, Kind, ViewImage, open_view,
-                      read_view, schema_of, unwrap_u64, wrap_u64, write_view)
+from .columns import (BadMagicError, ChecksumError, ColumnImage, FormatError, Kind,
+                      TruncatedError, UnknownColumnError, UnsupportedVersionError, ViewImage,
+                      open_view, read_view, schema_of, unwrap_u64, wrap_u64, write_view)
 from .config import (BatchInvariantError, CleanConfigError, CleanPolicy, ConfigError,
                      EmitError, JsonExtraction, LayerExecutionError, MergeUniquenessError,
                      PipelineConfig, PoolExhausted, StageError, UnsupportedOnDevice,
@@ -28,4 +29,7 @@ def __getattr__(name):
                 "RunReport", "DeviceView", "parse_report_block"):
         from . import engine
         return getattr(engine, name)
+    if name == "run_sharded":
+        from . import sharded
+        return sharded.run_sharded
     raise AttributeError(name)

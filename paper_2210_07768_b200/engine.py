@@ -32,7 +32,7 @@ from typing import Mapping
 import numpy as np
 
 from . import codegen, placement, runtime
-from .columns import ColumnImage, Kind, ViewImage, open_view, read_view
+from .columns import Kind, ViewImage, open_view, read_view
 from .config import (ConfigError, EmitError, BatchInvariantError, CleanConfigError,
                      LayerExecutionError, MergeUniquenessError, PipelineConfig, PoolExhausted,
                      StageError, UnsupportedOnDevice, bind_filter, cleaned_kinds,
