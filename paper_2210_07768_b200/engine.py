@@ -1667,7 +1667,10 @@ def _prepared(config: PipelineConfig) -> Prepared:
     """prepare() once per plan key (_config_key): the plan cache.  The returned
     Prepared carries the CALL's config (its dictionary tables)."""
     import dataclasses
-    key = _config_key(config)
+    try:
+        key = _config_key(config)
+    except Exception:  # noqa: BLE001 -- an unreadable file: prepare raises the reference's error
+        return prepare(config)
     prep = _PREPARED.get(key)
     if prep is None:
         prep = prepare(config)
