@@ -10,6 +10,8 @@ kernel by ``codegen.py``.
 
 from __future__ import annotations
 
+import os
+
 import json
 import re
 import struct
@@ -288,6 +290,31 @@ class ViewSource:
     path: Path
     columns: tuple[str, ...] | None
     policy: CleanPolicy
+
+
+def host_worker_count(requested: int | None = None) -> int:
+    """Effective host workers (device.py:81-96): the requested count (else the CPU
+    count), capped by FEATUREBOX_THREADS when it is set; a bad cap is a ValueError
+    (a ConfigError once a run starts, pipeline.py:697-701)."""
+    base = requested if requested is not None else (os.cpu_count() or 1)
+    cap_text = os.environ.get("FEATUREBOX_THREADS")
+    if cap_text:
+        try:
+            cap = int(cap_text)
+        except ValueError:
+            raise ValueError(f"FEATUREBOX_THREADS={cap_text!r} is not an integer") from None
+        if cap < 1:
+            raise ValueError("FEATUREBOX_THREADS must be >= 1")
+        base = min(base, cap)
+    return max(1, base)
+
+
+def run_workers(config: "PipelineConfig") -> int:
+    """host_worker_count for a run: ConfigError on a bad FEATUREBOX_THREADS."""
+    try:
+        return host_worker_count(config.workers)
+    except ValueError as exc:
+        raise ConfigError(str(exc)) from exc
 
 
 @dataclass(frozen=True)

@@ -36,7 +36,7 @@ from .columns import Kind, ViewImage, open_view, read_view
 from .config import (ConfigError, EmitError, BatchInvariantError, CleanConfigError,
                      LayerExecutionError, MergeUniquenessError, PipelineConfig, PoolExhausted,
                      StageError, UnsupportedOnDevice, bind_filter, cleaned_kinds,
-                     validate_clean_policy)
+                     validate_clean_policy, run_workers)
 from .featureops import FeatureConfigError, output_domains, resolve_function
 from .opgraph import (DEVICE, OperatorDag, LayerPlan, PlacementBudget, expand_call_graph,
                       layer_schedule, place_operators, reference_node_order,
@@ -1633,7 +1633,8 @@ def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: Vie
         intermediate_bytes_written=0, intermediate_files=(),
         rows_dropped=total.malformed + eng.prepare_counters.malformed,
         rows_filtered=total.filtered + eng.prepare_counters.filtered,
-        batch_size=bs, workers=1, wall_seconds=time.perf_counter() - t0, stage_seconds=stage)
+        batch_size=bs, workers=run_workers(config), wall_seconds=time.perf_counter() - t0,
+        stage_seconds=stage)
     return RunResult(rep, csr)
 
 
@@ -1727,6 +1728,7 @@ class _StreamedRun:
     stage: dict
     t0: float
     read_failure: "StageError | None" = None
+    workers: int = 1
 
     def first_failure(self) -> tuple[int, int]:
         """(error key, detail) of the run's first failure; a read failure is
@@ -1762,7 +1764,7 @@ class _StreamedRun:
             bytes_h2d=self.bytes_h2d if bytes_h2d is None else bytes_h2d,
             transfer_seconds=self.transfer_s, intermediate_bytes_written=0,
             intermediate_files=(), rows_dropped=c.malformed + pc.malformed,
-            rows_filtered=c.filtered + pc.filtered, batch_size=bs, workers=1,
+            rows_filtered=c.filtered + pc.filtered, batch_size=bs, workers=self.workers,
             wall_seconds=time.perf_counter() - self.t0, stage_seconds=self.stage)
 
 
@@ -1792,6 +1794,7 @@ def _stream_pipelined(config: PipelineConfig, slice_rows: int = 1 << 19,
     t0 = time.perf_counter()
     stage: dict[str, float] = {}
     prep = _prepared(config)
+    workers = run_workers(config)  # the reference's ExecContext (pipeline.py:697-701)
     drv_cfg = config.view(config.driver)
     torch = _torch()
     try:
@@ -1905,7 +1908,7 @@ def _stream_pipelined(config: PipelineConfig, slice_rows: int = 1 << 19,
                      st["filtered"], st["joined"], t["slices"])
     stage["stream"] = time.perf_counter() - t1
     return _StreamedRun(config, eng, st, c, launches, launch_s, bytes_h2d, transfer_s, stage, t0,
-                        read_failure)
+                        read_failure, workers)
 
 
 def run_pipeline(config: PipelineConfig, mode: str | None = None) -> RunReport:

@@ -290,6 +290,9 @@ def host_threads() -> int:
         n = len(os.sched_getaffinity(0))
     except (AttributeError, OSError):
         n = os.cpu_count() or 1
+    cap = os.environ.get("FEATUREBOX_THREADS", "")  # the reference's host-thread cap
+    if cap.isdigit() and int(cap) >= 1:
+        n = min(n, int(cap))
     return max(1, min(32, n))
 
 

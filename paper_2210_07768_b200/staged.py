@@ -316,6 +316,8 @@ def run_staged(config: PipelineConfig):
     prepare(config, compile_program=False)  # the reference's validation (ConfigError)
     if config.staging_dir is None:
         raise ConfigError("staged mode requires staging_dir")
+    from .config import run_workers
+    workers = run_workers(config)  # the reference's ExecContext (pipeline.py:697-701)
     staging = Path(config.staging_dir)
     staging.mkdir(parents=True, exist_ok=True)
     stream = torch.cuda.current_stream().cuda_stream
@@ -441,7 +443,7 @@ def run_staged(config: PipelineConfig):
         intermediate_bytes_written=intermediate,
         intermediate_files=tuple(sorted(f.name for f in files)),
         rows_dropped=counters["malformed"], rows_filtered=counters["filtered"],
-        batch_size=config.batch_size, workers=1, wall_seconds=time.perf_counter() - wall0,
+        batch_size=config.batch_size, workers=workers, wall_seconds=time.perf_counter() - wall0,
         stage_seconds=stage_seconds)
 
 
