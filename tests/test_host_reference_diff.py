@@ -1,0 +1,142 @@
+"""CPU: the host-side drop-in surface against the UNMODIFIED reference (baseline/_ref
+or /root/reference, imported read-only; skipped without it): the filter grammar,
+the clean-policy and JSON-path validation, the feature-op helpers and the
+dictionary-table loader give the same results, exception types and messages."""
+
+from __future__ import annotations
+
+import sys
+
+import pytest
+
+from conftest import reference_package_path
+
+REF = reference_package_path()
+pytestmark = pytest.mark.skipif(REF is None, reason="reference package not installed")
+
+
+def _ref(mod):
+    if str(REF) not in sys.path:
+        sys.path.insert(0, str(REF))
+    import importlib
+    return importlib.import_module(f"featurebox.{mod}")
+
+
+def _outcome(fn, *a, **kw):
+    try:
+        return ("ok", repr(fn(*a, **kw)))
+    except Exception as exc:  # noqa: BLE001
+        return ("err", type(exc).__name__, str(exc))
+
+
+FILTERS = ["age <= 120", "score > -1.5", "city == 'nyc'", 'city != "sf"',
+           "a == 1 or b == 2 and c == 3", "(a == 1 or b == 2) and c == 3", "a == 1 && b == 2",
+           "a == 1 || b == 2", "", "age", "age <=", "age <= <=", "<= 120", "age ~ 5",
+           "(age <= 120", "age <= 120)", "age <= 120 extra", "age <= 'x' @", "age <= 1e3",
+           "x == -0.0", "x == 'it''s'", "x==1", "not x == 1", "x == 1 and",
+           "x == 99999999999999999999999", "((a == 1))", "a == 1 or (b == 2 or c == 3)",
+           "a == 'é'", "a >= 0.1 and b < 2 or not c == 'z'"]
+
+
+@pytest.mark.parametrize("text", FILTERS)
+def test_filter_grammar(text):
+    from paper_2210_07768_b200.config import parse_filter
+    assert _outcome(parse_filter, text) == _outcome(_ref("viewpipe").parse_filter, text)
+
+
+@pytest.mark.parametrize("path", ["a", "u.city", "", "a..b", ".a", "a.", "a b", "é.x"])
+def test_json_extraction_paths(path):
+    from paper_2210_07768_b200.columns import Kind
+    from paper_2210_07768_b200.config import JsonExtraction
+    rv = _ref("viewpipe")
+    rk = _ref("columnstore").Kind
+    got = _outcome(JsonExtraction, "meta", path, "o", Kind.UTF8)
+    want = _outcome(rv.JsonExtraction, "meta", path, "o", rk.UTF8)
+    assert got[0] == want[0] and got[1:2] == want[1:2] if got[0] == "err" else got[0] == "ok"
+    if got[0] == "err":
+        assert got[2] == want[2]
+
+
+def _policies(cfg, kind_mod):
+    K = kind_mod
+    X = cfg.JsonExtraction
+    return [
+        cfg.CleanPolicy(fills={"ghost": 1}),
+        cfg.CleanPolicy(fills={"age": "old"}),
+        cfg.CleanPolicy(fills={"age": True}),
+        cfg.CleanPolicy(fills={"query": 3}),
+        cfg.CleanPolicy(fills={"age": 2 ** 70}),
+        cfg.CleanPolicy(extractions=(X("ghost", "a", "o", K.UTF8),)),
+        cfg.CleanPolicy(extractions=(X("query", "a", "o", K.UTF8),)),
+        cfg.CleanPolicy(extractions=(X("meta", "a", "age", K.UTF8),)),
+        cfg.CleanPolicy(extractions=(X("meta", "a", "age", K.INT64),)),
+        cfg.CleanPolicy(fills={"age": 0, "query": ""}),
+    ]
+
+
+def test_clean_policy_validation():
+    from paper_2210_07768_b200 import config as C
+    from paper_2210_07768_b200.columns import Kind
+    rv, rc = _ref("viewpipe"), _ref("columnstore")
+    ours = _policies(C, Kind)
+    theirs = _policies(rv, rc.Kind)
+    kinds = {"age": Kind.INT64, "query": Kind.UTF8, "meta": Kind.JSON}
+    schema = rc.ColumnBatch.from_pydict([("age", rc.Kind.INT64), ("query", rc.Kind.UTF8),
+                                         ("meta", rc.Kind.JSON)],
+                                        {"age": [], "query": [], "meta": []}).schema
+    for mine, ref in zip(ours, theirs):
+        got = _outcome(C.validate_clean_policy, kinds, mine)
+        want = _outcome(rv.validate_clean_policy, schema, ref)
+        assert got == want, (mine, got, want)
+    X, XR = C.JsonExtraction, rv.JsonExtraction
+    dup = (lambda M, K: M.CleanPolicy(extractions=(M.JsonExtraction("meta", "a", "o", K.UTF8),
+                                                   M.JsonExtraction("meta", "b", "o", K.UTF8))))
+    assert _outcome(dup, C, Kind) == _outcome(dup, rv, rc.Kind)
+    del X, XR
+
+
+@pytest.mark.parametrize("s,d", [("a b  c", " "), ("", " "), ("x", "x"), ("a|b|", "|"),
+                                 ("é é", " "), ("abc", "ab"), ("abc", ""), ("a b", "é")])
+def test_split_string(s, d):
+    from paper_2210_07768_b200.featureops import split_string
+    assert _outcome(split_string, s, d) == _outcome(_ref("featureops").split_string, s, d)
+
+
+@pytest.mark.parametrize("values,slot", [([b"a"], 0), ([b"", b"x"], 65535), ([b"q" * 70], 7),
+                                         ([b"a", b"b", b"c"], 300), ([b"a"], 65536), ([], 3),
+                                         ([b"a"], -1)])
+def test_hash_combine_and_fnv(values, slot):
+    from paper_2210_07768_b200.featureops import fnv1a64, hash_combine
+    rf = _ref("featureops")
+    assert _outcome(hash_combine, values, slot) == _outcome(rf.hash_combine, values, slot)
+    for v in values:
+        assert fnv1a64(v) == rf.fnv1a64(v)
+
+
+SPECS = ["lower", "trim", "id", "mix", "fold", "token: :0", "token:,:3", "token::1", "token: ",
+         "token: :-1", "token: :x", "hash:0", "hash:65535", "hash:65536", "hash:-1", "hash:x",
+         "concat:", "concat:|", "lookup:ghost", "nope", "", "token:ab:1", "hash:07"]
+
+
+@pytest.mark.parametrize("spec", SPECS)
+def test_resolve_function_errors(spec):
+    """Spec grammar errors (featureops.py:370-446): same exception type and text;
+    accepted specs are accepted by both (the B200 side returns device op codes)."""
+    from paper_2210_07768_b200.featureops import resolve_function
+    got = _outcome(resolve_function, spec, {})
+    want = _outcome(_ref("featureops").resolve_function, spec, {})
+    assert got[0] == want[0], (spec, got, want)
+    if got[0] == "err":
+        assert got[1:] == want[1:], spec
+
+
+@pytest.mark.parametrize("text", ["a\t1\nb\t2\n", "a\t1\na\t2\n", "a 1\n", "a\tx\n", "\t5\n",
+                                  "a\t-1\n", "a\t18446744073709551616\n", "", "# c\na\t1\n",
+                                  "a\t1\n\nb\t2\n", "é\t7\n"])
+def test_load_dict_table(text, tmp_path):
+    from paper_2210_07768_b200.featureops import load_dict_table
+    f = tmp_path / "t.tsv"
+    f.write_text(text, encoding="utf-8")
+    got = _outcome(lambda: dict(load_dict_table(f, 0).entries))
+    want = _outcome(lambda: dict(_ref("featureops").load_dict_table(f, 0).entries))
+    assert got == want, (text, got, want)
