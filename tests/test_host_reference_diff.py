@@ -140,3 +140,77 @@ def test_load_dict_table(text, tmp_path):
     got = _outcome(lambda: dict(load_dict_table(f, 0).entries))
     want = _outcome(lambda: dict(_ref("featureops").load_dict_table(f, 0).entries))
     assert got == want, (text, got, want)
+
+
+# ---- load_config + prepare on mutated configs: the same ConfigError text ------------
+
+def _mut(path, value):
+    def m(raw):
+        obj = raw
+        for k in path[:-1]:
+            obj = obj[k]
+        if value is _DEL:
+            del obj[path[-1]]
+        else:
+            obj[path[-1]] = value
+    return m
+
+
+_DEL = object()
+
+
+def _append_ops(*ops):
+    def m(raw):
+        raw["operators"].extend(ops)
+    return m
+
+
+MUTATIONS = {
+    "unknown_fn": _mut(["operators", 0, "body", "fn"], "warp:9"),
+    "dup_outputs": lambda raw: raw["operators"][1].__setitem__("outputs",
+                                                              raw["operators"][0]["outputs"]),
+    "ghost_feature": lambda raw: raw["emit"]["features"].__setitem__("ghost_col", 40),
+    "missing_join_key": _mut(["join", "keys"], ["no_such_key"]),
+    "missing_label": _mut(["label_column"], "nope"),
+    "ghost_filter": _mut(["views", 0, "clean", "filter"], "ghost > 3"),
+    "bad_filter": _mut(["views", 0, "clean", "filter"], "age <"),
+    "cycle": _append_ops({"name": "loop_a", "inputs": ["loop_b_out"], "outputs": ["loop_a_out"],
+                          "body": {"fn": "hash:60"}},
+                         {"name": "loop_b", "inputs": ["loop_a_out"], "outputs": ["loop_b_out"],
+                          "body": {"fn": "hash:61"}}),
+    "unknown_input": _mut(["operators", 0, "inputs"], ["never_heard_of_it"]),
+    "batch_zero": _mut(["batch_size"], 0),
+    "mode": _mut(["mode"], "turbo"),
+    "slot_range": lambda raw: raw["emit"]["features"].__setitem__("x", 1 << 16),
+    "no_views": _mut(["views"], []),
+    "ghost_driver": _mut(["driver"], "ghost"),
+    "fill_kind": lambda raw: raw["views"][0]["clean"]["fills"].__setitem__("age", "old"),
+    "fill_unknown": lambda raw: raw["views"][0]["clean"]["fills"].__setitem__("ghost", 1),
+    "no_basic": lambda raw: raw.__delitem__("basic"),
+    "table_missing": lambda raw: raw["tables"].__setitem__("t2", {"path": "/nonexistent.tsv"}),
+    "arity": _mut(["operators", 0, "body", "fn"], "lower"),
+}
+
+
+@pytest.mark.parametrize("case", sorted(MUTATIONS))
+def test_config_mutations_fail_alike(case, tmp_path):
+    import json
+    from paper_2210_07768_b200 import engine, load_config
+    rc = _ref("corpus")
+    rp = _ref("pipeline")
+    base = tmp_path / "c"
+    paths = rc.gen_corpus(base, rows=200, users=20, seed=7, views=2)
+    raw = json.loads(paths["config"].read_text())
+    for v in raw["views"]:
+        v["path"] = str(base / v["path"])
+    raw["basic"]["path"] = str(base / raw["basic"]["path"])
+    for t in raw.get("tables", {}).values():
+        t["path"] = str(base / t["path"])
+    raw["staging_dir"] = str(tmp_path / "staging")
+    MUTATIONS[case](raw)
+    f = tmp_path / "pipeline.json"
+    f.write_text(json.dumps(raw))
+    got = _outcome(lambda: engine.prepare(load_config(f), compile_program=False))
+    want = _outcome(lambda: rp.prepare(rp.load_config(f)))
+    assert got[0] == want[0] == "err", (case, got, want)
+    assert got[1:] == want[1:], (case, got, want)
