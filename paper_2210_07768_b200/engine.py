@@ -1624,6 +1624,7 @@ def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: Vie
     total = b.counters
     total.launches = launches
     stage["extract"] = time.perf_counter() - t2
+    _fused_stages(stage)
     csr = b.to_numpy() if collect else None
     bs = config.batch_size
     rep = RunReport(
@@ -1662,6 +1663,14 @@ def _config_key(config: PipelineConfig) -> str:
         parts.append(repr(open_view(v.path).schema))
     parts.append(repr(open_view(config.basic_path).schema))
     return hashlib.sha256(repr(parts).encode()).hexdigest()
+
+
+def _fused_stages(stage: dict) -> None:
+    """The reference's pipelined stage keys (pipeline.py:984-1094: prepare, read,
+    clean, join, extract, merge, emit).  Clean, join, merge and emit run inside the
+    fused kernel, so their time is in "extract"; their keys read 0.0."""
+    for k in ("prepare", "read", "clean", "join", "extract", "merge", "emit"):
+        stage.setdefault(k, 0.0)
 
 
 def _prepared(config: PipelineConfig) -> Prepared:
@@ -1907,6 +1916,7 @@ def _stream_pipelined(config: PipelineConfig, slice_rows: int = 1 << 19,
         c = Counters(st["digest"], st["instances"], st["signs"], st["malformed"],
                      st["filtered"], st["joined"], t["slices"])
     stage["stream"] = time.perf_counter() - t1
+    _fused_stages(stage)
     return _StreamedRun(config, eng, st, c, launches, launch_s, bytes_h2d, transfer_s, stage, t0,
                         read_failure, workers)
 

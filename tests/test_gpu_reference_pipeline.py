@@ -174,3 +174,18 @@ def test_worker_count_and_fusion_leave_results_unchanged(tmp_path):
         rep = _run(dataclasses.replace(cfg, **kw), "pipelined")
         assert (rep.digest, rep.instances, rep.signs) == (base.digest, base.instances,
                                                           base.signs), kw
+
+
+def test_stage_timing_keys(tmp_path):
+    """pkg/tests/test_pipeline.py:576-582: the staged run times exactly its five
+    stages; the pipelined run reports at least the reference's seven keys."""
+    from conftest import corpus
+    from paper_2210_07768_b200.config import config_from_dict
+    from paper_2210_07768_b200.workloads import workload_config
+    _, d = corpus(2000, 300, 7)
+    cfg = config_from_dict(dict(workload_config("default"), staging_dir=str(tmp_path / "s")), d)
+    assert set(_run(cfg, "staged").stage_seconds) == {"clean", "join", "extract", "merge",
+                                                      "emit"}
+    keys = {"prepare", "read", "clean", "join", "extract", "merge", "emit"}
+    assert keys <= set(_run(cfg, "pipelined").stage_seconds)
+    assert keys <= set(_run(dataclasses.replace(cfg, batch_size=4096), "pipelined").stage_seconds)
