@@ -3,13 +3,16 @@
 Workload (BASELINE.json configs[1]): the 1M-record synthetic ads log
 (gen_corpus rows=1,000,000 users=5,000 seed=11) through the sign-heavy DAG
  with the reference's full emit (basic merge
-included).  A *step* is one pass of the hot path over the whole log:
-clean -> side join -> 18-node DAG -> uniqueness check + basic merge ->
-sorted/deduplicated CSR + digests.  Every step's digest is checked against
-the reference golden (0xb30824efab77470b).
+included).  A *step* is one pass of the hot path over the whole log: the
+per-run side / basic index builds, then clean -> side join -> 18-node DAG ->
+uniqueness check + basic merge -> sorted/deduplicated CSR + digests, replayed
+as one captured CUDA graph (--no-graph: kernel by kernel).  Every shard's
+digest is checked against the unmodified reference's (0xb30824efab77470b for
+this log); the L2 is flushed between steps.  `e2e` is the reference-facing
+run_pipelined(config) over the log's files, one call per step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--dag sign_heavy]
-    python bench.py --impl reference ...   # the CPU reference arm (oracle port)
+    python bench.py --impl reference ...   # the unmodified reference on the host cores
 
 N > 1 runs under torchrun: one record shard (its own 1M-row log, seed 11 + r)
 per GPU, no per-record communication, one NCCL all-gather of the per-shard
