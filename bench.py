@@ -388,7 +388,9 @@ def main():
             giev = tuple(torch.cuda.Event(enable_timing=True, external=True) for _ in range(2))
             g = torch.cuda.CUDAGraph()
             cap.wait_stream(torch.cuda.current_stream(dev))
-            with torch.cuda.graph(g, stream=cap):
+            # thread_local: the NCCL watchdog's event queries (torchrun) must not
+            # invalidate the capture
+            with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
                 run_shard(e, corp.driver.row_count, gev, giev, cap)
             graphs.append((g, gev, giev, streams[j % nstreams]))
         graph_launches = launches[0]
