@@ -310,11 +310,21 @@ def host_worker_count(requested: int | None = None) -> int:
 
 
 def run_workers(config: "PipelineConfig") -> int:
-    """host_worker_count for a run: ConfigError on a bad FEATUREBOX_THREADS."""
+    """The run-start checks of the reference's ExecContext (pipeline.py:697-711,
+    device.py:116-125): host_worker_count (a bad FEATUREBOX_THREADS is a
+    ConfigError), then the device shape, fusion mode and bandwidth (ValueError,
+    raised as the reference raises it).  Returns the effective host workers."""
     try:
-        return host_worker_count(config.workers)
+        workers = host_worker_count(config.workers)
     except ValueError as exc:
         raise ConfigError(str(exc)) from exc
+    if config.fusion not in ("fused", "unfused"):
+        raise ValueError("fusion must be 'fused' or 'unfused'")
+    if config.lanes_per_group < 1 or config.work_groups < 1:
+        raise ValueError("device shape must be at least 1x1")
+    if not config.bandwidth_bytes_per_s > 0:
+        raise ValueError("bandwidth must be positive")
+    return workers
 
 
 @dataclass(frozen=True)

@@ -1593,6 +1593,7 @@ def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: Vie
     t0 = time.perf_counter()
     stage: dict[str, float] = {}
     prep = prepared or prepare(config, views, basic)
+    workers = run_workers(config)  # the reference's ExecContext checks (pipeline.py:697-711)
     stage["prepare"] = time.perf_counter() - t0
     eng = Engine(prep, views, basic, device=device, max_rows_per_launch=max_rows_per_launch)
     torch = eng.torch
@@ -1634,7 +1635,7 @@ def run_views(config: PipelineConfig, views: Mapping[str, ViewImage], basic: Vie
         intermediate_bytes_written=0, intermediate_files=(),
         rows_dropped=total.malformed + eng.prepare_counters.malformed,
         rows_filtered=total.filtered + eng.prepare_counters.filtered,
-        batch_size=bs, workers=run_workers(config), wall_seconds=time.perf_counter() - t0,
+        batch_size=bs, workers=workers, wall_seconds=time.perf_counter() - t0,
         stage_seconds=stage)
     return RunResult(rep, csr)
 

@@ -189,6 +189,13 @@ MUTATIONS = {
     "no_basic": lambda raw: raw.__delitem__("basic"),
     "table_missing": lambda raw: raw["tables"].__setitem__("t2", {"path": "/nonexistent.tsv"}),
     "arity": _mut(["operators", 0, "body", "fn"], "lower"),
+    "pool_bytes": lambda raw: raw.setdefault("device", {}).__setitem__("pool_bytes", 100),
+    "queue_depth": _mut(["queue_depth"], 0),
+    "workers_zero": _mut(["workers"], 0),
+    "budget": lambda raw: raw.setdefault("device", {}).__setitem__("budget_bytes", -1),
+    "dup_view": lambda raw: raw["views"].append(dict(raw["views"][0])),
+    "no_join": lambda raw: raw.__delitem__("join"),
+    "feature_not_int": lambda raw: raw["emit"]["features"].__setitem__("q_sig", "x"),
 }
 
 
@@ -214,3 +221,32 @@ def test_config_mutations_fail_alike(case, tmp_path):
     want = _outcome(lambda: rp.prepare(rp.load_config(f)))
     assert got[0] == want[0] == "err", (case, got, want)
     assert got[1:] == want[1:], (case, got, want)
+
+
+RUN_START = {
+    "fusion": lambda raw: raw.setdefault("device", {}).__setitem__("fusion", "sideways"),
+    "lanes": lambda raw: raw.setdefault("device", {}).__setitem__("lanes_per_group", 0),
+    "work_groups": lambda raw: raw.setdefault("device", {}).__setitem__("work_groups", 0),
+    "bandwidth": lambda raw: raw.setdefault("device", {}).__setitem__("bandwidth_bytes_per_s", 0),
+    "fine": lambda raw: None,
+}
+
+
+@pytest.mark.parametrize("case", sorted(RUN_START))
+def test_run_start_checks_fail_alike(case, tmp_path, monkeypatch):
+    """Checks the reference makes when a run starts (its ExecContext): the same
+    exception type and text before any data moves."""
+    import json
+    from paper_2210_07768_b200 import load_config
+    from paper_2210_07768_b200.config import run_workers
+    monkeypatch.delenv("FEATUREBOX_THREADS", raising=False)
+    rc, rp = _ref("corpus"), _ref("pipeline")
+    base = tmp_path / "c"
+    paths = rc.gen_corpus(base, rows=50, users=5, seed=7, views=2)
+    raw = json.loads(paths["config"].read_text())
+    RUN_START[case](raw)
+    f = base / "pipeline.json"
+    f.write_text(json.dumps(raw))
+    got = _outcome(lambda: run_workers(load_config(f)) and None)
+    want = _outcome(lambda: rp._make_ctx(rp.prepare(rp.load_config(f))) and None)
+    assert got == want, (case, got, want)
