@@ -196,6 +196,19 @@ MUTATIONS = {
     "dup_view": lambda raw: raw["views"].append(dict(raw["views"][0])),
     "no_join": lambda raw: raw.__delitem__("join"),
     "feature_not_int": lambda raw: raw["emit"]["features"].__setitem__("q_sig", "x"),
+    "ghost_projection": _mut(["views", 0, "columns"], ["instance_id", "ghost"]),
+    "projection_drops_label": _mut(["views", 0, "columns"], ["instance_id", "user_id", "query"]),
+    "extract_kind": lambda raw: raw["views"][0]["clean"].__setitem__(
+        "extract", [{"source": "meta", "path": "u.city", "output": "cx", "kind": "blob"}]),
+    "extract_source": lambda raw: raw["views"][0]["clean"].__setitem__(
+        "extract", [{"source": "query", "path": "u.city", "output": "cx", "kind": "utf8"}]),
+    "table_default": lambda raw: [t.__setitem__("default", "x") for t in raw["tables"].values()],
+    "table_path": lambda raw: [t.__setitem__("path", "/nope/none.tsv") for t in raw["tables"].values()],
+    "op_no_body": lambda raw: raw["operators"][0].__delitem__("body"),
+    "op_bad_pre": _mut(["operators", 0, "pre"], [{"fn": "hash:3"}]),
+    "basic_columns": lambda raw: raw["basic"].__setitem__("columns", ["basic_a"]),
+    "label_kind": _mut(["label_column"], "query"),
+    "instance_kind": _mut(["instance_column"], "query"),
 }
 
 
